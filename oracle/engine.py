@@ -1,0 +1,201 @@
+"""ORACLE -- test infrastructure, NOT product code (see oracle/__init__.py).
+
+O7: continuous-batching replay of one decode iteration per step
+(SURVEY.md §8(a) S1 -> S7), driven by step latencies logged from the GPU run.
+
+The paper describes the control loop only at the level of Fig. 1 / Alg. 1-2:
+b_t is decided per scheduling interval from telemetry and bounds the number of
+requests in the running batch.  The step semantics
+below are the readings R17-R22 of DESIGN.md (SPEC.md:381-404 engine, adapted
+to paged blocks):
+
+ 1. release arrivals with arrival_ns <= clock into the FCFS queue;
+ 2. admission: while the queue is non-empty and |running| < b_t (this rank's
+    share of b_t), take the head r; it needs ceil((T_r + 1) / P) free pages
+    with T_r = l_in + generated_r (recompute after preemption); otherwise
+    stop (head-of-line blocking).  Admitted: append T_r tokens (prefill);
+ 3. page growth: every running request appends its decode token; while the
+    pages this needs exceed the free pages, preempt the most recently admitted
+    running request (LIFO; its pages are released, it goes to the queue head,
+    its generated tokens are kept for recompute); then append (all-or-nothing);
+ 4. decode: the running requests in admission order attend over ctx_i tokens;
+    the batch statistics record is formed (O3);
+ 5. retire requests with generated = l_out (release pages);
+ 6. clock += step_ns (device-timed); release arrivals; N^p = queue length;
+ 7. b_{t+1} from the scheduler on the (global) record (O5/O6).
+An idle engine (nothing running or queued) jumps the clock to the next arrival.
+"""
+from __future__ import annotations
+
+from collections import deque
+
+from . import stats as ostats
+from .allocator import PagedKV
+from .policy import Scheduler
+
+FNV_OFFSET = 0xCBF29CE484222325
+FNV_PRIME = 0x100000001B3
+M64 = (1 << 64) - 1
+
+
+def fnv1a64(values, h=FNV_OFFSET):
+    """FNV-1a over the little-endian bytes of 64-bit integers (checksum of tables)."""
+    for v in values:
+        v &= M64
+        for k in range(8):
+            h ^= (v >> (8 * k)) & 0xFF
+            h = (h * FNV_PRIME) & M64
+    return h
+
+
+class RankEngine:
+    """One GPU's request shard (DP) or the whole batch (G = 1 / TP)."""
+
+    def __init__(self, req_ids, arrival_ns, l_in, l_out, cap_pages, page_size, rank=0, world=1):
+        self.req_ids = list(req_ids)
+        self.arrival = [int(a) for a in arrival_ns]
+        self.l_in = {r: int(x) for r, x in zip(self.req_ids, l_in)}
+        self.l_out = {r: int(x) for r, x in zip(self.req_ids, l_out)}
+        self.kv = PagedKV(cap_pages, page_size)
+        self.P = page_size
+        self.cap = cap_pages
+        self.rank, self.world = rank, world
+        self.next = 0
+        self.queue = deque()
+        self.running = []
+        self.gen = {r: 0 for r in self.req_ids}
+        self.finished = 0
+        for r in self.req_ids:
+            if -(-(self.l_in[r] + self.l_out[r]) // page_size) > cap_pages:
+                raise RuntimeError(f"request {r} cannot fit the cap alone")
+
+    def release_arrivals(self, clock):
+        while self.next < len(self.req_ids) and self.arrival[self.next] <= clock:
+            self.queue.append(self.req_ids[self.next])
+            self.next += 1
+
+    def idle(self):
+        return not self.running and not self.queue
+
+    def done(self):
+        return self.idle() and self.next >= len(self.req_ids)
+
+    def next_arrival(self):
+        return self.arrival[self.next] if self.next < len(self.req_ids) else None
+
+    def admit_and_grow(self, b_share):
+        admitted = preempted = 0
+        while self.queue and len(self.running) < b_share:           # step 2
+            r = self.queue[0]
+            T = self.l_in[r] + self.gen[r]
+            if self.kv.alloc.free < -(-(T + 1) // self.P):
+                break
+            self.queue.popleft()
+            self.kv.begin(r)
+            self.kv.append([r], [T])
+            self.running.append(r)
+            admitted += 1
+        while True:                                                    # step 3
+            need = sum(1 for r in self.running if self.kv.ctx[r] % self.P == 0)
+            if need <= self.kv.alloc.free:
+                break
+            victim = self.running.pop()
+            self.kv.release(victim)
+            self.queue.appendleft(victim)
+            preempted += 1
+        self.kv.append(self.running, [1] * len(self.running))
+        for r in self.running:
+            self.gen[r] += 1
+        return admitted, preempted
+
+    def batch(self):
+        """The decode launch's batch: (req_ids, ctx, l_in, l_out, pages) in batch order."""
+        rs = list(self.running)
+        return (rs, [self.kv.ctx[r] for r in rs], [self.l_in[r] for r in rs],
+                [self.l_out[r] for r in rs], [list(self.kv.pages[r]) for r in rs])
+
+    def local_stats(self):
+        rs, ctx, li, lo, pages = self.batch()
+        return ostats.batch_stats(ctx, li, lo, pages, self.P, self.cap)
+
+    def table_hash(self):
+        h = FNV_OFFSET
+        for r in self.running:
+            h = fnv1a64([r, self.kv.ctx[r], len(self.kv.pages[r])] + self.kv.pages[r], h)
+        return h
+
+    def retire(self):
+        keep, fin = [], 0
+        for r in self.running:
+            if self.gen[r] == self.l_out[r]:
+                self.kv.release(r)
+                fin += 1
+            else:
+                keep.append(r)
+        self.running = keep
+        self.finished += fin
+        return fin
+
+
+def b_share(b, rank, world):
+    """This rank's share of the global b_t (DP request shards, reading R21)."""
+    return b // world + (1 if rank < b % world else 0)
+
+
+class Replay:
+    """Lock-step replay of G rank engines sharing one scheduling decision per step."""
+
+    def __init__(self, ranks, sched_cfg, mem_cap_bytes_total):
+        self.ranks = ranks
+        self.sched = Scheduler(sched_cfg)
+        self.mem_cap = int(mem_cap_bytes_total)
+        self.clock = 0
+        self.t = 0
+        self.b = self.sched.b
+
+    def done(self):
+        return all(e.done() for e in self.ranks)
+
+    def step(self, step_ns):
+        """One iteration; step_ns = the logged device time (max over ranks).  Returns the record."""
+        G = len(self.ranks)
+        for e in self.ranks:
+            e.release_arrivals(self.clock)
+        if all(e.idle() for e in self.ranks):
+            nxt = [a for a in (e.next_arrival() for e in self.ranks) if a is not None]
+            if not nxt:
+                raise RuntimeError("replay finished")
+            self.clock = max(self.clock, min(nxt))
+            for e in self.ranks:
+                e.release_arrivals(self.clock)
+        clock0 = self.clock
+        adm = pre = 0
+        for e in self.ranks:
+            a, p = e.admit_and_grow(b_share(self.b, e.rank, G))
+            adm += a
+            pre += p
+        recs = [e.local_stats() for e in self.ranks]
+        batches = [e.batch() for e in self.ranks]
+        hashes = [e.table_hash() for e in self.ranks]
+        used = [e.kv.alloc.used for e in self.ranks]
+        fin = sum(e.retire() for e in self.ranks)
+        self.clock += int(step_ns)
+        for e in self.ranks:
+            e.release_arrivals(self.clock)
+        waiting = sum(len(e.queue) for e in self.ranks)
+        for r in recs:
+            r["step_ns"] = int(step_ns)
+            r["n_waiting"] = 0
+        g = ostats.reduce_records(recs, "dp") if G > 1 else dict(recs[0])
+        g["n_waiting"] = waiting
+        assert g["n_finished"] == fin
+        b_t = self.b
+        self.b, rationale = self.sched.decide(g, self.mem_cap, waiting)
+        rec = dict(t=self.t, clock_ns=clock0, b_t=b_t, n_admitted=adm, n_preempted=pre,
+                   n_decode=g["n_active"], n_finished=fin, sum_ctx=g["sum_ctx"],
+                   used_pages=sum(used), step_ns=int(step_ns), b_next=self.b, rationale=rationale,
+                   L0=self.sched.L0, b_quad=self.sched.bq, b_mem=self.sched.b_mem,
+                   b_sla=self.sched.b_sla, table_hash=hashes[0] if G == 1 else tuple(hashes),
+                   stats=g, local_stats=recs, batches=batches)
+        self.t += 1
+        return rec

@@ -1,0 +1,79 @@
+"""Counter-based synthetic value generator (input generation only).
+
+value(seed, kind, req, pos, layer, head, dim):
+    key1 = splitmix64(seed ^ (kind << 56) ^ req)
+    word = (pos << 32) | (layer << 20) | (head << 8) | (dim >> 3)
+    key2 = splitmix64(key1 ^ word)
+    byte = (key2 >> (8 * (dim & 7))) & 0xFF
+    value = (byte - 128) / 128 * 2**scale_log2
+
+One 64-bit hash yields the 8 consecutive dims [8g, 8g+8) so the device side
+can emit one 16-byte store per hash.  |byte-128| <= 128 needs at most 8
+significant bits, so every value is exact in fp16 and in bf16 (8-bit
+significand) for any power-of-two scale within range.
+
+Coordinate limits: req < 2**56, pos < 2**31, layer < 2**12, head < 2**12,
+dim < 2**11.  kind: 0 = q, 1 = K, 2 = V.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+KIND_Q, KIND_K, KIND_V = 0, 1, 2
+
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser on uint64 arrays (wrap-around arithmetic)."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = x + _GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * _M1
+        z = (z ^ (z >> np.uint64(27))) * _M2
+    return z ^ (z >> np.uint64(31))
+
+
+def gen_bytes(seed, kind, req, pos, layer, head, d):
+    """Raw bytes in [0, 256) with shape broadcast(req, pos, layer, head) + (d,)."""
+    if d % 8:
+        raise ValueError("head dim must be a multiple of 8")
+    req = np.asarray(req, dtype=np.uint64)
+    pos = np.asarray(pos, dtype=np.uint64)
+    layer = np.asarray(layer, dtype=np.uint64)
+    head = np.asarray(head, dtype=np.uint64)
+    shape = np.broadcast_shapes(req.shape, pos.shape, layer.shape, head.shape)
+    key1 = splitmix64(np.uint64(seed) ^ (np.uint64(kind) << np.uint64(56)) ^ req)
+    word = (pos << np.uint64(32)) | (layer << np.uint64(20)) | (head << np.uint64(8))
+    key1 = np.broadcast_to(key1, shape)[..., None]
+    word = np.broadcast_to(word, shape)[..., None]
+    g = np.arange(d // 8, dtype=np.uint64)
+    key2 = splitmix64(key1 ^ (word | g))  # shape + (d/8,)
+    shifts = (np.arange(8, dtype=np.uint64) * np.uint64(8))
+    b = (key2[..., None] >> shifts) & np.uint64(0xFF)  # shape + (d/8, 8)
+    return b.reshape(shape + (d,)).astype(np.int32)
+
+
+def gen_values(seed, kind, req, pos, layer, head, d, scale_log2=0) -> np.ndarray:
+    """float64 values (k/128) * 2**scale_log2, k in [-128, 127]."""
+    b = gen_bytes(seed, kind, req, pos, layer, head, d)
+    return (b - 128).astype(np.float64) / 128.0 * (2.0 ** scale_log2)
+
+
+def to_bits(values: np.ndarray, dtype: str) -> np.ndarray:
+    """Encode exactly-representable float values as fp16 / bf16 bit patterns (uint16)."""
+    v = np.asarray(values, dtype=np.float64)
+    if dtype == "f16":
+        h = v.astype(np.float16)
+        if not np.array_equal(h.astype(np.float64), v):
+            raise ValueError("value not exact in fp16")
+        return h.view(np.uint16)
+    if dtype == "bf16":
+        f = v.astype(np.float32)
+        u = f.view(np.uint32)
+        if np.any(u & np.uint32(0xFFFF)) or not np.array_equal(f.astype(np.float64), v):
+            raise ValueError("value not exact in bf16")
+        return (u >> np.uint32(16)).astype(np.uint16)
+    raise ValueError(dtype)
