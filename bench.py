@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark: continuous-batching decode iterations of the Llama-2-7B-shaped workload
+(BASELINE.json configs[1]) through the C-ABI engine on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+A step = one engine iteration = admission + prefill fill + page growth + KV append +
+paged decode attention over all L layers (batch statistics fused into layer 0) +
+statistics D2H + the host batch-size decision (Algorithm 1).  Prints one JSON line.
+N > 1 (torchrun): request-sharded DP, per-GPU work fixed (weak scaling), the 128-byte
+statistics records all-gathered over NCCL every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import configs, trace  # noqa: E402
+
+CFG_NAME = "llama2-7b"
+METRIC = "decode tokens/s"
+UNIT = "tokens/s"
+GB = 1e9
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per decode launch from the committed ncu --set full summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(rank=0, world=1, n_req=None):
+    c = configs.CONFIGS[CFG_NAME]
+    t = c["trace"]
+    n = (n_req or c["n_requests"]) * world
+    tr = trace.make_trace(n, t["mean_in"], t["mean_out"], t["L_max"], t["seed"], dist=t["dist"])
+    return c, tr
+
+
+def sched_kwargs(c, beta):
+    pr = configs.prior_record(c)
+    return dict(policy=1, b_static=256, b_min=c["b_min"], b_max=c["b_max"], b0=c["b_min"],
+                eps_m=c["eps_m"], bytes_per_token=beta, page_size=c["page_size"], refresh_steps=100,
+                w_len=256, w_sla=20, alpha=8, delta=2, prior=tuple(pr.values()))
+
+
+def setup_engine(device=0, rank=0, world=1, cap_bytes=None, time_attention=True, out_dtype=0,
+                 seed=2024, n_req=None):
+    """Pool sized from free HBM (cap = free - modeled 7B weights - reserve), memory policy."""
+    import torch
+
+    import paper_2503_05248_b200 as dbk
+    c, tr = make_workload(rank, world, n_req)
+    L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
+    beta = configs.kv_bytes_per_token(c)
+    max_req = c["b_max"] + 8
+    io_bytes = 2 * L * max_req * Hq * d * 4 + 2 * max_req * L * Hkv * d * 2
+    free, _ = torch.cuda.mem_get_info(device)
+    if cap_bytes is None:
+        cap_bytes = free - c["weights_bytes"] - c["reserve_bytes"] - io_bytes
+    cap_pages = int(cap_bytes // (P * beta))
+    maxp = -(-c["trace"]["L_max"] // P)
+    pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, "f16", device=device)
+    mem_cap_total = cap_pages * P * beta * world
+    sched = dbk.Scheduler(**sched_kwargs(c, beta))
+    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap_total, seed=seed,
+                     out_dtype=out_dtype, time_attention=time_attention, rank=rank, world=world)
+    et = torch.float32 if out_dtype == 2 else torch.float16
+    qd = torch.empty(L, max_req, Hq, d, dtype=torch.float16, device=f"cuda:{device}")
+    od = torch.empty(L, max_req, Hq, d, dtype=et, device=f"cuda:{device}")
+    kvd = torch.empty(2, max_req, L, Hkv, d, dtype=torch.float16, device=f"cuda:{device}")
+    return dict(dbk=dbk, c=c, tr=tr, pool=pool, sched=sched, eng=eng, qd=qd, od=od, kvd=kvd,
+                cap_pages=cap_pages, beta=beta, max_req=max_req, mem_cap_total=mem_cap_total, seed=seed)
+
+
+def run_steps(S, k, bufs, stream, comm_world=1, dist=None):
+    """k engine steps; returns (records, device ms) timed with CUDA events on `stream`."""
+    import torch
+    eng = S["eng"]
+    recs = []
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        if eng.done():
+            break
+        recs.append(eng.step(bufs, stream))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    return recs, e0.elapsed_time(e1)
+
+
+def cpu_baseline(S, budget_s=15.0, threads=None):
+    """The oracle (plain C, fp64) on a bounded sample of the current decode batch."""
+    from oracle import attention as oatt
+    c = S["c"]
+    L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
+    ids, ctx = S["eng"].last_batch()
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(0)
+    order = rng.permutation(len(ids))
+    done_req, secs, layers_used, k0 = 0, 0.0, 0, 0
+    kk = 8
+    while secs < budget_s and layers_used < L:
+        sel = order[k0:k0 + kk]
+        if len(sel) == 0:
+            k0 = 0
+            layers_used += 1
+            continue
+        pages, nxt = [], 0
+        for cx in ctx[sel]:
+            np_ = -(-int(cx) // P)
+            pages.append(list(range(nxt, nxt + np_)))
+            nxt += np_
+        bt, pk, pv, qq = oatt.synth_paged_batch(S["seed"], [int(x) for x in ids[sel]], ctx[sel], pages,
+                                                layers_used, Hq, Hkv, d, P, "f16")
+        t0 = time.perf_counter()
+        oatt.paged_decode_attention(ctx[sel], bt, pk, pv, qq, "f16", nthreads=threads)
+        dt = time.perf_counter() - t0
+        secs += dt
+        done_req += len(sel)
+        k0 += len(sel)
+        kk = int(min(128, max(8, kk * max(1.0, (budget_s - secs) / max(dt, 1e-3) / 4))))
+    tok_s = done_req / L / secs
+    return {"value": round(tok_s, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{done_req} request-layers (random requests of the timed batch, mean ctx "
+                      f"{float(np.mean(ctx)):.0f}), fp64 paged attention, {secs:.1f} s; tokens/s = "
+                      f"request-layers / L / time"}
+
+
+def run_gpu(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    S = setup_engine(device=local, rank=rank, world=world)
+    dbk = S["dbk"]
+    if world > 1:
+        idb = bytearray(128)
+        if rank == 0:
+            import ctypes
+            buf = (ctypes.c_char * 128)()
+            dbk._lib.dbk_comm_unique_id(buf)
+            idb = bytearray(buf.raw)
+        obj = [bytes(idb)]
+        dist.broadcast_object_list(obj, src=0)
+        import ctypes
+        idbuf = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        comm = ctypes.c_void_p()
+        dbk._lib.dbk_comm_create(world, rank, idbuf, local, ctypes.byref(comm))
+        dbk._lib.dbk_engine_attach_comm(S["eng"].h, comm, dbk._lib.MODE_DP)
+    stream = torch.cuda.current_stream()
+    eng = S["eng"]
+    bufs = eng.buffers(S["qd"], S["od"])
+    # fast-forward to the steady state (untimed), then W warm-up steps (untimed)
+    run_steps(S, args.ff, bufs, stream, dist=dist)
+    run_steps(S, args.warmup, bufs, stream, dist=dist)
+    eng.attn_timing(reset=True)
+    with ClockSampler(local) as clk:
+        recs, ms = run_steps(S, args.steps, bufs, stream, dist=dist)
+    att_ms, att_launches, att_bytes = eng.attn_timing(reset=True)
+    ms_t = torch.tensor([ms], device="cuda")
+    tok_t = torch.tensor([float(sum(r["n_decode"] for r in recs))], device="cuda")
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    # decode tokens of the whole job: every rank's batch counts (DP shards are disjoint)
+    if dist is not None:
+        dist.all_reduce(tok_t)
+    toks = float(tok_t.item())
+    # end-to-end through the same API with pinned host buffers (q, new K/V in; out back)
+    c = S["c"]
+    L, Hq, Hkv, d = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"]
+    mr = S["max_req"]
+    hq = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
+    hk = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
+    hv = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
+    ho = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True)
+    ebufs = eng.buffers(S["qd"], S["od"], S["kvd"], hq, hk, hv, ho)
+    run_steps(S, 2, ebufs, stream, dist=dist)
+    with ClockSampler(local) as clk2:
+        erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
+    ems_t = torch.tensor([ems], device="cuda")
+    etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs))], device="cuda")
+    if dist is not None:
+        dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(etok_t)
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        achieved = att_bytes / 1e9 / (att_ms / 1e3) if att_ms > 0 else 0.0
+        traffic, traffic_alg = ncu_traffic()
+        clocks = clk.summary()
+        n_steps = len(recs)
+        line = {
+            "metric": METRIC, "value": round(toks / (ms_max / 1e3), 2), "unit": UNIT, "n_gpus": world,
+            "steps": n_steps, "warmup": args.warmup, "ms_per_step": round(ms_max / max(n_steps, 1), 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic (seeded lognormal trace, hash-generated q/K/V; no weights on this path)",
+            "config": {"workload": configs.CONFIGS[CFG_NAME]["name"], "layers": L, "q_heads": Hq,
+                       "kv_heads": Hkv, "head_dim": d, "page_size": 16, "kv_dtype": "fp16",
+                       "out_dtype": "fp16", "policy": "memory-aware (Alg. 1 + Eq. 11 L0)",
+                       "requests_per_gpu": configs.CONFIGS[CFG_NAME]["n_requests"],
+                       "trace": "all-at-once, lognormal CV=1, means 191.0/381.9 (PAPER.md:266)",
+                       "cap_pages_per_gpu": S["cap_pages"],
+                       "kv_cap_gb_per_gpu": round(S["cap_pages"] * 16 * S["beta"] / GB, 2),
+                       "mean_batch": round(float(np.mean([r["n_decode"] for r in recs])), 1) if recs else 0,
+                       "mean_ctx": round(float(np.mean([r["sum_ctx"] / max(r["n_decode"], 1) for r in recs])), 1) if recs else 0,
+                       "fast_forward_steps": args.ff, "parallelism": f"dp{world} (request shards)",
+                       "l2": "inputs > L2 (~1e2 GB of KV read per step vs 126 MB L2)"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "decode_kernel (paged decode attention, K1)",
+                         "bytes_per_launch": int(att_bytes / max(att_launches, 1)),
+                         "ms_per_launch": round(att_ms / max(att_launches, 1), 4), "peak_source": peak_src,
+                         "share_of_step": round(att_ms / max(ms, 1e-9), 4)},
+            "e2e": {"value": round(float(etok_t.item()) / (float(ems_t.item()) / 1e3), 2), "unit": UNIT,
+                    "h2d_bytes_per_step": int(np.mean([r["h2d_bytes"] for r in erecs])) if erecs else 0,
+                    "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in erecs])) if erecs else 0},
+            "gpu_launches": int(sum(r["launches"] for r in recs)),
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(S)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The oracle as the reference arm (no GPU): each step = fp64 paged attention on a bounded
+    sample of one layer of the steady-state batch + the oracle's batch-size decision."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import attention as oatt
+    from oracle import engine as oeng
+    from oracle import policy as opol
+    c, tr = make_workload()
+    L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
+    beta = configs.kv_bytes_per_token(c)
+    free = 178_000_000_000  # same sizing rule as the GPU arm on a 180 GB part
+    cap_pages = int((free - c["weights_bytes"] - c["reserve_bytes"]) // (P * beta))
+    kw = sched_kwargs(c, beta)
+    rp = oeng.Replay([oeng.RankEngine(list(range(len(tr))), tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P)],
+                     opol.SchedConfig(**kw), cap_pages * P * beta)
+    for _ in range(args.ff):           # steady state: same fast-forward as the GPU arm (modeled 25 ms steps)
+        rp.step(25_000_000)
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(1)
+    per_step = 8
+    times, toks = [], 0
+    for s in range(args.warmup + args.steps):
+        rec = rp.step(25_000_000)
+        rs, ctx, li, lo, pages = rec["batches"][0]
+        sel = rng.choice(len(rs), size=min(per_step, len(rs)), replace=False)
+        cp, nxt = [], 0
+        for i in sel:
+            m = -(-ctx[i] // P)
+            cp.append(list(range(nxt, nxt + m)))
+            nxt += m
+        bt, pk, pv, qq = oatt.synth_paged_batch(2024, [rs[i] for i in sel], [ctx[i] for i in sel], cp,
+                                                s % L, Hq, Hkv, d, P, "f16")
+        t0 = time.perf_counter()
+        oatt.paged_decode_attention(np.asarray([ctx[i] for i in sel]), bt, pk, pv, qq, "f16", nthreads=threads)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            toks += len(sel)
+    secs = sum(times)
+    value = toks / L / secs
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / max(len(times), 1), 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (same trace and generator as the GPU arm)",
+            "config": {"workload": c["name"], "layers": L, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d},
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"per step {per_step} random requests of the steady-state batch at one "
+                                       f"layer (fp64 C oracle); tokens/s = request-layers / L / time"},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--ff", type=int, default=300, help="untimed fast-forward steps to the steady state")
+    ap.add_argument("--impl", default="dbk", choices=["dbk", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,298 @@
+/*
+ * dbk.h -- C-ABI of the B200-native decode hot path of arXiv 2503.05248
+ * ("dynamic batching": memory-aware and SLA-constrained batch sizing).
+ *
+ * One continuous-batching decode iteration = paged KV-cache decode attention
+ * over the active batch ("decoding latency ... increases with batch
+ * size"; PAPER.md:71 PagedAttention) + the device-side batch telemetry that
+ * feeds Algorithm 1 and Algorithm 2,
+ * which run on the host in this library.  See DESIGN.md for the readings of
+ * the paper (R1..R23) referenced below.
+ *
+ * Conventions (every entry point):
+ *  - returns dbk_status, 0 = DBK_OK; never throws, never aborts;
+ *  - on error, dbk_last_error() returns a thread-local message; the call has
+ *    no effect unless stated otherwise;
+ *  - "device" pointers are CUDA global-memory pointers on the pool's device
+ *    (e.g. torch tensor data_ptr()); "host" pointers are CPU memory;
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  A pool, a
+ *    scheduler and an engine are NOT thread-safe; use one host thread and one
+ *    stream per pool (the library orders its own uploads on that stream);
+ *  - the library never allocates KV storage: the caller passes the KV memory
+ *    (ownership stays with the caller, who keeps it alive until destroy).  It
+ *    allocates only small device metadata (block tables, work lists,
+ *    split-K workspace, the stats record) with cudaMalloc;
+ *  - there is no CPU fallback: without a usable CUDA device the GPU entry
+ *    points fail with DBK_ECUDA.
+ */
+#ifndef DBK_H_
+#define DBK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dbk_status {
+    DBK_OK = 0,
+    DBK_EINVAL = 1,       /* bad argument / configuration                          */
+    DBK_ECAP = 2,         /* would exceed the page cap; nothing changed (R8)       */
+    DBK_ENOENT = 3,       /* unknown request id                                    */
+    DBK_EINFEASIBLE = 4,  /* no b >= 1 meets the constraint                        */
+    DBK_ECUDA = 5,        /* CUDA runtime error (message has the CUDA error text)  */
+    DBK_ENCCL = 6,        /* NCCL error                                            */
+    DBK_EFATAL = 7        /* a single request exceeds the cap alone        */
+} dbk_status;
+
+const char *dbk_last_error(void);
+const char *dbk_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* KV pool: paged KV cache + page allocator + request table                  */
+/* ------------------------------------------------------------------------ */
+
+/* Shapes of one GPU's share of the model (KV-head TP: pass the local heads).
+ * Device layout of the caller-provided KV memory:
+ *   kv[layer][page][kv_head][2 (K,V)][page_size][head_dim], element kv_dtype.
+ * Constraints: q_heads % kv_heads == 0, q_heads/kv_heads in {1,2,4,8},
+ * head_dim in {64,128}, page_size == 16, kv_dtype 0 = fp16, 1 = bf16. */
+typedef struct dbk_pool_config {
+    int32_t layers, q_heads, kv_heads, head_dim, page_size, kv_dtype;
+    int64_t cap_pages;          /* M_max in pages (R4)          */
+    int32_t max_requests;       /* request slots (rows of the block table)   */
+    int32_t max_pages_per_req;  /* block-table row width = ceil(L_max / P)   */
+    int32_t device;             /* CUDA device ordinal                       */
+    int32_t _reserved;
+} dbk_pool_config;
+
+typedef struct dbk_pool dbk_pool;
+
+/* Bytes of KV memory the pool needs: layers*cap_pages*kv_heads*2*P*d*2. */
+size_t dbk_kv_pool_bytes(const dbk_pool_config *cfg);
+
+/* kv_mem: caller-owned device memory of >= dbk_kv_pool_bytes(cfg) bytes,
+ * 256-byte aligned.  Contents need not be initialised (never-written slots
+ * are masked).  EINVAL on bad shapes, ECUDA if the device is unusable. */
+dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t kv_bytes,
+                              dbk_pool **out);
+dbk_status dbk_kv_pool_destroy(dbk_pool *pool);
+
+/* Register request req_id (>= 0) with prompt length l_in >= 1 and target
+ * output length l_out >= 1 (l_in,i / l_out,i).  It holds 0
+ * tokens and a free request slot.  EINVAL if it already exists or no slot
+ * is free; EFATAL if ceil((l_in + l_out)/P) > cap_pages or > max_pages_per_req. */
+dbk_status dbk_request_begin(dbk_pool *pool, int64_t req_id, int32_t l_in, int32_t l_out);
+
+/* Append n_tok[i] tokens to request req_ids[i] (host arrays, batch order).
+ * Pages come lowest-free-first in batch order (R7, R8); all-or-nothing:
+ * DBK_ECAP if the batch needs more pages than are free, state unchanged.
+ * k, v: device [sum(n_tok)][layers][kv_heads][head_dim] in kv_dtype, rows in
+ * batch order; or both NULL = synthetic values from the seeded generator
+ * (synth/hashgen.py, kinds K/V, pos = the token's position) with synth_seed.
+ * Async on `stream`. */
+dbk_status dbk_append_tokens(dbk_pool *pool, int32_t n_req, const int64_t *req_ids,
+                             const int32_t *n_tok, const void *k, const void *v,
+                             uint64_t synth_seed, void *stream);
+
+/* Finish or preempt: all pages of each request return to the free set (R9),
+ * the slot is freed and its device block-table row is cleared before the
+ * next launch.  ENOENT on an unknown id (earlier ids are released). */
+dbk_status dbk_release(dbk_pool *pool, int32_t n_req, const int64_t *req_ids);
+
+/* Host view of one request: ctx (tokens held), n_pages, slot, and up to
+ * pages_cap page ids (logical order) into pages_out (nullable). */
+dbk_status dbk_request_info(dbk_pool *pool, int64_t req_id, int32_t *ctx, int32_t *n_pages,
+                            int32_t *slot, int32_t *pages_out, int32_t pages_cap);
+dbk_status dbk_pool_usage(dbk_pool *pool, int64_t *used_pages, int64_t *free_pages);
+
+/* Copy the device block table [max_requests][max_pages_per_req] int32
+ * (-1 = empty) to host memory (synchronous on `stream`). */
+dbk_status dbk_block_table_d2h(dbk_pool *pool, int32_t *host_out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Decode step: paged decode attention (+ fused batch statistics)           */
+/* ------------------------------------------------------------------------ */
+
+typedef struct dbk_batch {
+    int32_t n;             /* active requests (0 = no-op)                        */
+    int32_t layer;         /* 0 .. layers-1                                       */
+    int32_t fuse_stats;    /* 1: also produce the dbk_stats record (S4)           */
+    int32_t _reserved;
+    const int64_t *req_ids;/* host [n], batch order                               */
+} dbk_batch;
+
+/* For each request i and q-head h (kv head g = h / (q_heads/kv_heads)):
+ *   out[i][h][:] = sum_{j < ctx_i} softmax_j(q[i][h].K_{i,g,j} / sqrt(d)) V_{i,g,j}
+ * over the request's paged KV of `layer` (R1, R2; oracle O1).  q: device
+ * [n][q_heads][head_dim] kv_dtype; out: device [n][q_heads][head_dim] of
+ * out_dtype (0 fp16, 1 bf16, 2 fp32).  fp32 accumulation.  With fuse_stats
+ * the same launch reduces the batch statistics record (O3).  Async. */
+dbk_status dbk_decode_step(dbk_pool *pool, const dbk_batch *batch, const void *q, void *out,
+                           int32_t out_dtype, void *stream);
+
+/* Batch statistics of the last fused launch (oracle O3).
+ * 16 x int64 = 128 bytes.  step_ns and n_waiting are filled by the host
+ * (engine) -- zero from dbk_batch_stats. */
+typedef struct dbk_stats {
+    int64_t n_active, sum_ctx, sum_ctx_sq, max_ctx, sum_pages, cap_pages, free_pages, over_cap,
+        table_mismatch, n_finished, fin_sum_lin, fin_sum_lin_sq, fin_sum_lout, fin_sum_lout_sq,
+        step_ns, n_waiting;
+} dbk_stats;
+
+/* Copies the device record to host_out; synchronises `stream`. */
+dbk_status dbk_batch_stats(dbk_pool *pool, dbk_stats *host_out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Synthetic input generator (input side only; none of the method's math)  */
+/* ------------------------------------------------------------------------ */
+
+/* out[r][h][e] = value(seed, kind, req[r], pos[r], layer, h, e) * 2^scale_log2,
+ * the generator of synth/hashgen.py, for r < n_rows, h < n_heads, e < d.
+ * req, pos: host arrays [n_rows]; out: device, dtype 0 fp16 / 1 bf16 / 2 fp32. */
+dbk_status dbk_synth_fill(uint64_t seed, int32_t kind, int32_t n_rows, const int64_t *req,
+                          const int32_t *pos, int32_t layer, int32_t n_heads, int32_t d,
+                          int32_t scale_log2, int32_t dtype, void *out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Scheduler: Algorithm 1 (memory), Algorithm 2 (SLA), min, static          */
+/* ------------------------------------------------------------------------ */
+
+enum { DBK_POLICY_STATIC = 0, DBK_POLICY_MEMORY = 1, DBK_POLICY_SLA = 2, DBK_POLICY_COMBINED = 3 };
+enum { DBK_R_STATIC = 0, DBK_R_MEMORY = 1, DBK_R_SLA = 2, DBK_R_MIN = 3, DBK_R_CARRY = 4 };
+
+typedef struct dbk_sched_config {
+    int32_t policy;                 /* DBK_POLICY_*                                       */
+    int32_t b_static;               /* static baseline b                    */
+    int32_t b_min, b_max, b0;       /* B_min, B_max; b_0                    */
+    int32_t alpha, delta;           /* Alg. 2 constants (R15)               */
+    int32_t w_len;                  /* moments window, completed requests (R11)           */
+    int32_t w_sla;                  /* SLA window, decode steps (R14)                     */
+    int32_t refresh_steps;          /* L0 refresh period (R12)                            */
+    int32_t page_size, _reserved;
+    double eps_m;                   /* epsilon_M in (0, 0.5] (Eq. 2; R5)     */
+    double d_sla_ms, eps_d_ms;      /* D_SLA, epsilon_D (Eq. 3)              */
+    int64_t bytes_per_token;        /* beta: KV bytes per token, all layers, this GPU     */
+    int64_t prior_n, prior_sum_lin, prior_sum_lin_sq, prior_sum_lout, prior_sum_lout_sq;
+} dbk_sched_config;
+
+typedef struct dbk_sched dbk_sched;
+
+dbk_status dbk_sched_create(const dbk_sched_config *cfg, dbk_sched **out);
+dbk_status dbk_sched_destroy(dbk_sched *s);
+
+/* Consume the GLOBAL statistics of the decode step just finished (step_ns
+ * filled) and return b_{t+1} (PAPER.md:219 b* = min{b_mem, b_SLA}).
+ * mem_cap_bytes: M_max of the whole job (eta via R4); sla_ms > 0 overrides
+ * cfg.d_sla_ms; n_prefill_waiting = N^p (R13).  rationale_out: DBK_R_*.
+ * Integer-exact (R6); EINFEASIBLE is never returned here (b_quad = 0 gives
+ * L0 = eta and b = N^d). */
+dbk_status dbk_choose_batch_size(dbk_sched *s, const dbk_stats *global, int64_t mem_cap_bytes,
+                                 double sla_ms, int32_t n_prefill_waiting, int32_t *b_out,
+                                 int32_t *rationale_out);
+
+typedef struct dbk_sched_state {
+    int64_t t, eta, L0, b_quad, theta_q;
+    int64_t win_n, win_S, win_V2;   /* window moments: n, S = sum(l_in+l_out), n^2 v */
+    int32_t b, b_mem, b_sla, b_low, b_high, sla_count;
+} dbk_sched_state;
+dbk_status dbk_sched_get_state(dbk_sched *s, dbk_sched_state *out);
+
+/* Pure helpers (host), exposed for tests: theta_q = floor(Theta^-1(1-eps)*2^24 + 1/2)
+ * (Wichura AS241); b_quad = largest b with the R6 predicate true (0 if none). */
+dbk_status dbk_theta_q(double eps_m, int64_t *theta_q_out);
+dbk_status dbk_b_quad(int64_t n, int64_t S, int64_t V2, int64_t eta, int64_t theta_q,
+                      int64_t *b_out);
+
+/* ------------------------------------------------------------------------ */
+/* Engine: one continuous-batching iteration per call (S1 -> S7, R17-R22)    */
+/* ------------------------------------------------------------------------ */
+
+typedef struct dbk_engine_config {
+    int32_t n_requests;
+    int32_t q_scale_log2;           /* synthetic q scale (peaked variant: 4)                */
+    const int64_t *arrival_ns;      /* host [n_requests], non-decreasing (copied)          */
+    const int32_t *l_in;            /* host [n_requests] (copied)                          */
+    const int32_t *l_out;           /* host [n_requests] (copied)                          */
+    const int64_t *req_ids;         /* host [n_requests] global ids, or NULL = 0..n-1      */
+    int64_t mem_cap_bytes;          /* M_max of the WHOLE job (all ranks)                  */
+    double sla_ms;                  /* <= 0: cfg value of the scheduler                    */
+    uint64_t synth_seed;
+    int32_t out_dtype;              /* 0 fp16, 1 bf16, 2 fp32                              */
+    int32_t time_attention;         /* 1: CUDA events around each attention launch         */
+    int32_t rank, world;            /* DP request shards (R21); 0, 1 for one GPU           */
+} dbk_engine_config;
+
+typedef struct dbk_engine dbk_engine;
+
+/* Buffers of one step.  Device-resident mode: host_* all NULL; the engine
+ * generates q (synthetic, pos = ctx-1) into q_dev and appends the decode
+ * token's K/V with the synthetic generator.  End-to-end mode: host_q
+ * [layers][n][q_heads][d], host_k / host_v [n][layers][kv_heads][d] (pinned
+ * host, kv_dtype) are copied H2D into q_dev / kv_dev each step and out is
+ * copied D2H into host_out [layers][n][q_heads][d] (out_dtype).
+ * q_dev: [layers][max_requests][q_heads][d]; out_dev: same shape, out_dtype;
+ * kv_dev: [2][max_requests][layers][kv_heads][d] (e2e only). */
+typedef struct dbk_engine_buffers {
+    void *q_dev, *out_dev, *kv_dev;
+    const void *host_q, *host_k, *host_v;
+    void *host_out;
+} dbk_engine_buffers;
+
+typedef struct dbk_step_record {
+    int64_t t, clock_ns, step_ns, sum_ctx, used_pages, table_hash;
+    int32_t b_t, b_next, n_admitted, n_preempted, n_decode, n_finished, rationale, n_waiting;
+    int64_t h2d_bytes, d2h_bytes;
+    int32_t launches, _reserved;
+} dbk_step_record;
+
+dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_config *cfg,
+                             dbk_engine **out);
+dbk_status dbk_engine_destroy(dbk_engine *e);
+
+/* Run one iteration (single GPU, or with a communicator attached).  Returns
+ * DBK_ENOENT (and does nothing) when every request has finished. */
+dbk_status dbk_engine_step(dbk_engine *e, const dbk_engine_buffers *bufs, void *stream,
+                           dbk_step_record *rec);
+/* Split form for multi-GPU with a caller-side exchange: launch the step and
+ * return this rank's record (stream synchronised) ... */
+dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs, void *stream,
+                                  dbk_stats *local_out);
+/* ... then finish it with the reduced global record (retire, windows, b_{t+1}). */
+dbk_status dbk_engine_step_finish(dbk_engine *e, const dbk_stats *global, dbk_step_record *rec);
+
+dbk_status dbk_engine_done(dbk_engine *e, int32_t *done);
+/* The last step's decode batch: n, then req_ids[n], ctx[n] (host, cap entries). */
+dbk_status dbk_engine_last_batch(dbk_engine *e, int32_t *n, int64_t *req_ids, int32_t *ctx,
+                                 int32_t cap);
+/* Attention timing accumulated with time_attention = 1: total ms of the
+ * attention launches (CUDA events on the launching stream), their count and
+ * the algorithmic bytes they moved. */
+dbk_status dbk_engine_attn_timing(dbk_engine *e, double *ms, int64_t *launches, int64_t *bytes,
+                                  int32_t reset);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU statistics exchange (NCCL over NVLink)        */
+/* ------------------------------------------------------------------------ */
+
+enum { DBK_MODE_DP = 0, DBK_MODE_TP = 1 };
+typedef struct dbk_comm dbk_comm;
+
+/* 128-byte ncclUniqueId, produced on rank 0 and broadcast by the caller. */
+dbk_status dbk_comm_unique_id(void *id_out_128);
+dbk_status dbk_comm_create(int32_t nranks, int32_t rank, const void *id_128, int32_t device,
+                           dbk_comm **out);
+dbk_status dbk_comm_destroy(dbk_comm *c);
+/* ncclAllGather of the 128-byte records, then dbk_stats_reduce. */
+dbk_status dbk_stats_allgather(dbk_comm *c, const dbk_stats *local, dbk_stats *all,
+                               dbk_stats *global, int32_t mode, void *stream);
+/* Host reduction: DP = SUM (max_ctx MAX, over_cap OR); TP = all equal
+ * (EINVAL otherwise); both: step_ns = MAX. */
+dbk_status dbk_stats_reduce(const dbk_stats *all, int32_t nranks, int32_t mode, dbk_stats *global);
+dbk_status dbk_engine_attach_comm(dbk_engine *e, dbk_comm *c, int32_t mode);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBK_H_ */

@@ -1,0 +1,399 @@
+// Engine: one continuous-batching decode iteration per call (SURVEY.md §8(a) S1-S7,
+// DESIGN.md R17-R22).  The decode step's GPU work is timed with CUDA events; the
+// measured latency feeds Algorithm 2 and advances the engine clock.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <new>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+#include "pool.h"
+
+using namespace dbk;
+
+struct dbk_engine {
+    dbk_pool *pool = nullptr;
+    dbk_sched *sched = nullptr;
+    dbk_engine_config cfg{};
+    // full (global) trace; this rank serves indices i with i % world == rank
+    std::vector<int64_t> arrival, ids;
+    std::vector<int32_t> l_in, l_out, gen;
+    std::vector<int32_t> mine;        // local trace indices in arrival order
+    size_t next_local = 0;            // next local index to release
+    size_t next_global = 0;           // first global index with arrival > clock
+    std::deque<int32_t> queue;        // local waiting (trace indices)
+    std::vector<int32_t> running;     // local running, admission order
+    int64_t clock = 0, t = 0;
+    int32_t b = 1;
+    int64_t fin_global = 0;           // cumulative finished (global)
+    bool prev_known = false;
+    int64_t prev_running_g = 0, prev_waiting_g = 0;
+    // step state between launch and finish
+    bool in_step = false;
+    int64_t step_clock0 = 0;
+    int32_t step_b = 0, step_adm = 0, step_pre = 0, step_launches = 0;
+    uint64_t step_hash = 0;
+    int64_t step_h2d = 0, step_d2h = 0;
+    std::vector<int64_t> batch_ids;
+    std::vector<int32_t> batch_ctx;
+    dbk_stats local{};
+    // events
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> att0, att1;
+    double att_ms = 0;
+    int64_t att_launches = 0, att_bytes = 0;
+    std::vector<int64_t> layer_bytes;
+    dbk_comm *comm = nullptr;
+    int32_t comm_mode = DBK_MODE_DP;
+    ~dbk_engine() {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        for (auto e : att0) cudaEventDestroy(e);
+        for (auto e : att1) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+int32_t b_share(int32_t b, int32_t rank, int32_t world) {  // R21
+    return b / world + (rank < b % world ? 1 : 0);
+}
+
+void release_arrivals(dbk_engine *e) {
+    while (e->next_local < e->mine.size() && e->arrival[e->mine[e->next_local]] <= e->clock)
+        e->queue.push_back(e->mine[e->next_local++]);
+    while (e->next_global < e->arrival.size() && e->arrival[e->next_global] <= e->clock) ++e->next_global;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+extern "C" {
+
+dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_config *cfg,
+                             dbk_engine **out) {
+    if (!pool || !sched || !cfg || !out) return fail(DBK_EINVAL, "engine_create: null argument");
+    const dbk_engine_config &c = *cfg;
+    if (c.n_requests < 0 || (c.n_requests > 0 && (!c.arrival_ns || !c.l_in || !c.l_out)))
+        return fail(DBK_EINVAL, "engine_create: trace arrays missing");
+    if (c.world < 1 || c.rank < 0 || c.rank >= c.world) return fail(DBK_EINVAL, "engine_create: bad rank/world");
+    if (c.out_dtype < 0 || c.out_dtype > 2) return fail(DBK_EINVAL, "engine_create: bad out_dtype");
+    for (int i = 0; i < c.n_requests; ++i) {
+        if (c.l_in[i] < 1 || c.l_out[i] < 1) return fail(DBK_EINVAL, "engine_create: lengths must be >= 1");
+        if (i && c.arrival_ns[i] < c.arrival_ns[i - 1]) return fail(DBK_EINVAL, "engine_create: arrivals must be sorted");
+        const int64_t need = ceil_div(static_cast<int64_t>(c.l_in[i]) + c.l_out[i], pool->cfg.page_size);
+        if (need > pool->cfg.cap_pages || need > pool->cfg.max_pages_per_req)
+            return fail(DBK_EFATAL, "engine_create: request %d cannot fit the cap alone", i);
+    }
+    dbk_engine *e = new (std::nothrow) dbk_engine();
+    if (!e) return fail(DBK_EINVAL, "out of host memory");
+    e->pool = pool;
+    e->sched = sched;
+    e->cfg = c;
+    e->arrival.assign(c.arrival_ns, c.arrival_ns + c.n_requests);
+    e->l_in.assign(c.l_in, c.l_in + c.n_requests);
+    e->l_out.assign(c.l_out, c.l_out + c.n_requests);
+    e->gen.assign(c.n_requests, 0);
+    e->ids.resize(c.n_requests);
+    for (int i = 0; i < c.n_requests; ++i) e->ids[i] = c.req_ids ? c.req_ids[i] : i;
+    for (int i = c.rank; i < c.n_requests; i += c.world) e->mine.push_back(i);
+    dbk_sched_state st;
+    dbk_sched_get_state(sched, &st);
+    e->b = st.b;
+    e->cfg.arrival_ns = nullptr;
+    e->cfg.l_in = nullptr;
+    e->cfg.l_out = nullptr;
+    e->cfg.req_ids = nullptr;
+    cudaSetDevice(pool->cfg.device);
+    if (cudaEventCreate(&e->ev0) != cudaSuccess || cudaEventCreate(&e->ev1) != cudaSuccess) {
+        delete e;
+        return fail(DBK_ECUDA, "engine_create: cudaEventCreate failed");
+    }
+    const int L = pool->cfg.layers;
+    e->att0.resize(L);
+    e->att1.resize(L);
+    for (int l = 0; l < L; ++l) {
+        if (cudaEventCreate(&e->att0[l]) != cudaSuccess || cudaEventCreate(&e->att1[l]) != cudaSuccess) {
+            delete e;
+            return fail(DBK_ECUDA, "engine_create: cudaEventCreate failed");
+        }
+    }
+    e->layer_bytes.assign(L, 0);
+    *out = e;
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_destroy(dbk_engine *e) {
+    delete e;
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_done(dbk_engine *e, int32_t *done) {
+    if (!e || !done) return fail(DBK_EINVAL, "engine_done: null argument");
+    *done = e->fin_global >= static_cast<int64_t>(e->arrival.size()) ? 1 : 0;
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_attach_comm(dbk_engine *e, dbk_comm *c, int32_t mode) {
+    if (!e || (mode != DBK_MODE_DP && mode != DBK_MODE_TP)) return fail(DBK_EINVAL, "attach_comm: bad argument");
+    e->comm = c;
+    e->comm_mode = mode;
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs, void *stream,
+                                  dbk_stats *local_out) {
+    if (!e || !bufs || !local_out) return fail(DBK_EINVAL, "engine_step_launch: null argument");
+    if (e->in_step) return fail(DBK_EINVAL, "engine_step_launch: previous step not finished");
+    if (e->fin_global >= static_cast<int64_t>(e->arrival.size())) return fail(DBK_ENOENT, "engine: all requests finished");
+    dbk_pool *p = e->pool;
+    const dbk_pool_config &pc = p->cfg;
+    const bool e2e = bufs->host_q != nullptr;
+    if (!bufs->q_dev || !bufs->out_dev) return fail(DBK_EINVAL, "engine_step_launch: q_dev and out_dev are required");
+    if (e2e && (!bufs->host_k || !bufs->host_v || !bufs->kv_dev))
+        return fail(DBK_EINVAL, "engine_step_launch: end-to-end mode needs host_q, host_k, host_v and kv_dev");
+    DBK_CUDA(cudaSetDevice(pc.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t P = pc.page_size;
+    const int64_t launches0 = p->n_launches;
+
+    // S1: arrivals, idle jump (global, R19)
+    release_arrivals(e);
+    const bool idle_g = e->prev_known ? (e->prev_running_g == 0 && e->prev_waiting_g == 0)
+                                      : (e->next_global == 0);
+    if (idle_g && e->next_global < e->arrival.size()) {
+        e->clock = std::max(e->clock, e->arrival[e->next_global]);
+        release_arrivals(e);
+    }
+    e->step_clock0 = e->clock;
+    e->step_b = e->b;
+    DBK_CUDA(cudaEventRecord(e->ev0, s));
+
+    // S1: FCFS admission with head-of-line blocking (R17); prefill = synthetic fill of T tokens
+    const int32_t share = b_share(e->b, e->cfg.rank, e->cfg.world);
+    std::vector<int64_t> adm_ids;
+    std::vector<int32_t> adm_tok;
+    int64_t free_pages = p->pages.free_count;
+    int32_t adm = 0, pre = 0;
+    while (!e->queue.empty() && static_cast<int32_t>(e->running.size()) < share) {
+        const int32_t r = e->queue.front();
+        const int64_t T = static_cast<int64_t>(e->l_in[r]) + e->gen[r];
+        if (free_pages < ceil_div(T + 1, P)) break;
+        e->queue.pop_front();
+        DBK_TRY(dbk_request_begin(p, e->ids[r], e->l_in[r], e->l_out[r]));
+        free_pages -= ceil_div(T, P);
+        adm_ids.push_back(e->ids[r]);
+        adm_tok.push_back(static_cast<int32_t>(T));
+        e->running.push_back(r);
+        ++adm;
+    }
+    if (!adm_ids.empty())
+        DBK_TRY(dbk_append_tokens(p, static_cast<int32_t>(adm_ids.size()), adm_ids.data(), adm_tok.data(),
+                                  nullptr, nullptr, e->cfg.synth_seed, s));
+
+    // S1/S2: page growth for this step's decode token; LIFO preemption on overflow (R18)
+    for (;;) {
+        int64_t need = 0;
+        for (int32_t r : e->running) {
+            int32_t ctx;
+            dbk_request_info(p, e->ids[r], &ctx, nullptr, nullptr, nullptr, 0);
+            if (ctx % P == 0) ++need;
+        }
+        if (need <= p->pages.free_count) break;
+        const int32_t victim = e->running.back();
+        e->running.pop_back();
+        const int64_t vid = e->ids[victim];
+        DBK_TRY(dbk_release(p, 1, &vid));
+        e->queue.push_front(victim);
+        ++pre;
+    }
+    const int32_t n = static_cast<int32_t>(e->running.size());
+    e->batch_ids.resize(n);
+    e->batch_ctx.resize(n);
+    std::vector<int32_t> ones(n, 1);
+    for (int32_t x = 0; x < n; ++x) e->batch_ids[x] = e->ids[e->running[x]];
+    e->step_h2d = e->step_d2h = 0;
+    const size_t qrow = static_cast<size_t>(pc.q_heads) * pc.head_dim * 2;
+    const size_t kvrow = static_cast<size_t>(pc.layers) * pc.kv_heads * pc.head_dim * 2;
+    const size_t orow = static_cast<size_t>(pc.q_heads) * pc.head_dim * (e->cfg.out_dtype == 2 ? 4 : 2);
+    if (n > 0) {
+        if (e2e) {
+            // end-to-end: this step's new K/V rows and q come from pinned host memory
+            uint8_t *kd = static_cast<uint8_t *>(bufs->kv_dev);
+            uint8_t *vd = kd + static_cast<size_t>(pc.max_requests) * kvrow;
+            DBK_CUDA(cudaMemcpyAsync(kd, bufs->host_k, n * kvrow, cudaMemcpyHostToDevice, s));
+            DBK_CUDA(cudaMemcpyAsync(vd, bufs->host_v, n * kvrow, cudaMemcpyHostToDevice, s));
+            e->step_h2d += 2 * static_cast<int64_t>(n * kvrow);
+            DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), kd, vd, 0, s));
+            for (int l = 0; l < pc.layers; ++l) {
+                uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
+                const uint8_t *qh = static_cast<const uint8_t *>(bufs->host_q) + static_cast<size_t>(l) * n * qrow;
+                DBK_CUDA(cudaMemcpyAsync(qd, qh, n * qrow, cudaMemcpyHostToDevice, s));
+            }
+            e->step_h2d += static_cast<int64_t>(pc.layers) * n * qrow;
+        } else {
+            DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), nullptr, nullptr, e->cfg.synth_seed, s));
+        }
+    }
+    uint64_t h = kFnvOffset;
+    for (int32_t x = 0; x < n; ++x) {
+        const int32_t r = e->running[x];
+        e->gen[r] += 1;
+        const Request &rq = p->reqs.at(e->ids[r]);
+        e->batch_ctx[x] = rq.ctx;
+        h = fnv1a64(h, rq.id);
+        h = fnv1a64(h, rq.ctx);
+        h = fnv1a64(h, static_cast<int64_t>(rq.pages.size()));
+        for (int32_t pg : rq.pages) h = fnv1a64(h, pg);
+    }
+    e->step_hash = h;
+
+    // S3/S4: decode attention for every layer; statistics fused into layer 0
+    dbk_batch bt;
+    bt.n = n;
+    bt.req_ids = e->batch_ids.data();
+    if (n > 0) DBK_TRY(prepare_batch(p, n, e->batch_ids.data(), s));
+    for (int l = 0; l < pc.layers; ++l) {
+        uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
+        uint8_t *od = static_cast<uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;
+        if (n > 0 && !e2e) {
+            DBK_CUDA(launch_synth_q(e->cfg.synth_seed, p->d_req, n, l, pc.q_heads, pc.head_dim,
+                                    e->cfg.q_scale_log2, pc.kv_dtype, qd, s));
+            ++p->n_launches;
+        }
+        bt.layer = l;
+        bt.fuse_stats = l == 0 ? 1 : 0;
+        if (e->cfg.time_attention && n > 0) DBK_CUDA(cudaEventRecord(e->att0[l], s));
+        DBK_TRY(dbk_decode_step(p, &bt, qd, od, e->cfg.out_dtype, s));
+        if (e->cfg.time_attention && n > 0) DBK_CUDA(cudaEventRecord(e->att1[l], s));
+        e->layer_bytes[l] = p->last_decode_bytes;
+    }
+    if (e2e && n > 0 && bufs->host_out) {
+        for (int l = 0; l < pc.layers; ++l) {
+            const uint8_t *od = static_cast<const uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;
+            uint8_t *oh = static_cast<uint8_t *>(bufs->host_out) + static_cast<size_t>(l) * n * orow;
+            DBK_CUDA(cudaMemcpyAsync(oh, od, n * orow, cudaMemcpyDeviceToHost, s));
+        }
+        e->step_d2h += static_cast<int64_t>(pc.layers) * n * orow;
+    }
+    DBK_CUDA(cudaEventRecord(e->ev1, s));
+    // S5: statistics record (synchronises the stream) and device-timed step latency
+    DBK_TRY(dbk_batch_stats(p, &e->local, s));
+    float ms = 0.f;
+    DBK_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    e->local.step_ns = std::llround(static_cast<double>(ms) * 1e6);
+    e->local.n_waiting = static_cast<int64_t>(e->queue.size());
+    if (e->cfg.time_attention && n > 0) {
+        for (int l = 0; l < pc.layers; ++l) {
+            float a = 0.f;
+            DBK_CUDA(cudaEventElapsedTime(&a, e->att0[l], e->att1[l]));
+            e->att_ms += a;
+            e->att_bytes += e->layer_bytes[l];
+            ++e->att_launches;
+        }
+    }
+    e->step_adm = adm;
+    e->step_pre = pre;
+    e->step_launches = static_cast<int32_t>(p->n_launches - launches0);
+    e->in_step = true;
+    *local_out = e->local;
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_step_finish(dbk_engine *e, const dbk_stats *global, dbk_step_record *rec) {
+    if (!e || !global) return fail(DBK_EINVAL, "engine_step_finish: null argument");
+    if (!e->in_step) return fail(DBK_EINVAL, "engine_step_finish: no step in flight");
+    dbk_pool *p = e->pool;
+    // S5': retire finished requests (release their pages)
+    std::vector<int32_t> keep;
+    std::vector<int64_t> done_ids;
+    keep.reserve(e->running.size());
+    for (int32_t r : e->running) {
+        if (e->gen[r] == e->l_out[r]) done_ids.push_back(e->ids[r]);
+        else keep.push_back(r);
+    }
+    if (!done_ids.empty()) DBK_TRY(dbk_release(p, static_cast<int32_t>(done_ids.size()), done_ids.data()));
+    e->running.swap(keep);
+    // S6: clock, arrivals, global N^p / N^d
+    e->clock += global->step_ns;
+    release_arrivals(e);
+    e->fin_global += global->n_finished;
+    const int64_t running_g = global->n_active - global->n_finished;
+    const int64_t waiting_g = static_cast<int64_t>(e->next_global) - running_g - e->fin_global;
+    dbk_stats g = *global;
+    g.n_waiting = waiting_g;
+    // S7: b_{t+1}
+    int32_t b_next = e->b, why = DBK_R_CARRY;
+    DBK_TRY(dbk_choose_batch_size(e->sched, &g, e->cfg.mem_cap_bytes, e->cfg.sla_ms,
+                                  static_cast<int32_t>(waiting_g), &b_next, &why));
+    if (rec) {
+        std::memset(rec, 0, sizeof *rec);
+        rec->t = e->t;
+        rec->clock_ns = e->step_clock0;
+        rec->step_ns = global->step_ns;
+        rec->sum_ctx = global->sum_ctx;
+        rec->used_pages = global->sum_pages;
+        rec->table_hash = static_cast<int64_t>(e->step_hash);
+        rec->b_t = e->step_b;
+        rec->b_next = b_next;
+        rec->n_admitted = e->step_adm;
+        rec->n_preempted = e->step_pre;
+        rec->n_decode = static_cast<int32_t>(global->n_active);
+        rec->n_finished = static_cast<int32_t>(global->n_finished);
+        rec->rationale = why;
+        rec->n_waiting = static_cast<int32_t>(waiting_g);
+        rec->h2d_bytes = e->step_h2d;
+        rec->d2h_bytes = e->step_d2h;
+        rec->launches = e->step_launches;
+    }
+    e->b = b_next;
+    e->prev_known = true;
+    e->prev_running_g = running_g;
+    e->prev_waiting_g = waiting_g;
+    e->t += 1;
+    e->in_step = false;
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_step(dbk_engine *e, const dbk_engine_buffers *bufs, void *stream, dbk_step_record *rec) {
+    if (!e) return fail(DBK_EINVAL, "engine_step: null engine");
+    dbk_stats local;
+    DBK_TRY(dbk_engine_step_launch(e, bufs, stream, &local));
+    dbk_stats global = local;
+    if (e->comm) {
+        std::vector<dbk_stats> all(static_cast<size_t>(e->cfg.world));
+        DBK_TRY(dbk_stats_allgather(e->comm, &local, all.data(), &global, e->comm_mode, stream));
+    } else if (e->cfg.world != 1) {
+        return fail(DBK_EINVAL, "engine_step: world > 1 needs a communicator (or use step_launch/finish)");
+    }
+    return dbk_engine_step_finish(e, &global, rec);
+}
+
+dbk_status dbk_engine_last_batch(dbk_engine *e, int32_t *n, int64_t *ids, int32_t *ctx, int32_t cap) {
+    if (!e || !n) return fail(DBK_EINVAL, "engine_last_batch: null argument");
+    *n = static_cast<int32_t>(e->batch_ids.size());
+    for (int32_t x = 0; x < cap && x < *n; ++x) {
+        if (ids) ids[x] = e->batch_ids[x];
+        if (ctx) ctx[x] = e->batch_ctx[x];
+    }
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_attn_timing(dbk_engine *e, double *ms, int64_t *launches, int64_t *bytes, int32_t reset) {
+    if (!e) return fail(DBK_EINVAL, "engine_attn_timing: null engine");
+    if (ms) *ms = e->att_ms;
+    if (launches) *launches = e->att_launches;
+    if (bytes) *bytes = e->att_bytes;
+    if (reset) {
+        e->att_ms = 0;
+        e->att_launches = 0;
+        e->att_bytes = 0;
+    }
+    return DBK_OK;
+}
+
+}  // extern "C"

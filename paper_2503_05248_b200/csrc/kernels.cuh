@@ -1,0 +1,83 @@
+// Device-side data structures and kernel launchers (internal to libdbk).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dbk {
+
+// Per-request metadata of one decode batch (uploaded once per batch change).
+struct ReqMeta {
+    int64_t req_id;
+    int32_t slot;        // block-table row
+    int32_t ctx;         // tokens in KV incl. this step's token
+    int32_t l_in, l_out; // for the finishing statistics (O3)
+    int32_t chunk_base;  // first work item of this request (split-K workspace row)
+    int32_t nchunks;     // work items of this request
+};
+static_assert(sizeof(ReqMeta) == 32, "ReqMeta layout");
+
+struct DecodeParams {
+    const uint8_t *kv_layer;     // KV base of this layer
+    int64_t page_stride;         // bytes per (layer, page): kv_heads * tile_bytes
+    const int32_t *block_table;  // [max_requests][bt_stride]
+    int32_t bt_stride;
+    int32_t n;                   // requests in the batch
+    const ReqMeta *req;          // [n]
+    const int2 *work;            // [n_items] (batch index, chunk index)
+    int32_t n_items;
+    int32_t chunk_pages;         // pages per work item
+    const void *q;               // [n][q_heads][D]
+    void *out;                   // [n][q_heads][D]
+    int32_t out_dtype;           // 0 fp16, 1 bf16, 2 fp32
+    int32_t q_heads;
+    float scale_log2;            // log2(e) / sqrt(D)
+    float *ws_o;                 // [n_items][q_heads][D] split-K partial numerators
+    float2 *ws_ml;               // [n_items][q_heads] (running max in log2 units, denominator)
+    int32_t *counters;           // [n][kv_heads] arrival counters (zero between launches)
+    // fused batch statistics (S4)
+    int32_t fuse_stats;
+    int32_t max_pages_per_req;
+    unsigned long long *stats;   // 16 x u64, zeroed before the launch
+    int32_t *stats_done;         // zero between launches
+    int64_t cap_pages;
+};
+
+struct AppendJob {
+    int64_t req_id;
+    int32_t pos0;     // position of the first token written by this job
+    int32_t ntok;     // tokens in this job (all in one page)
+    int32_t phys;     // physical page
+    int32_t src_row;  // first source row (explicit K/V), -1 = synthetic
+};
+static_assert(sizeof(AppendJob) == 24, "AppendJob layout");
+
+struct AppendParams {
+    uint8_t *kv;                 // pool base
+    int64_t layer_stride, page_stride, tile_bytes;
+    const AppendJob *jobs;
+    int32_t n_jobs, layers, kv_heads;
+    const void *k_src, *v_src;   // [rows][layers][kv_heads][D] or null (synthetic)
+    uint64_t seed;
+};
+
+struct BtDelta {
+    int32_t slot, idx, val;
+};
+
+// launchers (return cudaGetLastError() of the launch)
+cudaError_t launch_decode(const DecodeParams &p, int kv_dtype, int head_dim, int group,
+                          int kv_heads, cudaStream_t s);
+cudaError_t launch_append(const AppendParams &p, int kv_dtype, int head_dim, cudaStream_t s);
+cudaError_t launch_bt_apply(int32_t *bt, int32_t stride, const BtDelta *d, int32_t n,
+                            cudaStream_t s);
+cudaError_t launch_synth_rows(uint64_t seed, int kind, int n_rows, const int64_t *req,
+                              const int32_t *pos, int layer, int n_heads, int d, int scale_log2,
+                              int dtype, void *out, cudaStream_t s);
+// q[i][h][:] = synth(seed, q, req_i, ctx_i - 1, layer, h) for the batch in `req`.
+cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layer, int q_heads,
+                           int d, int scale_log2, int dtype, void *q, cudaStream_t s);
+int decode_ctas_per_sm(int kv_dtype, int head_dim, int group);
+
+}  // namespace dbk

@@ -1,0 +1,530 @@
+// KV pool: page allocator (host source of truth), request table, device block
+// tables and the decode / append launches.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <new>
+#include <queue>
+#include <unordered_map>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+#include "pool.h"
+
+namespace dbk {
+
+thread_local std::string g_err;
+
+void set_error(const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+dbk_status fail(dbk_status st, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+dbk_status UploadBuffer::reserve(size_t bytes) {
+    if (bytes <= cap) return DBK_OK;
+    if (pending) DBK_CUDA(cudaEventSynchronize(done));
+    pending = false;
+    release();
+    size_t c = 4096;
+    while (c < bytes) c *= 2;
+    DBK_CUDA(cudaMallocHost(&host, c));
+    DBK_CUDA(cudaMalloc(&dev, c));
+    if (!done) DBK_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    cap = c;
+    return DBK_OK;
+}
+
+dbk_status UploadBuffer::upload(const void *src, size_t bytes, cudaStream_t s) {
+    DBK_TRY(reserve(bytes));
+    if (pending) DBK_CUDA(cudaEventSynchronize(done));
+    std::memcpy(host, src, bytes);
+    DBK_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s));
+    DBK_CUDA(cudaEventRecord(done, s));
+    pending = true;
+    return DBK_OK;
+}
+
+void UploadBuffer::release() {
+    if (host) cudaFreeHost(host);
+    if (dev) cudaFree(dev);
+    host = dev = nullptr;
+    cap = 0;
+}
+
+// ---------------------------------------------------------------- allocator (R7)
+void PageBitmap::init(int64_t cap) {
+    words.assign(static_cast<size_t>((cap + 63) / 64), ~0ULL);
+    if (cap % 64) words.back() = (1ULL << (cap % 64)) - 1;
+    free_count = cap;
+    hint = 0;
+}
+int64_t PageBitmap::take_lowest() {
+    for (size_t w = hint; w < words.size(); ++w) {
+        if (words[w]) {
+            const int b = __builtin_ctzll(words[w]);
+            words[w] &= words[w] - 1;
+            hint = w;
+            --free_count;
+            return static_cast<int64_t>(w) * 64 + b;
+        }
+    }
+    return -1;
+}
+void PageBitmap::give_back(int64_t p) {
+    const size_t w = static_cast<size_t>(p / 64);
+    words[w] |= 1ULL << (p % 64);
+    ++free_count;
+    if (w < hint) hint = w;
+}
+
+}  // namespace dbk
+
+using namespace dbk;
+
+static bool pool_cfg_ok(const dbk_pool_config *c) {
+    if (!c) return false;
+    if (c->layers < 1 || c->q_heads < 1 || c->kv_heads < 1 || c->q_heads % c->kv_heads) return false;
+    const int g = c->q_heads / c->kv_heads;
+    if (g != 1 && g != 2 && g != 4 && g != 8) return false;
+    if (c->head_dim != 64 && c->head_dim != 128) return false;
+    if (c->page_size != 16 || (c->kv_dtype != 0 && c->kv_dtype != 1)) return false;
+    if (c->cap_pages < 1 || c->cap_pages > (1LL << 31) - 1 || c->max_requests < 1 ||
+        c->max_pages_per_req < 1)
+        return false;
+    return true;
+}
+
+extern "C" {
+
+const char *dbk_last_error(void) { return dbk::g_err.c_str(); }
+const char *dbk_version(void) { return "dbk 0.1 (sm_100a)"; }
+
+size_t dbk_kv_pool_bytes(const dbk_pool_config *c) {
+    if (!pool_cfg_ok(c)) return 0;
+    return static_cast<size_t>(c->layers) * static_cast<size_t>(c->cap_pages) * c->kv_heads * 2 *
+           c->page_size * c->head_dim * 2;
+}
+
+dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t kv_bytes, dbk_pool **out) {
+    if (!out) return fail(DBK_EINVAL, "pool_create: null output");
+    if (!pool_cfg_ok(cfg))
+        return fail(DBK_EINVAL, "pool_create: invalid config (heads, head_dim in {64,128}, page_size 16, dtype)");
+    const size_t need = dbk_kv_pool_bytes(cfg);
+    if (!kv_mem || kv_bytes < need || (reinterpret_cast<uintptr_t>(kv_mem) & 255))
+        return fail(DBK_EINVAL, "pool_create: kv_mem must be 256-B aligned and >= %zu bytes", need);
+    DBK_CUDA(cudaSetDevice(cfg->device));
+    dbk_pool *p = new (std::nothrow) dbk_pool();
+    if (!p) return fail(DBK_EINVAL, "out of host memory");
+    p->cfg = *cfg;
+    p->kv = static_cast<uint8_t *>(kv_mem);
+    p->kv_bytes = kv_bytes;
+    p->elt = 2;
+    p->tile_bytes = 2LL * cfg->page_size * cfg->head_dim * p->elt;
+    p->page_stride = p->tile_bytes * cfg->kv_heads;
+    p->layer_stride = p->page_stride * cfg->cap_pages;
+    p->pages.init(cfg->cap_pages);
+    for (int s = 0; s < cfg->max_requests; ++s) p->free_slots.push(s);
+    const size_t bt_n = static_cast<size_t>(cfg->max_requests) * cfg->max_pages_per_req;
+    auto cleanup = [&](dbk_status st) {
+        dbk_kv_pool_destroy(p);
+        return st;
+    };
+    if (cudaMalloc(&p->d_bt, bt_n * sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(p->d_bt, 0xFF, bt_n * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&p->d_counters, static_cast<size_t>(cfg->max_requests) * cfg->kv_heads * sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(p->d_counters, 0, static_cast<size_t>(cfg->max_requests) * cfg->kv_heads * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&p->d_stats, 128 + 64) != cudaSuccess ||
+        cudaMemset(p->d_stats, 0, 128 + 64) != cudaSuccess ||
+        cudaMallocHost(&p->h_stats, sizeof(dbk_stats)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+        return cleanup(fail(DBK_ECUDA, "pool_create: %s", cudaGetErrorString(cudaGetLastError())));
+    p->d_stats_done = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(p->d_stats) + 128);
+    p->host_bt.assign(bt_n, -1);
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    p->num_sms = dev_sms;
+    p->ctas_per_sm = decode_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, cfg->q_heads / cfg->kv_heads);
+    if (const char *e = std::getenv("DBK_CHUNK_PAGES")) {  // tuning override (multiple of 4, <= 64)
+        const long long v = std::atoll(e);
+        if (v >= 4 && v <= 64 && v % 4 == 0) p->force_chunk_pages = v;
+    }
+    *out = p;
+    return DBK_OK;
+}
+
+dbk_status dbk_kv_pool_destroy(dbk_pool *p) {
+    if (!p) return DBK_OK;
+    cudaSetDevice(p->cfg.device);
+    cudaDeviceSynchronize();
+    if (p->d_bt) cudaFree(p->d_bt);
+    if (p->d_counters) cudaFree(p->d_counters);
+    if (p->d_stats) cudaFree(p->d_stats);
+    if (p->h_stats) cudaFreeHost(p->h_stats);
+    if (p->d_ws_o) cudaFree(p->d_ws_o);
+    if (p->d_ws_ml) cudaFree(p->d_ws_ml);
+    p->up_delta.release();
+    p->up_append.release();
+    p->up_meta.release();
+    p->up_rows.release();
+    if (p->up_delta.done) cudaEventDestroy(p->up_delta.done);
+    if (p->up_append.done) cudaEventDestroy(p->up_append.done);
+    if (p->up_meta.done) cudaEventDestroy(p->up_meta.done);
+    if (p->up_rows.done) cudaEventDestroy(p->up_rows.done);
+    delete p;
+    return DBK_OK;
+}
+
+dbk_status dbk_request_begin(dbk_pool *p, int64_t id, int32_t l_in, int32_t l_out) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if (id < 0 || l_in < 1 || l_out < 1) return fail(DBK_EINVAL, "request_begin: need id >= 0, l_in >= 1, l_out >= 1");
+    if (p->reqs.count(id)) return fail(DBK_EINVAL, "request %lld already active", static_cast<long long>(id));
+    const int64_t P = p->cfg.page_size;
+    const int64_t need = (static_cast<int64_t>(l_in) + l_out + P - 1) / P;
+    if (need > p->cfg.cap_pages || need > p->cfg.max_pages_per_req)
+        return fail(DBK_EFATAL, "request %lld needs %lld pages alone (cap %lld, row %d)", static_cast<long long>(id),
+                    static_cast<long long>(need), static_cast<long long>(p->cfg.cap_pages), p->cfg.max_pages_per_req);
+    if (p->free_slots.empty()) return fail(DBK_EINVAL, "no free request slot (max_requests = %d)", p->cfg.max_requests);
+    Request r;
+    r.id = id;
+    r.l_in = l_in;
+    r.l_out = l_out;
+    r.ctx = 0;
+    r.slot = p->free_slots.top();
+    p->free_slots.pop();
+    p->reqs.emplace(id, std::move(r));
+    ++p->epoch;
+    return DBK_OK;
+}
+
+}  // extern "C"
+
+namespace dbk {
+dbk_status flush_deltas(dbk_pool *p, cudaStream_t s) {
+    if (p->pending.empty()) return DBK_OK;
+    DBK_TRY(p->up_delta.upload(p->pending.data(), p->pending.size() * sizeof(BtDelta), s));
+    DBK_CUDA(launch_bt_apply(p->d_bt, p->cfg.max_pages_per_req, static_cast<const BtDelta *>(p->up_delta.dev),
+                             static_cast<int32_t>(p->pending.size()), s));
+    ++p->n_launches;
+    p->pending.clear();
+    return DBK_OK;
+}
+}  // namespace dbk
+
+extern "C" {
+
+dbk_status dbk_append_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok,
+                             const void *k, const void *v, uint64_t seed, void *stream) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if (n < 0 || (n > 0 && (!ids || !n_tok))) return fail(DBK_EINVAL, "append_tokens: bad arrays");
+    if ((k == nullptr) != (v == nullptr)) return fail(DBK_EINVAL, "append_tokens: k and v must both be given or both NULL");
+    const int64_t P = p->cfg.page_size;
+    // validate and count pages first: all-or-nothing (R8)
+    std::vector<Request *> rs(n);
+    int64_t need = 0;
+    for (int i = 0; i < n; ++i) {
+        auto it = p->reqs.find(ids[i]);
+        if (it == p->reqs.end()) return fail(DBK_ENOENT, "append_tokens: unknown request %lld", static_cast<long long>(ids[i]));
+        Request &r = it->second;
+        if (n_tok[i] < 0) return fail(DBK_EINVAL, "append_tokens: negative token count");
+        const int64_t nc = static_cast<int64_t>(r.ctx) + n_tok[i];
+        const int64_t np = (nc + P - 1) / P;
+        if (np > p->cfg.max_pages_per_req) return fail(DBK_EINVAL, "append_tokens: request %lld exceeds max_pages_per_req", static_cast<long long>(ids[i]));
+        need += np - static_cast<int64_t>(r.pages.size());
+        rs[i] = &r;
+    }
+    {
+        std::vector<int64_t> sorted(ids, ids + n);
+        std::sort(sorted.begin(), sorted.end());
+        if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+            return fail(DBK_EINVAL, "append_tokens: duplicate request id in one call");
+    }
+    if (need > p->pages.free_count)
+        return fail(DBK_ECAP, "append_tokens: needs %lld pages, %lld free", static_cast<long long>(need),
+                    static_cast<long long>(p->pages.free_count));
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    p->jobs.clear();
+    int32_t src_row = 0;
+    for (int i = 0; i < n; ++i) {
+        Request &r = *rs[i];
+        const int32_t c0 = r.ctx, c1 = r.ctx + n_tok[i];
+        while (static_cast<int64_t>(r.pages.size()) * P < c1) {
+            const int64_t pg = p->pages.take_lowest();
+            const int32_t idx = static_cast<int32_t>(r.pages.size());
+            r.pages.push_back(static_cast<int32_t>(pg));
+            p->host_bt[static_cast<size_t>(r.slot) * p->cfg.max_pages_per_req + idx] = static_cast<int32_t>(pg);
+            p->pending.push_back({r.slot, idx, static_cast<int32_t>(pg)});
+        }
+        for (int32_t pos = c0; pos < c1;) {
+            const int32_t in_page = static_cast<int32_t>(P - pos % P);
+            const int32_t cnt = std::min(in_page, c1 - pos);
+            AppendJob j;
+            j.req_id = r.id;
+            j.pos0 = pos;
+            j.ntok = cnt;
+            j.phys = r.pages[pos / P];
+            j.src_row = k ? src_row + (pos - c0) : -1;
+            p->jobs.push_back(j);
+            pos += cnt;
+        }
+        src_row += n_tok[i];
+        r.ctx = c1;
+    }
+    ++p->epoch;
+    DBK_TRY(flush_deltas(p, s));
+    if (!p->jobs.empty()) {
+        DBK_TRY(p->up_append.upload(p->jobs.data(), p->jobs.size() * sizeof(AppendJob), s));
+        AppendParams ap;
+        ap.kv = p->kv;
+        ap.layer_stride = p->layer_stride;
+        ap.page_stride = p->page_stride;
+        ap.tile_bytes = p->tile_bytes;
+        ap.jobs = static_cast<const AppendJob *>(p->up_append.dev);
+        ap.n_jobs = static_cast<int32_t>(p->jobs.size());
+        ap.layers = p->cfg.layers;
+        ap.kv_heads = p->cfg.kv_heads;
+        ap.k_src = k;
+        ap.v_src = v;
+        ap.seed = seed;
+        DBK_CUDA(launch_append(ap, p->cfg.kv_dtype, p->cfg.head_dim, s));
+        ++p->n_launches;
+    }
+    return DBK_OK;
+}
+
+dbk_status dbk_release(dbk_pool *p, int32_t n, const int64_t *ids) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "release: bad arrays");
+    for (int i = 0; i < n; ++i) {
+        auto it = p->reqs.find(ids[i]);
+        if (it == p->reqs.end()) return fail(DBK_ENOENT, "release: unknown request %lld", static_cast<long long>(ids[i]));
+        Request &r = it->second;
+        for (size_t x = 0; x < r.pages.size(); ++x) {
+            p->pages.give_back(r.pages[x]);
+            p->host_bt[static_cast<size_t>(r.slot) * p->cfg.max_pages_per_req + x] = -1;
+            p->pending.push_back({r.slot, static_cast<int32_t>(x), -1});
+        }
+        p->free_slots.push(r.slot);
+        p->reqs.erase(it);
+    }
+    ++p->epoch;
+    return DBK_OK;
+}
+
+dbk_status dbk_request_info(dbk_pool *p, int64_t id, int32_t *ctx, int32_t *n_pages, int32_t *slot,
+                            int32_t *pages_out, int32_t pages_cap) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    auto it = p->reqs.find(id);
+    if (it == p->reqs.end()) return fail(DBK_ENOENT, "request_info: unknown request %lld", static_cast<long long>(id));
+    const Request &r = it->second;
+    if (ctx) *ctx = r.ctx;
+    if (n_pages) *n_pages = static_cast<int32_t>(r.pages.size());
+    if (slot) *slot = r.slot;
+    if (pages_out)
+        for (int32_t x = 0; x < pages_cap && x < static_cast<int32_t>(r.pages.size()); ++x) pages_out[x] = r.pages[x];
+    return DBK_OK;
+}
+
+dbk_status dbk_pool_usage(dbk_pool *p, int64_t *used, int64_t *free_pages) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if (used) *used = p->cfg.cap_pages - p->pages.free_count;
+    if (free_pages) *free_pages = p->pages.free_count;
+    return DBK_OK;
+}
+
+dbk_status dbk_block_table_d2h(dbk_pool *p, int32_t *host_out, void *stream) {
+    if (!p || !host_out) return fail(DBK_EINVAL, "block_table_d2h: null argument");
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DBK_TRY(flush_deltas(p, s));
+    const size_t bytes = static_cast<size_t>(p->cfg.max_requests) * p->cfg.max_pages_per_req * sizeof(int32_t);
+    DBK_CUDA(cudaMemcpyAsync(host_out, p->d_bt, bytes, cudaMemcpyDeviceToHost, s));
+    DBK_CUDA(cudaStreamSynchronize(s));
+    return DBK_OK;
+}
+
+}  // extern "C"
+
+namespace dbk {
+
+// Build (or reuse) the device metadata of a decode batch: per-request ReqMeta and
+// the split-K work list.  Reused while the batch and the pool state are unchanged
+// (the L per-layer launches of one step upload once).
+dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_t s) {
+    if (p->meta_valid && p->meta_epoch == p->epoch && p->meta_ids.size() == static_cast<size_t>(n) &&
+        std::equal(p->meta_ids.begin(), p->meta_ids.end(), ids))
+        return DBK_OK;
+    const int64_t P = p->cfg.page_size;
+    p->meta_req.resize(n);
+    int64_t total_pages = 0;
+    for (int i = 0; i < n; ++i) {
+        auto it = p->reqs.find(ids[i]);
+        if (it == p->reqs.end()) return fail(DBK_ENOENT, "decode_step: unknown request %lld", static_cast<long long>(ids[i]));
+        const Request &r = it->second;
+        if (r.ctx < 1) return fail(DBK_EINVAL, "decode_step: request %lld holds no tokens", static_cast<long long>(ids[i]));
+        ReqMeta &m = p->meta_req[i];
+        m.req_id = r.id;
+        m.slot = r.slot;
+        m.ctx = r.ctx;
+        m.l_in = r.l_in;
+        m.l_out = r.l_out;
+        total_pages += (r.ctx + P - 1) / P;
+    }
+    // chunk size: aim for >= 4 waves of CTAs over the chip, chunks of 4..64 pages (multiple of 4 warps)
+    const int64_t target = static_cast<int64_t>(p->num_sms) * p->ctas_per_sm * 4;
+    int64_t cp = (total_pages * p->cfg.kv_heads + target - 1) / target;
+    cp = (cp + 3) / 4 * 4;
+    cp = std::max<int64_t>(4, std::min<int64_t>(p->max_chunk_pages, cp));
+    if (p->force_chunk_pages > 0) cp = p->force_chunk_pages;
+    p->meta_work.clear();
+    int32_t base = 0;
+    for (int i = 0; i < n; ++i) {
+        ReqMeta &m = p->meta_req[i];
+        const int32_t pages = static_cast<int32_t>((m.ctx + P - 1) / P);
+        const int32_t nc = static_cast<int32_t>((pages + cp - 1) / cp);
+        m.chunk_base = base;
+        m.nchunks = nc;
+        for (int32_t c = 0; c < nc; ++c) p->meta_work.push_back(make_int2(i, c));
+        base += nc;
+    }
+    p->meta_items = base;
+    p->meta_chunk_pages = static_cast<int32_t>(cp);
+    const size_t rb = sizeof(ReqMeta) * static_cast<size_t>(n);
+    const size_t wb = sizeof(int2) * p->meta_work.size();
+    p->meta_blob.resize(rb + wb);
+    if (rb) std::memcpy(p->meta_blob.data(), p->meta_req.data(), rb);
+    if (wb) std::memcpy(p->meta_blob.data() + rb, p->meta_work.data(), wb);
+    DBK_TRY(p->up_meta.upload(p->meta_blob.data(), p->meta_blob.size(), s));
+    p->d_req = static_cast<const ReqMeta *>(p->up_meta.dev);
+    p->d_work = reinterpret_cast<const int2 *>(static_cast<const uint8_t *>(p->up_meta.dev) + rb);
+    // split-K workspace
+    const size_t need = static_cast<size_t>(base) * p->cfg.q_heads;
+    if (need > p->ws_cap) {
+        size_t c = std::max<size_t>(need, p->ws_cap * 2);
+        DBK_CUDA(cudaStreamSynchronize(s));
+        if (p->d_ws_o) cudaFree(p->d_ws_o);
+        if (p->d_ws_ml) cudaFree(p->d_ws_ml);
+        p->d_ws_o = nullptr;
+        p->d_ws_ml = nullptr;
+        p->ws_cap = 0;
+        DBK_CUDA(cudaMalloc(&p->d_ws_o, c * p->cfg.head_dim * sizeof(float)));
+        DBK_CUDA(cudaMalloc(&p->d_ws_ml, c * sizeof(float2)));
+        p->ws_cap = c;
+    }
+    p->meta_ids.assign(ids, ids + n);
+    p->meta_epoch = p->epoch;
+    p->meta_valid = true;
+    return DBK_OK;
+}
+
+int64_t decode_bytes(const dbk_pool *p, int out_dtype) {
+    // algorithmic bytes of one decode launch
+    const int64_t P = p->cfg.page_size, d = p->cfg.head_dim;
+    int64_t ctx_sum = 0, pages = 0;
+    for (const ReqMeta &m : p->meta_req) {
+        ctx_sum += m.ctx;
+        pages += (m.ctx + P - 1) / P;
+    }
+    const int64_t n = static_cast<int64_t>(p->meta_req.size());
+    const int64_t eo = out_dtype == 2 ? 4 : 2;
+    return ctx_sum * 2 * p->cfg.kv_heads * d * 2 + n * p->cfg.q_heads * d * 2 + n * p->cfg.q_heads * d * eo + pages * 4;
+}
+
+}  // namespace dbk
+
+extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const void *q, void *out,
+                                      int32_t out_dtype, void *stream) {
+    if (!p || !b) return fail(DBK_EINVAL, "decode_step: null argument");
+    if (b->n < 0 || (b->n > 0 && (!b->req_ids || !q || !out))) return fail(DBK_EINVAL, "decode_step: bad arrays");
+    if (b->layer < 0 || b->layer >= p->cfg.layers) return fail(DBK_EINVAL, "decode_step: layer out of range");
+    if (out_dtype < 0 || out_dtype > 2) return fail(DBK_EINVAL, "decode_step: out_dtype must be 0, 1 or 2");
+    if (b->n > p->cfg.max_requests) return fail(DBK_EINVAL, "decode_step: n > max_requests");
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
+        return fail(DBK_EINVAL, "decode_step: q and out must be 16-byte aligned");
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DBK_TRY(flush_deltas(p, s));
+    if (b->fuse_stats) DBK_CUDA(cudaMemsetAsync(p->d_stats, 0, 128, s));
+    if (b->n == 0) return DBK_OK;
+    DBK_TRY(prepare_batch(p, b->n, b->req_ids, s));
+    DecodeParams dp;
+    dp.kv_layer = p->kv + static_cast<size_t>(b->layer) * p->layer_stride;
+    dp.page_stride = p->page_stride;
+    dp.block_table = p->d_bt;
+    dp.bt_stride = p->cfg.max_pages_per_req;
+    dp.n = b->n;
+    dp.req = p->d_req;
+    dp.work = p->d_work;
+    dp.n_items = p->meta_items;
+    dp.chunk_pages = p->meta_chunk_pages;
+    dp.q = q;
+    dp.out = out;
+    dp.out_dtype = out_dtype;
+    dp.q_heads = p->cfg.q_heads;
+    dp.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(p->cfg.head_dim)));
+    dp.ws_o = p->d_ws_o;
+    dp.ws_ml = p->d_ws_ml;
+    dp.counters = p->d_counters;
+    dp.fuse_stats = b->fuse_stats ? 1 : 0;
+    dp.max_pages_per_req = p->cfg.max_pages_per_req;
+    dp.stats = reinterpret_cast<unsigned long long *>(p->d_stats);
+    dp.stats_done = p->d_stats_done;
+    dp.cap_pages = p->cfg.cap_pages;
+    DBK_CUDA(launch_decode(dp, p->cfg.kv_dtype, p->cfg.head_dim, p->cfg.q_heads / p->cfg.kv_heads,
+                           p->cfg.kv_heads, s));
+    ++p->n_launches;
+    p->last_decode_bytes = decode_bytes(p, out_dtype);
+    return DBK_OK;
+}
+
+extern "C" dbk_status dbk_batch_stats(dbk_pool *p, dbk_stats *host_out, void *stream) {
+    if (!p || !host_out) return fail(DBK_EINVAL, "batch_stats: null argument");
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DBK_CUDA(cudaMemcpyAsync(p->h_stats, p->d_stats, sizeof(dbk_stats), cudaMemcpyDeviceToHost, s));
+    DBK_CUDA(cudaStreamSynchronize(s));
+    *host_out = *p->h_stats;
+    host_out->step_ns = 0;
+    host_out->n_waiting = 0;
+    return DBK_OK;
+}
+
+extern "C" dbk_status dbk_synth_fill(uint64_t seed, int32_t kind, int32_t n_rows, const int64_t *req,
+                                     const int32_t *pos, int32_t layer, int32_t n_heads, int32_t d,
+                                     int32_t scale_log2, int32_t dtype, void *out, void *stream) {
+    if (n_rows < 0 || (n_rows > 0 && (!req || !pos || !out)) || d % 8 || d < 8 || n_heads < 1 ||
+        kind < 0 || kind > 2 || dtype < 0 || dtype > 2 || layer < 0)
+        return fail(DBK_EINVAL, "synth_fill: bad arguments");
+    if (n_rows == 0) return DBK_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<uint8_t> blob(static_cast<size_t>(n_rows) * 12);
+    std::memcpy(blob.data(), req, static_cast<size_t>(n_rows) * 8);
+    std::memcpy(blob.data() + static_cast<size_t>(n_rows) * 8, pos, static_cast<size_t>(n_rows) * 4);
+    int64_t *d_req = nullptr;
+    DBK_CUDA(cudaMalloc(&d_req, blob.size()));
+    cudaError_t e = cudaMemcpyAsync(d_req, blob.data(), blob.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = launch_synth_rows(seed, kind, n_rows, d_req, reinterpret_cast<const int32_t *>(d_req + n_rows), layer,
+                              n_heads, d, scale_log2, dtype, out, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(d_req);
+    if (e != cudaSuccess) return fail(DBK_ECUDA, "synth_fill: %s", cudaGetErrorString(e));
+    return DBK_OK;
+}

@@ -1,0 +1,72 @@
+// Internal definition of dbk_pool (host bookkeeping + device metadata).
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <queue>
+#include <unordered_map>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+
+namespace dbk {
+
+// Free-page bitmap; take_lowest() returns the lowest-numbered free page (R7).
+struct PageBitmap {
+    std::vector<uint64_t> words;  // bit = 1: free
+    int64_t free_count = 0;
+    size_t hint = 0;              // no free page below word `hint`
+    void init(int64_t cap);
+    int64_t take_lowest();
+    void give_back(int64_t page);
+};
+
+struct Request {
+    int64_t id = 0;
+    int32_t l_in = 0, l_out = 0, ctx = 0, slot = -1;
+    std::vector<int32_t> pages;   // logical page -> physical page
+};
+
+dbk_status flush_deltas(dbk_pool *p, cudaStream_t s);
+dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_t s);
+
+}  // namespace dbk
+
+struct dbk_pool {
+    dbk_pool_config cfg{};
+    uint8_t *kv = nullptr;
+    size_t kv_bytes = 0;
+    int64_t elt = 2, tile_bytes = 0, page_stride = 0, layer_stride = 0;
+    dbk::PageBitmap pages;
+    std::unordered_map<int64_t, dbk::Request> reqs;
+    std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_slots;
+    std::vector<int32_t> host_bt;             // mirror of the device table
+    int32_t *d_bt = nullptr;
+    std::vector<dbk::BtDelta> pending;        // device-table updates not yet applied
+    std::vector<dbk::AppendJob> jobs;
+    dbk::UploadBuffer up_delta, up_append, up_meta, up_rows;
+    uint64_t epoch = 1;                       // bumped by every mutation
+    // cached decode-batch metadata
+    bool meta_valid = false;
+    uint64_t meta_epoch = 0;
+    std::vector<int64_t> meta_ids;
+    std::vector<dbk::ReqMeta> meta_req;
+    std::vector<int2> meta_work;
+    std::vector<uint8_t> meta_blob;
+    int32_t meta_items = 0, meta_chunk_pages = 0;
+    const dbk::ReqMeta *d_req = nullptr;
+    const int2 *d_work = nullptr;
+    // split-K workspace, arrival counters, statistics record
+    float *d_ws_o = nullptr;
+    float2 *d_ws_ml = nullptr;
+    size_t ws_cap = 0;
+    int32_t *d_counters = nullptr;
+    int64_t *d_stats = nullptr;
+    int32_t *d_stats_done = nullptr;
+    dbk_stats *h_stats = nullptr;
+    int num_sms = 148, ctas_per_sm = 1;
+    int64_t max_chunk_pages = 64, force_chunk_pages = 0;
+    int64_t last_decode_bytes = 0;
+    int64_t n_launches = 0;                   // kernels launched by this pool (gpu_launches)
+};

@@ -1,0 +1,120 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/dbk.h
+declares, and its host-only logic (scheduler, chance constraint, stats
+reduction) matches the oracle decision for decision.  No compute calls."""
+import os
+import random
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="session")
+def dbk():
+    from conftest import build_lib
+    build_lib()
+    import paper_2503_05248_b200 as m
+    return m
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "dbk.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dbk_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(dbk):
+    names = _declared_functions()
+    assert len(names) >= 30
+    out = subprocess.run(["nm", "-D", "--defined-only", dbk._lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (dbk_[a-z0-9_]+)$", out, flags=re.M))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    for n in names:
+        assert hasattr(dbk._lib.lib(), n)
+        assert n in dbk._lib.SIGNATURES, f"binding lacks {n}"
+    assert dbk._lib.lib().dbk_version().startswith(b"dbk")
+
+
+def test_sass_is_sm100a(dbk):
+    out = subprocess.run(["cuobjdump", "--list-elf", dbk._lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", dbk._lib.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert "UBLKCP" in sass  # 1-D TMA bulk copies in the decode kernel
+
+
+def test_error_paths_without_gpu(dbk):
+    with pytest.raises(dbk.DbkError) as e:
+        dbk.Scheduler(policy=1, b_min=5, b_max=2)
+    assert e.value.status == dbk._lib.DBK_EINVAL
+    with pytest.raises(dbk.DbkError):
+        dbk.theta_q(0.7)       # reading R5
+    cfg = dbk.dbk_pool_config(1, 8, 8, 96, 16, 0, 16, 4, 4, 0, 0)  # head_dim 96 unsupported
+    import ctypes as C
+    assert dbk._lib.dbk_kv_pool_bytes(C.byref(cfg)) == 0
+
+
+def test_theta_and_b_quad_match_oracle(dbk):
+    from oracle import chance
+    for eps in (0.001, 0.01, 0.02, 0.05, 0.1, 0.25, 0.5):
+        assert dbk.theta_q(eps) == chance.theta_q(eps)
+    rng = random.Random(2)
+    for _ in range(3000):
+        n = rng.randint(1, 600)
+        S = rng.randint(2 * n, 4000 * n)
+        V2 = rng.randint(0, S * S // 3)
+        eta = rng.randint(1, 4_000_000)
+        tq = chance.theta_q(rng.choice([0.01, 0.02, 0.05, 0.3, 0.5]))
+        assert dbk.b_quad(n, S, V2, eta, tq) == chance.b_quad(n, S, V2, eta, tq)
+
+
+def test_stats_reduce_matches_oracle(dbk):
+    from oracle import stats as ostats
+    a = ostats.batch_stats([5, 9], [2, 3], [3, 6], [[0], [1]], 16, 10)
+    b = ostats.batch_stats([40, 3], [1, 1], [39, 2], [[2, 3, 4], [5]], 16, 10)
+    a["step_ns"], b["step_ns"] = 7, 9
+    a["n_waiting"], b["n_waiting"] = 1, 2
+    assert dbk.stats_reduce([a, b], 0) == ostats.reduce_records([a, b], "dp")
+    assert dbk.stats_reduce([a, dict(a)], 1) == ostats.reduce_records([a, dict(a)], "tp")
+    with pytest.raises(dbk.DbkError):
+        dbk.stats_reduce([a, b], 1)
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+def test_scheduler_matches_oracle_decision_for_decision(dbk, policy):
+    from oracle import policy as opol
+    from oracle import stats as ostats
+    rng = random.Random(100 + policy)
+    prior = (32, 32 * 191, 32 * 2 * 191**2, 32 * 382, 32 * 2 * 382**2)
+    kw = dict(policy=policy, b_static=128, b_min=2, b_max=400, b0=3, alpha=8, delta=2, w_len=64,
+              w_sla=7, refresh_steps=13, page_size=16, eps_m=0.02, d_sla_ms=20.0, eps_d_ms=0.5,
+              bytes_per_token=524288)
+    cs = dbk.Scheduler(prior=prior, **kw)
+    os_ = opol.Scheduler(opol.SchedConfig(prior=prior, **kw))
+    mem_cap = 150 * 10**9
+    for step in range(4000):
+        na = rng.randint(0, 450)
+        nf = rng.randint(0, min(na, 6))
+        lins = [rng.randint(1, 900) for _ in range(nf)]
+        louts = [rng.randint(1, 2000) for _ in range(nf)]
+        st = dict.fromkeys(ostats.FIELDS, 0)
+        st.update(n_active=na, n_finished=nf, step_ns=rng.randint(1, 40_000_000),
+                  fin_sum_lin=sum(lins), fin_sum_lin_sq=sum(x * x for x in lins),
+                  fin_sum_lout=sum(louts), fin_sum_lout_sq=sum(x * x for x in louts))
+        npw = rng.choice([0, 0, 1, 5, 300])
+        if step % 500 == 499:
+            mem_cap = rng.randint(10**9, 170 * 10**9)
+        got = cs.choose(st, mem_cap, 0.0, npw)
+        exp = os_.decide(st, mem_cap, npw)
+        assert got == exp, (step, got, exp)
+        s = cs.state()
+        assert (s["b_mem"], s["b_sla"], s["L0"], s["b_quad"]) == (os_.b_mem, os_.b_sla, os_.L0, os_.bq)
+        if policy in (2, 3):
+            assert (s["b_low"], s["b_high"]) == (os_.sla.low, os_.sla.high)
+        if policy in (1, 3):
+            assert (s["win_n"], s["win_S"], s["win_V2"]) == os_.moments()

@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle, element by element.
+
+Bars (R23): block tables, KV-token counts, statistics and
+every scheduling decision bit-exact; attention rows within 2e-3 relative (fp32
+out).  The oracle's inputs come only from synth/ and oracle/ -- never from the GPU."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import attention as oatt  # noqa: E402
+from oracle import engine as oeng  # noqa: E402
+from oracle import policy as opol  # noqa: E402
+from oracle import stats as ostats  # noqa: E402
+from oracle.allocator import PagedKV  # noqa: E402
+from synth import configs, hashgen, trace  # noqa: E402
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def dbk():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from conftest import build_lib
+    build_lib()
+    import paper_2503_05248_b200 as m
+    return m
+
+
+def row_err(got, want):
+    return (np.abs(got - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)).max()
+
+
+def dt_name(kv_dtype):
+    return "f16" if kv_dtype == 0 else "bf16"
+
+
+def torch_from_bits(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).cuda()
+
+
+def run_decode_case(dbk, L, Hq, Hkv, d, dtype, ctx_list, seed=7, explicit_kv=False, cap=None,
+                    layer=None, q_scale_log2=0, chunk_pages=None, out_dtype=2, monkeypatch=None):
+    P = 16
+    n = len(ctx_list)
+    ctx = np.asarray(ctx_list, np.int32)
+    l_in = np.maximum(1, ctx - 3)
+    l_out = ctx - l_in + np.arange(n) % 2          # odd entries are not finishing
+    max_pages = int(max(-(-(ctx + 1) // P))) + 1
+    cap = cap or int(sum(-(-ctx // P))) + 7
+    pool = dbk.KVPool(L, Hq, Hkv, d, cap, n + 3, max_pages, dtype)
+    ref = PagedKV(cap, P)
+    ids = np.arange(n, dtype=np.int64) * 7919 + 11
+    for r, a, b in zip(ids, l_in, l_out):
+        pool.request_begin(r, a, b)
+        ref.begin(int(r))
+    # append in two rounds (prefill-like then decode-like) to exercise page growth
+    first = np.maximum(1, ctx // 2)
+    for part in (first, ctx - first):
+        if explicit_kv:
+            rows_k, rows_v = [], []
+            for r, c0, k in zip(ids, [ref.ctx[int(r)] for r in ids], part):
+                pos = np.arange(c0, c0 + k)[:, None, None]
+                lay = np.arange(L)[None, :, None]
+                hd = np.arange(Hkv)[None, None, :]
+                rows_k.append(hashgen.to_bits(hashgen.gen_values(seed, 1, int(r), pos, lay, hd, d), dtype))
+                rows_v.append(hashgen.to_bits(hashgen.gen_values(seed, 2, int(r), pos, lay, hd, d), dtype))
+            kt = torch_from_bits(np.concatenate(rows_k)) if sum(part) else None
+            vt = torch_from_bits(np.concatenate(rows_v)) if sum(part) else None
+            if kt is None:
+                pool.append_tokens(ids, part, seed=seed)
+            else:
+                pool.append_tokens(ids, part, kt, vt)
+        else:
+            pool.append_tokens(ids, part, seed=seed)
+        ref.append([int(r) for r in ids], [int(x) for x in part])
+    # block tables and counts: bit-exact
+    bt_dev = pool.block_table()
+    for r in ids:
+        c, slot, pages = pool.request_info(r)
+        assert c == ref.ctx[int(r)] and pages == ref.pages[int(r)]
+        row = bt_dev[slot]
+        assert list(row[:len(pages)]) == pages and np.all(row[len(pages):] == -1)
+    layers = [layer] if layer is not None else list(range(L))
+    results = []
+    for lay in layers:
+        qv = np.stack([hashgen.gen_values(seed, 0, int(r), int(c) - 1, lay, np.arange(Hq), d, q_scale_log2)
+                       for r, c in zip(ids, ctx)])
+        qb = hashgen.to_bits(qv, dtype)
+        q = torch_from_bits(qb)
+        out = torch.empty(n, Hq, d, dtype={2: torch.float32, 0: torch.float16, 1: torch.bfloat16}[out_dtype],
+                          device="cuda")
+        pool.decode_step(ids, lay, q, out, out_dtype=out_dtype, fuse_stats=(lay == layers[0]))
+        st = pool.batch_stats()
+        exp = ostats.batch_stats(ctx, l_in, l_out, [ref.pages[int(r)] for r in ids], P, cap)
+        assert st == exp
+        bt, pk, pv, qq = oatt.synth_paged_batch(seed, [int(r) for r in ids], ctx,
+                                                [ref.pages[int(r)] for r in ids], lay, Hq, Hkv, d, P,
+                                                dtype, q_scale_log2=q_scale_log2, n_phys=cap)
+        assert np.array_equal(qq, qb)
+        want = oatt.paged_decode_attention(ctx, bt, pk, pv, qq, dtype, nthreads=8)
+        got = out.float().cpu().numpy().astype(np.float64)
+        results.append((got, want))
+    pool.close()
+    return results
+
+
+def test_device_generator_matches_host_generator(dbk):
+    seed = 99
+    req = np.array([0, 5, 1 << 40, 12345678901], np.int64)
+    pos = np.array([0, 17, 4095, 2 ** 31 - 1], np.int32)
+    for kind in (0, 1, 2):
+        for scale in (0, 4):
+            out = torch.empty(4, 6, 128, dtype=torch.float32, device="cuda")
+            dbk.synth_fill(seed, kind, req, pos, 3, 6, 128, out, scale_log2=scale, dtype=2)
+            want = hashgen.gen_values(seed, kind, req[:, None], pos[:, None], 3, np.arange(6)[None, :], 128, scale)
+            assert np.array_equal(out.cpu().numpy().astype(np.float64), want)
+    for dt, name in ((0, "f16"), (1, "bf16")):
+        out = torch.empty(4, 6, 64, dtype=torch.int16, device="cuda")
+        dbk.synth_fill(seed, 1, req, pos, 0, 6, 64, out, dtype=dt)
+        want = hashgen.to_bits(hashgen.gen_values(seed, 1, req[:, None], pos[:, None], 0, np.arange(6)[None, :], 64), name)
+        assert np.array_equal(out.cpu().numpy().view(np.uint16), want)
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("Hq,Hkv,d", [(8, 8, 64), (4, 4, 128), (8, 2, 64), (16, 2, 128), (8, 4, 128)])
+def test_decode_parity_shapes(dbk, dtype, Hq, Hkv, d):
+    rng = np.random.default_rng(Hq * 100 + d)
+    ctx = [1, 2, 15, 16, 17, 31, 32, 33] + list(rng.integers(1, 700, 6)) + [1500, 4100]
+    for got, want in run_decode_case(dbk, 2, Hq, Hkv, d, dtype, ctx):
+        assert row_err(got, want) <= TOL
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_decode_parity_explicit_kv_and_peaked_q(dbk, dtype):
+    ctx = [3, 40, 129, 600, 1025]
+    for got, want in run_decode_case(dbk, 3, 8, 8, 64, dtype, ctx, explicit_kv=True, q_scale_log2=4):
+        assert row_err(got, want) <= TOL
+
+
+def test_decode_parity_toy_config(dbk):
+    c = configs.CONFIGS["toy"]
+    tr = trace.make_trace(c["n_requests"], **c["trace"])
+    ctx = list(tr.l_in + tr.l_out)
+    for got, want in run_decode_case(dbk, 1, 8, 8, 64, "f16", ctx, cap=256):
+        assert row_err(got, want) <= TOL
+
+
+def test_decode_output_dtypes(dbk):
+    ctx = [5, 77, 300]
+    for od in (0, 1):
+        for got, want in run_decode_case(dbk, 1, 8, 8, 128, "f16", ctx, out_dtype=od):
+            # output rounding adds at most half an ulp of the output format
+            ulp = 2.0 ** -11 if od == 0 else 2.0 ** -8
+            assert row_err(got, want) <= TOL + ulp
+
+
+def test_decode_chunking_is_invariant(dbk, monkeypatch):
+    outs = []
+    for cp in (4, 16, 64):
+        monkeypatch.setenv("DBK_CHUNK_PAGES", str(cp))
+        (got, want), = run_decode_case(dbk, 1, 8, 2, 128, "bf16", [2000, 700, 16, 4096], layer=0)
+        assert row_err(got, want) <= TOL
+        outs.append(got)
+    assert max(row_err(o, outs[0]) for o in outs) < 1e-5
+
+
+def test_append_cap_is_all_or_nothing(dbk):
+    pool = dbk.KVPool(1, 8, 8, 64, 4, 4, 8, "f16")
+    pool.request_begin(1, 10, 10)
+    pool.request_begin(2, 10, 10)
+    pool.append_tokens([1, 2], [17, 16])
+    with pytest.raises(dbk.DbkError) as e:
+        pool.append_tokens([1, 2], [16, 17])
+    assert e.value.status == dbk._lib.DBK_ECAP
+    assert pool.usage() == (3, 1)
+    assert pool.request_info(1)[0] == 17 and pool.request_info(2)[0] == 16
+    pool.release([1])
+    assert pool.usage() == (1, 3)
+    bt = pool.block_table()
+    assert np.all(bt[0] == -1)
+    with pytest.raises(dbk.DbkError):
+        pool.request_begin(3, 40, 40)    # ceil(80/16) = 5 pages > cap 4: fatal
+    pool.close()
+
+
+# ------------------------------------------------------------------ engine replay
+def _engine_vs_replay(dbk, cfgname, n_req=None, policy=None, sla_ms=None, tr=None, cap_pages=None,
+                      layers=None, check_attention_every=0, dtype="f16"):
+    c = dict(configs.CONFIGS[cfgname])
+    if tr is None:
+        t = c["trace"]
+        tr = trace.make_trace(n_req or c["n_requests"], t["mean_in"], t["mean_out"], t["L_max"], t["seed"],
+                              dist=t["dist"])
+    L = layers or c["layers"]
+    Hq, Hkv, d, P = c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
+    cap_pages = cap_pages or c["cap_tokens"] // P
+    beta = 2 * L * Hkv * d * 2
+    mem_cap = cap_pages * P * beta
+    pr = configs.prior_record(c)
+    kw = dict(policy=policy if policy is not None else opol.MEMORY, b_static=c["b_max"], b_min=c["b_min"],
+              b_max=c["b_max"], b0=c["b_min"], eps_m=c["eps_m"], bytes_per_token=beta, page_size=P,
+              refresh_steps=5, w_len=16, w_sla=4, alpha=4, delta=1, d_sla_ms=sla_ms or 50.0, eps_d_ms=0.01)
+    sched = dbk.Scheduler(prior=tuple(pr.values()), **kw)
+    max_req = c["b_max"] + 2
+    maxp = -(-c["trace"]["L_max"] // P)
+    pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, dtype)
+    seed = 31
+    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap, seed=seed, out_dtype=2)
+    et = torch.float16 if dtype == "f16" else torch.bfloat16
+    qd = torch.empty(L, max_req, Hq, d, dtype=et, device="cuda")
+    od = torch.empty(L, max_req, Hq, d, dtype=torch.float32, device="cuda")
+    bufs = eng.buffers(qd, od)
+    recs = []
+    ids = list(range(len(tr)))
+    rp = oeng.Replay([oeng.RankEngine(ids, tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P)],
+                     opol.SchedConfig(prior=tuple(pr.values()), **kw), mem_cap)
+    checked = 0
+    while not eng.done():
+        g = eng.step(bufs)
+        recs.append(g)
+        o = rp.step(g["step_ns"])
+        for k in ("t", "clock_ns", "b_t", "b_next", "n_admitted", "n_preempted", "n_decode", "n_finished",
+                  "sum_ctx", "used_pages", "rationale"):
+            assert g[k] == o[k], (k, g, {kk: o[kk] for kk in g if kk in o})
+        assert (g["table_hash"] & ((1 << 64) - 1)) == o["table_hash"]
+        assert g["n_waiting"] == o["stats"]["n_waiting"]
+        if check_attention_every and g["t"] % check_attention_every == 0 and g["n_decode"]:
+            rs, ctx, li, lo, pages = o["batches"][0]
+            bid, bctx = eng.last_batch()
+            assert list(bid) == rs and list(bctx) == ctx
+            n = len(rs)
+            remap = {p: i for i, p in enumerate(sorted({x for pg in pages for x in pg}))}
+            cp = [[remap[x] for x in pg] for pg in pages]
+            lay = g["t"] % L
+            bt, pk, pv, qq = oatt.synth_paged_batch(seed, rs, ctx, cp, lay, Hq, Hkv, d, P, dtype)
+            want = oatt.paged_decode_attention(ctx, bt, pk, pv, qq, dtype, nthreads=8)
+            got = od[lay, :n].cpu().numpy().astype(np.float64)
+            assert row_err(got, want) <= TOL
+            checked += 1
+    assert rp.done()
+    assert sum(r["n_finished"] for r in recs) == len(tr)
+    pool.close()
+    return recs, checked
+
+
+def test_engine_toy_memory_policy_replays_bit_exact(dbk):
+    recs, checked = _engine_vs_replay(dbk, "toy", check_attention_every=3)
+    assert checked > 0
+    assert max(r["b_t"] for r in recs) == 8        # b_quad = 27 clamps to B_max (non-binding)
+
+
+def test_engine_toy_tight_preempts_and_replays(dbk):
+    c = configs.CONFIGS["toy-tight"]
+    tr = trace.make_trace(40, 128, 128, 256, seed=1, dist="uniform")
+    # static b = 8 over-commits the 64-page cap: exercises LIFO preemption + recompute
+    recs, _ = _engine_vs_replay(dbk, "toy-tight", tr=tr, policy=opol.STATIC, check_attention_every=7)
+    assert sum(r["n_preempted"] for r in recs) > 0
+    recs, _ = _engine_vs_replay(dbk, "toy-tight", tr=tr, policy=opol.MEMORY)
+    assert all(r["used_pages"] <= c["cap_tokens"] // 16 for r in recs)
+
+
+def test_engine_combined_sla_poisson_replays(dbk):
+    tr = trace.make_trace(60, 100, 100, 256, seed=5, dist="uniform", arrival="poisson", rate_qps=400.0)
+    recs, checked = _engine_vs_replay(dbk, "toy", tr=tr, policy=opol.COMBINED, sla_ms=0.05,
+                                      check_attention_every=5, dtype="bf16")
+    assert checked > 0
+    assert any(r["rationale"] == opol.R_SLA for r in recs) or any(r["rationale"] == opol.R_MEMORY for r in recs)
