@@ -169,6 +169,70 @@ __device__ void batch_stats_warp(const DecodeParams &p, const ReqMeta &rm, int l
     }
 }
 
+// ------------------------------------------------------------------ CTA epilogue (K1, K2) + K3
+// sm_m/sm_l/sm_acc hold NG online-softmax states (running max in log2 units, denominator,
+// unnormalised numerator) per q-head of the group.  Merge them; a single-chunk request
+// writes out directly, otherwise the partial goes to the split-K workspace and the
+// last-arriving CTA of (request, kv head) merges all chunks (no second launch).
+template <int GQ, int D, int NG, int NT>
+__device__ void merge_and_store(const DecodeParams &p, const ReqMeta &rm, int i, int c, int g,
+                                const float *sm_acc, const float *sm_m, const float *sm_l,
+                                int *s_last) {
+    const int kv_heads = gridDim.y;
+    const bool split = rm.nchunks > 1;
+    const int wi = rm.chunk_base + c;
+    for (int idx = threadIdx.x; idx < GQ * D; idx += NT) {
+        const int t = idx / D, e = idx % D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int x = 0; x < NG; ++x) M = fmaxf(M, sm_m[x * GQ + t]);
+        float L = 0.f, O = 0.f;
+#pragma unroll
+        for (int x = 0; x < NG; ++x) {
+            const float mx = sm_m[x * GQ + t];
+            if (mx != -INFINITY) {
+                const float f = exp2f(mx - M);
+                L += f * sm_l[x * GQ + t];
+                O += f * sm_acc[(x * GQ + t) * D + e];
+            }
+        }
+        const int h = g * GQ + t;
+        if (!split) {
+            store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
+        } else {
+            p.ws_o[(static_cast<size_t>(wi) * p.q_heads + h) * D + e] = O;
+            if (e == 0) p.ws_ml[static_cast<size_t>(wi) * p.q_heads + h] = make_float2(M, L);
+        }
+    }
+    if (!split) return;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(p.counters + i * kv_heads + g, 1);
+        *s_last = (prev == rm.nchunks - 1);
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    for (int idx = threadIdx.x; idx < GQ * D; idx += NT) {
+        const int t = idx / D, e = idx % D;
+        const int h = g * GQ + t;
+        float M = -INFINITY;
+        for (int x = 0; x < rm.nchunks; ++x)
+            M = fmaxf(M, __ldcg(&p.ws_ml[static_cast<size_t>(rm.chunk_base + x) * p.q_heads + h]).x);
+        float L = 0.f, O = 0.f;
+        for (int x = 0; x < rm.nchunks; ++x) {
+            const size_t w = static_cast<size_t>(rm.chunk_base + x);
+            const float2 ml = __ldcg(&p.ws_ml[w * p.q_heads + h]);
+            const float f = exp2f(ml.x - M);
+            L += f * ml.y;
+            O += f * __ldcg(&p.ws_o[(w * p.q_heads + h) * D + e]);
+        }
+        store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
+    }
+    if (threadIdx.x == 0) p.counters[i * kv_heads + g] = 0;
+}
+
 // ------------------------------------------------------------------ K1/K3: paged decode attention
 // CTA = (work item = (request, chunk of chunk_pages pages), kv head g); it serves the
 // GQ q-heads g*GQ .. g*GQ+GQ-1.  Each warp streams pages pg0+warp, pg0+warp+WARPS, ...
@@ -196,7 +260,6 @@ decode_kernel(const DecodeParams p) {
     const int2 item = p.work[blockIdx.x];
     const int i = item.x, c = item.y;
     const int g = blockIdx.y;
-    const int kv_heads = gridDim.y;
     const ReqMeta rm = p.req[i];
     const int npages = (rm.ctx + kP - 1) / kP;
     const int pg0 = c * p.chunk_pages;
@@ -352,60 +415,7 @@ decode_kernel(const DecodeParams p) {
         }
     }
     __syncthreads();
-    const bool split = rm.nchunks > 1;
-    const int wi = rm.chunk_base + c;
-    for (int idx = threadIdx.x; idx < GQ * D; idx += WARPS * 32) {
-        const int t = idx / D, e = idx % D;
-        float M = -INFINITY;
-#pragma unroll
-        for (int x = 0; x < NG; ++x) M = fmaxf(M, sm_m[x * GQ + t]);
-        float L = 0.f, O = 0.f;
-#pragma unroll
-        for (int x = 0; x < NG; ++x) {
-            const float mx = sm_m[x * GQ + t];
-            if (mx != -INFINITY) {
-                const float f = exp2f(mx - M);
-                L += f * sm_l[x * GQ + t];
-                O += f * sm_acc[(x * GQ + t) * D + e];
-            }
-        }
-        const int h = g * GQ + t;
-        if (!split) {
-            store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
-        } else {
-            p.ws_o[(static_cast<size_t>(wi) * p.q_heads + h) * D + e] = O;
-            if (e == 0) p.ws_ml[static_cast<size_t>(wi) * p.q_heads + h] = make_float2(M, L);
-        }
-    }
-    if (!split) return;
-
-    // ---- K3: split-K merge by the last-arriving CTA of (request, kv head)
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int prev = atomicAdd(p.counters + i * kv_heads + g, 1);
-        s_last = (prev == rm.nchunks - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int idx = threadIdx.x; idx < GQ * D; idx += WARPS * 32) {
-        const int t = idx / D, e = idx % D;
-        const int h = g * GQ + t;
-        float M = -INFINITY;
-        for (int x = 0; x < rm.nchunks; ++x)
-            M = fmaxf(M, __ldcg(&p.ws_ml[static_cast<size_t>(rm.chunk_base + x) * p.q_heads + h]).x);
-        float L = 0.f, O = 0.f;
-        for (int x = 0; x < rm.nchunks; ++x) {
-            const size_t w = static_cast<size_t>(rm.chunk_base + x);
-            const float2 ml = __ldcg(&p.ws_ml[w * p.q_heads + h]);
-            const float f = exp2f(ml.x - M);
-            L += f * ml.y;
-            O += f * __ldcg(&p.ws_o[(w * p.q_heads + h) * D + e]);
-        }
-        store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
-    }
-    if (threadIdx.x == 0) p.counters[i * kv_heads + g] = 0;
+    merge_and_store<GQ, D, NG, WARPS * 32>(p, rm, i, c, g, sm_acc, sm_m, sm_l, &s_last);
 }
 
 template <int D>

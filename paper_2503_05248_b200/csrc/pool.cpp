@@ -218,6 +218,22 @@ dbk_status dbk_request_begin(dbk_pool *p, int64_t id, int32_t l_in, int32_t l_ou
 namespace dbk {
 dbk_status flush_deltas(dbk_pool *p, cudaStream_t s) {
     if (p->pending.empty()) return DBK_OK;
+    // The apply kernel writes deltas in parallel, so keep only the LAST delta per entry
+    // (a slot released and reused before a flush has a clear followed by a new page).
+    {
+        std::unordered_map<int64_t, size_t> last;
+        last.reserve(p->pending.size() * 2);
+        for (size_t k = 0; k < p->pending.size(); ++k)
+            last[static_cast<int64_t>(p->pending[k].slot) * p->cfg.max_pages_per_req + p->pending[k].idx] = k;
+        if (last.size() != p->pending.size()) {
+            std::vector<BtDelta> uniq;
+            uniq.reserve(last.size());
+            for (size_t k = 0; k < p->pending.size(); ++k)
+                if (last[static_cast<int64_t>(p->pending[k].slot) * p->cfg.max_pages_per_req + p->pending[k].idx] == k)
+                    uniq.push_back(p->pending[k]);
+            p->pending.swap(uniq);
+        }
+    }
     DBK_TRY(p->up_delta.upload(p->pending.data(), p->pending.size() * sizeof(BtDelta), s));
     DBK_CUDA(launch_bt_apply(p->d_bt, p->cfg.max_pages_per_req, static_cast<const BtDelta *>(p->up_delta.dev),
                              static_cast<int32_t>(p->pending.size()), s));

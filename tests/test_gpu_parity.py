@@ -47,7 +47,7 @@ def run_decode_case(dbk, L, Hq, Hkv, d, dtype, ctx_list, seed=7, explicit_kv=Fal
     n = len(ctx_list)
     ctx = np.asarray(ctx_list, np.int32)
     l_in = np.maximum(1, ctx - 3)
-    l_out = ctx - l_in + np.arange(n) % 2          # odd entries are not finishing
+    l_out = np.maximum(1, ctx - l_in + np.arange(n) % 2)   # odd entries are not finishing
     max_pages = int(max(-(-(ctx + 1) // P))) + 1
     cap = cap or int(sum(-(-ctx // P))) + 7
     pool = dbk.KVPool(L, Hq, Hkv, d, cap, n + 3, max_pages, dtype)
