@@ -1,0 +1,237 @@
+// Device helpers shared by the decode kernels (K1 CUDA-core, K2 tensor-core): PTX wrappers
+// for mbarriers / TMA, element conversions, the synthetic generator, the fused batch
+// statistics (K4) and the CTA epilogue with the split-K merge (K3).  Internal to libdbk.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "kernels.cuh"
+
+namespace dbk {
+namespace dev {
+
+constexpr int kP = 16;          // tokens per page
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D TMA (bulk copy) global -> shared, completion counted on `bar`; the KV
+// stream is read once per step, so it is marked evict-first in L2.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// ------------------------------------------------------------------ element types
+template <typename T>
+struct Elt;
+template <>
+struct Elt<__half> {
+    __device__ static float2 to_f2(uint32_t u) {
+        return __half22float2(*reinterpret_cast<const __half2 *>(&u));
+    }
+    __device__ static uint32_t from_f2(float a, float b) {
+        __half2 h = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+    __device__ static void store(void *p, float x) { *reinterpret_cast<__half *>(p) = __float2half_rn(x); }
+};
+template <>
+struct Elt<__nv_bfloat16> {
+    __device__ static float2 to_f2(uint32_t u) {
+        return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u));
+    }
+    __device__ static uint32_t from_f2(float a, float b) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+    __device__ static void store(void *p, float x) {
+        *reinterpret_cast<__nv_bfloat16 *>(p) = __float2bfloat16_rn(x);
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint4 &u, float f[8]) {
+    float2 a = Elt<T>::to_f2(u.x), b = Elt<T>::to_f2(u.y), c = Elt<T>::to_f2(u.z),
+           d = Elt<T>::to_f2(u.w);
+    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+    f[4] = c.x; f[5] = c.y; f[6] = d.x; f[7] = d.y;
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack8(const float f[8]) {
+    return make_uint4(Elt<T>::from_f2(f[0], f[1]), Elt<T>::from_f2(f[2], f[3]),
+                      Elt<T>::from_f2(f[4], f[5]), Elt<T>::from_f2(f[6], f[7]));
+}
+
+__device__ __forceinline__ void store_out(void *out, size_t idx, int dtype, float x) {
+    if (dtype == 2)
+        reinterpret_cast<float *>(out)[idx] = x;
+    else if (dtype == 0)
+        reinterpret_cast<__half *>(out)[idx] = __float2half_rn(x);
+    else
+        reinterpret_cast<__nv_bfloat16 *>(out)[idx] = __float2bfloat16_rn(x);
+}
+
+// ------------------------------------------------------------------ synthetic generator
+// Same definition as synth/hashgen.py (input generation only).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t synth_key(uint64_t seed, int kind, int64_t req, int pos,
+                                              int layer, int head, int g) {
+    uint64_t k1 = splitmix64(seed ^ (static_cast<uint64_t>(kind) << 56) ^ static_cast<uint64_t>(req));
+    uint64_t w = (static_cast<uint64_t>(static_cast<uint32_t>(pos)) << 32) |
+                 (static_cast<uint64_t>(layer) << 20) | (static_cast<uint64_t>(head) << 8) |
+                 static_cast<uint64_t>(g);
+    return splitmix64(k1 ^ w);
+}
+__device__ __forceinline__ void synth_vals(uint64_t key, float scale, float f[8]) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) f[b] = static_cast<float>(static_cast<int>((key >> (8 * b)) & 0xFF) - 128) * scale;
+}
+
+// ------------------------------------------------------------------ K4: fused batch statistics
+// One warp per request (the CTA holding chunk 0 of kv-head 0).  Integer atomics:
+// order-independent, bit-exact with the oracle O3.
+__device__ __forceinline__ void batch_stats_warp(const DecodeParams &p, const ReqMeta &rm, int lane) {
+    const int32_t *row = p.block_table + static_cast<size_t>(rm.slot) * p.bt_stride;
+    int cnt = 0;
+    for (int b = 0; b < p.max_pages_per_req; b += 32) {
+        const bool v = (b + lane < p.max_pages_per_req) && __ldg(row + b + lane) >= 0;
+        cnt += __popc(__ballot_sync(kFull, v));
+    }
+    if (lane == 0) {
+        unsigned long long *st = p.stats;
+        const unsigned long long c = static_cast<unsigned long long>(rm.ctx);
+        atomicAdd(st + 0, 1ull);
+        atomicAdd(st + 1, c);
+        atomicAdd(st + 2, c * c);
+        atomicMax(st + 3, c);
+        atomicAdd(st + 4, static_cast<unsigned long long>(cnt));
+        if (cnt != (rm.ctx + kP - 1) / kP) atomicAdd(st + 8, 1ull);
+        if (rm.ctx == rm.l_in + rm.l_out) {
+            const unsigned long long a = rm.l_in, b = rm.l_out;
+            atomicAdd(st + 9, 1ull);
+            atomicAdd(st + 10, a);
+            atomicAdd(st + 11, a * a);
+            atomicAdd(st + 12, b);
+            atomicAdd(st + 13, b * b);
+        }
+        __threadfence();
+        const int done = atomicAdd(p.stats_done, 1);
+        if (done == p.n - 1) {  // last request: derived fields against the cap
+            __threadfence();
+            const long long pages = static_cast<long long>(atomicAdd(st + 4, 0ull));
+            st[5] = static_cast<unsigned long long>(p.cap_pages);
+            st[6] = static_cast<unsigned long long>(p.cap_pages - pages);
+            st[7] = pages > p.cap_pages ? 1ull : 0ull;
+            *p.stats_done = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ CTA epilogue (K1, K2) + K3
+// sm_m/sm_l/sm_acc hold NG online-softmax states (running max in log2 units, denominator,
+// unnormalised numerator) per q-head of the group.  Merge them; a single-chunk request
+// writes out directly, otherwise the partial goes to the split-K workspace and the
+// last-arriving CTA of (request, kv head) merges all chunks (no second launch).
+template <int GQ, int D, int NG, int NT>
+__device__ void merge_and_store(const DecodeParams &p, const ReqMeta &rm, int i, int c, int g,
+                                const float *sm_acc, const float *sm_m, const float *sm_l,
+                                int *s_last) {
+    const int kv_heads = gridDim.y;
+    const bool split = rm.nchunks > 1;
+    const int wi = rm.chunk_base + c;
+    for (int idx = threadIdx.x; idx < GQ * D; idx += NT) {
+        const int t = idx / D, e = idx % D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int x = 0; x < NG; ++x) M = fmaxf(M, sm_m[x * GQ + t]);
+        float L = 0.f, O = 0.f;
+#pragma unroll
+        for (int x = 0; x < NG; ++x) {
+            const float mx = sm_m[x * GQ + t];
+            if (mx != -INFINITY) {
+                const float f = exp2f(mx - M);
+                L += f * sm_l[x * GQ + t];
+                O += f * sm_acc[(x * GQ + t) * D + e];
+            }
+        }
+        const int h = g * GQ + t;
+        if (!split) {
+            store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
+        } else {
+            p.ws_o[(static_cast<size_t>(wi) * p.q_heads + h) * D + e] = O;
+            if (e == 0) p.ws_ml[static_cast<size_t>(wi) * p.q_heads + h] = make_float2(M, L);
+        }
+    }
+    if (!split) return;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(p.counters + i * kv_heads + g, 1);
+        *s_last = (prev == rm.nchunks - 1);
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    for (int idx = threadIdx.x; idx < GQ * D; idx += NT) {
+        const int t = idx / D, e = idx % D;
+        const int h = g * GQ + t;
+        float M = -INFINITY;
+        for (int x = 0; x < rm.nchunks; ++x)
+            M = fmaxf(M, __ldcg(&p.ws_ml[static_cast<size_t>(rm.chunk_base + x) * p.q_heads + h]).x);
+        float L = 0.f, O = 0.f;
+        for (int x = 0; x < rm.nchunks; ++x) {
+            const size_t w = static_cast<size_t>(rm.chunk_base + x);
+            const float2 ml = __ldcg(&p.ws_ml[w * p.q_heads + h]);
+            const float f = exp2f(ml.x - M);
+            L += f * ml.y;
+            O += f * __ldcg(&p.ws_o[(w * p.q_heads + h) * D + e]);
+        }
+        store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
+    }
+    if (threadIdx.x == 0) p.counters[i * kv_heads + g] = 0;
+}
+
+}  // namespace dev
+}  // namespace dbk

@@ -257,14 +257,14 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     bt.n = n;
     bt.req_ids = e->batch_ids.data();
     if (n > 0) DBK_TRY(prepare_batch(p, n, e->batch_ids.data(), s));
+    if (n > 0 && !e2e) {  // synthetic q of all layers (stands in for the QKV projection), one launch
+        DBK_CUDA(launch_synth_q(e->cfg.synth_seed, p->d_req, n, pc.layers, pc.max_requests, pc.q_heads,
+                                pc.head_dim, e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
+        ++p->n_launches;
+    }
     for (int l = 0; l < pc.layers; ++l) {
         uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
         uint8_t *od = static_cast<uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;
-        if (n > 0 && !e2e) {
-            DBK_CUDA(launch_synth_q(e->cfg.synth_seed, p->d_req, n, l, pc.q_heads, pc.head_dim,
-                                    e->cfg.q_scale_log2, pc.kv_dtype, qd, s));
-            ++p->n_launches;
-        }
         bt.layer = l;
         bt.fuse_stats = l == 0 ? 1 : 0;
         if (e->cfg.time_attention && n > 0) DBK_CUDA(cudaEventRecord(e->att0[l], s));

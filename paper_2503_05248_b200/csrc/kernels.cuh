@@ -1,6 +1,7 @@
 // Device-side data structures and kernel launchers (internal to libdbk).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -42,6 +43,9 @@ struct DecodeParams {
     unsigned long long *stats;   // 16 x u64, zeroed before the launch
     int32_t *stats_done;         // zero between launches
     int64_t cap_pages;
+    // K2 (tensor-core GQA) addressing through the pool-wide 2-D tensor map
+    int32_t layer;
+    int32_t kv_heads;
 };
 
 struct AppendJob {
@@ -67,17 +71,21 @@ struct BtDelta {
 };
 
 // launchers (return cudaGetLastError() of the launch)
+// tmap != nullptr and group >= 2 selects K2 (tensor cores); otherwise K1 (CUDA cores).
 cudaError_t launch_decode(const DecodeParams &p, int kv_dtype, int head_dim, int group,
-                          int kv_heads, cudaStream_t s);
+                          int kv_heads, const CUtensorMap *tmap, cudaStream_t s);
+cudaError_t launch_decode_gqa(const DecodeParams &p, int kv_dtype, int head_dim, int group,
+                              int kv_heads, const CUtensorMap &tmap, cudaStream_t s);
+int decode_gqa_ctas_per_sm(int kv_dtype, int head_dim, int group);
 cudaError_t launch_append(const AppendParams &p, int kv_dtype, int head_dim, cudaStream_t s);
 cudaError_t launch_bt_apply(int32_t *bt, int32_t stride, const BtDelta *d, int32_t n,
                             cudaStream_t s);
 cudaError_t launch_synth_rows(uint64_t seed, int kind, int n_rows, const int64_t *req,
                               const int32_t *pos, int layer, int n_heads, int d, int scale_log2,
                               int dtype, void *out, cudaStream_t s);
-// q[i][h][:] = synth(seed, q, req_i, ctx_i - 1, layer, h) for the batch in `req`.
-cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layer, int q_heads,
-                           int d, int scale_log2, int dtype, void *q, cudaStream_t s);
+// q[l][i][h][:] = synth(seed, q, req_i, ctx_i - 1, l, h) for all layers, layer stride layer_rows rows.
+cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
+                           int q_heads, int d, int scale_log2, int dtype, void *q, cudaStream_t s);
 int decode_ctas_per_sm(int kv_dtype, int head_dim, int group);
 
 }  // namespace dbk

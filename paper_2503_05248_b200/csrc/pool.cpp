@@ -1,5 +1,7 @@
 // KV pool: page allocator (host source of truth), request table, device block
 // tables and the decode / append launches.
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -98,6 +100,28 @@ void PageBitmap::give_back(int64_t p) {
 
 using namespace dbk;
 
+// K2's tensor map over the whole pool: a 2-D tensor of rows = layers*cap*kv_heads*2*16
+// token rows x head_dim elements; one box = 16 rows x 64 elements with the 128-byte swizzle.
+static bool make_pool_tmap(dbk_pool *p) {
+    const dbk_pool_config &c = p->cfg;
+    const uint64_t rows = static_cast<uint64_t>(c.layers) * c.cap_pages * c.kv_heads * 2 * c.page_size;
+    if (rows >= (1ull << 31)) return false;  // int32 TMA coordinates
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess)
+        return false;
+    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(c.head_dim), rows};
+    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(c.head_dim) * 2};
+    const cuuint32_t box[2] = {64, 16};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->kv, gdim, gstride, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 static bool pool_cfg_ok(const dbk_pool_config *c) {
     if (!c) return false;
     if (c->layers < 1 || c->q_heads < 1 || c->kv_heads < 1 || c->q_heads % c->kv_heads) return false;
@@ -160,7 +184,11 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
     p->num_sms = dev_sms;
-    p->ctas_per_sm = decode_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, cfg->q_heads / cfg->kv_heads);
+    const int group = cfg->q_heads / cfg->kv_heads;
+    const char *cc = std::getenv("DBK_GQA_CUDA_CORE");  // 1: force K1 for GQA (comparison runs)
+    if (group >= 2 && !(cc && cc[0] == '1')) p->has_tmap = make_pool_tmap(p);
+    p->ctas_per_sm = p->has_tmap ? decode_gqa_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group)
+                                 : decode_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group);
     if (const char *e = std::getenv("DBK_CHUNK_PAGES")) {  // tuning override (multiple of 4, <= 64)
         const long long v = std::atoll(e);
         if (v >= 4 && v <= 64 && v % 4 == 0) p->force_chunk_pages = v;
@@ -503,8 +531,10 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     dp.stats = reinterpret_cast<unsigned long long *>(p->d_stats);
     dp.stats_done = p->d_stats_done;
     dp.cap_pages = p->cfg.cap_pages;
+    dp.layer = b->layer;
+    dp.kv_heads = p->cfg.kv_heads;
     DBK_CUDA(launch_decode(dp, p->cfg.kv_dtype, p->cfg.head_dim, p->cfg.q_heads / p->cfg.kv_heads,
-                           p->cfg.kv_heads, s));
+                           p->cfg.kv_heads, p->has_tmap ? &p->tmap : nullptr, s));
     ++p->n_launches;
     p->last_decode_bytes = decode_bytes(p, out_dtype);
     return DBK_OK;

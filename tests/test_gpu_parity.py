@@ -268,3 +268,67 @@ def test_engine_combined_sla_poisson_replays(dbk):
                                       check_attention_every=5, dtype="bf16")
     assert checked > 0
     assert any(r["rationale"] == opol.R_SLA for r in recs) or any(r["rationale"] == opol.R_MEMORY for r in recs)
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("Hq,Hkv,d", [(8, 2, 64), (16, 2, 128), (8, 4, 128), (16, 8, 64)])
+@pytest.mark.parametrize("path", ["tensor", "cuda_core"])
+def test_gqa_paths_parity(dbk, monkeypatch, dtype, Hq, Hkv, d, path):
+    """K2 (TMA tensor tiles + mma.sync) and K1 (CUDA cores) on the same GQA inputs."""
+    if path == "cuda_core":
+        monkeypatch.setenv("DBK_GQA_CUDA_CORE", "1")
+    else:
+        monkeypatch.delenv("DBK_GQA_CUDA_CORE", raising=False)
+    ctx = [1, 5, 16, 17, 100, 255, 256, 257, 1024, 3000]
+    for got, want in run_decode_case(dbk, 2, Hq, Hkv, d, dtype, ctx, q_scale_log2=(4 if Hq == 16 else 0)):
+        assert row_err(got, want) <= TOL
+
+
+def test_nccl_single_rank_allgather(dbk):
+    """The native NCCL exchange path (dbk_comm_*) with one rank on cuda:0."""
+    import ctypes
+    buf = (ctypes.c_char * 128)()
+    dbk._lib.dbk_comm_unique_id(buf)
+    comm = ctypes.c_void_p()
+    dbk._lib.dbk_comm_create(1, 0, buf, 0, ctypes.byref(comm))
+    rec = dict.fromkeys(dbk._lib.STATS_FIELDS, 0)
+    rec.update(n_active=7, sum_ctx=99, step_ns=1234, n_finished=2)
+    local = dbk.dbk_stats(*[rec[f] for f in dbk._lib.STATS_FIELDS])
+    allr = (dbk.dbk_stats * 1)()
+    glob = dbk.dbk_stats()
+    stream = torch.cuda.current_stream().cuda_stream
+    dbk._lib.dbk_stats_allgather(comm, ctypes.byref(local), allr, ctypes.byref(glob), 0, stream)
+    assert allr[0].as_dict() == rec and glob.as_dict()["sum_ctx"] == 99 and glob.as_dict()["step_ns"] == 1234
+    dbk._lib.dbk_comm_destroy(comm)
+
+
+def test_bench_config_sampled_parity(dbk):
+    """The bench's own launch configuration (Llama-2-7B shape, pool sized from free HBM,
+    memory policy): run engine steps, then compare sampled (request, q-head, layer)
+    outputs of the last step with the oracle computed from logical coordinates."""
+    import bench
+    S = bench.setup_engine(device=0, time_attention=True, out_dtype=2, n_req=1200)
+    eng = S["eng"]
+    bufs = eng.buffers(S["qd"], S["od"])
+    stream = torch.cuda.current_stream()
+    for _ in range(40):
+        rec = eng.step(bufs, stream)
+    torch.cuda.synchronize()
+    c = S["c"]
+    L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
+    ids, ctx = eng.last_batch()
+    assert rec["n_decode"] == len(ids) and rec["sum_ctx"] == int(ctx.sum())
+    rng = np.random.default_rng(5)
+    sel = rng.choice(len(ids), size=12, replace=False)
+    for lay in (0, L // 2, L - 1):
+        pages, nxt = [], 0
+        for cx in ctx[sel]:
+            m = -(-int(cx) // P)
+            pages.append(list(range(nxt, nxt + m)))
+            nxt += m
+        bt, pk, pv, qq = oatt.synth_paged_batch(S["seed"], [int(x) for x in ids[sel]], ctx[sel], pages, lay,
+                                                Hq, Hkv, d, P, "f16")
+        want = oatt.paged_decode_attention(ctx[sel], bt, pk, pv, qq, "f16", nthreads=8)
+        got = S["od"][lay, torch.as_tensor(sel, device="cuda")].cpu().numpy().astype(np.float64)
+        assert row_err(got, want) <= TOL
+    S["pool"].close()
