@@ -107,50 +107,63 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_workload(rank=0, world=1, n_req=None):
-    c = configs.CONFIGS[CFG_NAME]
+def make_workload(cfg_name=CFG_NAME, world=1, n_req=None):
+    """The config's trace; DP runs generate world x n_requests (weak scaling), shard i % world."""
+    c = configs.CONFIGS[cfg_name]
     t = c["trace"]
     n = (n_req or c["n_requests"]) * world
     tr = trace.make_trace(n, t["mean_in"], t["mean_out"], t["L_max"], t["seed"], dist=t["dist"])
     return c, tr
 
 
-def sched_kwargs(c, beta):
+POLICIES = {"static": 0, "memory": 1, "sla": 2, "combined": 3}
+
+
+def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None):
     pr = configs.prior_record(c)
-    return dict(policy=1, b_static=256, b_min=c["b_min"], b_max=c["b_max"], b0=c["b_min"],
+    pol = POLICIES[policy or c["policy"]]
+    return dict(policy=pol, b_static=b_static, b_min=c["b_min"], b_max=c["b_max"], b0=c["b_min"],
                 eps_m=c["eps_m"], bytes_per_token=beta, page_size=c["page_size"], refresh_steps=100,
-                w_len=256, w_sla=20, alpha=8, delta=2, prior=tuple(pr.values()))
+                w_len=256, w_sla=20, alpha=c.get("alpha", 8), delta=c.get("delta", 2),
+                d_sla_ms=sla_ms or c.get("sla_ms", 50.0), eps_d_ms=c.get("eps_d_ms", 2.0),
+                prior=tuple(pr.values()))
 
 
-def setup_engine(device=0, rank=0, world=1, cap_bytes=None, time_attention=True, out_dtype=0,
-                 seed=2024, n_req=None):
-    """Pool sized from free HBM (cap = free - modeled 7B weights - reserve), memory policy."""
+def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
+                 out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1):
+    """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
+    config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
 
     import paper_2503_05248_b200 as dbk
-    c, tr = make_workload(rank, world, n_req)
-    L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
-    beta = configs.kv_bytes_per_token(c)
+    c, tr = make_workload(cfg_name, world if tp == 1 else 1, n_req)
+    L, Hq, Hkv, d, P = c["layers"], c["q_heads"] // tp, c["kv_heads"] // tp, c["head_dim"], c["page_size"]
+    beta = configs.kv_bytes_per_token(c, tp=tp)
     max_req = c["b_max"] + 8
     io_bytes = 2 * L * max_req * Hq * d * 4 + 2 * max_req * L * Hkv * d * 2
     free, _ = torch.cuda.mem_get_info(device)
     if cap_bytes is None and os.environ.get("DBK_BENCH_KV_GB"):  # profiling runs only (smaller pool)
         cap_bytes = int(float(os.environ["DBK_BENCH_KV_GB"]) * GB)
+    if cap_bytes is None and "cap_bytes_per_gpu" in c:
+        cap_bytes = c["cap_bytes_per_gpu"]
     if cap_bytes is None:
-        cap_bytes = free - c["weights_bytes"] - c["reserve_bytes"] - io_bytes
+        cap_bytes = free - c["weights_bytes"] // tp - c["reserve_bytes"] - io_bytes
     cap_pages = int(cap_bytes // (P * beta))
     maxp = -(-c["trace"]["L_max"] // P)
     pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, "f16", device=device)
-    mem_cap_total = cap_pages * P * beta * world
-    sched = dbk.Scheduler(**sched_kwargs(c, beta))
+    # M_max of the whole job: DP shards add their pools; TP ranks hold the same tokens
+    mem_cap_total = cap_pages * P * beta * (world if tp == 1 else 1)
+    sched = dbk.Scheduler(**sched_kwargs(c, beta, policy, b_static, sla_ms))
     eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap_total, seed=seed,
-                     out_dtype=out_dtype, time_attention=time_attention, rank=rank, world=world)
+                     out_dtype=out_dtype, time_attention=time_attention,
+                     rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0)
     et = torch.float32 if out_dtype == 2 else torch.float16
     qd = torch.empty(L, max_req, Hq, d, dtype=torch.float16, device=f"cuda:{device}")
     od = torch.empty(L, max_req, Hq, d, dtype=et, device=f"cuda:{device}")
     kvd = torch.empty(2, max_req, L, Hkv, d, dtype=torch.float16, device=f"cuda:{device}")
-    return dict(dbk=dbk, c=c, tr=tr, pool=pool, sched=sched, eng=eng, qd=qd, od=od, kvd=kvd,
-                cap_pages=cap_pages, beta=beta, max_req=max_req, mem_cap_total=mem_cap_total, seed=seed)
+    return dict(dbk=dbk, c=c, tr=tr, pool=pool, sched=sched, eng=eng, qd=qd, od=od, kvd=kvd, tp=tp,
+                cap_pages=cap_pages, beta=beta, max_req=max_req, mem_cap_total=mem_cap_total, seed=seed,
+                L=L, Hq=Hq, Hkv=Hkv, d=d)
 
 
 def run_steps(S, k, bufs, stream, comm_world=1, dist=None):
@@ -206,6 +219,20 @@ def cpu_baseline(S, budget_s=15.0, threads=None):
                       f"request-layers / L / time"}
 
 
+def _make_comm(dbk, dist, world, rank, local):
+    """ncclUniqueId from rank 0 (dbk_comm_unique_id), broadcast over torch.distributed."""
+    import ctypes
+    buf = (ctypes.c_char * 128)()
+    if rank == 0:
+        dbk._lib.dbk_comm_unique_id(buf)
+    obj = [bytes(buf.raw)]
+    dist.broadcast_object_list(obj, src=0)
+    idbuf = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+    comm = ctypes.c_void_p()
+    dbk._lib.dbk_comm_create(world, rank, idbuf, local, ctypes.byref(comm))
+    return comm
+
+
 def run_gpu(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -218,24 +245,16 @@ def run_gpu(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    S = setup_engine(device=local, rank=rank, world=world)
+    # configs[3] (70B GQA) is sharded by KV heads (TP); the others by requests (DP)
+    tp = world if args.config == "llama3-70b-gqa" else 1
+    S = setup_engine(device=local, rank=rank, world=world, cfg_name=args.config, policy=args.policy,
+                     b_static=args.b_static, sla_ms=args.sla_ms, tp=tp)
     dbk = S["dbk"]
-    if world > 1:
-        idb = bytearray(128)
-        if rank == 0:
-            import ctypes
-            buf = (ctypes.c_char * 128)()
-            dbk._lib.dbk_comm_unique_id(buf)
-            idb = bytearray(buf.raw)
-        obj = [bytes(idb)]
-        dist.broadcast_object_list(obj, src=0)
-        import ctypes
-        idbuf = (ctypes.c_char * 128).from_buffer_copy(obj[0])
-        comm = ctypes.c_void_p()
-        dbk._lib.dbk_comm_create(world, rank, idbuf, local, ctypes.byref(comm))
-        dbk._lib.dbk_engine_attach_comm(S["eng"].h, comm, dbk._lib.MODE_DP)
-    stream = torch.cuda.current_stream()
     eng = S["eng"]
+    if world > 1:
+        comm = _make_comm(dbk, dist, world, rank, local)
+        dbk._lib.dbk_engine_attach_comm(eng.h, comm, dbk._lib.MODE_TP if tp > 1 else dbk._lib.MODE_DP)
+    stream = torch.cuda.current_stream()
     bufs = eng.buffers(S["qd"], S["od"])
     # fast-forward to the steady state (untimed), then W warm-up steps (untimed)
     run_steps(S, args.ff, bufs, stream, dist=dist)
@@ -244,65 +263,68 @@ def run_gpu(args):
     with ClockSampler(local) as clk:
         recs, ms = run_steps(S, args.steps, bufs, stream, dist=dist)
     att_ms, att_launches, att_bytes = eng.attn_timing(reset=True)
+    info = S["pool"].info()
+    # decode tokens of the whole job: DP shards are disjoint (sum over ranks); TP ranks
+    # serve the same requests (count once)
     ms_t = torch.tensor([ms], device="cuda")
-    tok_t = torch.tensor([float(sum(r["n_decode"] for r in recs))], device="cuda")
+    tok_t = torch.tensor([float(sum(r["n_decode"] for r in recs)) / (world if tp > 1 else 1)], device="cuda")
     if dist is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    # decode tokens of the whole job: every rank's batch counts (DP shards are disjoint)
-    if dist is not None:
         dist.all_reduce(tok_t)
-    toks = float(tok_t.item())
+    ms_max, toks = float(ms_t.item()), float(tok_t.item())
     # end-to-end through the same API with pinned host buffers (q, new K/V in; out back)
-    c = S["c"]
-    L, Hq, Hkv, d = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"]
-    mr = S["max_req"]
+    L, Hq, Hkv, d, mr = S["L"], S["Hq"], S["Hkv"], S["d"], S["max_req"]
     hq = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
     hk = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
     hv = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
     ho = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True)
     ebufs = eng.buffers(S["qd"], S["od"], S["kvd"], hq, hk, hv, ho)
     run_steps(S, 2, ebufs, stream, dist=dist)
-    with ClockSampler(local) as clk2:
-        erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
+    erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
     ems_t = torch.tensor([ems], device="cuda")
-    etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs))], device="cuda")
+    etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / (world if tp > 1 else 1)], device="cuda")
     if dist is not None:
         dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(etok_t)
     if rank == 0:
         peak, peak_src = measured_peaks()
         achieved = att_bytes / 1e9 / (att_ms / 1e3) if att_ms > 0 else 0.0
-        traffic, traffic_alg = ncu_traffic()
-        clocks = clk.summary()
+        traffic = None
+        if args.config == CFG_NAME and tp == 1:
+            traffic, _ = ncu_traffic()
+        c = S["c"]
         n_steps = len(recs)
+        kname = "decode_gqa_kernel (K2, tensor cores)" if info["decode_path"] == 2 else \
+            "decode_kernel (K1, paged decode attention)"
         line = {
             "metric": METRIC, "value": round(toks / (ms_max / 1e3), 2), "unit": UNIT, "n_gpus": world,
             "steps": n_steps, "warmup": args.warmup, "ms_per_step": round(ms_max / max(n_steps, 1), 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None,
+            "dtype": "f16",
             "data": "synthetic (seeded lognormal trace, hash-generated q/K/V; no weights on this path)",
-            "config": {"workload": configs.CONFIGS[CFG_NAME]["name"], "layers": L, "q_heads": Hq,
-                       "kv_heads": Hkv, "head_dim": d, "page_size": 16, "kv_dtype": "fp16",
-                       "out_dtype": "fp16", "policy": "memory-aware (Alg. 1 + Eq. 11 L0)",
-                       "requests_per_gpu": configs.CONFIGS[CFG_NAME]["n_requests"],
-                       "trace": "all-at-once, lognormal CV=1, means 191.0/381.9 (PAPER.md:266)",
+            "config": {"workload": c["name"], "layers": L, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d,
+                       "page_size": 16, "kv_dtype": "fp16", "out_dtype": "fp16",
+                       "policy": args.policy or c["policy"], "sla_ms": args.sla_ms or c.get("sla_ms"),
+                       "requests": len(S["tr"]),
+                       "trace": f"all-at-once, lognormal CV=1, means {c['trace']['mean_in']}/{c['trace']['mean_out']}",
                        "cap_pages_per_gpu": S["cap_pages"],
                        "kv_cap_gb_per_gpu": round(S["cap_pages"] * 16 * S["beta"] / GB, 2),
                        "mean_batch": round(float(np.mean([r["n_decode"] for r in recs])), 1) if recs else 0,
                        "mean_ctx": round(float(np.mean([r["sum_ctx"] / max(r["n_decode"], 1) for r in recs])), 1) if recs else 0,
-                       "fast_forward_steps": args.ff, "parallelism": f"dp{world} (request shards)",
+                       "fast_forward_steps": args.ff,
+                       "parallelism": f"tp{world} (KV-head shards)" if tp > 1 else f"dp{world} (request shards)",
                        "l2": "inputs > L2 (~1e2 GB of KV read per step vs 126 MB L2)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "decode_kernel (paged decode attention, K1)",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kname,
                          "bytes_per_launch": int(att_bytes / max(att_launches, 1)),
                          "ms_per_launch": round(att_ms / max(att_launches, 1), 4), "peak_source": peak_src,
-                         "share_of_step": round(att_ms / max(ms, 1e-9), 4)},
+                         "share_of_step": round(att_ms / max(ms, 1e-9), 4), "ctas_per_sm": info["ctas_per_sm"],
+                         "chunk_pages": info["chunk_pages"]},
             "e2e": {"value": round(float(etok_t.item()) / (float(ems_t.item()) / 1e3), 2), "unit": UNIT,
                     "h2d_bytes_per_step": int(np.mean([r["h2d_bytes"] for r in erecs])) if erecs else 0,
                     "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in erecs])) if erecs else 0},
             "gpu_launches": int(sum(r["launches"] for r in recs)),
-            "clocks": clocks,
+            "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(S)
@@ -321,12 +343,14 @@ def run_reference(args):
     from oracle import attention as oatt
     from oracle import engine as oeng
     from oracle import policy as opol
-    c, tr = make_workload()
+    c, tr = make_workload(args.config)
     L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
     beta = configs.kv_bytes_per_token(c)
     free = 178_000_000_000  # same sizing rule as the GPU arm on a 180 GB part
-    cap_pages = int((free - c["weights_bytes"] - c["reserve_bytes"]) // (P * beta))
-    kw = sched_kwargs(c, beta)
+    cap_bytes = c.get("cap_bytes_per_gpu") or (free - c["weights_bytes"] - c["reserve_bytes"])
+    cap_pages = int(cap_bytes // (P * beta))
+    kw = sched_kwargs(c, beta, args.policy, args.b_static, args.sla_ms)
+    kw["policy"] = min(kw["policy"], 1) if kw["policy"] != 3 else 1   # no device timing: memory rule
     rp = oeng.Replay([oeng.RankEngine(list(range(len(tr))), tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P)],
                      opol.SchedConfig(**kw), cap_pages * P * beta)
     for _ in range(args.ff):           # steady state: same fast-forward as the GPU arm (modeled 25 ms steps)
@@ -374,6 +398,10 @@ def main():
     ap.add_argument("--ff", type=int, default=300, help="untimed fast-forward steps to the steady state")
     ap.add_argument("--impl", default="dbk", choices=["dbk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default=CFG_NAME, choices=["llama2-7b", "llama2-13b-sla", "llama3-70b-gqa"])
+    ap.add_argument("--policy", default=None, choices=[None, "static", "memory", "sla", "combined"])
+    ap.add_argument("--b-static", type=int, default=256)
+    ap.add_argument("--sla-ms", type=float, default=None)
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

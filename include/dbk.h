@@ -111,6 +111,16 @@ dbk_status dbk_pool_usage(dbk_pool *pool, int64_t *used_pages, int64_t *free_pag
  * (-1 = empty) to host memory (synchronous on `stream`). */
 dbk_status dbk_block_table_d2h(dbk_pool *pool, int32_t *host_out, void *stream);
 
+/* Which decode kernel the pool launches and how: decode_path 1 = K1 (CUDA-core
+ * FMA, MHA or GQA fallback), 2 = K2 (tensor-core GQA: TMA tensor tiles + mma);
+ * ctas_per_sm = resident CTAs of that kernel; chunk_pages = pages per work item
+ * of the last decode batch; launches = kernels this pool has launched. */
+typedef struct dbk_pool_info {
+    int32_t decode_path, ctas_per_sm, chunk_pages, work_items;
+    int64_t launches, last_decode_bytes;
+} dbk_pool_info;
+dbk_status dbk_pool_get_info(dbk_pool *pool, dbk_pool_info *out);
+
 /* ------------------------------------------------------------------------ */
 /* Decode step: paged decode attention (+ fused batch statistics)           */
 /* ------------------------------------------------------------------------ */

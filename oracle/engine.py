@@ -39,12 +39,9 @@ M64 = (1 << 64) - 1
 
 
 def fnv1a64(values, h=FNV_OFFSET):
-    """FNV-1a over the little-endian bytes of 64-bit integers (checksum of tables)."""
+    """FNV-1a over 64-bit words, h = (h ^ v) * prime mod 2^64 (checksum of block tables)."""
     for v in values:
-        v &= M64
-        for k in range(8):
-            h ^= (v >> (8 * k)) & 0xFF
-            h = (h * FNV_PRIME) & M64
+        h = ((h ^ (v & M64)) * FNV_PRIME) & M64
     return h
 
 

@@ -98,6 +98,11 @@ class KVPool:
         _lib.dbk_pool_usage(self.h, C.byref(u), C.byref(f))
         return u.value, f.value
 
+    def info(self):
+        o = _lib.dbk_pool_info()
+        _lib.dbk_pool_get_info(self.h, C.byref(o))
+        return {f: getattr(o, f) for f, _ in o._fields_}
+
     def block_table(self, stream=None):
         out = np.zeros((self.cfg.max_requests, self.cfg.max_pages_per_req), np.int32)
         _lib.dbk_block_table_d2h(self.h, out.ctypes.data_as(C.POINTER(C.c_int32)), _stream(stream))

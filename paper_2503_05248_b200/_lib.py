@@ -33,6 +33,11 @@ class dbk_pool_config(C.Structure):
                 ("max_pages_per_req", C.c_int32), ("device", C.c_int32), ("_reserved", C.c_int32)]
 
 
+class dbk_pool_info(C.Structure):
+    _fields_ = [("decode_path", C.c_int32), ("ctas_per_sm", C.c_int32), ("chunk_pages", C.c_int32),
+                ("work_items", C.c_int32), ("launches", C.c_int64), ("last_decode_bytes", C.c_int64)]
+
+
 class dbk_batch(C.Structure):
     _fields_ = [("n", C.c_int32), ("layer", C.c_int32), ("fuse_stats", C.c_int32),
                 ("_reserved", C.c_int32), ("req_ids", C.POINTER(C.c_int64))]
@@ -111,6 +116,7 @@ SIGNATURES = {
     "dbk_request_info": [P, I64, PI32, PI32, PI32, PI32, I32],
     "dbk_pool_usage": [P, PI64, PI64],
     "dbk_block_table_d2h": [P, PI32, P],
+    "dbk_pool_get_info": [P, C.POINTER(dbk_pool_info)],
     "dbk_decode_step": [P, C.POINTER(dbk_batch), P, P, I32, P],
     "dbk_batch_stats": [P, C.POINTER(dbk_stats), P],
     "dbk_synth_fill": [U64, I32, I32, PI64, PI32, I32, I32, I32, I32, I32, P, P],

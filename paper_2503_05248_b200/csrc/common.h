@@ -45,14 +45,9 @@ struct UploadBuffer {
     void release();
 };
 
-// FNV-1a over little-endian int64 values (block-table checksum in step records).
+// FNV-1a over 64-bit words (block-table checksum in step records): h = (h ^ v) * prime.
 inline uint64_t fnv1a64(uint64_t h, int64_t v) {
-    uint64_t x = static_cast<uint64_t>(v);
-    for (int k = 0; k < 8; ++k) {
-        h ^= (x >> (8 * k)) & 0xFFu;
-        h *= 0x100000001B3ULL;
-    }
-    return h;
+    return (h ^ static_cast<uint64_t>(v)) * 0x100000001B3ULL;
 }
 constexpr uint64_t kFnvOffset = 0xCBF29CE484222325ULL;
 

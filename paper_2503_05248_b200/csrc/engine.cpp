@@ -196,16 +196,14 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
                                   nullptr, nullptr, e->cfg.synth_seed, s));
 
     // S1/S2: page growth for this step's decode token; LIFO preemption on overflow (R18)
-    for (;;) {
-        int64_t need = 0;
-        for (int32_t r : e->running) {
-            int32_t ctx;
-            dbk_request_info(p, e->ids[r], &ctx, nullptr, nullptr, nullptr, 0);
-            if (ctx % P == 0) ++need;
-        }
-        if (need <= p->pages.free_count) break;
+    // a running request holds ctx = l_in + generated tokens; it needs a page iff ctx % P == 0
+    int64_t need = 0;
+    for (int32_t r : e->running)
+        if ((static_cast<int64_t>(e->l_in[r]) + e->gen[r]) % P == 0) ++need;
+    while (need > p->pages.free_count) {
         const int32_t victim = e->running.back();
         e->running.pop_back();
+        if ((static_cast<int64_t>(e->l_in[victim]) + e->gen[victim]) % P == 0) --need;
         const int64_t vid = e->ids[victim];
         DBK_TRY(dbk_release(p, 1, &vid));
         e->queue.push_front(victim);

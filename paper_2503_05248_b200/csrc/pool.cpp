@@ -393,6 +393,17 @@ dbk_status dbk_pool_usage(dbk_pool *p, int64_t *used, int64_t *free_pages) {
     return DBK_OK;
 }
 
+dbk_status dbk_pool_get_info(dbk_pool *p, dbk_pool_info *o) {
+    if (!p || !o) return fail(DBK_EINVAL, "pool_get_info: null argument");
+    o->decode_path = p->has_tmap ? 2 : 1;
+    o->ctas_per_sm = p->ctas_per_sm;
+    o->chunk_pages = p->meta_chunk_pages;
+    o->work_items = p->meta_items;
+    o->launches = p->n_launches;
+    o->last_decode_bytes = p->last_decode_bytes;
+    return DBK_OK;
+}
+
 dbk_status dbk_block_table_d2h(dbk_pool *p, int32_t *host_out, void *stream) {
     if (!p || !host_out) return fail(DBK_EINVAL, "block_table_d2h: null argument");
     DBK_CUDA(cudaSetDevice(p->cfg.device));

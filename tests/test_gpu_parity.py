@@ -103,8 +103,13 @@ def run_decode_case(dbk, L, Hq, Hkv, d, dtype, ctx_list, seed=7, explicit_kv=Fal
         want = oatt.paged_decode_attention(ctx, bt, pk, pv, qq, dtype, nthreads=8)
         got = out.float().cpu().numpy().astype(np.float64)
         results.append((got, want))
+    LAST_INFO.clear()
+    LAST_INFO.update(pool.info())
     pool.close()
     return results
+
+
+LAST_INFO = {}
 
 
 def test_device_generator_matches_host_generator(dbk):
@@ -282,6 +287,7 @@ def test_gqa_paths_parity(dbk, monkeypatch, dtype, Hq, Hkv, d, path):
     ctx = [1, 5, 16, 17, 100, 255, 256, 257, 1024, 3000]
     for got, want in run_decode_case(dbk, 2, Hq, Hkv, d, dtype, ctx, q_scale_log2=(4 if Hq == 16 else 0)):
         assert row_err(got, want) <= TOL
+    assert LAST_INFO["decode_path"] == (2 if path == "tensor" else 1)
 
 
 def test_nccl_single_rank_allgather(dbk):
