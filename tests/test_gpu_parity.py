@@ -317,9 +317,10 @@ def test_bench_config_sampled_parity(dbk):
     eng = S["eng"]
     bufs = eng.buffers(S["qd"], S["od"])
     stream = torch.cuda.current_stream()
-    for _ in range(40):
-        rec = eng.step(bufs, stream)
+    recs = [eng.step(bufs, stream) for _ in range(40)]
+    rec = recs[-1]
     torch.cuda.synchronize()
+    _replay_full_size(S, recs)
     c = S["c"]
     L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
     ids, ctx = eng.last_batch()
@@ -337,4 +338,40 @@ def test_bench_config_sampled_parity(dbk):
         want = oatt.paged_decode_attention(ctx[sel], bt, pk, pv, qq, "f16", nthreads=8)
         got = S["od"][lay, torch.as_tensor(sel, device="cuda")].cpu().numpy().astype(np.float64)
         assert row_err(got, want) <= TOL
+    S["pool"].close()
+
+
+def _replay_full_size(S, recs):
+    """Oracle replay (O7) of a full-size GPU engine run from its logged step times: every
+    scheduling decision, admission/preemption count, token count, page count and block-table
+    checksum must agree bit for bit."""
+    import bench
+    c, tr, P = S["c"], S["tr"], S["c"]["page_size"]
+    kw = bench.sched_kwargs(c, S["beta"], S.get("policy"), 256, S.get("sla_ms"))
+    rp = oeng.Replay([oeng.RankEngine(list(range(len(tr))), tr.arrival_ns, tr.l_in, tr.l_out, S["cap_pages"], P)],
+                     opol.SchedConfig(**kw), S["mem_cap_total"])
+    for g in recs:
+        o = rp.step(g["step_ns"])
+        for k in ("t", "clock_ns", "b_t", "b_next", "n_admitted", "n_preempted", "n_decode", "n_finished",
+                  "sum_ctx", "used_pages", "rationale"):
+            assert g[k] == o[k], (k, g[k], o[k], g["t"])
+        assert (g["table_hash"] & ((1 << 64) - 1)) == o["table_hash"]
+
+
+def test_sla_binding_full_size_replay(dbk):
+    """13B shape, combined policy with a binding SLA (D below the memory-bound step time):
+    the device-timed step latencies drive Alg. 2 and the oracle replays the decisions."""
+    import bench
+    S = bench.setup_engine(device=0, cfg_name="llama2-13b-sla", time_attention=False, out_dtype=0,
+                           n_req=800, sla_ms=6.0)
+    S["policy"], S["sla_ms"] = None, 6.0
+    eng = S["eng"]
+    bufs = eng.buffers(S["qd"], S["od"])
+    stream = torch.cuda.current_stream()
+    recs = [eng.step(bufs, stream) for _ in range(120)]
+    _replay_full_size(S, recs)
+    assert any(r["rationale"] == opol.R_SLA for r in recs)       # the SLA search bound the batch
+    tail = [r for r in recs[-40:]]
+    mean_ms = np.mean([r["step_ns"] for r in tail]) / 1e6
+    assert mean_ms < 6.0 + 2.0 + 1.0                             # settles near D_SLA + eps_D
     S["pool"].close()
