@@ -1,17 +1,17 @@
 // K2: paged decode attention for grouped-query attention on the tensor cores (sm_100a).
 //
-// With GQA the GQ = q_heads/kv_heads query heads of a group share each K/V page, so
-// the page is a real dense contraction: S = Q_g K^T (GQ x 16 tokens x d) and
-// O_g += P V (GQ x d x 16 tokens) -- 8 flop/B at GQ = 8, more than the CUDA cores can
-// retire at HBM speed (SURVEY.md §7 "GQA is ALU-bound on CUDA cores").  Each page tile
-// is fetched by 2-D TMA (cp.async.bulk.tensor) through a pool-wide tensor map with the
-// 128-byte swizzle, so the ldmatrix fragment loads are bank-conflict free.  The tile is
-// consumed by warp-level mma.sync.m16n8k16 (rows = q-heads of the group, padded to 16;
-// fp32 accumulate).  The S accumulator fragment is re-used in registers as the A
-// operand of P V (no shared-memory round trip).  bf16 KV keeps P to ~16 bits by
-// splitting it into bf16 hi + lo parts (two MMAs), fp16 KV uses fp16 P (11 bits) -- both
-// well inside the 2e-3 bar (R23).  Work decomposition, online softmax in log2
-// units, the fused statistics and the split-K merge are the same as K1.
+// With GQA the GQ = q_heads/kv_heads query heads of a group share each K/V page, so the
+// page is a real dense contraction: S = Q_g K^T (GQ x 16 tokens x d) and O_g += P V
+// (GQ x d x 16 tokens) -- 8 flop/B at GQ = 8, more than the CUDA cores retire at HBM speed
+// (SURVEY.md §7 "GQA is ALU-bound on CUDA cores").  Each page tile is fetched by 2-D TMA
+// (cp.async.bulk.tensor) through a pool-wide tensor map with the 128-byte swizzle, so the
+// ldmatrix fragment loads are bank-conflict free, and consumed by warp-level
+// mma.sync.m16n8k16 (rows = the group's q-heads, padded to 16; fp32 accumulate).  The S
+// accumulator fragment is re-used in registers as the A operand of P V.  bf16 KV keeps P
+// to ~16 bits by splitting it into bf16 hi + lo parts (two MMAs); fp16 KV uses fp16 P
+// (11 bits) -- both well inside the 2e-3 bar (R23).  Work decomposition
+// (persistent warps, one task = (request chunk, kv head) per warp, rings that stream across
+// task boundaries), the fused statistics and the split-K merge are the same as K1.
 #include <type_traits>
 
 #include "device_common.cuh"
@@ -71,26 +71,14 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
 
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[WARPS][STAGES];
-    __shared__ int s_last;
     // 128B swizzle atoms need 1024-byte aligned destinations
     const uint32_t raw_off = smem_u32(smem_raw);
     uint8_t *smem = smem_raw + ((1024u - (raw_off & 1023u)) & 1023u);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gq = lane >> 2, cq = lane & 3;  // mma fragment row (q-head) / column pair
-    const int2 item = p.work[blockIdx.x];
-    const int i = item.x, c = item.y;
-    const int g = blockIdx.y;
-    const ReqMeta rm = p.req[i];
-    const int npages = (rm.ctx + kP - 1) / kP;
-    const int pg0 = c * p.chunk_pages;
-    const int pg1 = min(pg0 + p.chunk_pages, npages);
-    const int span = pg1 - pg0;
-    const int my_n = span > warp ? (span - warp + WARPS - 1) / WARPS : 0;
-
+    const int gq = lane >> 2, cq = lane & 3;   // mma fragment row (q-head) / column pair
+    const int mtx = lane >> 3, mr = lane & 7;  // ldmatrix: this lane addresses row mr of matrix mtx
     uint8_t *wbuf = smem + warp * STAGES * STAGE;
-    const int32_t *bt_row = p.block_table + static_cast<size_t>(rm.slot) * p.bt_stride;
-    const int phys_lane = lane < my_n ? __ldg(bt_row + pg0 + warp + lane * WARPS) : 0;
     const uint64_t pol = evict_first_policy();
     // row of the pool-wide tensor map: [layer][page][kv_head][K|V][16 tokens] x D elements
     const int64_t row_layer = static_cast<int64_t>(p.layer) * p.cap_pages;
@@ -101,163 +89,193 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
         fence_mbar_init();
     }
     __syncwarp();
-    auto issue = [&](int s, int ph) {
-        mbar_expect_tx(&bars[warp][s], STAGE);
-        const int row = static_cast<int>(((row_layer + ph) * p.kv_heads + g) * 32);
+    int f0 = task_fetch(p, lane), f1 = task_fetch(p, lane);
+    f0 = __shfl_sync(kFull, f0, 0);
+    f1 = __shfl_sync(kFull, f1, 0);
+    Task cur = load_task(p, f0, lane), nxt = load_task(p, f1, lane);
+    uint32_t seq_iss = 0, cur_start = 0;
+    auto top_up = [&](uint32_t seq_cons) {
+        while (seq_iss < seq_cons + STAGES) {
+            const int j = static_cast<int>(seq_iss - cur_start);
+            int ph, g;
+            if (j < cur.n) {
+                ph = __shfl_sync(kFull, cur.phys_lane, j);
+                g = cur.g;
+            } else if (j - cur.n < nxt.n) {
+                ph = __shfl_sync(kFull, nxt.phys_lane, j - cur.n);
+                g = nxt.g;
+            } else {
+                break;
+            }
+            if (lane == 0) {
+                const int s = seq_iss % STAGES;
+                fence_proxy_async();
+                mbar_expect_tx(&bars[warp][s], STAGE);
+                const int row = static_cast<int>(((row_layer + ph) * p.kv_heads + g) * 32);
 #pragma unroll
-        for (int kv = 0; kv < 2; ++kv)
+                for (int kv = 0; kv < 2; ++kv)
 #pragma unroll
-            for (int b = 0; b < NBOX; ++b)
-                tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox, &tmap, b * 64, row + kv * 16,
-                            &bars[warp][s], pol);
-    };
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) {
-        const int ph = __shfl_sync(kFull, phys_lane, s);
-        if (lane == 0 && s < my_n) issue(s, ph);
-    }
-
-    if (p.fuse_stats && c == 0 && g == 0 && warp == WARPS - 1) batch_stats_warp(p, rm, lane);
-
-    // Q fragments (A operand): row gq = q-head g*GQ+gq, columns = head dims
-    uint32_t qa[KSTEPS][2];
-    {
-        const T *qrow = reinterpret_cast<const T *>(p.q) + (static_cast<size_t>(i) * p.q_heads + g * GQ + gq) * D;
-#pragma unroll
-        for (int kk = 0; kk < KSTEPS; ++kk) {
-            qa[kk][0] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 2 * cq)) : 0u;
-            qa[kk][1] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 8 + 2 * cq)) : 0u;
+                    for (int b = 0; b < NBOX; ++b)
+                        tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox, &tmap, b * 64, row + kv * 16,
+                                    &bars[warp][s], pol);
+            }
+            ++seq_iss;
         }
-    }
+    };
+    top_up(0);
 
-    float o[NT][4];
+    while (cur.task < p.n_tasks) {
+        int fetched = task_fetch(p, lane);
+        const ReqMeta rm = p.req[cur.i];
+        const int i = cur.i, c = cur.c, g = cur.g;
+        if (p.fuse_stats && c == 0 && g == 0) batch_stats_warp(p, rm, lane);
+
+        // Q fragments (A operand): row gq = q-head g*GQ+gq, columns = head dims
+        uint32_t qa[KSTEPS][2];
+        {
+            const T *qrow = reinterpret_cast<const T *>(p.q) + (static_cast<size_t>(i) * p.q_heads + g * GQ + gq) * D;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    const int mtx = lane >> 3, mr = lane & 7;  // ldmatrix: this lane addresses row mr of matrix mtx
+            for (int kk = 0; kk < KSTEPS; ++kk) {
+                qa[kk][0] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 2 * cq)) : 0u;
+                qa[kk][1] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 8 + 2 * cq)) : 0u;
+            }
+        }
+        float o[NT][4];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+        float m = -INFINITY, l = 0.f;
 
-    for (int k = 0; k < my_n; ++k) {
-        const int s = k % STAGES;
-        mbar_wait(&bars[warp][s], (k / STAGES) & 1);
-        uint8_t *st = wbuf + s * STAGE;
-        const uint32_t kb_base = smem_u32(st), vb_base = smem_u32(st + NBOX * kBox);
-        const int valid = rm.ctx - (pg0 + warp + k * WARPS) * kP;
-        if (valid < kP) {  // last page: never-written V slots may hold NaN; P = 0 there is not enough
-            for (int x = lane; x < (kP - valid) * NBOX * 8; x += 32) {
-                const int row = valid + x / (NBOX * 8), rem = x % (NBOX * 8);
-                *reinterpret_cast<uint4 *>(st + NBOX * kBox + (rem >> 3) * kBox + row * 128 + (rem & 7) * 16) =
-                    make_uint4(0u, 0u, 0u, 0u);
+        for (int k = 0; k < cur.n; ++k) {
+            const uint32_t jseq = cur_start + k;
+            const int s = jseq % STAGES;
+            mbar_wait(&bars[warp][s], (jseq / STAGES) & 1);
+            uint8_t *st = wbuf + s * STAGE;
+            const uint32_t kb_base = smem_u32(st), vb_base = smem_u32(st + NBOX * kBox);
+            const int valid = rm.ctx - (cur.pg0 + k) * kP;
+            if (valid < kP) {  // last page: never-written V slots may hold NaN; P = 0 there is not enough
+                for (int x = lane; x < (kP - valid) * NBOX * 8; x += 32) {
+                    const int row = valid + x / (NBOX * 8), rem = x % (NBOX * 8);
+                    *reinterpret_cast<uint4 *>(st + NBOX * kBox + (rem >> 3) * kBox + row * 128 + (rem & 7) * 16) =
+                        make_uint4(0u, 0u, 0u, 0u);
+                }
+                __syncwarp();
+            }
+            // S = Q K^T for tokens 0-7 (s0) and 8-15 (s1)
+            float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int kk = 0; kk < KSTEPS; ++kk) {
+                const int tok = (mtx >> 1) * 8 + mr, ch = (kk & 3) * 2 + (mtx & 1);
+                uint32_t kb[4];
+                ldsm_x4(kb, kb_base + (kk >> 2) * kBox + tok * 128 + ((ch ^ (tok & 7)) << 4));
+                mma_pad<T>(s0, qa[kk][0], qa[kk][1], kb[0], kb[1]);
+                mma_pad<T>(s1, qa[kk][0], qa[kk][1], kb[2], kb[3]);
+            }
+            // online softmax for q-head gq over this lane's tokens 2cq, 2cq+1, 8+2cq, 9+2cq
+            const int t0 = 2 * cq;
+            float x[4] = {s0[0] * p.scale_log2, s0[1] * p.scale_log2, s1[0] * p.scale_log2, s1[1] * p.scale_log2};
+            if (t0 >= valid) x[0] = -INFINITY;
+            if (t0 + 1 >= valid) x[1] = -INFINITY;
+            if (t0 + 8 >= valid) x[2] = -INFINITY;
+            if (t0 + 9 >= valid) x[3] = -INFINITY;
+            float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 2));
+            const float m_new = fmaxf(m, mx);
+            const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
+            float pr[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pr[j] = (x[j] == -INFINITY) ? 0.f : exp2f(x[j] - m_new);
+            l = l * alpha + (pr[0] + pr[1]) + (pr[2] + pr[3]);
+            m = m_new;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                o[j][0] *= alpha;
+                o[j][1] *= alpha;
+            }
+            // P (A operand, straight from the S fragments) times V
+            const uint32_t pa0 = Elt<T>::from_f2(pr[0], pr[1]), pa2 = Elt<T>::from_f2(pr[2], pr[3]);
+            uint32_t pl0 = 0u, pl2 = 0u;
+            if constexpr (kBF16) {
+                const float2 h0 = Elt<T>::to_f2(pa0), h2 = Elt<T>::to_f2(pa2);
+                pl0 = Elt<T>::from_f2(pr[0] - h0.x, pr[1] - h0.y);
+                pl2 = Elt<T>::from_f2(pr[2] - h2.x, pr[3] - h2.y);
+            }
+#pragma unroll
+            for (int pp = 0; pp < D / 16; ++pp) {
+                const int tok = (mtx & 1) * 8 + mr, ch = (pp & 3) * 2 + (mtx >> 1);
+                uint32_t vb[4];
+                ldsm_x4_t(vb, vb_base + (pp >> 2) * kBox + tok * 128 + ((ch ^ (tok & 7)) << 4));
+                mma_pad<T>(o[2 * pp], pa0, pa2, vb[0], vb[1]);
+                mma_pad<T>(o[2 * pp + 1], pa0, pa2, vb[2], vb[3]);
+                if constexpr (kBF16) {
+                    mma_pad<T>(o[2 * pp], pl0, pl2, vb[0], vb[1]);
+                    mma_pad<T>(o[2 * pp + 1], pl0, pl2, vb[2], vb[3]);
+                }
             }
             __syncwarp();
+            top_up(jseq + 1);
         }
-        // S = Q K^T for tokens 0-7 (s0) and 8-15 (s1)
-        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+
+        // ---- end of task (warp-local): normalise and store, or write the split-K partial
+        l += __shfl_xor_sync(kFull, l, 1);
+        l += __shfl_xor_sync(kFull, l, 2);
+        const bool split = rm.nchunks > 1;
+        if (gq < GQ) {
+            const int h = g * GQ + gq;
+            if (!split) {
+                const float inv = 1.f / l;
+                const size_t base = (static_cast<size_t>(i) * p.q_heads + h) * D + 2 * cq;
 #pragma unroll
-        for (int kk = 0; kk < KSTEPS; ++kk) {
-            const int tok = (mtx >> 1) * 8 + mr, ch = (kk & 3) * 2 + (mtx & 1);
-            uint32_t kb[4];
-            ldsm_x4(kb, kb_base + (kk >> 2) * kBox + tok * 128 + ((ch ^ (tok & 7)) << 4));
-            mma_pad<T>(s0, qa[kk][0], qa[kk][1], kb[0], kb[1]);
-            mma_pad<T>(s1, qa[kk][0], qa[kk][1], kb[2], kb[3]);
-        }
-        // online softmax for q-head gq over this lane's tokens 2cq, 2cq+1, 8+2cq, 9+2cq
-        const int t0 = 2 * cq;
-        float x[4] = {s0[0] * p.scale_log2, s0[1] * p.scale_log2, s1[0] * p.scale_log2, s1[1] * p.scale_log2};
-        if (t0 >= valid) x[0] = -INFINITY;
-        if (t0 + 1 >= valid) x[1] = -INFINITY;
-        if (t0 + 8 >= valid) x[2] = -INFINITY;
-        if (t0 + 9 >= valid) x[3] = -INFINITY;
-        float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 2));
-        const float m_new = fmaxf(m, mx);
-        const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
-        float pr[4];
+                for (int j = 0; j < NT; ++j) {
+                    store_out(p.out, base + 8 * j, p.out_dtype, o[j][0] * inv);
+                    store_out(p.out, base + 8 * j + 1, p.out_dtype, o[j][1] * inv);
+                }
+            } else {
+                const int wi = rm.chunk_base + c;
+                float *w = p.ws_o + (static_cast<size_t>(wi) * p.q_heads + h) * D + 2 * cq;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) pr[j] = (x[j] == -INFINITY) ? 0.f : exp2f(x[j] - m_new);
-        l = l * alpha + (pr[0] + pr[1]) + (pr[2] + pr[3]);
-        m = m_new;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-            o[j][0] *= alpha;
-            o[j][1] *= alpha;
-        }
-        // P (A operand, straight from the S fragments) times V
-        const uint32_t pa0 = Elt<T>::from_f2(pr[0], pr[1]), pa2 = Elt<T>::from_f2(pr[2], pr[3]);
-        uint32_t pl0 = 0u, pl2 = 0u;
-        if constexpr (kBF16) {
-            const float2 h0 = Elt<T>::to_f2(pa0), h2 = Elt<T>::to_f2(pa2);
-            pl0 = Elt<T>::from_f2(pr[0] - h0.x, pr[1] - h0.y);
-            pl2 = Elt<T>::from_f2(pr[2] - h2.x, pr[3] - h2.y);
-        }
-#pragma unroll
-        for (int pp = 0; pp < D / 16; ++pp) {
-            const int tok = (mtx & 1) * 8 + mr, ch = (pp & 3) * 2 + (mtx >> 1);
-            uint32_t vb[4];
-            ldsm_x4_t(vb, vb_base + (pp >> 2) * kBox + tok * 128 + ((ch ^ (tok & 7)) << 4));
-            mma_pad<T>(o[2 * pp], pa0, pa2, vb[0], vb[1]);
-            mma_pad<T>(o[2 * pp + 1], pa0, pa2, vb[2], vb[3]);
-            if constexpr (kBF16) {
-                mma_pad<T>(o[2 * pp], pl0, pl2, vb[0], vb[1]);
-                mma_pad<T>(o[2 * pp + 1], pl0, pl2, vb[2], vb[3]);
+                for (int j = 0; j < NT; ++j) *reinterpret_cast<float2 *>(w + 8 * j) = make_float2(o[j][0], o[j][1]);
+                if (cq == 0) p.ws_ml[static_cast<size_t>(wi) * p.q_heads + h] = make_float2(m, l);
             }
         }
-        __syncwarp();
-        const int ph = __shfl_sync(kFull, phys_lane, (k + STAGES) & 31);
-        if (lane == 0 && k + STAGES < my_n) {
-            fence_proxy_async();
-            issue(s, ph);
-        }
-    }
+        if (split && split_arrive_last(p, i, g, rm.nchunks, lane)) split_merge_warp<GQ, D>(p, rm, i, g, lane);
 
-    l += __shfl_xor_sync(kFull, l, 1);
-    l += __shfl_xor_sync(kFull, l, 2);
-    __syncthreads();
-    float *sm_acc = reinterpret_cast<float *>(smem);  // [WARPS][GQ][D]
-    float *sm_m = sm_acc + WARPS * GQ * D;
-    float *sm_l = sm_m + WARPS * GQ;
-    if (gq < GQ) {
-#pragma unroll
-        for (int j = 0; j < NT; ++j)
-            *reinterpret_cast<float2 *>(sm_acc + (warp * GQ + gq) * D + 8 * j + 2 * cq) = make_float2(o[j][0], o[j][1]);
-        if (cq == 0) {
-            sm_m[warp * GQ + gq] = m;
-            sm_l[warp * GQ + gq] = l;
-        }
+        fetched = __shfl_sync(kFull, fetched, 0);
+        cur_start += cur.n;
+        cur = nxt;
+        nxt = load_task(p, fetched, lane);
+        top_up(cur_start);
     }
-    __syncthreads();
-    merge_and_store<GQ, D, WARPS, WARPS * 32>(p, rm, i, c, g, sm_acc, sm_m, sm_l, &s_last);
+    task_exit(p, lane, static_cast<int>(gridDim.x) * WARPS);
 }
 
 constexpr int kWarps = 4;
 template <int D>
-constexpr int gqa_stages() { return D == 128 ? 3 : 4; }
+constexpr int gqa_stages() { return D == 128 ? 3 : 5; }
 
-template <typename T, int D, int GQ>
-size_t gqa_smem() {
-    const size_t stage = static_cast<size_t>(kWarps) * gqa_stages<D>() * 2 * (D / 64) * kBox;
-    const size_t merge = static_cast<size_t>(kWarps) * GQ * (D + 2) * sizeof(float);
-    return (stage > merge ? stage : merge) + 1024;
+template <typename T, int D>
+constexpr size_t gqa_smem() {
+    return static_cast<size_t>(kWarps) * gqa_stages<D>() * 2 * (D / 64) * kBox + 1024;
 }
 
 template <typename T, int D, int GQ>
-cudaError_t launch_gqa_t(const DecodeParams &p, int kv_heads, const CUtensorMap &tmap, cudaStream_t s) {
+cudaError_t launch_gqa_t(const DecodeParams &p, int ctas, const CUtensorMap &tmap, cudaStream_t s) {
     auto kern = decode_gqa_kernel<T, D, GQ, kWarps, gqa_stages<D>()>;
-    const size_t smem = gqa_smem<T, D, GQ>();
+    constexpr size_t smem = gqa_smem<T, D>();
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    kern<<<dim3(p.n_items, kv_heads), kWarps * 32, smem, s>>>(p, tmap);
+    kern<<<ctas, kWarps * 32, smem, s>>>(p, tmap);
     return cudaGetLastError();
 }
 
 template <typename T, int D, int GQ>
 int gqa_occ_t() {
     auto kern = decode_gqa_kernel<T, D, GQ, kWarps, gqa_stages<D>()>;
-    const size_t smem = gqa_smem<T, D, GQ>();
+    constexpr size_t smem = gqa_smem<T, D>();
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kWarps * 32, smem) != cudaSuccess) n = 1;
@@ -265,11 +283,11 @@ int gqa_occ_t() {
 }
 
 template <typename T, int D>
-cudaError_t gqa_group(const DecodeParams &p, int group, int kv_heads, const CUtensorMap &tmap, cudaStream_t s) {
+cudaError_t gqa_group(const DecodeParams &p, int group, int ctas, const CUtensorMap &tmap, cudaStream_t s) {
     switch (group) {
-        case 2: return launch_gqa_t<T, D, 2>(p, kv_heads, tmap, s);
-        case 4: return launch_gqa_t<T, D, 4>(p, kv_heads, tmap, s);
-        case 8: return launch_gqa_t<T, D, 8>(p, kv_heads, tmap, s);
+        case 2: return launch_gqa_t<T, D, 2>(p, ctas, tmap, s);
+        case 4: return launch_gqa_t<T, D, 4>(p, ctas, tmap, s);
+        case 8: return launch_gqa_t<T, D, 8>(p, ctas, tmap, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -285,14 +303,14 @@ int gqa_occ_group(int group) {
 
 }  // namespace
 
-cudaError_t launch_decode_gqa(const DecodeParams &p, int kv_dtype, int head_dim, int group, int kv_heads,
+cudaError_t launch_decode_gqa(const DecodeParams &p, int kv_dtype, int head_dim, int group, int ctas,
                               const CUtensorMap &tmap, cudaStream_t s) {
     if (kv_dtype == 0) {
-        if (head_dim == 128) return gqa_group<__half, 128>(p, group, kv_heads, tmap, s);
-        if (head_dim == 64) return gqa_group<__half, 64>(p, group, kv_heads, tmap, s);
+        if (head_dim == 128) return gqa_group<__half, 128>(p, group, ctas, tmap, s);
+        if (head_dim == 64) return gqa_group<__half, 64>(p, group, ctas, tmap, s);
     } else {
-        if (head_dim == 128) return gqa_group<__nv_bfloat16, 128>(p, group, kv_heads, tmap, s);
-        if (head_dim == 64) return gqa_group<__nv_bfloat16, 64>(p, group, kv_heads, tmap, s);
+        if (head_dim == 128) return gqa_group<__nv_bfloat16, 128>(p, group, ctas, tmap, s);
+        if (head_dim == 64) return gqa_group<__nv_bfloat16, 64>(p, group, ctas, tmap, s);
     }
     return cudaErrorInvalidValue;
 }

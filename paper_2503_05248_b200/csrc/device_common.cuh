@@ -169,52 +169,78 @@ __device__ __forceinline__ void batch_stats_warp(const DecodeParams &p, const Re
     }
 }
 
-// ------------------------------------------------------------------ CTA epilogue (K1, K2) + K3
-// sm_m/sm_l/sm_acc hold NG online-softmax states (running max in log2 units, denominator,
-// unnormalised numerator) per q-head of the group.  Merge them; a single-chunk request
-// writes out directly, otherwise the partial goes to the split-K workspace and the
-// last-arriving CTA of (request, kv head) merges all chunks (no second launch).
-template <int GQ, int D, int NG, int NT>
-__device__ void merge_and_store(const DecodeParams &p, const ReqMeta &rm, int i, int c, int g,
-                                const float *sm_acc, const float *sm_m, const float *sm_l,
-                                int *s_last) {
-    const int kv_heads = gridDim.y;
-    const bool split = rm.nchunks > 1;
-    const int wi = rm.chunk_base + c;
-    for (int idx = threadIdx.x; idx < GQ * D; idx += NT) {
-        const int t = idx / D, e = idx % D;
-        float M = -INFINITY;
-#pragma unroll
-        for (int x = 0; x < NG; ++x) M = fmaxf(M, sm_m[x * GQ + t]);
-        float L = 0.f, O = 0.f;
-#pragma unroll
-        for (int x = 0; x < NG; ++x) {
-            const float mx = sm_m[x * GQ + t];
-            if (mx != -INFINITY) {
-                const float f = exp2f(mx - M);
-                L += f * sm_l[x * GQ + t];
-                O += f * sm_acc[(x * GQ + t) * D + e];
-            }
-        }
-        const int h = g * GQ + t;
-        if (!split) {
-            store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
-        } else {
-            p.ws_o[(static_cast<size_t>(wi) * p.q_heads + h) * D + e] = O;
-            if (e == 0) p.ws_ml[static_cast<size_t>(wi) * p.q_heads + h] = make_float2(M, L);
+// ------------------------------------------------------------------ persistent warp tasks
+// A task is (work item, kv head) = up to 32 pages of one request for one kv head, served
+// by ONE warp from start to end (no CTA-wide barriers anywhere).  Tasks are handed out by
+// an atomic counter in the order of the work list (the host sorts it longest-first).  A
+// warp streams the concatenation of its current and next task's pages through its ring,
+// so the DRAM stream does not pause at task boundaries (epilogue, q load, metadata).
+struct Task {
+    int task;        // >= n_tasks: no task
+    int i, c, g;     // batch index, chunk, kv head
+    int pg0, n;      // first page of the chunk and its page count (<= 32)
+    int phys_lane;   // physical page of the chunk's k-th page, held by lane k
+};
+
+__device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int lane) {
+    Task t;
+    t.task = task;
+    t.n = 0;
+    t.phys_lane = 0;
+    t.i = t.c = t.g = t.pg0 = 0;
+    if (task >= p.n_tasks) {
+        t.task = p.n_tasks;
+        return t;
+    }
+    const int item = task / p.kv_heads;
+    t.g = task - item * p.kv_heads;
+    const int2 w = __ldg(p.work + item);
+    t.i = w.x;
+    t.c = w.y;
+    const ReqMeta rm = p.req[t.i];
+    const int npages = (rm.ctx + kP - 1) / kP;
+    t.pg0 = t.c * p.chunk_pages;
+    t.n = min(t.pg0 + p.chunk_pages, npages) - t.pg0;
+    const int32_t *row = p.block_table + static_cast<size_t>(rm.slot) * p.bt_stride;
+    t.phys_lane = lane < t.n ? __ldg(row + t.pg0 + lane) : 0;
+    return t;
+}
+
+// lane 0 takes the next task index (the caller broadcasts it when it needs it, so the
+// atomic's latency hides behind the current task)
+__device__ __forceinline__ int task_fetch(const DecodeParams &p, int lane) {
+    return lane == 0 ? atomicAdd(p.task_counter, 1) : 0;
+}
+
+// A warp with no task left: the last one resets the counters for the next launch.
+__device__ __forceinline__ void task_exit(const DecodeParams &p, int lane, int total_warps) {
+    if (lane == 0) {
+        __threadfence();
+        const int e = atomicAdd(p.task_counter + 1, 1);
+        if (e == total_warps - 1) {
+            p.task_counter[0] = 0;
+            p.task_counter[1] = 0;
         }
     }
-    if (!split) return;
+}
+
+// Split-K bookkeeping after a warp wrote its chunk's partial: returns true in every lane
+// of the warp whose chunk arrived last for (request, kv head); that warp merges.
+__device__ __forceinline__ bool split_arrive_last(const DecodeParams &p, int i, int g, int nchunks, int lane) {
     __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int prev = atomicAdd(p.counters + i * kv_heads + g, 1);
-        *s_last = (prev == rm.nchunks - 1);
-    }
-    __syncthreads();
-    if (!*s_last) return;
-    __threadfence();
-    for (int idx = threadIdx.x; idx < GQ * D; idx += NT) {
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(p.counters + i * p.kv_heads + g, 1) == nchunks - 1;
+    last = __shfl_sync(kFull, last, 0);
+    if (last) __threadfence();
+    return last != 0;
+}
+
+// The last warp merges the chunks' (m, l, O) of q-heads g*GQ .. g*GQ+GQ-1 and writes out.
+template <int GQ, int D>
+__device__ __forceinline__ void split_merge_warp(const DecodeParams &p, const ReqMeta &rm, int i, int g,
+                                                 int lane) {
+    for (int idx = lane; idx < GQ * D; idx += 32) {
         const int t = idx / D, e = idx % D;
         const int h = g * GQ + t;
         float M = -INFINITY;
@@ -224,13 +250,28 @@ __device__ void merge_and_store(const DecodeParams &p, const ReqMeta &rm, int i,
         for (int x = 0; x < rm.nchunks; ++x) {
             const size_t w = static_cast<size_t>(rm.chunk_base + x);
             const float2 ml = __ldcg(&p.ws_ml[w * p.q_heads + h]);
-            const float f = exp2f(ml.x - M);
-            L += f * ml.y;
-            O += f * __ldcg(&p.ws_o[(w * p.q_heads + h) * D + e]);
+            if (ml.x != -INFINITY) {
+                const float f = exp2f(ml.x - M);
+                L += f * ml.y;
+                O += f * __ldcg(&p.ws_o[(w * p.q_heads + h) * D + e]);
+            }
         }
         store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
     }
-    if (threadIdx.x == 0) p.counters[i * kv_heads + g] = 0;
+    if (lane == 0) p.counters[i * p.kv_heads + g] = 0;
+}
+
+// 8 consecutive outputs (fp32 / fp16 / bf16) from registers.
+__device__ __forceinline__ void store8_out(void *out, size_t elem, int dtype, const float f[8]) {
+    if (dtype == 2) {
+        float4 *o = reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + elem);
+        o[0] = make_float4(f[0], f[1], f[2], f[3]);
+        o[1] = make_float4(f[4], f[5], f[6], f[7]);
+    } else if (dtype == 0) {
+        *reinterpret_cast<uint4 *>(reinterpret_cast<__half *>(out) + elem) = pack8<__half>(f);
+    } else {
+        *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(out) + elem) = pack8<__nv_bfloat16>(f);
+    }
 }
 
 }  // namespace dev

@@ -48,11 +48,21 @@ struct dbk_engine {
     std::vector<int64_t> layer_bytes;
     dbk_comm *comm = nullptr;
     int32_t comm_mode = DBK_MODE_DP;
+    // end-to-end mode: host<->device copies on their own streams, ordered by events
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_kv = nullptr, ev_d2h = nullptr;
+    std::vector<cudaEvent_t> ev_q, ev_o;
     ~dbk_engine() {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (auto e : att0) cudaEventDestroy(e);
         for (auto e : att1) cudaEventDestroy(e);
+        for (auto e : ev_q) cudaEventDestroy(e);
+        for (auto e : ev_o) cudaEventDestroy(e);
+        if (ev_kv) cudaEventDestroy(ev_kv);
+        if (ev_d2h) cudaEventDestroy(ev_d2h);
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
     }
 };
 
@@ -69,6 +79,22 @@ void release_arrivals(dbk_engine *e) {
 }
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+dbk_status ensure_copy_streams(dbk_engine *e) {
+    if (e->h2d) return DBK_OK;
+    const int L = e->pool->cfg.layers;
+    DBK_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
+    DBK_CUDA(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
+    DBK_CUDA(cudaEventCreateWithFlags(&e->ev_kv, cudaEventDisableTiming));
+    DBK_CUDA(cudaEventCreateWithFlags(&e->ev_d2h, cudaEventDisableTiming));
+    e->ev_q.assign(L, nullptr);
+    e->ev_o.assign(L, nullptr);
+    for (int l = 0; l < L; ++l) {
+        DBK_CUDA(cudaEventCreateWithFlags(&e->ev_q[l], cudaEventDisableTiming));
+        DBK_CUDA(cudaEventCreateWithFlags(&e->ev_o[l], cudaEventDisableTiming));
+    }
+    return DBK_OK;
+}
 
 }  // namespace
 
@@ -220,19 +246,26 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     const size_t orow = static_cast<size_t>(pc.q_heads) * pc.head_dim * (e->cfg.out_dtype == 2 ? 4 : 2);
     if (n > 0) {
         if (e2e) {
-            // end-to-end: this step's new K/V rows and q come from pinned host memory
+            // end-to-end: this step's new K/V rows and every layer's q come from pinned host
+            // memory on a copy stream (inside the timed region: it waits on ev0); layer l's
+            // attention waits only for q[l], so the PCIe transfers overlap the attention
+            DBK_TRY(ensure_copy_streams(e));
             uint8_t *kd = static_cast<uint8_t *>(bufs->kv_dev);
             uint8_t *vd = kd + static_cast<size_t>(pc.max_requests) * kvrow;
-            DBK_CUDA(cudaMemcpyAsync(kd, bufs->host_k, n * kvrow, cudaMemcpyHostToDevice, s));
-            DBK_CUDA(cudaMemcpyAsync(vd, bufs->host_v, n * kvrow, cudaMemcpyHostToDevice, s));
+            DBK_CUDA(cudaStreamWaitEvent(e->h2d, e->ev0, 0));
+            DBK_CUDA(cudaMemcpyAsync(kd, bufs->host_k, n * kvrow, cudaMemcpyHostToDevice, e->h2d));
+            DBK_CUDA(cudaMemcpyAsync(vd, bufs->host_v, n * kvrow, cudaMemcpyHostToDevice, e->h2d));
+            DBK_CUDA(cudaEventRecord(e->ev_kv, e->h2d));
             e->step_h2d += 2 * static_cast<int64_t>(n * kvrow);
-            DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), kd, vd, 0, s));
             for (int l = 0; l < pc.layers; ++l) {
                 uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
                 const uint8_t *qh = static_cast<const uint8_t *>(bufs->host_q) + static_cast<size_t>(l) * n * qrow;
-                DBK_CUDA(cudaMemcpyAsync(qd, qh, n * qrow, cudaMemcpyHostToDevice, s));
+                DBK_CUDA(cudaMemcpyAsync(qd, qh, n * qrow, cudaMemcpyHostToDevice, e->h2d));
+                DBK_CUDA(cudaEventRecord(e->ev_q[l], e->h2d));
             }
             e->step_h2d += static_cast<int64_t>(pc.layers) * n * qrow;
+            DBK_CUDA(cudaStreamWaitEvent(s, e->ev_kv, 0));
+            DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), kd, vd, 0, s));
         } else {
             DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), nullptr, nullptr, e->cfg.synth_seed, s));
         }
@@ -265,18 +298,22 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         uint8_t *od = static_cast<uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;
         bt.layer = l;
         bt.fuse_stats = l == 0 ? 1 : 0;
+        if (e2e && n > 0) DBK_CUDA(cudaStreamWaitEvent(s, e->ev_q[l], 0));
         if (e->cfg.time_attention && n > 0) DBK_CUDA(cudaEventRecord(e->att0[l], s));
         DBK_TRY(dbk_decode_step(p, &bt, qd, od, e->cfg.out_dtype, s));
         if (e->cfg.time_attention && n > 0) DBK_CUDA(cudaEventRecord(e->att1[l], s));
         e->layer_bytes[l] = p->last_decode_bytes;
-    }
-    if (e2e && n > 0 && bufs->host_out) {
-        for (int l = 0; l < pc.layers; ++l) {
-            const uint8_t *od = static_cast<const uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;
+        if (e2e && n > 0 && bufs->host_out) {  // layer l's output goes back while l+1 computes
+            DBK_CUDA(cudaEventRecord(e->ev_o[l], s));
+            DBK_CUDA(cudaStreamWaitEvent(e->d2h, e->ev_o[l], 0));
             uint8_t *oh = static_cast<uint8_t *>(bufs->host_out) + static_cast<size_t>(l) * n * orow;
-            DBK_CUDA(cudaMemcpyAsync(oh, od, n * orow, cudaMemcpyDeviceToHost, s));
+            DBK_CUDA(cudaMemcpyAsync(oh, od, n * orow, cudaMemcpyDeviceToHost, e->d2h));
         }
-        e->step_d2h += static_cast<int64_t>(pc.layers) * n * orow;
+    }
+    if (e2e && n > 0) {
+        if (bufs->host_out) e->step_d2h += static_cast<int64_t>(pc.layers) * n * orow;
+        DBK_CUDA(cudaEventRecord(e->ev_d2h, e->d2h));
+        DBK_CUDA(cudaStreamWaitEvent(s, e->ev_d2h, 0));  // the step ends after the last copy
     }
     DBK_CUDA(cudaEventRecord(e->ev1, s));
     // S5: statistics record (synchronises the stream) and device-timed step latency

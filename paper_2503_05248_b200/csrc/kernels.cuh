@@ -46,6 +46,10 @@ struct DecodeParams {
     // K2 (tensor-core GQA) addressing through the pool-wide 2-D tensor map
     int32_t layer;
     int32_t kv_heads;
+    // persistent CTAs: tasks t = work_item * kv_heads + kv_head handed out by an atomic
+    // counter; task_counter[0] = next task, [1] = exited CTAs (both reset by the last CTA)
+    int32_t n_tasks;
+    int32_t *task_counter;
 };
 
 struct AppendJob {
@@ -72,10 +76,11 @@ struct BtDelta {
 
 // launchers (return cudaGetLastError() of the launch)
 // tmap != nullptr and group >= 2 selects K2 (tensor cores); otherwise K1 (CUDA cores).
+// Persistent launch of min(ctas, p.n_tasks) CTAs (ctas = SMs x resident CTAs per SM).
 cudaError_t launch_decode(const DecodeParams &p, int kv_dtype, int head_dim, int group,
-                          int kv_heads, const CUtensorMap *tmap, cudaStream_t s);
+                          int ctas, const CUtensorMap *tmap, cudaStream_t s);
 cudaError_t launch_decode_gqa(const DecodeParams &p, int kv_dtype, int head_dim, int group,
-                              int kv_heads, const CUtensorMap &tmap, cudaStream_t s);
+                              int ctas, const CUtensorMap &tmap, cudaStream_t s);
 int decode_gqa_ctas_per_sm(int kv_dtype, int head_dim, int group);
 cudaError_t launch_append(const AppendParams &p, int kv_dtype, int head_dim, cudaStream_t s);
 cudaError_t launch_bt_apply(int32_t *bt, int32_t stride, const BtDelta *d, int32_t n,

@@ -180,6 +180,7 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
         cudaDeviceSynchronize() != cudaSuccess)
         return cleanup(fail(DBK_ECUDA, "pool_create: %s", cudaGetErrorString(cudaGetLastError())));
     p->d_stats_done = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(p->d_stats) + 128);
+    p->d_task_counter = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(p->d_stats) + 160);
     p->host_bt.assign(bt_n, -1);
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -442,12 +443,12 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
         m.l_out = r.l_out;
         total_pages += (r.ctx + P - 1) / P;
     }
-    // chunk size: aim for >= 4 waves of CTAs over the chip, chunks of 4..64 pages (multiple of 4 warps)
-    const int64_t target = static_cast<int64_t>(p->num_sms) * p->ctas_per_sm * 4;
-    int64_t cp = (total_pages * p->cfg.kv_heads + target - 1) / target;
-    cp = (cp + 3) / 4 * 4;
+    // chunk size (pages per warp task, <= 32): at least ~4 tasks per resident warp, so the
+    // dynamic task queue balances; otherwise as large as possible (fewer split-K merges)
+    const int64_t warps = static_cast<int64_t>(p->num_sms) * p->ctas_per_sm * 4;
+    int64_t cp = (total_pages * p->cfg.kv_heads + 4 * warps - 1) / (4 * warps);
     cp = std::max<int64_t>(4, std::min<int64_t>(p->max_chunk_pages, cp));
-    if (p->force_chunk_pages > 0) cp = p->force_chunk_pages;
+    if (p->force_chunk_pages > 0) cp = std::min<int64_t>(p->force_chunk_pages, p->max_chunk_pages);
     p->meta_work.clear();
     int32_t base = 0;
     for (int i = 0; i < n; ++i) {
@@ -459,6 +460,12 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
         for (int32_t c = 0; c < nc; ++c) p->meta_work.push_back(make_int2(i, c));
         base += nc;
     }
+    // longest task first: the dynamic queue then ends on short tasks (small tail)
+    std::stable_sort(p->meta_work.begin(), p->meta_work.end(), [&](const int2 &a, const int2 &b) {
+        const int64_t pa = std::min<int64_t>(cp, (p->meta_req[a.x].ctx + P - 1) / P - a.y * cp);
+        const int64_t pb = std::min<int64_t>(cp, (p->meta_req[b.x].ctx + P - 1) / P - b.y * cp);
+        return pa > pb;
+    });
     p->meta_items = base;
     p->meta_chunk_pages = static_cast<int32_t>(cp);
     const size_t rb = sizeof(ReqMeta) * static_cast<size_t>(n);
@@ -544,8 +551,12 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     dp.cap_pages = p->cfg.cap_pages;
     dp.layer = b->layer;
     dp.kv_heads = p->cfg.kv_heads;
-    DBK_CUDA(launch_decode(dp, p->cfg.kv_dtype, p->cfg.head_dim, p->cfg.q_heads / p->cfg.kv_heads,
-                           p->cfg.kv_heads, p->has_tmap ? &p->tmap : nullptr, s));
+    dp.n_tasks = p->meta_items * p->cfg.kv_heads;
+    dp.task_counter = p->d_task_counter;
+    // persistent grid: every resident CTA slot (4 warps each), or fewer for small batches
+    const int ctas = std::max(1, std::min(p->num_sms * p->ctas_per_sm, (dp.n_tasks + 3) / 4));
+    DBK_CUDA(launch_decode(dp, p->cfg.kv_dtype, p->cfg.head_dim, p->cfg.q_heads / p->cfg.kv_heads, ctas,
+                           p->has_tmap ? &p->tmap : nullptr, s));
     ++p->n_launches;
     p->last_decode_bytes = decode_bytes(p, out_dtype);
     return DBK_OK;
