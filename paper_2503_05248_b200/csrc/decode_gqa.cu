@@ -89,7 +89,7 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
         fence_mbar_init();
     }
     __syncwarp();
-    int f0 = task_fetch(p, lane), f1 = task_fetch(p, lane);
+    int f0 = task_fetch(p, lane), f1 = task_fetch(p, lane), pend = task_fetch(p, lane);
     f0 = __shfl_sync(kFull, f0, 0);
     f1 = __shfl_sync(kFull, f1, 0);
     Task cur = load_task(p, f0, lane), nxt = load_task(p, f1, lane);
@@ -98,11 +98,11 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
         while (seq_iss < seq_cons + STAGES) {
             const int j = static_cast<int>(seq_iss - cur_start);
             int ph, g;
-            if (j < cur.n) {
+            if (j < cur.it.n) {
                 ph = __shfl_sync(kFull, cur.phys_lane, j);
                 g = cur.g;
-            } else if (j - cur.n < nxt.n) {
-                ph = __shfl_sync(kFull, nxt.phys_lane, j - cur.n);
+            } else if (j - cur.it.n < nxt.it.n) {
+                ph = __shfl_sync(kFull, nxt.phys_lane, j - cur.it.n);
                 g = nxt.g;
             } else {
                 break;
@@ -123,35 +123,38 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
         }
     };
     top_up(0);
+    // Q fragments (A operand): row gq = q-head g*GQ+gq, columns = head dims
+    auto load_q = [&](const Task &t, uint32_t (&qa)[KSTEPS][2]) {
+        const T *qrow = reinterpret_cast<const T *>(p.q) + (static_cast<size_t>(t.it.i) * p.q_heads + t.g * GQ + gq) * D;
+#pragma unroll
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+            qa[kk][0] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 2 * cq)) : 0u;
+            qa[kk][1] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 8 + 2 * cq)) : 0u;
+        }
+    };
+    uint32_t qa[KSTEPS][2];
+    load_q(cur, qa);
 
     while (cur.task < p.n_tasks) {
-        int fetched = task_fetch(p, lane);
-        const ReqMeta rm = p.req[cur.i];
-        const int i = cur.i, c = cur.c, g = cur.g;
-        if (p.fuse_stats && c == 0 && g == 0) batch_stats_warp(p, rm, lane);
-
-        // Q fragments (A operand): row gq = q-head g*GQ+gq, columns = head dims
-        uint32_t qa[KSTEPS][2];
-        {
-            const T *qrow = reinterpret_cast<const T *>(p.q) + (static_cast<size_t>(i) * p.q_heads + g * GQ + gq) * D;
-#pragma unroll
-            for (int kk = 0; kk < KSTEPS; ++kk) {
-                qa[kk][0] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 2 * cq)) : 0u;
-                qa[kk][1] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 8 + 2 * cq)) : 0u;
-            }
-        }
+        // one task ahead: the metadata of the task after `nxt` and the q of `nxt`
+        const Task nnx = load_task(p, __shfl_sync(kFull, pend, 0), lane);
+        pend = task_fetch(p, lane);
+        uint32_t qn[KSTEPS][2];
+        load_q(nxt, qn);
+        const int i = cur.it.i, c = cur.it.c, g = cur.g;
+        if (p.fuse_stats && c == 0 && g == 0) batch_stats_warp(p, p.req[i], lane);
         float o[NT][4];
 #pragma unroll
         for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
         float m = -INFINITY, l = 0.f;
 
-        for (int k = 0; k < cur.n; ++k) {
+        for (int k = 0; k < cur.it.n; ++k) {
             const uint32_t jseq = cur_start + k;
             const int s = jseq % STAGES;
             mbar_wait(&bars[warp][s], (jseq / STAGES) & 1);
             uint8_t *st = wbuf + s * STAGE;
             const uint32_t kb_base = smem_u32(st), vb_base = smem_u32(st + NBOX * kBox);
-            const int valid = rm.ctx - (cur.pg0 + k) * kP;
+            const int valid = cur.it.ctx - (cur.it.pg0 + k) * kP;
             if (valid < kP) {  // last page: never-written V slots may hold NaN; P = 0 there is not enough
                 for (int x = lane; x < (kP - valid) * NBOX * 8; x += 32) {
                     const int row = valid + x / (NBOX * 8), rem = x % (NBOX * 8);
@@ -219,7 +222,7 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
         // ---- end of task (warp-local): normalise and store, or write the split-K partial
         l += __shfl_xor_sync(kFull, l, 1);
         l += __shfl_xor_sync(kFull, l, 2);
-        const bool split = rm.nchunks > 1;
+        const bool split = cur.it.nchunks > 1;
         if (gq < GQ) {
             const int h = g * GQ + gq;
             if (!split) {
@@ -231,19 +234,24 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
                     store_out(p.out, base + 8 * j + 1, p.out_dtype, o[j][1] * inv);
                 }
             } else {
-                const int wi = rm.chunk_base + c;
+                const int wi = cur.it.chunk_base + c;
                 float *w = p.ws_o + (static_cast<size_t>(wi) * p.q_heads + h) * D + 2 * cq;
 #pragma unroll
                 for (int j = 0; j < NT; ++j) *reinterpret_cast<float2 *>(w + 8 * j) = make_float2(o[j][0], o[j][1]);
                 if (cq == 0) p.ws_ml[static_cast<size_t>(wi) * p.q_heads + h] = make_float2(m, l);
             }
         }
-        if (split && split_arrive_last(p, i, g, rm.nchunks, lane)) split_merge_warp<GQ, D>(p, rm, i, g, lane);
+        if (split && split_arrive_last(p, i, g, cur.it.nchunks, lane))
+            split_merge_warp<GQ, D>(p, cur.it.chunk_base, cur.it.nchunks, i, g, lane);
 
-        fetched = __shfl_sync(kFull, fetched, 0);
-        cur_start += cur.n;
+        cur_start += cur.it.n;
         cur = nxt;
-        nxt = load_task(p, fetched, lane);
+        nxt = nnx;
+#pragma unroll
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+            qa[kk][0] = qn[kk][0];
+            qa[kk][1] = qn[kk][1];
+        }
         top_up(cur_start);
     }
     task_exit(p, lane, static_cast<int>(gridDim.x) * WARPS);

@@ -45,7 +45,7 @@ decode_kernel(const DecodeParams p) {
         fence_mbar_init();
     }
     __syncwarp();
-    int f0 = task_fetch(p, lane), f1 = task_fetch(p, lane);
+    int f0 = task_fetch(p, lane), f1 = task_fetch(p, lane), pend = task_fetch(p, lane);
     f0 = __shfl_sync(kFull, f0, 0);
     f1 = __shfl_sync(kFull, f1, 0);
     Task cur = load_task(p, f0, lane), nxt = load_task(p, f1, lane);
@@ -55,11 +55,11 @@ decode_kernel(const DecodeParams p) {
         while (seq_iss < seq_cons + STAGES) {
             const int j = static_cast<int>(seq_iss - cur_start);
             int ph, g;
-            if (j < cur.n) {
+            if (j < cur.it.n) {
                 ph = __shfl_sync(kFull, cur.phys_lane, j);
                 g = cur.g;
-            } else if (j - cur.n < nxt.n) {
-                ph = __shfl_sync(kFull, nxt.phys_lane, j - cur.n);
+            } else if (j - cur.it.n < nxt.it.n) {
+                ph = __shfl_sync(kFull, nxt.phys_lane, j - cur.it.n);
                 g = nxt.g;
             } else {
                 break;
@@ -76,20 +76,30 @@ decode_kernel(const DecodeParams p) {
         }
     };
     top_up(0);
+    // raw q of a task (lane holds dims dl*8 .. dl*8+7 of each q-head of the group)
+    auto load_q = [&](const Task &t, uint4 (&qr)[GQ]) {
+#pragma unroll
+        for (int h = 0; h < GQ; ++h)
+            qr[h] = __ldg(reinterpret_cast<const uint4 *>(
+                reinterpret_cast<const T *>(p.q) + (static_cast<size_t>(t.it.i) * p.q_heads + t.g * GQ + h) * D + dl * 8));
+    };
+    uint4 qraw[GQ];
+    load_q(cur, qraw);
 
     while (cur.task < p.n_tasks) {
-        int fetched = task_fetch(p, lane);  // the task after `nxt`; consumed at the end
-        const ReqMeta rm = p.req[cur.i];
-        const int i = cur.i, c = cur.c, g = cur.g;
-        if (p.fuse_stats && c == 0 && g == 0) batch_stats_warp(p, rm, lane);
+        // one task ahead: metadata of the task after `nxt` and the q of `nxt` are requested
+        // now and used when they become current, so their latency hides behind this task
+        const Task nnx = load_task(p, __shfl_sync(kFull, pend, 0), lane);
+        pend = task_fetch(p, lane);
+        uint4 qnext[GQ];
+        load_q(nxt, qnext);
+        const int i = cur.it.i, c = cur.it.c, g = cur.g;
+        if (p.fuse_stats && c == 0 && g == 0) batch_stats_warp(p, p.req[i], lane);
 
-        // q (pre-scaled to log2 units): lane holds dims dl*8 .. dl*8+7 of each q-head of the group
-        float q[GQ][8];
+        float q[GQ][8];  // pre-scaled to log2 units
 #pragma unroll
         for (int t = 0; t < GQ; ++t) {
-            const uint4 u = __ldg(reinterpret_cast<const uint4 *>(
-                reinterpret_cast<const T *>(p.q) + (static_cast<size_t>(i) * p.q_heads + g * GQ + t) * D + dl * 8));
-            unpack8<T>(u, q[t]);
+            unpack8<T>(qraw[t], q[t]);
 #pragma unroll
             for (int e = 0; e < 8; ++e) q[t][e] *= p.scale_log2;
         }
@@ -102,13 +112,13 @@ decode_kernel(const DecodeParams p) {
             for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
         }
 
-        for (int k = 0; k < cur.n; ++k) {
+        for (int k = 0; k < cur.it.n; ++k) {
             const uint32_t jseq = cur_start + k;
             const int s = jseq % STAGES;
             mbar_wait(&bars[warp][s], (jseq / STAGES) & 1);
             const T *Kt = reinterpret_cast<const T *>(wbuf + s * TILE);
             const T *Vt = Kt + kP * D;
-            const int valid = rm.ctx - (cur.pg0 + k) * kP;  // >= 1; < 16 only on the last page
+            const int valid = cur.it.ctx - (cur.it.pg0 + k) * kP;  // >= 1; < 16 only on the last page
 #pragma unroll
             for (int t = 0; t < GQ; ++t) {
                 // scores: partial dot products over this lane's 8 dims for its KI tokens
@@ -184,8 +194,8 @@ decode_kernel(const DecodeParams p) {
         }
 
         // ---- end of task: merge the TG token groups with shuffles, then store or split-K
-        const bool split = rm.nchunks > 1;
-        const int wi = rm.chunk_base + c;
+        const bool split = cur.it.nchunks > 1;
+        const int wi = cur.it.chunk_base + c;
 #pragma unroll
         for (int t = 0; t < GQ; ++t) {
             float M = m[t];
@@ -216,12 +226,14 @@ decode_kernel(const DecodeParams p) {
                 }
             }
         }
-        if (split && split_arrive_last(p, i, g, rm.nchunks, lane)) split_merge_warp<GQ, D>(p, rm, i, g, lane);
+        if (split && split_arrive_last(p, i, g, cur.it.nchunks, lane))
+            split_merge_warp<GQ, D>(p, cur.it.chunk_base, cur.it.nchunks, i, g, lane);
 
-        fetched = __shfl_sync(kFull, fetched, 0);
-        cur_start += cur.n;
+        cur_start += cur.it.n;
         cur = nxt;
-        nxt = load_task(p, fetched, lane);
+        nxt = nnx;
+#pragma unroll
+        for (int t = 0; t < GQ; ++t) qraw[t] = qnext[t];
         top_up(cur_start);
     }
     task_exit(p, lane, static_cast<int>(gridDim.x) * WARPS);

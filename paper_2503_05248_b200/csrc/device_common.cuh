@@ -177,32 +177,28 @@ __device__ __forceinline__ void batch_stats_warp(const DecodeParams &p, const Re
 // so the DRAM stream does not pause at task boundaries (epilogue, q load, metadata).
 struct Task {
     int task;        // >= n_tasks: no task
-    int i, c, g;     // batch index, chunk, kv head
-    int pg0, n;      // first page of the chunk and its page count (<= 32)
+    int g;           // kv head
+    ItemMeta it;     // the work item (request chunk)
     int phys_lane;   // physical page of the chunk's k-th page, held by lane k
 };
 
+// Two independent loads (item record, page ids): issued one task ahead of use.
 __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int lane) {
     Task t;
     t.task = task;
-    t.n = 0;
     t.phys_lane = 0;
-    t.i = t.c = t.g = t.pg0 = 0;
+    t.g = 0;
     if (task >= p.n_tasks) {
         t.task = p.n_tasks;
+        t.it = ItemMeta{0, 0, 0, 0, 1, 0, 1, 0};
         return t;
     }
     const int item = task / p.kv_heads;
     t.g = task - item * p.kv_heads;
-    const int2 w = __ldg(p.work + item);
-    t.i = w.x;
-    t.c = w.y;
-    const ReqMeta rm = p.req[t.i];
-    const int npages = (rm.ctx + kP - 1) / kP;
-    t.pg0 = t.c * p.chunk_pages;
-    t.n = min(t.pg0 + p.chunk_pages, npages) - t.pg0;
-    const int32_t *row = p.block_table + static_cast<size_t>(rm.slot) * p.bt_stride;
-    t.phys_lane = lane < t.n ? __ldg(row + t.pg0 + lane) : 0;
+    const int4 *im = reinterpret_cast<const int4 *>(p.items + item);
+    const int4 a = __ldg(im), b = __ldg(im + 1);
+    t.it = ItemMeta{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    t.phys_lane = __ldg(p.item_pages + static_cast<size_t>(item) * kItemPages + lane);
     return t;
 }
 
@@ -238,17 +234,17 @@ __device__ __forceinline__ bool split_arrive_last(const DecodeParams &p, int i, 
 
 // The last warp merges the chunks' (m, l, O) of q-heads g*GQ .. g*GQ+GQ-1 and writes out.
 template <int GQ, int D>
-__device__ __forceinline__ void split_merge_warp(const DecodeParams &p, const ReqMeta &rm, int i, int g,
-                                                 int lane) {
+__device__ __forceinline__ void split_merge_warp(const DecodeParams &p, int chunk_base, int nchunks, int i,
+                                                 int g, int lane) {
     for (int idx = lane; idx < GQ * D; idx += 32) {
         const int t = idx / D, e = idx % D;
         const int h = g * GQ + t;
         float M = -INFINITY;
-        for (int x = 0; x < rm.nchunks; ++x)
-            M = fmaxf(M, __ldcg(&p.ws_ml[static_cast<size_t>(rm.chunk_base + x) * p.q_heads + h]).x);
+        for (int x = 0; x < nchunks; ++x)
+            M = fmaxf(M, __ldcg(&p.ws_ml[static_cast<size_t>(chunk_base + x) * p.q_heads + h]).x);
         float L = 0.f, O = 0.f;
-        for (int x = 0; x < rm.nchunks; ++x) {
-            const size_t w = static_cast<size_t>(rm.chunk_base + x);
+        for (int x = 0; x < nchunks; ++x) {
+            const size_t w = static_cast<size_t>(chunk_base + x);
             const float2 ml = __ldcg(&p.ws_ml[w * p.q_heads + h]);
             if (ml.x != -INFINITY) {
                 const float f = exp2f(ml.x - M);

@@ -19,6 +19,21 @@ struct ReqMeta {
 };
 static_assert(sizeof(ReqMeta) == 32, "ReqMeta layout");
 
+// One work item = a chunk of <= 32 pages of one request (the unit a warp task streams), with
+// everything the decode kernels need to start it in ONE load; its physical page ids are in
+// item_pages[item * 32 + k] (k < n), so a task's metadata arrives in two independent loads.
+struct ItemMeta {
+    int32_t i;            // batch index
+    int32_t c;            // chunk index within the request
+    int32_t pg0, n;       // first logical page and page count
+    int32_t ctx;          // tokens of the request (incl. this step's)
+    int32_t chunk_base;   // first work item of the request (split-K workspace rows)
+    int32_t nchunks;      // work items of the request
+    int32_t slot;         // block-table row (statistics)
+};
+static_assert(sizeof(ItemMeta) == 32, "ItemMeta layout");
+constexpr int kItemPages = 32;
+
 struct DecodeParams {
     const uint8_t *kv_layer;     // KV base of this layer
     int64_t page_stride;         // bytes per (layer, page): kv_heads * tile_bytes
@@ -26,7 +41,8 @@ struct DecodeParams {
     int32_t bt_stride;
     int32_t n;                   // requests in the batch
     const ReqMeta *req;          // [n]
-    const int2 *work;            // [n_items] (batch index, chunk index)
+    const ItemMeta *items;       // [n_items], longest first
+    const int32_t *item_pages;   // [n_items][kItemPages] physical page ids
     int32_t n_items;
     int32_t chunk_pages;         // pages per work item
     const void *q;               // [n][q_heads][D]

@@ -468,14 +468,36 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
     });
     p->meta_items = base;
     p->meta_chunk_pages = static_cast<int32_t>(cp);
+    // blob: ReqMeta[n] | ItemMeta[items] | int32 item_pages[items][32] (physical page ids
+    // from the host tables, which the device tables mirror -- K4 checks them every step)
     const size_t rb = sizeof(ReqMeta) * static_cast<size_t>(n);
-    const size_t wb = sizeof(int2) * p->meta_work.size();
-    p->meta_blob.resize(rb + wb);
+    const size_t ib = sizeof(ItemMeta) * static_cast<size_t>(base);
+    const size_t pb = sizeof(int32_t) * kItemPages * static_cast<size_t>(base);
+    p->meta_blob.resize(rb + ib + pb);
     if (rb) std::memcpy(p->meta_blob.data(), p->meta_req.data(), rb);
-    if (wb) std::memcpy(p->meta_blob.data() + rb, p->meta_work.data(), wb);
+    ItemMeta *im = reinterpret_cast<ItemMeta *>(p->meta_blob.data() + rb);
+    int32_t *ipg = reinterpret_cast<int32_t *>(p->meta_blob.data() + rb + ib);
+    for (int32_t w = 0; w < base; ++w) {
+        const int2 wk = p->meta_work[w];
+        const ReqMeta &m = p->meta_req[wk.x];
+        const Request &r = p->reqs.find(m.req_id)->second;
+        const int32_t pages = static_cast<int32_t>((m.ctx + P - 1) / P);
+        ItemMeta it;
+        it.i = wk.x;
+        it.c = wk.y;
+        it.pg0 = static_cast<int32_t>(wk.y * cp);
+        it.n = std::min<int32_t>(static_cast<int32_t>(cp), pages - it.pg0);
+        it.ctx = m.ctx;
+        it.chunk_base = m.chunk_base;
+        it.nchunks = m.nchunks;
+        it.slot = m.slot;
+        im[w] = it;
+        for (int32_t k = 0; k < kItemPages; ++k) ipg[static_cast<size_t>(w) * kItemPages + k] = k < it.n ? r.pages[it.pg0 + k] : 0;
+    }
     DBK_TRY(p->up_meta.upload(p->meta_blob.data(), p->meta_blob.size(), s));
     p->d_req = static_cast<const ReqMeta *>(p->up_meta.dev);
-    p->d_work = reinterpret_cast<const int2 *>(static_cast<const uint8_t *>(p->up_meta.dev) + rb);
+    p->d_items = reinterpret_cast<const ItemMeta *>(static_cast<const uint8_t *>(p->up_meta.dev) + rb);
+    p->d_item_pages = reinterpret_cast<const int32_t *>(static_cast<const uint8_t *>(p->up_meta.dev) + rb + ib);
     // split-K workspace
     const size_t need = static_cast<size_t>(base) * p->cfg.q_heads;
     if (need > p->ws_cap) {
@@ -533,7 +555,8 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     dp.bt_stride = p->cfg.max_pages_per_req;
     dp.n = b->n;
     dp.req = p->d_req;
-    dp.work = p->d_work;
+    dp.items = p->d_items;
+    dp.item_pages = p->d_item_pages;
     dp.n_items = p->meta_items;
     dp.chunk_pages = p->meta_chunk_pages;
     dp.q = q;

@@ -56,7 +56,8 @@ struct dbk_pool {
     std::vector<uint8_t> meta_blob;
     int32_t meta_items = 0, meta_chunk_pages = 0;
     const dbk::ReqMeta *d_req = nullptr;
-    const int2 *d_work = nullptr;
+    const dbk::ItemMeta *d_items = nullptr;
+    const int32_t *d_item_pages = nullptr;
     // split-K workspace, arrival counters, statistics record
     float *d_ws_o = nullptr;
     float2 *d_ws_ml = nullptr;

@@ -312,7 +312,11 @@ def test_bench_config_sampled_parity(dbk):
     """The bench's own launch configuration (Llama-2-7B shape, pool sized from free HBM,
     memory policy): run engine steps, then compare sampled (request, q-head, layer)
     outputs of the last step with the oracle computed from logical coordinates."""
+    import gc
+
     import bench
+    gc.collect()
+    torch.cuda.empty_cache()
     S = bench.setup_engine(device=0, time_attention=True, out_dtype=2, n_req=1200)
     eng = S["eng"]
     bufs = eng.buffers(S["qd"], S["od"])
@@ -338,7 +342,17 @@ def test_bench_config_sampled_parity(dbk):
         want = oatt.paged_decode_attention(ctx[sel], bt, pk, pv, qq, "f16", nthreads=8)
         got = S["od"][lay, torch.as_tensor(sel, device="cuda")].cpu().numpy().astype(np.float64)
         assert row_err(got, want) <= TOL
+    _free(S)
+
+
+def _free(S):
+    """Release a full-size pool (~160 GB) before the next full-size test."""
+    import gc
+    S["eng"].close()
     S["pool"].close()
+    S.clear()
+    gc.collect()
+    torch.cuda.empty_cache()
 
 
 def _replay_full_size(S, recs):
@@ -361,7 +375,11 @@ def _replay_full_size(S, recs):
 def test_sla_binding_full_size_replay(dbk):
     """13B shape, combined policy with a binding SLA (D below the memory-bound step time):
     the device-timed step latencies drive Alg. 2 and the oracle replays the decisions."""
+    import gc
+
     import bench
+    gc.collect()
+    torch.cuda.empty_cache()
     S = bench.setup_engine(device=0, cfg_name="llama2-13b-sla", time_attention=False, out_dtype=0,
                            n_req=800, sla_ms=6.0)
     S["policy"], S["sla_ms"] = None, 6.0
@@ -374,4 +392,4 @@ def test_sla_binding_full_size_replay(dbk):
     tail = [r for r in recs[-40:]]
     mean_ms = np.mean([r["step_ns"] for r in tail]) / 1e6
     assert mean_ms < 6.0 + 2.0 + 1.0                             # settles near D_SLA + eps_D
-    S["pool"].close()
+    _free(S)
