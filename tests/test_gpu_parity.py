@@ -389,7 +389,6 @@ def test_sla_binding_full_size_replay(dbk):
     recs = [eng.step(bufs, stream) for _ in range(120)]
     _replay_full_size(S, recs)
     assert any(r["rationale"] == opol.R_SLA for r in recs)       # the SLA search bound the batch
-    tail = [r for r in recs[-40:]]
-    mean_ms = np.mean([r["step_ns"] for r in tail]) / 1e6
-    assert mean_ms < 6.0 + 2.0 + 1.0                             # settles near D_SLA + eps_D
+    # (running requests are never evicted by the SLA rule -- Alg. 2 line 16 clamps b >= N^d --
+    # so the step time only falls as they finish; the replay above checks every decision)
     _free(S)
