@@ -1,0 +1,113 @@
+#!/usr/bin/env python
+"""B200 analogs of the paper's experiments on the decode hot path.
+
+  python experiments/paper_tables.py [--fig3] [--table1] [--sla] [--out gpurun_out/paper_tables.json]
+
+* --fig3   : static-b sweep on the Llama-2-7B shape (steady state after a fast-forward):
+             tau_step(b) and Phi(b) = b / tau_step(b) (Eq. 6), OLS fit tau = a0 + a1 b
+             (Fig. 3).  Attention-only step: no weights, so a0 is small.
+* --table1 : whole-trace throughput (generated tokens / total device time, all-at-once
+             arrivals) for static b in {64, 128, 256} vs the memory-aware rule (Alg. 1),
+             the shape of Table I row 3 -- attention-only.
+* --sla    : the SLA feedback (Alg. 2 + min with Alg. 1) on the 13B shape with a binding
+             D_SLA = tau(b_mem / 2) from the sweep's fit, and the literal 50 ms.
+Every run goes through the C-ABI engine; numbers are device-timed (CUDA events).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def _run(cfg, policy, b_static=256, sla_ms=None, ff=300, steps=40, full=False, n_req=None):
+    import gc
+
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+    S = bench.setup_engine(cfg_name=cfg, policy=policy, b_static=b_static, sla_ms=sla_ms, time_attention=False,
+                           n_req=n_req)
+    eng = S["eng"]
+    bufs = eng.buffers(S["qd"], S["od"])
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    if full:
+        recs, ms = bench.run_steps(S, 10 ** 9, bufs, stream)
+    else:
+        bench.run_steps(S, ff, bufs, stream)
+        recs, ms = bench.run_steps(S, steps, bufs, stream)
+    out = dict(policy=policy, b_static=b_static if policy == "static" else None, sla_ms=sla_ms,
+               steps=len(recs), device_ms=ms, tokens=int(sum(r["n_decode"] for r in recs)),
+               mean_batch=float(np.mean([r["n_decode"] for r in recs])),
+               mean_step_ms=float(np.mean([r["step_ns"] for r in recs]) / 1e6),
+               preemptions=int(sum(r["n_preempted"] for r in recs)), wall_s=time.time() - t0)
+    out["tokens_per_s"] = out["tokens"] / (ms / 1e3)
+    if not full:
+        out["b_trace_tail"] = [r["b_next"] for r in recs[-10:]]
+    S["eng"].close()
+    S["pool"].close()
+    S.clear()
+    return out
+
+
+def fig3(cfg="llama2-7b", bs=(16, 32, 64, 128, 192, 256, 384, 512)):
+    rows = [_run(cfg, "static", b_static=b) for b in bs]
+    b = np.array([r["mean_batch"] for r in rows])
+    tau = np.array([r["mean_step_ms"] for r in rows])
+    a1, a0 = np.polyfit(b, tau, 1)
+    return dict(config=cfg, rows=rows, fit=dict(a0_ms=float(a0), a1_ms=float(a1)),
+                phi=[float(x) for x in 1000.0 * b / tau])
+
+
+def table1(cfg="llama2-7b"):
+    rows = [_run(cfg, "static", b_static=b, full=True) for b in (64, 128, 256)]
+    rows.append(_run(cfg, "memory", full=True))
+    return dict(config=cfg, rows=rows)
+
+
+def sla(fit=None, cfg="llama2-13b-sla"):
+    rows = [_run(cfg, "combined", sla_ms=50.0, ff=200, steps=60)]
+    if fit is not None:
+        rows.append(_run(cfg, "combined", sla_ms=fit, ff=200, steps=60))
+    return dict(config=cfg, rows=rows)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--fig3", action="store_true")
+    ap.add_argument("--table1", action="store_true")
+    ap.add_argument("--sla", action="store_true")
+    ap.add_argument("--out", default="gpurun_out/paper_tables.json")
+    a = ap.parse_args()
+    import torch
+    torch.cuda.set_device(0)
+    res = {}
+    if a.fig3:
+        res["fig3"] = fig3()
+        print(json.dumps(res["fig3"]["fit"]), flush=True)
+    if a.table1:
+        res["table1"] = table1()
+    if a.sla:
+        f13 = fig3("llama2-13b-sla", bs=(32, 64, 128, 256))
+        res["fig3_13b"] = f13
+        b_mem = max(r["mean_batch"] for r in f13["rows"])
+        d = f13["fit"]["a0_ms"] + f13["fit"]["a1_ms"] * b_mem / 2
+        res["sla"] = sla(fit=round(d, 3))
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(res, f, indent=1)
+    print(json.dumps({k: (v.get("fit") if isinstance(v, dict) else None) for k, v in res.items()}))
+
+
+if __name__ == "__main__":
+    main()

@@ -99,10 +99,10 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
             const int j = static_cast<int>(seq_iss - cur_start);
             int ph, g;
             if (j < cur.it.n) {
-                ph = __shfl_sync(kFull, cur.phys_lane, j);
+                ph = page_of(cur, j);
                 g = cur.g;
             } else if (j - cur.it.n < nxt.it.n) {
-                ph = __shfl_sync(kFull, nxt.phys_lane, j - cur.it.n);
+                ph = page_of(nxt, j - cur.it.n);
                 g = nxt.g;
             } else {
                 break;
@@ -229,10 +229,7 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
                 const float inv = 1.f / l;
                 const size_t base = (static_cast<size_t>(i) * p.q_heads + h) * D + 2 * cq;
 #pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    store_out(p.out, base + 8 * j, p.out_dtype, o[j][0] * inv);
-                    store_out(p.out, base + 8 * j + 1, p.out_dtype, o[j][1] * inv);
-                }
+                for (int j = 0; j < NT; ++j) store2_out(p.out, base + 8 * j, p.out_dtype, o[j][0] * inv, o[j][1] * inv);
             } else {
                 const int wi = cur.it.chunk_base + c;
                 float *w = p.ws_o + (static_cast<size_t>(wi) * p.q_heads + h) * D + 2 * cq;

@@ -56,10 +56,10 @@ decode_kernel(const DecodeParams p) {
             const int j = static_cast<int>(seq_iss - cur_start);
             int ph, g;
             if (j < cur.it.n) {
-                ph = __shfl_sync(kFull, cur.phys_lane, j);
+                ph = page_of(cur, j);
                 g = cur.g;
             } else if (j - cur.it.n < nxt.it.n) {
-                ph = __shfl_sync(kFull, nxt.phys_lane, j - cur.it.n);
+                ph = page_of(nxt, j - cur.it.n);
                 g = nxt.g;
             } else {
                 break;

@@ -108,6 +108,18 @@ __device__ __forceinline__ void store_out(void *out, size_t idx, int dtype, floa
         reinterpret_cast<__nv_bfloat16 *>(out)[idx] = __float2bfloat16_rn(x);
 }
 
+// Two consecutive outputs (fp32 / fp16 / bf16) from registers, one store.
+__device__ __forceinline__ void store2_out(void *out, size_t elem, int dtype, float a, float b) {
+    if (dtype == 2) {
+        *reinterpret_cast<float2 *>(reinterpret_cast<float *>(out) + elem) = make_float2(a, b);
+    } else if (dtype == 0) {
+        *reinterpret_cast<uint32_t *>(reinterpret_cast<__half *>(out) + elem) = Elt<__half>::from_f2(a, b);
+    } else {
+        *reinterpret_cast<uint32_t *>(reinterpret_cast<__nv_bfloat16 *>(out) + elem) =
+            Elt<__nv_bfloat16>::from_f2(a, b);
+    }
+}
+
 // ------------------------------------------------------------------ synthetic generator
 // Same definition as synth/hashgen.py (input generation only).
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -179,14 +191,21 @@ struct Task {
     int task;        // >= n_tasks: no task
     int g;           // kv head
     ItemMeta it;     // the work item (request chunk)
-    int phys_lane;   // physical page of the chunk's k-th page, held by lane k
+    int phys_lane;   // physical page of the chunk's k-th page, held by lane k (k < 32)
+    int phys_lane2;  // ... of page 32 + k
 };
+
+// Physical page of the task's j-th page (j warp-uniform, j < 64).
+__device__ __forceinline__ int page_of(const Task &t, int j) {
+    return __shfl_sync(kFull, j < 32 ? t.phys_lane : t.phys_lane2, j & 31);
+}
 
 // Two independent loads (item record, page ids): issued one task ahead of use.
 __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int lane) {
     Task t;
     t.task = task;
     t.phys_lane = 0;
+    t.phys_lane2 = 0;
     t.g = 0;
     if (task >= p.n_tasks) {
         t.task = p.n_tasks;
@@ -199,6 +218,7 @@ __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int l
     const int4 a = __ldg(im), b = __ldg(im + 1);
     t.it = ItemMeta{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     t.phys_lane = __ldg(p.item_pages + static_cast<size_t>(item) * kItemPages + lane);
+    t.phys_lane2 = __ldg(p.item_pages + static_cast<size_t>(item) * kItemPages + 32 + lane);
     return t;
 }
 
@@ -223,12 +243,20 @@ __device__ __forceinline__ void task_exit(const DecodeParams &p, int lane, int t
 // Split-K bookkeeping after a warp wrote its chunk's partial: returns true in every lane
 // of the warp whose chunk arrived last for (request, kv head); that warp merges.
 __device__ __forceinline__ bool split_arrive_last(const DecodeParams &p, int i, int g, int nchunks, int lane) {
-    __threadfence();
+    // The warp's partial stores happen-before lane 0's acq_rel RMW (__syncwarp + cumulativity),
+    // which releases them at gpu scope; the last arriver's acquire makes every chunk's partial
+    // visible (read with ld.global.cg, which bypasses L1) -- no full fences / L1 invalidation.
     __syncwarp();
     int last = 0;
-    if (lane == 0) last = atomicAdd(p.counters + i * p.kv_heads + g, 1) == nchunks - 1;
+    if (lane == 0) {
+        int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(prev)
+                     : "l"(p.counters + i * p.kv_heads + g)
+                     : "memory");
+        last = prev == nchunks - 1;
+    }
     last = __shfl_sync(kFull, last, 0);
-    if (last) __threadfence();
     return last != 0;
 }
 
@@ -236,26 +264,50 @@ __device__ __forceinline__ bool split_arrive_last(const DecodeParams &p, int i, 
 template <int GQ, int D>
 __device__ __forceinline__ void split_merge_warp(const DecodeParams &p, int chunk_base, int nchunks, int i,
                                                  int g, int lane) {
-    for (int idx = lane; idx < GQ * D; idx += 32) {
-        const int t = idx / D, e = idx % D;
-        const int h = g * GQ + t;
-        float M = -INFINITY;
-        for (int x = 0; x < nchunks; ++x)
-            M = fmaxf(M, __ldcg(&p.ws_ml[static_cast<size_t>(chunk_base + x) * p.q_heads + h]).x);
-        float L = 0.f, O = 0.f;
-        for (int x = 0; x < nchunks; ++x) {
-            const size_t w = static_cast<size_t>(chunk_base + x);
-            const float2 ml = __ldcg(&p.ws_ml[w * p.q_heads + h]);
-            if (ml.x != -INFINITY) {
-                const float f = exp2f(ml.x - M);
-                L += f * ml.y;
-                O += f * __ldcg(&p.ws_o[(w * p.q_heads + h) * D + e]);
-            }
+    // Online merge over the chunks: lane owns dims lane*PL .. lane*PL+PL-1 of all GQ heads;
+    // each chunk's loads (GQ (m, l) pairs + GQ x PL partial sums) are independent of the
+    // running state, so they are in flight together.
+    constexpr int PL = D / 32;
+    float M[GQ], L[GQ], acc[GQ][PL];
+#pragma unroll
+    for (int t = 0; t < GQ; ++t) {
+        M[t] = -INFINITY;
+        L[t] = 0.f;
+#pragma unroll
+        for (int e = 0; e < PL; ++e) acc[t][e] = 0.f;
+    }
+    for (int x = 0; x < nchunks; ++x) {
+        const size_t w0 = static_cast<size_t>(chunk_base + x) * p.q_heads + g * GQ;
+        float2 ml[GQ];
+        float v[GQ][PL];
+#pragma unroll
+        for (int t = 0; t < GQ; ++t) {
+            ml[t] = __ldcg(&p.ws_ml[w0 + t]);  // same address in every lane: one broadcast load
+            const float *src = p.ws_o + (w0 + t) * D + lane * PL;
+#pragma unroll
+            for (int e = 0; e < PL; ++e) v[t][e] = __ldcg(src + e);
         }
-        store_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + e, p.out_dtype, O / L);
+#pragma unroll
+        for (int t = 0; t < GQ; ++t) {
+            if (ml[t].x == -INFINITY) continue;
+            const float Mn = fmaxf(M[t], ml[t].x);
+            const float a = (M[t] == -INFINITY) ? 0.f : exp2f(M[t] - Mn), b = exp2f(ml[t].x - Mn);
+            L[t] = L[t] * a + ml[t].y * b;
+#pragma unroll
+            for (int e = 0; e < PL; ++e) acc[t][e] = acc[t][e] * a + v[t][e] * b;
+            M[t] = Mn;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < GQ; ++t) {
+        const float inv = 1.f / L[t];
+        const size_t ob = (static_cast<size_t>(i) * p.q_heads + g * GQ + t) * D + lane * PL;
+#pragma unroll
+        for (int e = 0; e < PL; e += 2) store2_out(p.out, ob + e, p.out_dtype, acc[t][e] * inv, acc[t][e + 1] * inv);
     }
     if (lane == 0) p.counters[i * p.kv_heads + g] = 0;
 }
+
 
 // 8 consecutive outputs (fp32 / fp16 / bf16) from registers.
 __device__ __forceinline__ void store8_out(void *out, size_t elem, int dtype, const float f[8]) {

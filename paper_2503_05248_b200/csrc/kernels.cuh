@@ -32,7 +32,7 @@ struct ItemMeta {
     int32_t slot;         // block-table row (statistics)
 };
 static_assert(sizeof(ItemMeta) == 32, "ItemMeta layout");
-constexpr int kItemPages = 32;
+constexpr int kItemPages = 64;
 
 struct DecodeParams {
     const uint8_t *kv_layer;     // KV base of this layer
