@@ -286,6 +286,14 @@ def run_gpu(args):
     if dist is not None:
         dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(etok_t)
+    # read-only streaming probe over (part of) the KV pool on this GPU: the achievable
+    # read bandwidth beside which the attention kernel's is reported
+    import ctypes
+    probe_ms = ctypes.c_double()
+    probe_bytes = min(S["pool"].kv.numel(), 32 * 10 ** 9) // 16 * 16
+    dbk._lib.dbk_probe_read_bandwidth(S["pool"].kv.data_ptr(), probe_bytes, local, stream.cuda_stream,
+                                      ctypes.byref(probe_ms))
+    probe_gbs = probe_bytes / 1e9 / (probe_ms.value / 1e3)
     if rank == 0:
         peak, peak_src = measured_peaks()
         achieved = att_bytes / 1e9 / (att_ms / 1e3) if att_ms > 0 else 0.0
@@ -319,7 +327,8 @@ def run_gpu(args):
                          "bytes_per_launch": int(att_bytes / max(att_launches, 1)),
                          "ms_per_launch": round(att_ms / max(att_launches, 1), 4), "peak_source": peak_src,
                          "share_of_step": round(att_ms / max(ms, 1e-9), 4), "ctas_per_sm": info["ctas_per_sm"],
-                         "chunk_pages": info["chunk_pages"]},
+                         "chunk_pages": info["chunk_pages"], "read_probe_gbs": round(probe_gbs, 1),
+                         "frac_of_read_probe": round(achieved / probe_gbs, 4)},
             "e2e": {"value": round(float(etok_t.item()) / (float(ems_t.item()) / 1e3), 2), "unit": UNIT,
                     "h2d_bytes_per_step": int(np.mean([r["h2d_bytes"] for r in erecs])) if erecs else 0,
                     "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in erecs])) if erecs else 0},

@@ -165,6 +165,13 @@ dbk_status dbk_synth_fill(uint64_t seed, int32_t kind, int32_t n_rows, const int
                           const int32_t *pos, int32_t layer, int32_t n_heads, int32_t d,
                           int32_t scale_log2, int32_t dtype, void *out, void *stream);
 
+/* Measurement utility (not part of the method): read `bytes` (multiple of 16) of device
+ * memory once with 16-byte streaming loads and return the kernel's CUDA-event time in
+ * ms -- the read-only HBM bandwidth of this GPU, reported beside the attention
+ * kernel's.  Synchronous on `stream`. */
+dbk_status dbk_probe_read_bandwidth(const void *buf, size_t bytes, int32_t device, void *stream,
+                                    double *ms_out);
+
 /* ------------------------------------------------------------------------ */
 /* Scheduler: Algorithm 1 (memory), Algorithm 2 (SLA), min, static          */
 /* ------------------------------------------------------------------------ */

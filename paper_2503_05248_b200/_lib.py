@@ -120,6 +120,7 @@ SIGNATURES = {
     "dbk_decode_step": [P, C.POINTER(dbk_batch), P, P, I32, P],
     "dbk_batch_stats": [P, C.POINTER(dbk_stats), P],
     "dbk_synth_fill": [U64, I32, I32, PI64, PI32, I32, I32, I32, I32, I32, P, P],
+    "dbk_probe_read_bandwidth": [P, C.c_size_t, I32, P, C.POINTER(C.c_double)],
     "dbk_sched_create": [C.POINTER(dbk_sched_config), C.POINTER(P)],
     "dbk_sched_destroy": [P],
     "dbk_choose_batch_size": [P, C.POINTER(dbk_stats), I64, D, I32, PI32, PI32],

@@ -153,4 +153,33 @@ cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layers,
     return cudaGetLastError();
 }
 
+// Read-only streaming probe (measurement utility, not part of the method): every byte of
+// `buf` is read once with 16-byte non-allocating loads, 8 independent loads in flight per
+// thread, grid = SMs x 8 CTAs; the XOR of the data goes to `sink` so nothing is elided.
+__global__ void __launch_bounds__(512) read_probe_kernel(const uint4 *__restrict__ buf, size_t n16, uint32_t *sink) {
+    uint32_t x = 0;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    for (; k + 7 * stride < n16; k += 8 * stride) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                         : "l"(buf + k + u * stride));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+    for (; k < n16; k += stride) {
+        const uint4 v = buf[k];
+        x ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (x == 0x9E3779B9u) sink[0] = x;  // practically never taken; keeps the loads live
+}
+
+cudaError_t launch_read_probe(const void *buf, size_t bytes, uint32_t *sink, int sms, cudaStream_t s) {
+    read_probe_kernel<<<sms * 4, 512, 0, s>>>(static_cast<const uint4 *>(buf), bytes / 16, sink);
+    return cudaGetLastError();
+}
+
 }  // namespace dbk

@@ -108,5 +108,6 @@ cudaError_t launch_synth_rows(uint64_t seed, int kind, int n_rows, const int64_t
 cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
                            int q_heads, int d, int scale_log2, int dtype, void *q, cudaStream_t s);
 int decode_ctas_per_sm(int kv_dtype, int head_dim, int group);
+cudaError_t launch_read_probe(const void *buf, size_t bytes, uint32_t *sink, int sms, cudaStream_t s);
 
 }  // namespace dbk

@@ -597,6 +597,33 @@ extern "C" dbk_status dbk_batch_stats(dbk_pool *p, dbk_stats *host_out, void *st
     return DBK_OK;
 }
 
+extern "C" dbk_status dbk_probe_read_bandwidth(const void *buf, size_t bytes, int32_t device, void *stream,
+                                                double *ms_out) {
+    if (!buf || !ms_out || bytes < 16 || bytes % 16) return fail(DBK_EINVAL, "probe_read_bandwidth: bad arguments");
+    DBK_CUDA(cudaSetDevice(device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    uint32_t *sink = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    DBK_CUDA(cudaMalloc(&sink, sizeof(uint32_t)));
+    cudaError_t e = cudaEventCreate(&a);
+    if (e == cudaSuccess) e = cudaEventCreate(&b);
+    if (e == cudaSuccess) e = launch_read_probe(buf, bytes, sink, sms, s);  // warm-up
+    if (e == cudaSuccess) e = cudaEventRecord(a, s);
+    if (e == cudaSuccess) e = launch_read_probe(buf, bytes, sink, sms, s);
+    if (e == cudaSuccess) e = cudaEventRecord(b, s);
+    if (e == cudaSuccess) e = cudaEventSynchronize(b);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return fail(DBK_ECUDA, "probe_read_bandwidth: %s", cudaGetErrorString(e));
+    *ms_out = ms;
+    return DBK_OK;
+}
+
 extern "C" dbk_status dbk_synth_fill(uint64_t seed, int32_t kind, int32_t n_rows, const int64_t *req,
                                      const int32_t *pos, int32_t layer, int32_t n_heads, int32_t d,
                                      int32_t scale_log2, int32_t dtype, void *out, void *stream) {

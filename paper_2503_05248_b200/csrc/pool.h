@@ -68,7 +68,8 @@ struct dbk_pool {
     int32_t *d_task_counter = nullptr;        // persistent decode: next task, exited CTAs
     dbk_stats *h_stats = nullptr;
     int num_sms = 148, ctas_per_sm = 1;
-    int64_t max_chunk_pages = 64, force_chunk_pages = 0;  // <= 64: two page ids per lane
+    // pages per warp task: <= 64 (two page ids per lane); 32 measured best (profiles/r01_tune.txt)
+    int64_t max_chunk_pages = 32, force_chunk_pages = 0;
     int64_t last_decode_bytes = 0;
     int64_t n_launches = 0;                   // kernels launched by this pool (gpu_launches)
     // pool-wide 2-D tensor map (rows of head_dim elements, 16 x 64 boxes, 128B swizzle) for K2
