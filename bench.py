@@ -119,24 +119,28 @@ def make_workload(cfg_name=CFG_NAME, world=1, n_req=None):
 POLICIES = {"static": 0, "memory": 1, "sla": 2, "combined": 3}
 
 
-def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None):
+def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None):
     pr = configs.prior_record(c)
     pol = POLICIES[policy or c["policy"]]
     return dict(policy=pol, b_static=b_static, b_min=c["b_min"], b_max=c["b_max"], b0=c["b_min"],
                 eps_m=c["eps_m"], bytes_per_token=beta, page_size=c["page_size"], refresh_steps=100,
                 w_len=256, w_sla=20, alpha=c.get("alpha", 8), delta=c.get("delta", 2),
-                d_sla_ms=sla_ms or c.get("sla_ms", 50.0), eps_d_ms=c.get("eps_d_ms", 2.0),
+                d_sla_ms=sla_ms or c.get("sla_ms", 50.0),
+                eps_d_ms=eps_d_ms if eps_d_ms is not None else c.get("eps_d_ms", 2.0),
                 prior=tuple(pr.values()))
 
 
 def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
-                 out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1):
+                 out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1,
+                 trace_override=None, eps_d_ms=None):
     """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
     config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
 
     import paper_2503_05248_b200 as dbk
     c, tr = make_workload(cfg_name, world if tp == 1 else 1, n_req)
+    if trace_override is not None:
+        tr = trace_override
     L, Hq, Hkv, d, P = c["layers"], c["q_heads"] // tp, c["kv_heads"] // tp, c["head_dim"], c["page_size"]
     beta = configs.kv_bytes_per_token(c, tp=tp)
     max_req = c["b_max"] + 8
@@ -153,7 +157,7 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, "f16", device=device)
     # M_max of the whole job: DP shards add their pools; TP ranks hold the same tokens
     mem_cap_total = cap_pages * P * beta * (world if tp == 1 else 1)
-    sched = dbk.Scheduler(**sched_kwargs(c, beta, policy, b_static, sla_ms))
+    sched = dbk.Scheduler(**sched_kwargs(c, beta, policy, b_static, sla_ms, eps_d_ms))
     eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap_total, seed=seed,
                      out_dtype=out_dtype, time_attention=time_attention,
                      rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0)

@@ -82,11 +82,68 @@ def sla(fit=None, cfg="llama2-13b-sla"):
     return dict(config=cfg, rows=rows)
 
 
+def _tbt_p99(recs):
+    """p99 time between tokens over all generated tokens (every token of a step waits the
+    step's latency; nearest rank)."""
+    lat = np.array([r["step_ns"] for r in recs], np.float64) / 1e6
+    w = np.array([r["n_decode"] for r in recs], np.int64)
+    order = np.argsort(lat)
+    cum = np.cumsum(w[order])
+    k = int(np.ceil(0.99 * cum[-1]))
+    return float(lat[order][np.searchsorted(cum, k)])
+
+
+def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, n_req=1500, policies=("static", "combined"),
+             b_static=None, lo=5.0, hi=400.0, tol=0.05):
+    """Table II / Fig. 5 analog: the largest Poisson rate (qps) at which the p99
+    TBT stays <= D_SLA + eps_D (capacity, Sarathi's definition quoted at P:298), found by
+    bisection on the rate for the static baseline and for Alg. 2 + Alg. 1."""
+    from synth import configs, trace
+    c = configs.CONFIGS[cfg]
+    t = c["trace"]
+    out = dict(config=cfg, d_sla_ms=d_sla, eps_d_ms=eps_d, n_requests=n_req, rows=[])
+
+    def ok(policy, qps):
+        tr = trace.make_trace(n_req, t["mean_in"], t["mean_out"], t["L_max"], t["seed"], dist=t["dist"],
+                              arrival="poisson", rate_qps=qps)
+        import gc
+
+        import torch
+        gc.collect()
+        torch.cuda.empty_cache()
+        S = bench.setup_engine(cfg_name=cfg, policy=policy, b_static=b_static or 256, sla_ms=d_sla,
+                               eps_d_ms=eps_d, time_attention=False, trace_override=tr)
+        eng = S["eng"]
+        bufs = eng.buffers(S["qd"], S["od"])
+        recs, ms = bench.run_steps(S, 10 ** 9, bufs, torch.cuda.current_stream())
+        p99 = _tbt_p99(recs)
+        tok_s = sum(r["n_decode"] for r in recs) / (sum(r["step_ns"] for r in recs) / 1e9)
+        S["eng"].close()
+        S["pool"].close()
+        S.clear()
+        return p99 <= d_sla + eps_d, p99, tok_s
+
+    for pol in policies:
+        a, b = lo, hi
+        best = None
+        while b - a > tol * a:
+            mid = (a * b) ** 0.5
+            good, p99, tok_s = ok(pol, mid)
+            if good:
+                a, best = mid, (mid, p99, tok_s)
+            else:
+                b = mid
+        out["rows"].append(dict(policy=pol, capacity_qps=a, p99_ms=best[1] if best else None,
+                                tokens_per_s=best[2] if best else None))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--fig3", action="store_true")
     ap.add_argument("--table1", action="store_true")
     ap.add_argument("--sla", action="store_true")
+    ap.add_argument("--capacity", action="store_true")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
     a = ap.parse_args()
     import torch
@@ -103,6 +160,13 @@ def main():
         b_mem = max(r["mean_batch"] for r in f13["rows"])
         d = f13["fit"]["a0_ms"] + f13["fit"]["a1_ms"] * b_mem / 2
         res["sla"] = sla(fit=round(d, 3))
+    if a.capacity:
+        f13 = res.get("fig3_13b") or fig3("llama2-13b-sla", bs=(32, 64, 128, 256))
+        res["fig3_13b"] = f13
+        # binding SLA: the step latency at half the largest static batch; eps_D = 4 % of D
+        b_mem = max(r["mean_batch"] for r in f13["rows"])
+        d = round(f13["fit"]["a0_ms"] + f13["fit"]["a1_ms"] * b_mem / 2, 3)
+        res["capacity"] = capacity(d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem))
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(res, f, indent=1)
