@@ -163,19 +163,21 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
                 }
                 __syncwarp();
             }
-            // S = Q K^T for tokens 0-7 (s0) and 8-15 (s1)
-            float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+            // S = Q K^T for tokens 0-7 (s0) and 8-15 (s1); even / odd k-steps accumulate in
+            // separate registers so the two dependent MMA chains are half as long
+            float s0[2][4] = {}, s1[2][4] = {};
 #pragma unroll
             for (int kk = 0; kk < KSTEPS; ++kk) {
                 const int tok = (mtx >> 1) * 8 + mr, ch = (kk & 3) * 2 + (mtx & 1);
                 uint32_t kb[4];
                 ldsm_x4(kb, kb_base + (kk >> 2) * kBox + tok * 128 + ((ch ^ (tok & 7)) << 4));
-                mma_pad<T>(s0, qa[kk][0], qa[kk][1], kb[0], kb[1]);
-                mma_pad<T>(s1, qa[kk][0], qa[kk][1], kb[2], kb[3]);
+                mma_pad<T>(s0[kk & 1], qa[kk][0], qa[kk][1], kb[0], kb[1]);
+                mma_pad<T>(s1[kk & 1], qa[kk][0], qa[kk][1], kb[2], kb[3]);
             }
             // online softmax for q-head gq over this lane's tokens 2cq, 2cq+1, 8+2cq, 9+2cq
             const int t0 = 2 * cq;
-            float x[4] = {s0[0] * p.scale_log2, s0[1] * p.scale_log2, s1[0] * p.scale_log2, s1[1] * p.scale_log2};
+            float x[4] = {(s0[0][0] + s0[1][0]) * p.scale_log2, (s0[0][1] + s0[1][1]) * p.scale_log2,
+                          (s1[0][0] + s1[1][0]) * p.scale_log2, (s1[0][1] + s1[1][1]) * p.scale_log2};
             if (t0 >= valid) x[0] = -INFINITY;
             if (t0 + 1 >= valid) x[1] = -INFINITY;
             if (t0 + 8 >= valid) x[2] = -INFINITY;
