@@ -93,17 +93,19 @@ def _tbt_p99(recs):
     return float(lat[order][np.searchsorted(cum, k)])
 
 
-def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, n_req=1500, policies=("static", "combined"),
-             b_static=None, lo=5.0, hi=400.0, tol=0.05):
+def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0, policies=("static", "combined"),
+             b_static=None, lo=20.0, hi=640.0, tol=0.05):
     """Table II / Fig. 5 analog: the largest Poisson rate (qps) at which the p99
     TBT stays <= D_SLA + eps_D (capacity, Sarathi's definition quoted at P:298), found by
-    bisection on the rate for the static baseline and for Alg. 2 + Alg. 1."""
+    bisection on the rate for the static baseline and for Alg. 2 + Alg. 1.  Each probe sends
+    qps x window_s requests (a fixed arrival window, so every probe costs about the same)."""
     from synth import configs, trace
     c = configs.CONFIGS[cfg]
     t = c["trace"]
-    out = dict(config=cfg, d_sla_ms=d_sla, eps_d_ms=eps_d, n_requests=n_req, rows=[])
+    out = dict(config=cfg, d_sla_ms=d_sla, eps_d_ms=eps_d, window_s=window_s, rows=[])
 
     def ok(policy, qps):
+        n_req = max(100, int(qps * window_s))
         tr = trace.make_trace(n_req, t["mean_in"], t["mean_out"], t["L_max"], t["seed"], dist=t["dist"],
                               arrival="poisson", rate_qps=qps)
         import gc
@@ -149,27 +151,31 @@ def main():
     import torch
     torch.cuda.set_device(0)
     res = {}
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+
+    def save():  # after every section, so a time-out keeps what finished
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
     if a.fig3:
         res["fig3"] = fig3()
         print(json.dumps(res["fig3"]["fit"]), flush=True)
+        save()
     if a.table1:
         res["table1"] = table1()
-    if a.sla:
-        f13 = fig3("llama2-13b-sla", bs=(32, 64, 128, 256))
-        res["fig3_13b"] = f13
-        b_mem = max(r["mean_batch"] for r in f13["rows"])
-        d = f13["fit"]["a0_ms"] + f13["fit"]["a1_ms"] * b_mem / 2
-        res["sla"] = sla(fit=round(d, 3))
-    if a.capacity:
-        f13 = res.get("fig3_13b") or fig3("llama2-13b-sla", bs=(32, 64, 128, 256))
-        res["fig3_13b"] = f13
+        save()
+    if a.sla or a.capacity:
+        res["fig3_13b"] = fig3("llama2-13b-sla", bs=(32, 64, 128, 256))
+        save()
         # binding SLA: the step latency at half the largest static batch; eps_D = 4 % of D
-        b_mem = max(r["mean_batch"] for r in f13["rows"])
-        d = round(f13["fit"]["a0_ms"] + f13["fit"]["a1_ms"] * b_mem / 2, 3)
-        res["capacity"] = capacity(d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem))
-    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
-    with open(a.out, "w") as f:
-        json.dump(res, f, indent=1)
+        b_mem = max(r["mean_batch"] for r in res["fig3_13b"]["rows"])
+        d = round(res["fig3_13b"]["fit"]["a0_ms"] + res["fig3_13b"]["fit"]["a1_ms"] * b_mem / 2, 3)
+        if a.sla:
+            res["sla"] = sla(fit=d)
+            save()
+        if a.capacity:
+            res["capacity"] = capacity(d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem))
+            save()
     print(json.dumps({k: (v.get("fit") if isinstance(v, dict) else None) for k, v in res.items()}))
 
 

@@ -118,6 +118,8 @@ dbk_status dbk_block_table_d2h(dbk_pool *pool, int32_t *host_out, void *stream);
 typedef struct dbk_pool_info {
     int32_t decode_path, ctas_per_sm, chunk_pages, work_items;
     int64_t launches, last_decode_bytes;
+    int32_t tma_rank;   /* K2 tile fetch: 5 = one 5-D TMA box per page tile, 2 = 2-D boxes */
+    int32_t _reserved;
 } dbk_pool_info;
 dbk_status dbk_pool_get_info(dbk_pool *pool, dbk_pool_info *out);
 

@@ -35,7 +35,8 @@ class dbk_pool_config(C.Structure):
 
 class dbk_pool_info(C.Structure):
     _fields_ = [("decode_path", C.c_int32), ("ctas_per_sm", C.c_int32), ("chunk_pages", C.c_int32),
-                ("work_items", C.c_int32), ("launches", C.c_int64), ("last_decode_bytes", C.c_int64)]
+                ("work_items", C.c_int32), ("launches", C.c_int64), ("last_decode_bytes", C.c_int64),
+                ("tma_rank", C.c_int32), ("_reserved", C.c_int32)]
 
 
 class dbk_batch(C.Structure):

@@ -29,6 +29,16 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// One (page, kv head) tile through the 5-D view {64, 16 tokens, d/64 halves, K|V, tile}: the
+// whole 2 x 16 x d tile in one TMA, landing as [K|V][half][token][64] with the 128B swizzle.
+__device__ __forceinline__ void tma_load_tile5(void *dst, const CUtensorMap *map, int tile, uint64_t *bar,
+                                               uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %2, %2, %2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(tile), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void ldsm_x4(uint32_t r[4], uint32_t addr) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
@@ -111,13 +121,17 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
                 const int s = seq_iss % STAGES;
                 fence_proxy_async();
                 mbar_expect_tx(&bars[warp][s], STAGE);
-                const int row = static_cast<int>(((row_layer + ph) * p.kv_heads + g) * 32);
+                const int tile = static_cast<int>((row_layer + ph) * p.kv_heads + g);
+                if (p.tma_rank == 5) {
+                    tma_load_tile5(wbuf + s * STAGE, &tmap, tile, &bars[warp][s], pol);
+                } else {
 #pragma unroll
-                for (int kv = 0; kv < 2; ++kv)
+                    for (int kv = 0; kv < 2; ++kv)
 #pragma unroll
-                    for (int b = 0; b < NBOX; ++b)
-                        tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox, &tmap, b * 64, row + kv * 16,
-                                    &bars[warp][s], pol);
+                        for (int b = 0; b < NBOX; ++b)
+                            tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox, &tmap, b * 64, tile * 32 + kv * 16,
+                                        &bars[warp][s], pol);
+                }
             }
             ++seq_iss;
         }

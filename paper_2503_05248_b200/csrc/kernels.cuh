@@ -66,6 +66,8 @@ struct DecodeParams {
     // counter; task_counter[0] = next task, [1] = exited CTAs (both reset by the last CTA)
     int32_t n_tasks;
     int32_t *task_counter;
+    int32_t tma_rank;            // K2: 5 = one 5-D box per tile, 2 = 2-D boxes of 16 x 64
+    int32_t _pad;
 };
 
 struct AppendJob {

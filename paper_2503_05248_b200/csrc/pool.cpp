@@ -102,23 +102,42 @@ using namespace dbk;
 
 // K2's tensor map over the whole pool: a 2-D tensor of rows = layers*cap*kv_heads*2*16
 // token rows x head_dim elements; one box = 16 rows x 64 elements with the 128-byte swizzle.
-static bool make_pool_tmap(dbk_pool *p) {
+static bool make_pool_tmap(dbk_pool *p, bool try5) {
     const dbk_pool_config &c = p->cfg;
-    const uint64_t rows = static_cast<uint64_t>(c.layers) * c.cap_pages * c.kv_heads * 2 * c.page_size;
-    if (rows >= (1ull << 31)) return false;  // int32 TMA coordinates
+    const uint64_t tiles = static_cast<uint64_t>(c.layers) * c.cap_pages * c.kv_heads;  // (layer, page, head)
+    if (tiles * 2 * c.page_size >= (1ull << 31)) return false;  // int32 TMA coordinates
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
         q != cudaDriverEntryPointSuccess)
         return false;
     auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(c.head_dim), rows};
-    const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(c.head_dim) * 2};
+    const cuuint32_t halves = static_cast<cuuint32_t>(c.head_dim / 64);
+    const cuuint64_t row = static_cast<cuuint64_t>(c.head_dim) * 2;  // one token row, bytes
+    // Preferred: ONE 8 KiB box per (page, head) tile -- a 5-D view {64 elements, 16 tokens,
+    // d/64 halves, K|V, tile} whose box lands in shared memory as [K|V][half][token][64],
+    // i.e. 128-B rows with the token index as the swizzle row (conflict-free ldmatrix).
+    if (try5) {
+        const cuuint64_t gdim[5] = {64, static_cast<cuuint64_t>(c.page_size), halves, 2, tiles};
+        const cuuint64_t gstride[4] = {row, 128, row * c.page_size, row * c.page_size * 2};
+        const cuuint32_t box[5] = {64, static_cast<cuuint32_t>(c.page_size), halves, 2, 1};
+        const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+        if (encode(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, p->kv, gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+            p->tma_rank = 5;
+            return true;
+        }
+    }
+    // Fallback: 2-D rows x d, boxes of 16 rows x 64 elements (2 * d/64 boxes per tile).
+    const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(c.head_dim), tiles * 2 * c.page_size};
+    const cuuint64_t gstride[1] = {row};
     const cuuint32_t box[2] = {64, 16};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->kv, gdim, gstride, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    p->tma_rank = 2;
     return r == CUDA_SUCCESS;
 }
 
@@ -187,7 +206,8 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     p->num_sms = dev_sms;
     const int group = cfg->q_heads / cfg->kv_heads;
     const char *cc = std::getenv("DBK_GQA_CUDA_CORE");  // 1: force K1 for GQA (comparison runs)
-    if (group >= 2 && !(cc && cc[0] == '1')) p->has_tmap = make_pool_tmap(p);
+    const char *t2 = std::getenv("DBK_GQA_TMA2");  // 1: force the 2-D boxes (comparison runs)
+    if (group >= 2 && !(cc && cc[0] == '1')) p->has_tmap = make_pool_tmap(p, !(t2 && t2[0] == '1'));
     p->ctas_per_sm = p->has_tmap ? decode_gqa_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group)
                                  : decode_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group);
     if (const char *e = std::getenv("DBK_CHUNK_PAGES")) {  // tuning override (multiple of 4, <= 64)
@@ -402,6 +422,8 @@ dbk_status dbk_pool_get_info(dbk_pool *p, dbk_pool_info *o) {
     o->work_items = p->meta_items;
     o->launches = p->n_launches;
     o->last_decode_bytes = p->last_decode_bytes;
+    o->tma_rank = p->has_tmap ? p->tma_rank : 0;
+    o->_reserved = 0;
     return DBK_OK;
 }
 
@@ -576,6 +598,8 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     dp.kv_heads = p->cfg.kv_heads;
     dp.n_tasks = p->meta_items * p->cfg.kv_heads;
     dp.task_counter = p->d_task_counter;
+    dp.tma_rank = p->tma_rank;
+    dp._pad = 0;
     // persistent grid: every resident CTA slot (4 warps each), or fewer for small batches
     const int ctas = std::max(1, std::min(p->num_sms * p->ctas_per_sm, (dp.n_tasks + 3) / 4));
     DBK_CUDA(launch_decode(dp, p->cfg.kv_dtype, p->cfg.head_dim, p->cfg.q_heads / p->cfg.kv_heads, ctas,

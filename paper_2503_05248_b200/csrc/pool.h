@@ -75,4 +75,5 @@ struct dbk_pool {
     // pool-wide 2-D tensor map (rows of head_dim elements, 16 x 64 boxes, 128B swizzle) for K2
     alignas(64) CUtensorMap tmap;
     bool has_tmap = false;
+    int tma_rank = 0;                         // 5: one box per tile; 2: 2*d/64 boxes per tile
 };

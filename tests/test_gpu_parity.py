@@ -277,17 +277,22 @@ def test_engine_combined_sla_poisson_replays(dbk):
 
 @pytest.mark.parametrize("dtype", ["f16", "bf16"])
 @pytest.mark.parametrize("Hq,Hkv,d", [(8, 2, 64), (16, 2, 128), (8, 4, 128), (16, 8, 64)])
-@pytest.mark.parametrize("path", ["tensor", "cuda_core"])
+@pytest.mark.parametrize("path", ["tensor", "tensor_tma2d", "cuda_core"])
 def test_gqa_paths_parity(dbk, monkeypatch, dtype, Hq, Hkv, d, path):
-    """K2 (TMA tensor tiles + mma.sync) and K1 (CUDA cores) on the same GQA inputs."""
+    """K2 (TMA tensor tiles + mma.sync; one 5-D box per tile, or 2-D boxes) and K1 (CUDA
+    cores) on the same GQA inputs."""
+    monkeypatch.delenv("DBK_GQA_CUDA_CORE", raising=False)
+    monkeypatch.delenv("DBK_GQA_TMA2", raising=False)
     if path == "cuda_core":
         monkeypatch.setenv("DBK_GQA_CUDA_CORE", "1")
-    else:
-        monkeypatch.delenv("DBK_GQA_CUDA_CORE", raising=False)
+    elif path == "tensor_tma2d":
+        monkeypatch.setenv("DBK_GQA_TMA2", "1")
     ctx = [1, 5, 16, 17, 100, 255, 256, 257, 1024, 3000]
     for got, want in run_decode_case(dbk, 2, Hq, Hkv, d, dtype, ctx, q_scale_log2=(4 if Hq == 16 else 0)):
         assert row_err(got, want) <= TOL
-    assert LAST_INFO["decode_path"] == (2 if path == "tensor" else 1)
+    assert LAST_INFO["decode_path"] == (1 if path == "cuda_core" else 2)
+    if path != "cuda_core":
+        assert LAST_INFO["tma_rank"] == (2 if path == "tensor_tma2d" else 5)
 
 
 def test_nccl_single_rank_allgather(dbk):
