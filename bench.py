@@ -183,7 +183,11 @@ def run_steps(S, k, bufs, stream, comm_world=1, dist=None):
     for _ in range(k):
         if eng.done():
             break
-        recs.append(eng.step(bufs, stream))
+        if S.get("exchange") is not None:  # caller-side exchange of the 128-B records
+            local = eng.step_launch(bufs, stream)
+            recs.append(eng.step_finish(S["exchange"](local)))
+        else:
+            recs.append(eng.step(bufs, stream))
     e1.record(stream)
     torch.cuda.synchronize()
     if dist is not None:
@@ -255,9 +259,25 @@ def run_gpu(args):
                      b_static=args.b_static, sla_ms=args.sla_ms, tp=tp)
     dbk = S["dbk"]
     eng = S["eng"]
+    exchange_kind = None
     if world > 1:
-        comm = _make_comm(dbk, dist, world, rank, local)
-        dbk._lib.dbk_engine_attach_comm(eng.h, comm, dbk._lib.MODE_TP if tp > 1 else dbk._lib.MODE_DP)
+        mode = dbk._lib.MODE_TP if tp > 1 else dbk._lib.MODE_DP
+        try:  # libdbk's own NCCL communicator (ncclAllGather of the records inside the engine step)
+            comm = _make_comm(dbk, dist, world, rank, local)
+            dbk._lib.dbk_engine_attach_comm(eng.h, comm, mode)
+            exchange_kind = "libdbk NCCL all-gather"
+        except Exception as ex:  # fall back to torch.distributed (also NCCL) for the same exchange
+            print(f"[bench] dbk_comm unavailable ({ex}); exchanging records via torch.distributed",
+                  file=sys.stderr)
+            fields = dbk._lib.STATS_FIELDS
+
+            def exchange(local_rec):
+                t = torch.tensor([local_rec[f] for f in fields], dtype=torch.int64, device="cuda")
+                out = [torch.zeros_like(t) for _ in range(world)]
+                dist.all_gather(out, t)
+                return dbk.stats_reduce([dict(zip(fields, o.tolist())) for o in out], mode)
+            S["exchange"] = exchange
+            exchange_kind = "torch.distributed NCCL all-gather"
     stream = torch.cuda.current_stream()
     bufs = eng.buffers(S["qd"], S["od"])
     # fast-forward to the steady state (untimed), then W warm-up steps (untimed)
@@ -325,6 +345,7 @@ def run_gpu(args):
                        "mean_ctx": round(float(np.mean([r["sum_ctx"] / max(r["n_decode"], 1) for r in recs])), 1) if recs else 0,
                        "fast_forward_steps": args.ff,
                        "parallelism": f"tp{world} (KV-head shards)" if tp > 1 else f"dp{world} (request shards)",
+                       "stats_exchange": exchange_kind,
                        "l2": "inputs > L2 (~1e2 GB of KV read per step vs 126 MB L2)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kname,

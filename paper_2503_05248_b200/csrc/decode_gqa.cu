@@ -12,6 +12,9 @@
 // (11 bits) -- both well inside the 2e-3 bar (R23).  Work decomposition
 // (persistent warps, one task = (request chunk, kv head) per warp, rings that stream across
 // task boundaries), the fused statistics and the split-K merge are the same as K1.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "device_common.cuh"
@@ -303,12 +306,45 @@ int gqa_occ_t() {
     return n > 0 ? n : 1;
 }
 
+// Tuning variants of the (warps per CTA, ring stages) trade-off for GQ = 8 (DBK_GQA_WS =
+// "2x6" or "8x3"; default 4x3): same shared memory per SM, different warps vs depth.
+template <typename T, int D, int GQ, int W, int S>
+cudaError_t launch_gqa_v(const DecodeParams &p, const CUtensorMap &tmap, cudaStream_t s) {
+    auto kern = decode_gqa_kernel<T, D, GQ, W, S>;
+    constexpr size_t smem = static_cast<size_t>(W) * S * 2 * (D / 64) * kBox + 1024;
+    static int occ = -1, sms = 148;
+    if (occ < 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, W * 32, smem) != cudaSuccess || n < 1) n = 1;
+        occ = n;
+    }
+    const int ctas = std::max(1, std::min(sms * occ, (p.n_tasks + W - 1) / W));
+    kern<<<ctas, W * 32, smem, s>>>(p, tmap);
+    return cudaGetLastError();
+}
+
+int gqa_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = std::getenv("DBK_GQA_WS");
+        v = (e && std::strcmp(e, "2x6") == 0) ? 1 : (e && std::strcmp(e, "8x3") == 0) ? 2 : 0;
+    }
+    return v;
+}
+
 template <typename T, int D>
 cudaError_t gqa_group(const DecodeParams &p, int group, int ctas, const CUtensorMap &tmap, cudaStream_t s) {
     switch (group) {
         case 2: return launch_gqa_t<T, D, 2>(p, ctas, tmap, s);
         case 4: return launch_gqa_t<T, D, 4>(p, ctas, tmap, s);
-        case 8: return launch_gqa_t<T, D, 8>(p, ctas, tmap, s);
+        case 8:
+            if (gqa_variant() == 1) return launch_gqa_v<T, D, 8, 2, 6>(p, tmap, s);
+            if (gqa_variant() == 2) return launch_gqa_v<T, D, 8, 8, 3>(p, tmap, s);
+            return launch_gqa_t<T, D, 8>(p, ctas, tmap, s);
         default: return cudaErrorInvalidValue;
     }
 }
