@@ -157,6 +157,33 @@ typedef struct dbk_stats {
 dbk_status dbk_batch_stats(dbk_pool *pool, dbk_stats *host_out, void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* Chunked prefill (PD fusion)          */
+/* ------------------------------------------------------------------------ */
+
+/* One prefill chunk per request: query tokens at positions q_start[i] ..
+ * q_start[i] + q_len[i] - 1 of request req_ids[i], whose K/V must already be
+ * appended (ctx >= q_start + q_len).  Rows of q / out are the chunks
+ * concatenated in batch order: row r = sum_{i' < i} q_len[i'] + j.            */
+typedef struct dbk_prefill_batch {
+    int32_t n;               /* chunks (0 = no-op)                               */
+    int32_t layer;           /* 0 .. layers-1                                     */
+    const int64_t *req_ids;  /* host [n]                                          */
+    const int32_t *q_start;  /* host [n], >= 0                                    */
+    const int32_t *q_len;    /* host [n], >= 1                                    */
+} dbk_prefill_batch;
+
+/* Causal paged attention of every chunk token (K7, tcgen05 tensor cores):
+ *   out[r][h][:] = sum_{k <= p} softmax_k(q[r][h].K_{i,g,k} / sqrt(d)) V_{i,g,k},
+ * p = q_start[i] + j the token's position, g = h / (q_heads / kv_heads) -- the
+ * decode formula (R1, R2; oracle O1) with ctx = p + 1 per query row.
+ * q: device [rows][q_heads][head_dim] kv_dtype, 16-B aligned; out: device
+ * [rows][q_heads][head_dim] out_dtype (0 fp16, 1 bf16, 2 fp32).  fp32
+ * accumulation.  EINVAL on a bad chunk or when the pool has no 5-D tensor map
+ * (tile index >= 2^31); ENOENT on an unknown id.  Async on `stream`. */
+dbk_status dbk_prefill_step(dbk_pool *pool, const dbk_prefill_batch *batch, const void *q, void *out,
+                            int32_t out_dtype, void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* Synthetic input generator (input side only; none of the method's math)  */
 /* ------------------------------------------------------------------------ */
 

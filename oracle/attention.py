@@ -74,6 +74,20 @@ def paged_decode_attention(ctx, block_table, pool_k, pool_v, q, dtype="f16", nth
     return out
 
 
+def paged_prefill_attention(q_start, q_len, block_table, pool_k, pool_v, q, dtype="f16", nthreads=1):
+    """O1 applied to a prefill chunk (PD fusion; R24): chunk i holds
+    query tokens at positions q_start[i] + j, j < q_len[i]; each attends causally to keys
+    0..q_start[i]+j of its request -- exactly the decode formula with ctx = position + 1.
+    q uint16 [sum q_len][Hq][d] (chunks concatenated); block_table int32 [n][W] (one row per
+    chunk).  Returns float64 [sum q_len][Hq][d]."""
+    q_start = np.asarray(q_start, np.int64)
+    q_len = np.asarray(q_len, np.int64)
+    bt = np.ascontiguousarray(block_table, dtype=np.int32)
+    rows_ctx = np.concatenate([s + np.arange(n) + 1 for s, n in zip(q_start, q_len)]).astype(np.int32)
+    rows_bt = np.repeat(bt, q_len, axis=0)
+    return paged_decode_attention(rows_ctx, rows_bt, pool_k, pool_v, q, dtype, nthreads)
+
+
 def max_threads() -> int:
     return int(lib().oracle_max_threads())
 

@@ -18,7 +18,8 @@ import numpy as np
 
 from . import _lib
 from ._lib import (DbkError, dbk_batch, dbk_engine_buffers, dbk_engine_config,  # noqa: F401
-                   dbk_pool_config, dbk_sched_config, dbk_sched_state, dbk_stats, dbk_step_record)
+                   dbk_pool_config, dbk_prefill_batch, dbk_sched_config, dbk_sched_state, dbk_stats,
+                   dbk_step_record)
 
 _lib.lib()  # load now: no silent fallback
 
@@ -112,6 +113,13 @@ class KVPool:
         ids, pids = _i64(req_ids)
         b = dbk_batch(len(ids), int(layer), 1 if fuse_stats else 0, 0, pids)
         _lib.dbk_decode_step(self.h, C.byref(b), _ptr(q), _ptr(out), int(out_dtype), _stream(stream))
+
+    def prefill_step(self, req_ids, q_start, q_len, layer, q, out, out_dtype=2, stream=None):
+        ids, pids = _i64(req_ids)
+        s0, ps0 = _i32(q_start)
+        ln, pln = _i32(q_len)
+        b = dbk_prefill_batch(len(ids), int(layer), pids, ps0, pln)
+        _lib.dbk_prefill_step(self.h, C.byref(b), _ptr(q), _ptr(out), int(out_dtype), _stream(stream))
 
     def batch_stats(self, stream=None):
         st = dbk_stats()

@@ -44,6 +44,11 @@ class dbk_batch(C.Structure):
                 ("_reserved", C.c_int32), ("req_ids", C.POINTER(C.c_int64))]
 
 
+class dbk_prefill_batch(C.Structure):
+    _fields_ = [("n", C.c_int32), ("layer", C.c_int32), ("req_ids", C.POINTER(C.c_int64)),
+                ("q_start", C.POINTER(C.c_int32)), ("q_len", C.POINTER(C.c_int32))]
+
+
 STATS_FIELDS = ("n_active", "sum_ctx", "sum_ctx_sq", "max_ctx", "sum_pages", "cap_pages",
                 "free_pages", "over_cap", "table_mismatch", "n_finished", "fin_sum_lin",
                 "fin_sum_lin_sq", "fin_sum_lout", "fin_sum_lout_sq", "step_ns", "n_waiting")
@@ -120,6 +125,7 @@ SIGNATURES = {
     "dbk_pool_get_info": [P, C.POINTER(dbk_pool_info)],
     "dbk_decode_step": [P, C.POINTER(dbk_batch), P, P, I32, P],
     "dbk_batch_stats": [P, C.POINTER(dbk_stats), P],
+    "dbk_prefill_step": [P, C.POINTER(dbk_prefill_batch), P, P, I32, P],
     "dbk_synth_fill": [U64, I32, I32, PI64, PI32, I32, I32, I32, I32, I32, P, P],
     "dbk_probe_read_bandwidth": [P, C.c_size_t, I32, P, C.POINTER(C.c_double)],
     "dbk_sched_create": [C.POINTER(dbk_sched_config), C.POINTER(P)],

@@ -92,6 +92,30 @@ struct BtDelta {
     int32_t slot, idx, val;
 };
 
+// K7 (chunked prefill): one tile = up to 128 / group query tokens of one request's chunk.
+struct PrefTile {
+    int32_t slot;      // block-table row
+    int32_t q_start;   // position of the chunk's first token
+    int32_t j0;        // first chunk token of this tile
+    int32_t rows_tok;  // tokens in this tile
+    int32_t q_row0;    // row of the chunk's first token in q / out ([rows][q_heads][D])
+    int32_t _pad[3];
+};
+static_assert(sizeof(PrefTile) == 32, "PrefTile layout");
+
+struct PrefillParams {
+    const int32_t *block_table;
+    int32_t bt_stride;
+    int32_t layer;
+    int64_t cap_pages;
+    int32_t kv_heads, q_heads;
+    const PrefTile *tiles;
+    const void *q;       // [rows][q_heads][D], pool dtype
+    void *out;           // [rows][q_heads][D]
+    int32_t out_dtype;
+    float scale_log2;
+};
+
 // launchers (return cudaGetLastError() of the launch)
 // tmap != nullptr and group >= 2 selects K2 (tensor cores); otherwise K1 (CUDA cores).
 // Persistent launch of min(ctas, p.n_tasks) CTAs (ctas = SMs x resident CTAs per SM).
@@ -110,6 +134,10 @@ cudaError_t launch_synth_rows(uint64_t seed, int kind, int n_rows, const int64_t
 cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
                            int q_heads, int d, int scale_log2, int dtype, void *q, cudaStream_t s);
 int decode_ctas_per_sm(int kv_dtype, int head_dim, int group);
+// K7: grid (n_tiles, kv_heads); needs the pool's 5-D tensor map.
+cudaError_t launch_prefill(const PrefillParams &p, int kv_dtype, int head_dim, int group, int n_tiles,
+                           int kv_heads, const CUtensorMap &tmap, cudaStream_t s);
+int prefill_rows_per_tile();
 cudaError_t launch_read_probe(const void *buf, size_t bytes, uint32_t *sink, int sms, cudaStream_t s);
 
 }  // namespace dbk

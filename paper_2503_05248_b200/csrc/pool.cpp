@@ -102,7 +102,7 @@ using namespace dbk;
 
 // K2's tensor map over the whole pool: a 2-D tensor of rows = layers*cap*kv_heads*2*16
 // token rows x head_dim elements; one box = 16 rows x 64 elements with the 128-byte swizzle.
-static bool make_pool_tmap(dbk_pool *p, bool try5) {
+static bool make_pool_tmap(dbk_pool *p, bool try5, CUtensorMap *dst, int *rank) {
     const dbk_pool_config &c = p->cfg;
     const uint64_t tiles = static_cast<uint64_t>(c.layers) * c.cap_pages * c.kv_heads;  // (layer, page, head)
     if (tiles * 2 * c.page_size >= (1ull << 31)) return false;  // int32 TMA coordinates
@@ -122,22 +122,23 @@ static bool make_pool_tmap(dbk_pool *p, bool try5) {
         const cuuint64_t gstride[4] = {row, 128, row * c.page_size, row * c.page_size * 2};
         const cuuint32_t box[5] = {64, static_cast<cuuint32_t>(c.page_size), halves, 2, 1};
         const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-        if (encode(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, p->kv, gdim, gstride, box, estr,
+        if (encode(dst, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, p->kv, gdim, gstride, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
-            p->tma_rank = 5;
+            *rank = 5;
             return true;
         }
+        if (dst == &p->ptmap) return false;  // K7 needs the 5-D boxes
     }
     // Fallback: 2-D rows x d, boxes of 16 rows x 64 elements (2 * d/64 boxes per tile).
     const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(c.head_dim), tiles * 2 * c.page_size};
     const cuuint64_t gstride[1] = {row};
     const cuuint32_t box[2] = {64, 16};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->kv, gdim, gstride, box, estr,
+    const CUresult r = encode(dst, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->kv, gdim, gstride, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    p->tma_rank = 2;
+    *rank = 2;
     return r == CUDA_SUCCESS;
 }
 
@@ -207,7 +208,10 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     const int group = cfg->q_heads / cfg->kv_heads;
     const char *cc = std::getenv("DBK_GQA_CUDA_CORE");  // 1: force K1 for GQA (comparison runs)
     const char *t2 = std::getenv("DBK_GQA_TMA2");  // 1: force the 2-D boxes (comparison runs)
-    if (group >= 2 && !(cc && cc[0] == '1')) p->has_tmap = make_pool_tmap(p, !(t2 && t2[0] == '1'));
+    if (group >= 2 && !(cc && cc[0] == '1'))
+        p->has_tmap = make_pool_tmap(p, !(t2 && t2[0] == '1'), &p->tmap, &p->tma_rank);
+    int prank = 0;
+    p->has_ptmap = make_pool_tmap(p, true, &p->ptmap, &prank);
     p->ctas_per_sm = p->has_tmap ? decode_gqa_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group)
                                  : decode_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group);
     if (const char *e = std::getenv("DBK_CHUNK_PAGES")) {  // tuning override (multiple of 4, <= 64)
@@ -232,6 +236,8 @@ dbk_status dbk_kv_pool_destroy(dbk_pool *p) {
     p->up_append.release();
     p->up_meta.release();
     p->up_rows.release();
+    p->up_pref.release();
+    if (p->up_pref.done) cudaEventDestroy(p->up_pref.done);
     if (p->up_delta.done) cudaEventDestroy(p->up_delta.done);
     if (p->up_append.done) cudaEventDestroy(p->up_append.done);
     if (p->up_meta.done) cudaEventDestroy(p->up_meta.done);
@@ -606,6 +612,67 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
                            p->has_tmap ? &p->tmap : nullptr, s));
     ++p->n_launches;
     p->last_decode_bytes = decode_bytes(p, out_dtype);
+    return DBK_OK;
+}
+
+extern "C" dbk_status dbk_prefill_step(dbk_pool *p, const dbk_prefill_batch *b, const void *q, void *out,
+                                       int32_t out_dtype, void *stream) {
+    if (!p || !b) return fail(DBK_EINVAL, "prefill_step: null argument");
+    if (b->n < 0 || (b->n > 0 && (!b->req_ids || !b->q_start || !b->q_len || !q || !out)))
+        return fail(DBK_EINVAL, "prefill_step: bad arrays");
+    if (b->layer < 0 || b->layer >= p->cfg.layers) return fail(DBK_EINVAL, "prefill_step: layer out of range");
+    if (out_dtype < 0 || out_dtype > 2) return fail(DBK_EINVAL, "prefill_step: out_dtype must be 0, 1 or 2");
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
+        return fail(DBK_EINVAL, "prefill_step: q and out must be 16-byte aligned");
+    if (!p->has_ptmap) return fail(DBK_EINVAL, "prefill_step: pool has no 5-D tensor map");
+    const int group = p->cfg.q_heads / p->cfg.kv_heads;
+    const int qb = prefill_rows_per_tile() / group;  // chunk tokens per tile
+    p->pref_tiles.clear();
+    int64_t row = 0, flops = 0;
+    for (int i = 0; i < b->n; ++i) {
+        auto it = p->reqs.find(b->req_ids[i]);
+        if (it == p->reqs.end())
+            return fail(DBK_ENOENT, "prefill_step: unknown request %lld", static_cast<long long>(b->req_ids[i]));
+        const Request &r = it->second;
+        const int32_t s0 = b->q_start[i], len = b->q_len[i];
+        if (s0 < 0 || len < 1 || static_cast<int64_t>(s0) + len > r.ctx)
+            return fail(DBK_EINVAL, "prefill_step: chunk %d [%d, %d) outside the %d tokens held", i, s0, s0 + len,
+                        r.ctx);
+        for (int32_t j0 = 0; j0 < len; j0 += qb) {
+            PrefTile t{};
+            t.slot = r.slot;
+            t.q_start = s0;
+            t.j0 = j0;
+            t.rows_tok = std::min(qb, len - j0);
+            t.q_row0 = static_cast<int32_t>(row);
+            p->pref_tiles.push_back(t);
+        }
+        // algorithmic flops: QK^T and PV over the causal triangle, 4 d per (query head, key)
+        for (int64_t j = 0; j < len; ++j) flops += 4LL * p->cfg.head_dim * p->cfg.q_heads * (s0 + j + 1);
+        row += len;
+    }
+    if (row >= (1LL << 31) / p->cfg.q_heads) return fail(DBK_EINVAL, "prefill_step: too many rows");
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DBK_TRY(flush_deltas(p, s));
+    if (b->n == 0) return DBK_OK;
+    DBK_TRY(p->up_pref.upload(p->pref_tiles.data(), p->pref_tiles.size() * sizeof(PrefTile), s));
+    PrefillParams pp;
+    pp.block_table = p->d_bt;
+    pp.bt_stride = p->cfg.max_pages_per_req;
+    pp.layer = b->layer;
+    pp.cap_pages = p->cfg.cap_pages;
+    pp.kv_heads = p->cfg.kv_heads;
+    pp.q_heads = p->cfg.q_heads;
+    pp.tiles = static_cast<const PrefTile *>(p->up_pref.dev);
+    pp.q = q;
+    pp.out = out;
+    pp.out_dtype = out_dtype;
+    pp.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(p->cfg.head_dim)));
+    DBK_CUDA(launch_prefill(pp, p->cfg.kv_dtype, p->cfg.head_dim, group, static_cast<int>(p->pref_tiles.size()),
+                            p->cfg.kv_heads, p->ptmap, s));
+    ++p->n_launches;
+    p->last_prefill_flops = flops;
     return DBK_OK;
 }
 

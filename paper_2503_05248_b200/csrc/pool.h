@@ -76,4 +76,10 @@ struct dbk_pool {
     alignas(64) CUtensorMap tmap;
     bool has_tmap = false;
     int tma_rank = 0;                         // 5: one box per tile; 2: 2*d/64 boxes per tile
+    // K7 (chunked prefill, any group size): always the 5-D one-box-per-tile map
+    alignas(64) CUtensorMap ptmap;
+    bool has_ptmap = false;
+    dbk::UploadBuffer up_pref;
+    std::vector<dbk::PrefTile> pref_tiles;
+    int64_t last_prefill_flops = 0;
 };

@@ -1,0 +1,110 @@
+"""GPU parity of K7 (chunked-prefill attention on tcgen05) through the
+C-ABI against the oracle (O1 with ctx = position + 1 per query row, R24).
+Bar: 2e-3 relative per row (fp32 out), as for decode (R23)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import attention as oatt  # noqa: E402
+from oracle.allocator import PagedKV  # noqa: E402
+from synth import hashgen  # noqa: E402
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def dbk():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from conftest import build_lib
+    build_lib()
+    import paper_2503_05248_b200 as m
+    return m
+
+
+def row_err(got, want):
+    return (np.abs(got - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)).max()
+
+
+def run_prefill_case(dbk, L, Hq, Hkv, d, dtype, ctx, q_start, q_len, seed=3, layer=1, out_dtype=2,
+                     q_scale_log2=0):
+    P = 16
+    n = len(ctx)
+    ctx = np.asarray(ctx, np.int32)
+    q_start = np.asarray(q_start, np.int32)
+    q_len = np.asarray(q_len, np.int32)
+    cap = int(sum(-(-ctx // P))) + 5
+    pool = dbk.KVPool(L, Hq, Hkv, d, cap, n + 2, int(max(-(-ctx // P))) + 1, dtype)
+    ref = PagedKV(cap, P)
+    ids = np.arange(n, dtype=np.int64) * 104729 + 5
+    for r, c in zip(ids, ctx):
+        pool.request_begin(r, int(c), 1)
+        ref.begin(int(r))
+    # two appends: pages of different requests interleave physically
+    first = ctx // 3
+    for part in (first, ctx - first):
+        pool.append_tokens(ids, part, seed=seed)
+        ref.append([int(r) for r in ids], [int(x) for x in part])
+    for r in ids:
+        c, slot, pages = pool.request_info(r)
+        assert c == ref.ctx[int(r)] and pages == ref.pages[int(r)]
+    qb = np.concatenate([
+        hashgen.to_bits(hashgen.gen_values(seed, hashgen.KIND_Q, int(r), np.arange(s, s + m)[:, None], layer,
+                                           np.arange(Hq)[None, :], d, q_scale_log2), dtype)
+        for r, s, m in zip(ids, q_start, q_len)])
+    q = torch.from_numpy(np.ascontiguousarray(qb).view(np.int16)).cuda()
+    tdt = {2: torch.float32, 0: torch.float16, 1: torch.bfloat16}[out_dtype]
+    out = torch.full((int(q_len.sum()), Hq, d), float("nan"), dtype=tdt, device="cuda")
+    pool.prefill_step(ids, q_start, q_len, layer, q, out, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    bt, pk, pv, _ = oatt.synth_paged_batch(seed, [int(r) for r in ids], ctx, [ref.pages[int(r)] for r in ids],
+                                           layer, Hq, Hkv, d, P, dtype, n_phys=cap)
+    want = oatt.paged_prefill_attention(q_start, q_len, bt, pk, pv, qb, dtype, nthreads=8)
+    got = out.float().cpu().numpy().astype(np.float64)
+    info = pool.info()
+    pool.close()
+    return got, want, info
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("Hq,Hkv,d", [(4, 4, 128), (8, 8, 64), (8, 2, 128), (16, 2, 64), (32, 4, 128)])
+def test_prefill_parity_shapes(dbk, dtype, Hq, Hkv, d):
+    # whole prompts (q_start 0), ragged chunk tails, chunks ending before ctx, 1-token chunks
+    ctx = [1, 16, 17, 70, 129, 300, 700, 64, 33]
+    q_start = [0, 0, 0, 0, 64, 100, 0, 63, 5]
+    q_len = [1, 16, 17, 70, 65, 200, 700, 1, 20]
+    got, want, _ = run_prefill_case(dbk, 2, Hq, Hkv, d, dtype, ctx, q_start, q_len)
+    assert not np.isnan(got).any()
+    assert row_err(got, want) <= TOL
+
+
+@pytest.mark.parametrize("out_dtype", [0, 1])
+def test_prefill_parity_out_dtypes_and_peaked_q(dbk, out_dtype):
+    got, want, _ = run_prefill_case(dbk, 1, 8, 8, 128, "bf16", [200, 45], [0, 30], [200, 15], layer=0,
+                                    out_dtype=out_dtype, q_scale_log2=4)
+    tol = 8e-3 if out_dtype == 1 else 2e-3  # output rounding: half an ulp of bf16 / fp16
+    assert row_err(got, want) <= tol
+
+
+def test_prefill_long_context_gqa(dbk):
+    # 4096-token prompt on the 70B head layout (8 q heads per kv head): many 16-token tiles
+    got, want, _ = run_prefill_case(dbk, 1, 16, 2, 128, "bf16", [4096, 2500], [3584, 2000], [512, 500], layer=0)
+    assert row_err(got, want) <= TOL
+
+
+def test_prefill_rejects_bad_chunks(dbk):
+    pool = dbk.KVPool(1, 4, 4, 64, 8, 2, 4, "f16")
+    pool.request_begin(1, 10, 1)
+    pool.append_tokens([1], [10], seed=1)
+    q = torch.zeros(16, 4, 64, dtype=torch.float16, device="cuda")
+    out = torch.zeros(16, 4, 64, dtype=torch.float32, device="cuda")
+    with pytest.raises(dbk.DbkError):
+        pool.prefill_step([1], [5], [6], 0, q, out)   # beyond the 10 tokens held
+    with pytest.raises(dbk.DbkError):
+        pool.prefill_step([2], [0], [1], 0, q, out)   # unknown request
+    with pytest.raises(dbk.DbkError):
+        pool.prefill_step([1], [0], [0], 0, q, out)   # empty chunk
+    pool.prefill_step([], [], [], 0, q, out)          # empty batch: no-op
+    pool.close()

@@ -76,6 +76,48 @@ def test_paged_matches_dense_bruteforce(dtype, Hq, Hkv, d, q_scale_log2):
             np.testing.assert_allclose(out[i, h], t, rtol=1e-12, atol=1e-14)
 
 
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+def test_prefill_oracle_matches_dense_causal_attention(dtype):
+    """Pin of the chunked-prefill reading (R24): every chunk row equals dense causal
+    attention over the request's whole prefix (torch SDPA with an explicit bottom-right
+    causal mask, no paging)."""
+    rng = np.random.default_rng(3)
+    P, seed, layer, Hq, Hkv, d = 16, 5, 1, 4, 2, 64
+    ctx = np.array([40, 17, 70])
+    q_start = np.array([0, 9, 33])
+    q_len = ctx - q_start
+    npg = [-(-int(c) // P) for c in ctx]
+    perm = rng.permutation(sum(npg) + 3)
+    pages, k = [], 0
+    for m in npg:
+        pages.append([int(x) for x in perm[k:k + m]])
+        k += m
+    req_ids = [101, 7, 1 << 33]
+    bt, pk, pv, _ = oatt.synth_paged_batch(seed, req_ids, ctx, pages, layer, Hq, Hkv, d, P, dtype)
+    qrows = [hashgen.to_bits(hashgen.gen_values(seed, hashgen.KIND_Q, r, np.arange(s, c)[:, None], layer,
+                                                np.arange(Hq)[None, :], d), dtype)
+             for r, s, c in zip(req_ids, q_start, ctx)]
+    out = oatt.paged_prefill_attention(q_start, q_len, bt, pk, pv, np.concatenate(qrows), dtype)
+    conv = oatt.lib().oracle_half_to_double if dtype == "f16" else oatt.lib().oracle_bf16_to_double
+    row = 0
+    for i, (r, s, c) in enumerate(zip(req_ids, q_start, ctx)):
+        K = hashgen.gen_values(seed, hashgen.KIND_K, r, np.arange(c)[:, None], layer, np.arange(Hkv)[None, :], d)
+        V = hashgen.gen_values(seed, hashgen.KIND_V, r, np.arange(c)[:, None], layer, np.arange(Hkv)[None, :], d)
+        # round K/V/q through the storage dtype exactly as the pool holds them
+        rnd = np.vectorize(lambda b: conv(int(b)))
+        K = rnd(hashgen.to_bits(K, dtype))
+        V = rnd(hashgen.to_bits(V, dtype))
+        Q = rnd(qrows[i])  # [c-s][Hq][d]
+        mask = np.arange(c)[None, :] <= np.arange(s, c)[:, None]
+        for h in range(Hq):
+            g = h // (Hq // Hkv)
+            t = torch.nn.functional.scaled_dot_product_attention(
+                torch.from_numpy(Q[:, h])[None, None], torch.from_numpy(K[:, g])[None, None],
+                torch.from_numpy(V[:, g])[None, None], attn_mask=torch.from_numpy(mask)[None, None])[0, 0].numpy()
+            np.testing.assert_allclose(out[row:row + c - s, h], t, rtol=1e-12, atol=1e-14)
+        row += c - s
+
+
 def test_ctx_one_returns_v0_exactly():
     rng = np.random.default_rng(1)
     req_ids, ctx, pages, bt, pk, pv, q = _random_case(rng, 6, 4, 4, 64, 16, "f16", 5, max_ctx=1)
