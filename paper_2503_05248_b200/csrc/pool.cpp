@@ -120,7 +120,9 @@ static bool make_pool_tmap(dbk_pool *p, bool try5, CUtensorMap *dst, int *rank) 
     if (try5) {
         const cuuint64_t gdim[5] = {64, static_cast<cuuint64_t>(c.page_size), halves, 2, tiles};
         const cuuint64_t gstride[4] = {row, 128, row * c.page_size, row * c.page_size * 2};
-        const cuuint32_t box[5] = {64, static_cast<cuuint32_t>(c.page_size), halves, 2, 1};
+        // K7 (prefill) fetches each d-half of K and V separately: box {64, 16, 1, 1, 1}
+        const bool split = dst == &p->ptmap;
+        const cuuint32_t box[5] = {64, static_cast<cuuint32_t>(c.page_size), split ? 1u : halves, split ? 1u : 2u, 1};
         const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
         if (encode(dst, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, p->kv, gdim, gstride, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

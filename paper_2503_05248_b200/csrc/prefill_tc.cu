@@ -4,17 +4,22 @@
 //
 // Query token j of a request's prefill chunk sits at position p = q_start + j and attends
 // causally to keys 0..p of that request's paged KV (the chunk's own K/V already appended).
-// CTA = (tile of 128 query rows, kv head g); a row is (chunk token, q-head of the group),
-// token-major, so GQA groups share every K/V page.  Warp roles (192 threads):
-//   warp 4      TMA producer: one 5-D tensor-map box per (page, kv head) tile into a ring
-//   warp 5      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 0..3  softmax / O correction / epilogue, thread t <-> TMEM lane t <-> query row t
-// Per block of 4 pages (64 keys): S = Q K^T (M = 128, N = 16 per page, K = d) lands in TMEM
-// (double buffered); the softmax threads read their row with tcgen05.ld, keep a per-row
-// running max in log2 units (O is rescaled in TMEM only when the max grows by > 2^8, so P
-// stays <= 256), write P to shared memory in the canonical no-swizzle K-major layout, and
-// O += P V runs as M = 128, N = d, K = 16 per page with V as an MN-major 128B-swizzled
-// operand straight from the TMA tile.  bf16 keeps P to ~16 bits with a hi + lo split.
+// A row is (chunk token, q-head of the kv group), token-major, so the GQA group shares every
+// K/V page.  CTA = (pair of 128-row tiles A, B of one chunk, kv head g): both tiles consume
+// the same K/V blocks (half the shared-memory traffic per flop of a single tile).
+//   warp 8       TMA producer: 64-key blocks (4 pages) into a ring of block stages laid out
+//                [K|V][d/64][64 keys][128 B] (128B swizzle), 4 boxes per page
+//   warp 9       TMEM allocator (all 512 columns) + single-thread tcgen05.mma issuer
+//   warps 0..3   softmax / correction / epilogue of tile A (thread t <-> TMEM lane t <-> row)
+//   warps 4..7   the same for tile B
+// Per 64-key block b and tile: S = Q K^T (M = 128, N = 64, K = d) lands in TMEM (double
+// buffered); the softmax threads read their row with tcgen05.ld, keep a running max in log2
+// units (O is rescaled in TMEM only when the max grows by > 2^8, so P <= 256), and write P
+// back over S as packed 16-bit pairs; O += P V then takes A = P straight from TMEM
+// (tcgen05.mma ... [tmem_a]) and B = V as an MN-major 128B-swizzled operand.  bf16 keeps P
+// to ~16 bits with a hi + lo split (two PV MMAs per 16 keys).  S(b+2) reuses the columns of
+// P(b), so it is issued only after PV(b) has completed (measured: without that wait the
+// tensor pipe can let S(b+2) overwrite P(b) while PV(b) still reads it).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -28,10 +33,10 @@ namespace dbk {
 namespace {
 using namespace dev;
 
-constexpr int kRows = 128;     // MMA M: query rows per tile
-constexpr int kNB = 4;         // pages per softmax block (64 keys)
-constexpr int kStages = 12;    // page-tile ring depth (>= 2 blocks in flight)
-constexpr int kThreads = 192;  // 4 softmax warps + producer + MMA
+constexpr int kRows = 128;      // MMA M: query rows per tile
+constexpr int kBK = 64;         // keys per block (4 pages)
+constexpr int kThreads = 320;   // 2 x 4 softmax warps + producer + MMA
+constexpr int kTileCols = 256;  // TMEM columns per tile: S0 | S1 (64 each) | O (d <= 128)
 
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     return static_cast<uint64_t>((addr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(lbo >> 4) << 16) |
@@ -48,6 +53,13 @@ __device__ __forceinline__ void umma_ss(uint32_t tmem_d, uint64_t a, uint64_t b,
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -57,8 +69,7 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-    uint32_t r[32];
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -67,294 +78,316 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
-#pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
 }
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
         "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
-        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
-        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])),
-        "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])), "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])),
-        "r"(__float_as_uint(v[20])), "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
-        "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])), "r"(__float_as_uint(v[27])),
-        "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31])));
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tma_tile5(void *dst, const CUtensorMap *map, int tile, uint64_t *bar) {
+// one {64 elements x 16 tokens} box (2 KiB) of the (page, kv head) tile: d-half h of K or V
+__device__ __forceinline__ void tma_box(void *dst, const CUtensorMap *map, int h, int kv, int tile, uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %2, %2, %2, %3}], [%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(tile), "r"(smem_u32(bar))
+        " [%0], [%1, {%2, %2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(h), "r"(kv), "r"(tile), "r"(smem_u32(bar))
         : "memory");
 }
 
-template <typename T, int D, int GQ>
+template <typename T, int D, int GQ, int STG>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int NBOX = D / 64;
-    constexpr int TILE = 2 * NBOX * 2048;            // K | V of one (page, kv head)
-    constexpr int QBYTES = NBOX * kRows * 128;       // Q tile, [half][row][128 B], 128B swizzle
-    constexpr int PSLICE = kRows * 16 * 2;           // P of one page: 128 rows x 16 keys
+    constexpr int HALF = kBK * 128;                  // one d-half of K or V of a block: 8 KiB
+    constexpr int STAGE = 2 * NBOX * HALF;           // K | V of a 64-key block
+    constexpr int QT = NBOX * kRows * 128;           // Q of one tile, [half][row][128 B]
     constexpr bool kBF16 = std::is_same<T, __nv_bfloat16>::value;
-    constexpr int NPBUF = kBF16 ? 2 : 1;             // hi (+ lo) parts of P
     constexpr int KSTEPS = D / 16;
     constexpr uint32_t kFmt = kBF16 ? 1u : 0u;
-    constexpr uint32_t ID_S = idesc_f16(kFmt, 0, kRows, 16);  // S = Q K^T per page
-    constexpr uint32_t ID_O = idesc_f16(kFmt, 1, kRows, D);   // O += P V per page (V MN-major)
-    constexpr int S_COLS = kNB * 16;                // TMEM columns per S buffer
-    constexpr uint32_t TM_COLS = (2 * S_COLS + D) <= 256 ? 256 : 512;
+    constexpr uint32_t ID_S = idesc_f16(kFmt, 0, kRows, kBK);  // S = Q K^T per block
+    constexpr uint32_t ID_O = idesc_f16(kFmt, 1, kRows, D);    // O += P V per 16 keys
+    constexpr int QB = kRows / GQ;                            // chunk tokens per tile
 
     extern __shared__ uint8_t smem_raw[];
-    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-    __shared__ __align__(8) uint64_t s_full[2], s_free[2], p_full, pv_done[2], q_ready;
+    __shared__ __align__(8) uint64_t kv_full[STG], kv_empty[STG];
+    __shared__ __align__(8) uint64_t s_full[2][2], p_full[2][2], pv_done[2], q_ready;
     __shared__ uint32_t tmem_base_sh;
 
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t *q_s = smem;
-    uint8_t *ring = smem + QBYTES;
-    uint8_t *p_s = ring + kStages * TILE;
+    uint8_t *q_s = smem;                 // [tile][half][row][128 B]
+    uint8_t *ring = smem + 2 * QT;       // [stage][K|V][half][key][128 B]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const PrefTile tl = p.tiles[blockIdx.x];
     const int g = blockIdx.y;
-    const int p_last = tl.q_start + tl.j0 + tl.rows_tok - 1;  // last query position of the tile
-    const int n_keys = p_last + 1;
+    const int pos0 = tl.q_start + tl.j0;              // position of the pair's first token
+    const int n_keys = pos0 + tl.rows_tok;            // keys seen by the pair's last token
     const int n_pages = (n_keys + kP - 1) / kP;
-    const int n_blk = (n_pages + kNB - 1) / kNB;
+    const int n_blk = (n_keys + kBK - 1) / kBK;
+    const bool has_b = tl.rows_tok > QB;
+    const int nblk_a = (pos0 + min(QB, tl.rows_tok) - 1) / kBK + 1;
     const int32_t *bt_row = p.block_table + static_cast<size_t>(tl.slot) * p.bt_stride;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+        for (int s = 0; s < STG; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
         }
-        for (int k = 0; k < 2; ++k) {
-            mbar_init(&s_full[k], 1);
-            mbar_init(&s_free[k], kRows);
-            mbar_init(&pv_done[k], 1);
+        for (int t = 0; t < 2; ++t) {
+            for (int k = 0; k < 2; ++k) {
+                mbar_init(&s_full[t][k], 1);
+                mbar_init(&p_full[t][k], kRows);
+            }
+            mbar_init(&pv_done[t], 1);
         }
-        mbar_init(&p_full, kRows);
-        mbar_init(&q_ready, kRows);
+        mbar_init(&q_ready, 2 * kRows);
         fence_mbar_init();
     }
-    if (warp == 5) {
+    if (warp == 9) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                     "r"(TM_COLS));
+                     "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
-    const uint32_t tm_s = tmem, tm_o = tmem + 2 * S_COLS;
 
-    if (warp == 4) {
-        // ---------------- TMA producer
+    if (warp == 8) {
+        // ---------------- TMA producer: block b = pages 4b .. 4b+3 into stage b % STG
         const int64_t tile_layer = static_cast<int64_t>(p.layer) * p.cap_pages;
-        for (int base = 0; base < n_pages; base += 32) {
-            const int ph_lane = base + lane < n_pages ? __ldg(bt_row + base + lane) : 0;
-            const int cnt = min(32, n_pages - base);
-            for (int k = 0; k < cnt; ++k) {
-                const int gi = base + k;
-                const int ph = __shfl_sync(kFull, ph_lane, k);
-                if (lane == 0) {
-                    const int st = gi % kStages;
-                    if (gi >= kStages) mbar_wait(&empty[st], ((gi / kStages) - 1) & 1);
-                    mbar_expect_tx(&full[st], TILE);
-                    tma_tile5(ring + st * TILE, &tmap, static_cast<int>((tile_layer + ph) * p.kv_heads + g), &full[st]);
-                }
+        for (int b = 0; b < n_blk; ++b) {
+            const int np = min(4, n_pages - 4 * b);
+            const int ph = lane < np ? __ldg(bt_row + 4 * b + lane) : 0;
+            const int st = b % STG;
+            if (lane == 0) {
+                if (b >= STG) mbar_wait(&kv_empty[st], ((b / STG) - 1) & 1);
+                mbar_expect_tx(&kv_full[st], np * 2 * NBOX * 2048);
+            }
+            __syncwarp();
+            if (lane < np) {
+                const int tile = static_cast<int>((tile_layer + ph) * p.kv_heads + g);
+                uint8_t *sb = ring + st * STAGE + lane * 2048;
+#pragma unroll
+                for (int kv = 0; kv < 2; ++kv)
+#pragma unroll
+                    for (int h = 0; h < NBOX; ++h) tma_box(sb + (kv * NBOX + h) * HALF, &tmap, h, kv, tile, &kv_full[st]);
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         // ---------------- MMA issuer (one thread)
         if (lane == 0) {
             mbar_wait(&q_ready, 0);
             tc_fence_after();
-            const uint32_t q_addr = smem_u32(q_s), ring_addr = smem_u32(ring), p_addr = smem_u32(p_s);
+            const uint32_t q_addr = smem_u32(q_s), ring_addr = smem_u32(ring);
             auto issue_pv = [&](int c) {
-                mbar_wait(&p_full, c & 1);
-                tc_fence_after();
-                const int np = min(kNB, n_pages - c * kNB);
-                for (int pj = 0; pj < np; ++pj) {
-                    const int gi = c * kNB + pj, st = gi % kStages;
-                    const uint64_t vdesc = smem_desc(ring_addr + st * TILE + NBOX * 2048, 2048, 1024, 2);
+                const int st = c % STG;
+                for (int t = 0; t < 2; ++t) {
+                    if (t == 0 ? c >= nblk_a : !has_b) continue;
+                    mbar_wait(&p_full[t][c & 1], (c >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t tp = tmem + t * kTileCols + (c & 1) * 64, to = tmem + t * kTileCols + 128;
 #pragma unroll
-                    for (int h = 0; h < NPBUF; ++h) {
-                        const uint64_t pdesc = smem_desc(p_addr + (h * kNB + pj) * PSLICE, 128, 256, 0);
-                        umma_ss(tm_o, pdesc, vdesc, ID_O, (c > 0 || pj > 0 || h > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t vdesc = smem_desc(ring_addr + st * STAGE + NBOX * HALF + kk * 2048, HALF, 1024, 2);
+                        umma_ts(to, tp + kk * 8, vdesc, ID_O, (c > 0 || kk > 0) ? 1u : 0u);
+                        if constexpr (kBF16) umma_ts(to, tp + 32 + kk * 8, vdesc, ID_O, 1u);
                     }
-                    umma_commit(&empty[st]);
+                    umma_commit(&pv_done[t]);
                 }
-                umma_commit(&pv_done[c & 1]);
+                umma_commit(&kv_empty[st]);
             };
             for (int b = 0; b < n_blk; ++b) {
-                if (b >= 2) mbar_wait(&s_free[b & 1], ((b >> 1) - 1) & 1);
+                const int st = b % STG;
+                mbar_wait(&kv_full[st], (b / STG) & 1);
                 tc_fence_after();
-                const int np = min(kNB, n_pages - b * kNB);
-                for (int pj = 0; pj < np; ++pj) {
-                    const int gi = b * kNB + pj, st = gi % kStages;
-                    mbar_wait(&full[st], (gi / kStages) & 1);
-                    tc_fence_after();
+                for (int t = 0; t < 2; ++t) {
+                    if (t == 0 ? b >= nblk_a : !has_b) continue;
+                    // S(b) overwrites P(b-2) in TMEM: PV(b-2) must have read it (the tensor
+                    // pipe orders accumulator hazards, not reads of a TMEM A operand)
+                    if (b >= 2) {
+                        mbar_wait(&pv_done[t], (b - 2) & 1);
+                        tc_fence_after();
+                    }
+                    const uint32_t ts = tmem + t * kTileCols + (b & 1) * 64;
 #pragma unroll
                     for (int kk = 0; kk < KSTEPS; ++kk) {
                         const uint32_t half = kk >> 2, koff = (kk & 3) * 32;
-                        const uint64_t qdesc = smem_desc(q_addr + half * (kRows * 128) + koff, 16, 1024, 2);
-                        const uint64_t kdesc = smem_desc(ring_addr + st * TILE + half * 2048 + koff, 16, 1024, 2);
-                        umma_ss(tm_s + (b & 1) * S_COLS + pj * 16, qdesc, kdesc, ID_S, kk > 0 ? 1u : 0u);
+                        const uint64_t qdesc = smem_desc(q_addr + t * QT + half * (kRows * 128) + koff, 16, 1024, 2);
+                        const uint64_t kdesc = smem_desc(ring_addr + st * STAGE + half * HALF + koff, 16, 1024, 2);
+                        umma_ss(ts, qdesc, kdesc, ID_S, kk > 0 ? 1u : 0u);
                     }
+                    umma_commit(&s_full[t][b & 1]);
                 }
-                umma_commit(&s_full[b & 1]);
                 if (b >= 1) issue_pv(b - 1);
             }
             issue_pv(n_blk - 1);
         }
         __syncwarp();
     } else {
-        // ---------------- softmax / correction / epilogue: thread t owns query row t
-        const int r = threadIdx.x;
-        const int jt = r / GQ;                     // token of this row within the tile
+        // ---------------- softmax / correction / epilogue: thread owns row r of tile t
+        const int t = warp >> 2;
+        const int r = threadIdx.x & 127;
+        const int jt = t * QB + r / GQ;            // token of this row within the pair
         const bool row_ok = jt < tl.rows_tok;
-        const int p_row = tl.q_start + tl.j0 + jt;
+        const int p_row = pos0 + jt;
         const int h = g * GQ + r % GQ;
-        // Q row -> shared memory, 128B-swizzled K-major (rows of the A operand)
-        {
+        {   // Q row -> shared memory, 128B-swizzled K-major (rows of the A operand)
             const T *src = reinterpret_cast<const T *>(p.q) +
                            (static_cast<size_t>(tl.q_row0 + tl.j0 + (row_ok ? jt : 0)) * p.q_heads + h) * D;
+            uint8_t *qt = q_s + t * QT;
 #pragma unroll
             for (int c = 0; c < D / 8; ++c) {
                 uint4 v = row_ok ? __ldg(reinterpret_cast<const uint4 *>(src) + c) : make_uint4(0u, 0u, 0u, 0u);
                 const int half = c >> 3, ch = c & 7;
-                *reinterpret_cast<uint4 *>(q_s + half * (kRows * 128) + r * 128 + ((ch ^ (r & 7)) << 4)) = v;
+                *reinterpret_cast<uint4 *>(qt + half * (kRows * 128) + r * 128 + ((ch ^ (r & 7)) << 4)) = v;
             }
             fence_proxy_async();
             mbar_arrive(&q_ready);
         }
-        const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+        const int my_blk = t == 0 ? nblk_a : (has_b ? n_blk : 0);
+        // the tile that processes the last block zeroes its never-valid V rows (P = 0 there,
+        // but 0 * NaN from never-written pool slots or stale shared memory would poison O)
+        const bool zero_tail = ((t == 0) == (nblk_a == n_blk)) && (n_keys & (kBK - 1)) != 0;
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t tm = tmem + t * kTileCols + lane_base;
+        const float c_log2 = p.scale_log2;
         float M = -INFINITY, L = 0.f;
-        for (int b = 0; b < n_blk; ++b) {
-            mbar_wait(&s_full[b & 1], (b >> 1) & 1);
+        for (int b = 0; b < my_blk; ++b) {
+            mbar_wait(&s_full[t][b & 1], (b >> 1) & 1);
             tc_fence_after();
-            float s[S_COLS];
-            tmem_ld32(tm_s + lane_base + (b & 1) * S_COLS, *reinterpret_cast<float(*)[32]>(s));
-            tmem_ld32(tm_s + lane_base + (b & 1) * S_COLS + 32, *reinterpret_cast<float(*)[32]>(s + 32));
+            const uint32_t ts = tm + (b & 1) * 64;
+            uint32_t u[64];
+            tmem_ld32(ts, *reinterpret_cast<uint32_t(*)[32]>(u));
+            tmem_ld32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
             tmem_ld_wait();
-            tc_fence_before();
-            mbar_arrive(&s_free[b & 1]);
+            float s[64];
             float bmax = -INFINITY;
+            const int vis = row_ok ? p_row - b * kBK : -1;  // keys k <= vis of this block are visible
+            if (vis >= kBK - 1) {
 #pragma unroll
-            for (int c = 0; c < S_COLS; ++c) {
-                const int key = b * S_COLS + c;
-                s[c] = (row_ok && key <= p_row) ? s[c] * p.scale_log2 : -INFINITY;
-                bmax = fmaxf(bmax, s[c]);
+                for (int k = 0; k < 64; ++k) {
+                    s[k] = __uint_as_float(u[k]);
+                    bmax = fmaxf(bmax, s[k]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 64; ++k) {
+                    s[k] = k <= vis ? __uint_as_float(u[k]) : -INFINITY;
+                    bmax = fmaxf(bmax, s[k]);
+                }
             }
-            if (b > 0) {  // PV of the previous block done: P buffer free, O stable
-                mbar_wait(&pv_done[(b - 1) & 1], ((b - 1) >> 1) & 1);
-                tc_fence_after();
-            }
-            const float m_new = fmaxf(M, bmax);
+            const float m_new = fmaxf(M, bmax * c_log2);
             const bool grow = m_new > M + 8.f;  // rescale only when the max grows by > 2^8
-            const float f = grow ? ((M == -INFINITY) ? 0.f : exp2f(M - m_new)) : 1.f;
             if (b > 0 && __any_sync(kFull, grow)) {
+                const float f = grow ? exp2f(M - m_new) : 1.f;
+                // O holds blocks < b.  Valid parity wait: S(b) implies PV(b-2) done (the MMA
+                // thread waited it), and PV(b) needs this block's P.
+                mbar_wait(&pv_done[t], (b - 1) & 1);
+                tc_fence_after();
 #pragma unroll
                 for (int c0 = 0; c0 < D; c0 += 32) {
-                    float o[32];
-                    tmem_ld32(tm_o + lane_base + c0, o);
+                    uint32_t o[32];
+                    tmem_ld32(tm + 128 + c0, o);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) o[k] *= f;
-                    tmem_st32(tm_o + lane_base + c0, o);
+                    for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * f);
+                    tmem_st32(tm + 128 + c0, o);
                 }
-                tmem_st_wait();
+                if (grow) L *= f;
             }
-            if (grow) {
-                L *= f;
-                M = m_new;
-            }
-            // P = exp2(s - M) (<= 2^8), stored per page as [16 row groups][2 k-halves][8 rows][16 B]
+            if (grow) M = m_new;
+            // P = exp2(s c - M) <= 2^8 as packed 16-bit pairs over S: hi in columns 0..31, lo in 32..63
+            const float nm = (M == -INFINITY) ? 0.f : -M;
 #pragma unroll
-            for (int pj = 0; pj < kNB; ++pj) {
-                float pv[16];
+            for (int k0 = 0; k0 < 64; k0 += 32) {
+                uint32_t hi[16], lo[16];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const float x = s[pj * 16 + k];
-                    pv[k] = (x == -INFINITY) ? 0.f : exp2f(x - M);
-                    L += pv[k];
-                }
-#pragma unroll
-                for (int kh = 0; kh < 2; ++kh) {
-                    float hi[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) hi[k] = pv[kh * 8 + k];
-                    const uint4 ph = pack8<T>(hi);
-                    uint8_t *dst = p_s + pj * PSLICE + (r >> 3) * 256 + kh * 128 + (r & 7) * 16;
-                    *reinterpret_cast<uint4 *>(dst) = ph;
+                for (int k = 0; k < 32; k += 2) {
+                    const float p0 = exp2f(fmaf(s[k0 + k], c_log2, nm)), p1 = exp2f(fmaf(s[k0 + k + 1], c_log2, nm));
+                    L += p0 + p1;
+                    hi[k >> 1] = Elt<T>::from_f2(p0, p1);
                     if constexpr (kBF16) {
-                        float lo[8], ht[8];
-                        unpack8<T>(ph, ht);
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) lo[k] = hi[k] - ht[k];
-                        *reinterpret_cast<uint4 *>(dst + kNB * PSLICE) = pack8<T>(lo);
+                        const float2 hf = Elt<T>::to_f2(hi[k >> 1]);
+                        lo[k >> 1] = Elt<T>::from_f2(p0 - hf.x, p1 - hf.y);
                     }
                 }
+                tmem_st16(ts + (k0 >> 1), hi);
+                if constexpr (kBF16) tmem_st16(ts + 32 + (k0 >> 1), lo);
             }
-            // never-written V slots of a partial last page could hold NaN: zero them (P = 0 there)
-            if (b == n_blk - 1 && (n_keys & (kP - 1))) {
-                const int gi = n_pages - 1, st = gi % kStages, v0 = n_keys & (kP - 1);
-                uint8_t *vt = ring + st * TILE + NBOX * 2048;
-                for (int x = r; x < (kP - v0) * NBOX * 8; x += kRows) {
+            if (zero_tail && b == n_blk - 1) {
+                uint8_t *vt = ring + (b % STG) * STAGE + NBOX * HALF;
+                const int v0 = n_keys & (kBK - 1);
+                for (int x = r; x < (kBK - v0) * NBOX * 8; x += kRows) {
                     const int row = v0 + x / (NBOX * 8), rem = x % (NBOX * 8);
-                    *reinterpret_cast<uint4 *>(vt + (rem >> 3) * 2048 + row * 128 + (rem & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
+                    *reinterpret_cast<uint4 *>(vt + (rem >> 3) * HALF + row * 128 + (rem & 7) * 16) = make_uint4(0u, 0u, 0u, 0u);
                 }
+                fence_proxy_async();
             }
-            fence_proxy_async();
+            tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(&p_full);
+            mbar_arrive(&p_full[t][b & 1]);
         }
-        // epilogue: O / L for this row
-        mbar_wait(&pv_done[(n_blk - 1) & 1], ((n_blk - 1) >> 1) & 1);
-        tc_fence_after();
-        const float inv = 1.f / L;
-        const size_t ob = (static_cast<size_t>(tl.q_row0 + tl.j0 + jt) * p.q_heads + h) * D;
+        if (my_blk > 0) {
+            // epilogue: O / L for this row.  A parity wait is only valid for the phase after
+            // the last completed one; S(my_blk-1) implies PV(my_blk-3) done, so wait the last
+            // two PV phases in order.
+            if (my_blk >= 2) mbar_wait(&pv_done[t], (my_blk - 2) & 1);
+            mbar_wait(&pv_done[t], (my_blk - 1) & 1);
+            tc_fence_after();
+            const float inv = 1.f / L;
+            const size_t ob = (static_cast<size_t>(tl.q_row0 + tl.j0 + jt) * p.q_heads + h) * D;
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-            float o[32];
-            tmem_ld32(tm_o + lane_base + c0, o);
-            tmem_ld_wait();
-            if (row_ok) {
+            for (int c0 = 0; c0 < D; c0 += 32) {
+                uint32_t o[32];
+                tmem_ld32(tm + 128 + c0, o);
+                tmem_ld_wait();
+                if (row_ok) {
 #pragma unroll
-                for (int k = 0; k < 32; k += 8) {
-                    float v8[8];
+                    for (int k = 0; k < 32; k += 8) {
+                        float v8[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) v8[e] = o[k + e] * inv;
-                    store8_out(p.out, ob + c0 + k, p.out_dtype, v8);
+                        for (int e = 0; e < 8; ++e) v8[e] = __uint_as_float(o[k + e]) * inv;
+                        store8_out(p.out, ob + c0 + k, p.out_dtype, v8);
+                    }
                 }
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == 9) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TM_COLS));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 
-template <typename T, int D>
+template <int D>
+constexpr int prefill_stages() {
+    return D == 128 ? 4 : 6;
+}
+template <int D>
 constexpr size_t prefill_smem() {
-    return static_cast<size_t>(D / 64) * kRows * 128 + static_cast<size_t>(kStages) * 2 * (D / 64) * 2048 +
-           (std::is_same<T, __nv_bfloat16>::value ? 2 : 1) * kNB * kRows * 32 + 1024;
+    return 2 * static_cast<size_t>(D / 64) * kRows * 128 +
+           static_cast<size_t>(prefill_stages<D>()) * 2 * (D / 64) * kBK * 128 + 1024;
 }
 
 template <typename T, int D, int GQ>
 cudaError_t launch_prefill_t(const PrefillParams &p, int n_tiles, int kv_heads, const CUtensorMap &tmap,
                              cudaStream_t s) {
-    auto kern = prefill_tc_kernel<T, D, GQ>;
-    constexpr size_t smem = prefill_smem<T, D>();
+    auto kern = prefill_tc_kernel<T, D, GQ, prefill_stages<D>()>;
+    constexpr size_t smem = prefill_smem<D>();
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -379,7 +412,7 @@ cudaError_t prefill_group(const PrefillParams &p, int group, int n_tiles, int kv
 
 }  // namespace
 
-int prefill_rows_per_tile() { return kRows; }
+int prefill_rows_per_tile() { return 2 * kRows; }
 
 cudaError_t launch_prefill(const PrefillParams &p, int kv_dtype, int head_dim, int group, int n_tiles,
                            int kv_heads, const CUtensorMap &tmap, cudaStream_t s) {
