@@ -85,6 +85,8 @@ def run_shape(dbk, torch, Hq, Hkv, d, n, S, q_start, reps=20, dtype="bf16"):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/prefill_bench.json")
+    ap.add_argument("--shape", type=int, default=-1, help="run only this shape index")
+    ap.add_argument("--reps", type=int, default=20)
     a = ap.parse_args()
     import torch
 
@@ -99,8 +101,10 @@ def main():
         (40, 40, 128, 8, 2048, 0),     # Llama-2-13B heads
     ]
     rows = []
+    if a.shape >= 0:
+        shapes = [shapes[a.shape]]
     for s in shapes:
-        r = run_shape(dbk, torch, *s)
+        r = run_shape(dbk, torch, *s, reps=a.reps)
         r["frac_of_peak"] = r["tflops"] / peak
         rows.append(r)
         print(json.dumps(r), flush=True)

@@ -9,7 +9,7 @@
 // the same K/V blocks (half the shared-memory traffic per flop of a single tile).
 //   warp 8       TMA producer: 64-key blocks (4 pages) into a ring of block stages laid out
 //                [K|V][d/64][64 keys][128 B] (128B swizzle), 4 boxes per page
-//   warp 9       TMEM allocator (all 512 columns) + single-thread tcgen05.mma issuer
+//   warp 9       TMEM allocator (all 512 columns) + tcgen05.mma issuer (elected lane)
 //   warps 0..3   softmax / correction / epilogue of tile A (thread t <-> TMEM lane t <-> row)
 //   warps 4..7   the same for tile B
 // Per 64-key block b and tile: S = Q K^T (M = 128, N = 64, K = d) lands in TMEM (double
@@ -48,21 +48,26 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t fmt, uint32_t b_mn_maj
 }
 __device__ __forceinline__ void umma_ss(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
         "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -93,6 +98,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
         "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
         "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+// 2^x on the SFU (flush-to-zero; -inf -> +0)
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -186,8 +197,9 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
             }
         }
     } else if (warp == 9) {
-        // ---------------- MMA issuer (one thread)
-        if (lane == 0) {
+        // ---------------- MMA issuer: the whole warp runs the schedule (warp-uniform
+        // descriptor math on the uniform datapath), one elected lane issues each tcgen05 op
+        {
             mbar_wait(&q_ready, 0);
             tc_fence_after();
             const uint32_t q_addr = smem_u32(q_s), ring_addr = smem_u32(ring);
@@ -234,7 +246,6 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
             }
             issue_pv(n_blk - 1);
         }
-        __syncwarp();
     } else {
         // ---------------- softmax / correction / epilogue: thread owns row r of tile t
         const int t = warp >> 2;
@@ -308,19 +319,27 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
                 if (grow) L *= f;
             }
             if (grow) M = m_new;
-            // P = exp2(s c - M) <= 2^8 as packed 16-bit pairs over S: hi in columns 0..31, lo in 32..63
+            // P = exp2(s c - M) <= 2^8 as packed 16-bit pairs over S: hi in columns 0..31, lo in
+            // 32..63.  bf16: hi = P truncated to its top 16 bits (one byte permute per pair),
+            // lo = the exact fp32 remainder rounded to bf16 -- ~17 significant bits in all.
             const float nm = (M == -INFINITY) ? 0.f : -M;
+            float La = 0.f, Lb = 0.f;
 #pragma unroll
             for (int k0 = 0; k0 < 64; k0 += 32) {
                 uint32_t hi[16], lo[16];
 #pragma unroll
                 for (int k = 0; k < 32; k += 2) {
-                    const float p0 = exp2f(fmaf(s[k0 + k], c_log2, nm)), p1 = exp2f(fmaf(s[k0 + k + 1], c_log2, nm));
-                    L += p0 + p1;
-                    hi[k >> 1] = Elt<T>::from_f2(p0, p1);
+                    const float p0 = ex2_approx(fmaf(s[k0 + k], c_log2, nm));
+                    const float p1 = ex2_approx(fmaf(s[k0 + k + 1], c_log2, nm));
+                    La += p0;
+                    Lb += p1;
                     if constexpr (kBF16) {
-                        const float2 hf = Elt<T>::to_f2(hi[k >> 1]);
-                        lo[k >> 1] = Elt<T>::from_f2(p0 - hf.x, p1 - hf.y);
+                        const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);
+                        hi[k >> 1] = __byte_perm(u0, u1, 0x7632);
+                        lo[k >> 1] = Elt<T>::from_f2(p0 - __uint_as_float(u0 & 0xFFFF0000u),
+                                                     p1 - __uint_as_float(u1 & 0xFFFF0000u));
+                    } else {
+                        hi[k >> 1] = Elt<T>::from_f2(p0, p1);
                     }
                 }
                 tmem_st16(ts + (k0 >> 1), hi);
@@ -335,6 +354,7 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
                 }
                 fence_proxy_async();
             }
+            L += La + Lb;
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&p_full[t][b & 1]);
