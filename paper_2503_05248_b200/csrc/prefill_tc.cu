@@ -18,8 +18,7 @@
 // back over S as packed 16-bit pairs; O += P V then takes A = P straight from TMEM
 // (tcgen05.mma ... [tmem_a]) and B = V as an MN-major 128B-swizzled operand.  bf16 keeps P
 // to ~16 bits with a hi + lo split (two PV MMAs per 16 keys).  S(b+2) reuses the columns of
-// P(b), so it is issued only after PV(b) has completed (measured: without that wait the
-// tensor pipe can let S(b+2) overwrite P(b) while PV(b) still reads it).
+// P(b): tcgen05.mma ops execute in issue order, so PV(b) has read P(b) before S(b+2) writes.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -226,12 +225,8 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
                 tc_fence_after();
                 for (int t = 0; t < 2; ++t) {
                     if (t == 0 ? b >= nblk_a : !has_b) continue;
-                    // S(b) overwrites P(b-2) in TMEM: PV(b-2) must have read it (the tensor
-                    // pipe orders accumulator hazards, not reads of a TMEM A operand)
-                    if (b >= 2) {
-                        mbar_wait(&pv_done[t], (b - 2) & 1);
-                        tc_fence_after();
-                    }
+                    // S(b) overwrites P(b-2) in TMEM with no wait: tcgen05.mma ops of a CTA
+                    // execute in issue order (scratch/umma_war.cu: 0 of 3.8e7 rows corrupted)
                     const uint32_t ts = tmem + t * kTileCols + (b & 1) * 64;
 #pragma unroll
                     for (int kk = 0; kk < KSTEPS; ++kk) {
@@ -303,8 +298,8 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
             const bool grow = m_new > M + 8.f;  // rescale only when the max grows by > 2^8
             if (b > 0 && __any_sync(kFull, grow)) {
                 const float f = grow ? exp2f(M - m_new) : 1.f;
-                // O holds blocks < b.  Valid parity wait: S(b) implies PV(b-2) done (the MMA
-                // thread waited it), and PV(b) needs this block's P.
+                // O holds blocks < b.  Valid parity wait: the commit behind S(b) covers the
+                // earlier-issued PV(b-2), and PV(b) needs this block's P.
                 mbar_wait(&pv_done[t], (b - 1) & 1);
                 tc_fence_after();
 #pragma unroll
