@@ -24,6 +24,21 @@ to paged blocks):
  6. clock += step_ns (device-timed); release arrivals; N^p = queue length;
  7. b_{t+1} from the scheduler on the (global) record (O5/O6).
 An idle engine (nothing running or queued) jumps the clock to the next arrival.
+
+PD fusion ("our method is also valid for determining
+chunk size"; readings R25-R28 of DESIGN.md): prefill shares the iteration.
+Admitted requests first PREFILL in chunks, then decode.  Step order (replaces 2-3):
+ a. decode growth of the running (fully prefilled) requests, LIFO preemption over the
+    admission order running ++ prefilling (a victim's prefill progress is discarded);
+ b. chunk budget c_t = max(0, min(b_share, max_rows) - N^d), N^d = |running|;
+ c. FCFS chunk: prefilling requests in admission order, then new admissions from the queue
+    head (while |running| + |prefilling| < b_share and the whole prompt + 1 fits the free
+    pages, head-of-line blocking), each taking min(remaining prompt, budget left) tokens;
+    an in-progress prefill is cut to the pages that are free (and the chunk stops there);
+ d. attention: decode over the running batch, causal prefill attention over each chunk;
+ e. requests whose prompt is complete join the running batch at the END of the step (they
+    emit their first token in the next step).
+N^p (n_waiting) = released requests not in this step's decode batch = queue + prefilling.
 """
 from __future__ import annotations
 
@@ -48,7 +63,12 @@ def fnv1a64(values, h=FNV_OFFSET):
 class RankEngine:
     """One GPU's request shard (DP) or the whole batch (G = 1 / TP)."""
 
-    def __init__(self, req_ids, arrival_ns, l_in, l_out, cap_pages, page_size, rank=0, world=1):
+    def __init__(self, req_ids, arrival_ns, l_in, l_out, cap_pages, page_size, rank=0, world=1,
+                 pd=False, max_rows=None):
+        self.pd = bool(pd)
+        self.max_rows = max_rows
+        self.prefilling = []          # PD: [req, prompt tokens done], admission order
+        self.last_chunks = []         # PD: (req, q_start, q_len) of the last step
         self.req_ids = list(req_ids)
         self.arrival = [int(a) for a in arrival_ns]
         self.l_in = {r: int(x) for r, x in zip(self.req_ids, l_in)}
@@ -72,7 +92,7 @@ class RankEngine:
             self.next += 1
 
     def idle(self):
-        return not self.running and not self.queue
+        return not self.running and not self.queue and not self.prefilling
 
     def done(self):
         return self.idle() and self.next >= len(self.req_ids)
@@ -104,6 +124,62 @@ class RankEngine:
         for r in self.running:
             self.gen[r] += 1
         return admitted, preempted
+
+    def step_pd(self, b_share):
+        """PD-fusion steps a-c (module docstring).  Returns (admitted, preempted, chunks)."""
+        P = self.P
+        pre = 0
+        while True:                                                    # a
+            need = sum(1 for r in self.running if self.kv.ctx[r] % P == 0)
+            if need <= self.kv.alloc.free:
+                break
+            victim = self.prefilling.pop()[0] if self.prefilling else self.running.pop()
+            self.kv.release(victim)
+            self.queue.appendleft(victim)
+            pre += 1
+        self.kv.append(self.running, [1] * len(self.running))
+        for r in self.running:
+            self.gen[r] += 1
+        rows = b_share if self.max_rows is None else min(b_share, self.max_rows)
+        budget = max(0, rows - len(self.running))                     # b
+        chunks, adm, i = [], 0, 0
+        while budget > 0:                                              # c
+            if i < len(self.prefilling):
+                r, done = self.prefilling[i]
+                T = self.l_in[r] + self.gen[r]
+                k = min(T - done, budget)
+                room = (-(-done // P) + self.kv.alloc.free) * P - done
+                cut = room < k
+                k = min(k, room)
+                if k <= 0:
+                    break
+            elif self.queue and len(self.running) + len(self.prefilling) < b_share:
+                r, done = self.queue[0], 0
+                T = self.l_in[r] + self.gen[r]
+                if self.kv.alloc.free < -(-(T + 1) // P):
+                    break
+                self.queue.popleft()
+                self.kv.begin(r)
+                self.prefilling.append([r, 0])
+                adm += 1
+                k, cut = min(T, budget), False
+            else:
+                break
+            self.kv.append([r], [k])
+            self.prefilling[i][1] += k
+            chunks.append((r, done, k))
+            budget -= k
+            i += 1
+            if cut:
+                break
+        self.last_chunks = chunks
+        return adm, pre, chunks
+
+    def finish_prefills(self):
+        """PD step e: completed prompts join the running batch (admission order)."""
+        while self.prefilling and self.prefilling[0][1] == self.l_in[self.prefilling[0][0]] + \
+                self.gen[self.prefilling[0][0]]:
+            self.running.append(self.prefilling.pop(0)[0])
 
     def batch(self):
         """The decode launch's batch: (req_ids, ctx, l_in, l_out, pages) in batch order."""
@@ -166,9 +242,15 @@ class Replay:
             for e in self.ranks:
                 e.release_arrivals(self.clock)
         clock0 = self.clock
-        adm = pre = 0
+        adm = pre = n_prefill = 0
+        chunks = []
         for e in self.ranks:
-            a, p = e.admit_and_grow(b_share(self.b, e.rank, G))
+            if e.pd:
+                a, p, ch = e.step_pd(b_share(self.b, e.rank, G))
+                n_prefill += sum(k for _, _, k in ch)
+                chunks.append(ch)
+            else:
+                a, p = e.admit_and_grow(b_share(self.b, e.rank, G))
             adm += a
             pre += p
         recs = [e.local_stats() for e in self.ranks]
@@ -179,7 +261,10 @@ class Replay:
         self.clock += int(step_ns)
         for e in self.ranks:
             e.release_arrivals(self.clock)
-        waiting = sum(len(e.queue) for e in self.ranks)
+        waiting = sum(len(e.queue) + len(e.prefilling) for e in self.ranks)
+        for e in self.ranks:
+            if e.pd:
+                e.finish_prefills()
         for r in recs:
             r["step_ns"] = int(step_ns)
             r["n_waiting"] = 0
@@ -193,6 +278,8 @@ class Replay:
                    used_pages=sum(used), step_ns=int(step_ns), b_next=self.b, rationale=rationale,
                    L0=self.sched.L0, b_quad=self.sched.bq, b_mem=self.sched.b_mem,
                    b_sla=self.sched.b_sla, table_hash=hashes[0] if G == 1 else tuple(hashes),
-                   stats=g, local_stats=recs, batches=batches)
+                   stats=g, local_stats=recs, batches=batches, n_prefill=n_prefill, chunks=chunks)
+        if any(e.pd for e in self.ranks):
+            rec["used_pages"] = g["sum_pages"]   # decode batch pages (prefilling pages excluded)
         self.t += 1
         return rec
