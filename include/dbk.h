@@ -268,13 +268,19 @@ typedef struct dbk_engine_config {
     int32_t out_dtype;              /* 0 fp16, 1 bf16, 2 fp32                              */
     int32_t time_attention;         /* 1: CUDA events around each attention launch         */
     int32_t rank, world;            /* DP request shards (R21); 0, 1 for one GPU           */
+    int32_t pd_fusion;              /* 1: PD fusion -- admitted prompts are prefilled in     *
+                                     * chunks of c_t = max(0, b_t - N^d) tokens inside the    *
+                                     * decode iteration (R25-R28; device-resident mode only)  */
+    int32_t _reserved;
 } dbk_engine_config;
 
 typedef struct dbk_engine dbk_engine;
 
 /* Buffers of one step.  Device-resident mode: host_* all NULL; the engine
  * generates q (synthetic, pos = ctx-1) into q_dev and appends the decode
- * token's K/V with the synthetic generator.  End-to-end mode: host_q
+ * token's K/V with the synthetic generator.  With PD fusion the prefill
+ * chunk's rows follow the decode rows in q_dev / out_dev: decode rows
+ * [0, N^d), chunk rows [N^d, N^d + c_t) (c_t is clamped to max_requests - N^d).  End-to-end mode: host_q
  * [layers][n][q_heads][d], host_k / host_v [n][layers][kv_heads][d] (pinned
  * host, kv_dtype) are copied H2D into q_dev / kv_dev each step and out is
  * copied D2H into host_out [layers][n][q_heads][d] (out_dtype).
@@ -290,7 +296,8 @@ typedef struct dbk_step_record {
     int64_t t, clock_ns, step_ns, sum_ctx, used_pages, table_hash;
     int32_t b_t, b_next, n_admitted, n_preempted, n_decode, n_finished, rationale, n_waiting;
     int64_t h2d_bytes, d2h_bytes;
-    int32_t launches, _reserved;
+    int32_t launches;
+    int32_t n_prefill;              /* PD fusion: prompt tokens prefilled this step (this rank) */
 } dbk_step_record;
 
 dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_config *cfg,

@@ -26,6 +26,17 @@ struct dbk_engine {
     size_t next_global = 0;           // first global index with arrival > clock
     std::deque<int32_t> queue;        // local waiting (trace indices)
     std::vector<int32_t> running;     // local running, admission order
+    // PD fusion (R25-R28): admitted requests still prefilling, admission order (all of them
+    // were admitted after every running request: prefill is FCFS)
+    struct Prefilling {
+        int32_t r, done;
+    };
+    std::vector<Prefilling> prefilling;
+    std::vector<int64_t> pf_ids;      // this step's chunk: request, first position, tokens
+    std::vector<int32_t> pf_start, pf_len;
+    std::vector<uint8_t> pf_rows;     // per chunk row: req id (int64) | position (int32)
+    UploadBuffer up_pf;
+    int32_t step_prefill = 0;
     int64_t clock = 0, t = 0;
     int32_t b = 1;
     int64_t fin_global = 0;           // cumulative finished (global)
@@ -53,6 +64,8 @@ struct dbk_engine {
     cudaEvent_t ev_kv = nullptr, ev_d2h = nullptr;
     std::vector<cudaEvent_t> ev_q, ev_o;
     ~dbk_engine() {
+        up_pf.release();
+        if (up_pf.done) cudaEventDestroy(up_pf.done);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (auto e : att0) cudaEventDestroy(e);
@@ -108,6 +121,8 @@ dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_
         return fail(DBK_EINVAL, "engine_create: trace arrays missing");
     if (c.world < 1 || c.rank < 0 || c.rank >= c.world) return fail(DBK_EINVAL, "engine_create: bad rank/world");
     if (c.out_dtype < 0 || c.out_dtype > 2) return fail(DBK_EINVAL, "engine_create: bad out_dtype");
+    if (c.pd_fusion != 0 && c.pd_fusion != 1) return fail(DBK_EINVAL, "engine_create: pd_fusion must be 0 or 1");
+    if (c.pd_fusion && !pool->has_ptmap) return fail(DBK_EINVAL, "engine_create: PD fusion needs the pool's prefill tensor map");
     for (int i = 0; i < c.n_requests; ++i) {
         if (c.l_in[i] < 1 || c.l_out[i] < 1) return fail(DBK_EINVAL, "engine_create: lengths must be >= 1");
         if (i && c.arrival_ns[i] < c.arrival_ns[i - 1]) return fail(DBK_EINVAL, "engine_create: arrivals must be sorted");
@@ -182,6 +197,8 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     if (!bufs->q_dev || !bufs->out_dev) return fail(DBK_EINVAL, "engine_step_launch: q_dev and out_dev are required");
     if (e2e && (!bufs->host_k || !bufs->host_v || !bufs->kv_dev))
         return fail(DBK_EINVAL, "engine_step_launch: end-to-end mode needs host_q, host_k, host_v and kv_dev");
+    const bool pd = e->cfg.pd_fusion != 0;
+    if (pd && e2e) return fail(DBK_EINVAL, "engine_step_launch: PD fusion runs in device-resident mode only");
     DBK_CUDA(cudaSetDevice(pc.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t P = pc.page_size;
@@ -205,7 +222,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     std::vector<int32_t> adm_tok;
     int64_t free_pages = p->pages.free_count;
     int32_t adm = 0, pre = 0;
-    while (!e->queue.empty() && static_cast<int32_t>(e->running.size()) < share) {
+    while (!pd && !e->queue.empty() && static_cast<int32_t>(e->running.size()) < share) {
         const int32_t r = e->queue.front();
         const int64_t T = static_cast<int64_t>(e->l_in[r]) + e->gen[r];
         if (free_pages < ceil_div(T + 1, P)) break;
@@ -222,14 +239,21 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
                                   nullptr, nullptr, e->cfg.synth_seed, s));
 
     // S1/S2: page growth for this step's decode token; LIFO preemption on overflow (R18)
-    // a running request holds ctx = l_in + generated tokens; it needs a page iff ctx % P == 0
+    // a running request holds ctx = l_in + generated tokens; it needs a page iff ctx % P == 0.
+    // PD fusion: the admission order is running ++ prefilling, so prefills are evicted first.
     int64_t need = 0;
     for (int32_t r : e->running)
         if ((static_cast<int64_t>(e->l_in[r]) + e->gen[r]) % P == 0) ++need;
     while (need > p->pages.free_count) {
-        const int32_t victim = e->running.back();
-        e->running.pop_back();
-        if ((static_cast<int64_t>(e->l_in[victim]) + e->gen[victim]) % P == 0) --need;
+        int32_t victim;
+        if (pd && !e->prefilling.empty()) {
+            victim = e->prefilling.back().r;
+            e->prefilling.pop_back();
+        } else {
+            victim = e->running.back();
+            e->running.pop_back();
+            if ((static_cast<int64_t>(e->l_in[victim]) + e->gen[victim]) % P == 0) --need;
+        }
         const int64_t vid = e->ids[victim];
         DBK_TRY(dbk_release(p, 1, &vid));
         e->queue.push_front(victim);
@@ -270,6 +294,79 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), nullptr, nullptr, e->cfg.synth_seed, s));
         }
     }
+    // PD fusion (R25-R27): chunk budget c_t = max(0, b_share - N^d) prompt tokens, FCFS over the
+    // in-progress prefills then new admissions; pages left after the decode growth
+    e->pf_ids.clear();
+    e->pf_start.clear();
+    e->pf_len.clear();
+    int32_t n_pf_rows = 0;
+    if (pd) {
+        int64_t budget = std::max<int64_t>(0, std::min<int64_t>(share, pc.max_requests) - n);
+        int64_t freep = p->pages.free_count;
+        size_t i = 0;
+        while (budget > 0) {
+            int32_t r, done;
+            int64_t k;
+            bool cut = false;
+            if (i < e->prefilling.size()) {
+                r = e->prefilling[i].r;
+                done = e->prefilling[i].done;
+                const int64_t T = static_cast<int64_t>(e->l_in[r]) + e->gen[r];
+                k = std::min<int64_t>(T - done, budget);
+                const int64_t room = (ceil_div(done, P) + freep) * P - done;
+                if (room < k) {
+                    cut = true;
+                    k = room;
+                }
+                if (k <= 0) break;
+                freep -= ceil_div(done + k, P) - ceil_div(done, P);
+            } else if (!e->queue.empty() &&
+                       static_cast<int64_t>(e->running.size() + e->prefilling.size()) < share) {
+                r = e->queue.front();
+                done = 0;
+                const int64_t T = static_cast<int64_t>(e->l_in[r]) + e->gen[r];
+                if (freep < ceil_div(T + 1, P)) break;
+                e->queue.pop_front();
+                DBK_TRY(dbk_request_begin(p, e->ids[r], e->l_in[r], e->l_out[r]));
+                e->prefilling.push_back({r, 0});
+                ++adm;
+                k = std::min<int64_t>(T, budget);
+                freep -= ceil_div(k, P);
+            } else {
+                break;
+            }
+            e->pf_ids.push_back(e->ids[r]);
+            e->pf_start.push_back(done);
+            e->pf_len.push_back(static_cast<int32_t>(k));
+            e->prefilling[i].done += static_cast<int32_t>(k);
+            n_pf_rows += static_cast<int32_t>(k);
+            budget -= k;
+            ++i;
+            if (cut) break;
+        }
+        if (!e->pf_ids.empty()) {
+            DBK_TRY(dbk_append_tokens(p, static_cast<int32_t>(e->pf_ids.size()), e->pf_ids.data(), e->pf_len.data(),
+                                      nullptr, nullptr, e->cfg.synth_seed, s));
+            // the chunk's q rows (synthetic, all layers) follow the decode rows: (req, position)
+            e->pf_rows.resize(static_cast<size_t>(n_pf_rows) * 12);
+            int64_t *rq = reinterpret_cast<int64_t *>(e->pf_rows.data());
+            int32_t *rp = reinterpret_cast<int32_t *>(e->pf_rows.data() + static_cast<size_t>(n_pf_rows) * 8);
+            int32_t x = 0;
+            for (size_t m = 0; m < e->pf_ids.size(); ++m)
+                for (int32_t j = 0; j < e->pf_len[m]; ++j, ++x) {
+                    rq[x] = e->pf_ids[m];
+                    rp[x] = e->pf_start[m] + j;
+                }
+            DBK_TRY(e->up_pf.upload(e->pf_rows.data(), e->pf_rows.size(), s));
+            const uint8_t *dev = static_cast<const uint8_t *>(e->up_pf.dev);
+            DBK_CUDA(launch_synth_rows_layers(e->cfg.synth_seed, 0, n_pf_rows, reinterpret_cast<const int64_t *>(dev),
+                                              reinterpret_cast<const int32_t *>(dev + static_cast<size_t>(n_pf_rows) * 8),
+                                              pc.layers, pc.max_requests, n, pc.q_heads, pc.head_dim,
+                                              e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
+            ++p->n_launches;
+        }
+    }
+    e->step_prefill = n_pf_rows;
     uint64_t h = kFnvOffset;
     for (int32_t x = 0; x < n; ++x) {
         const int32_t r = e->running[x];
@@ -303,6 +400,16 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         DBK_TRY(dbk_decode_step(p, &bt, qd, od, e->cfg.out_dtype, s));
         if (e->cfg.time_attention && n > 0) DBK_CUDA(cudaEventRecord(e->att1[l], s));
         e->layer_bytes[l] = p->last_decode_bytes;
+        if (n_pf_rows > 0) {  // causal attention of the prefill chunk (K7, tensor cores)
+            dbk_prefill_batch pb;
+            pb.n = static_cast<int32_t>(e->pf_ids.size());
+            pb.layer = l;
+            pb.req_ids = e->pf_ids.data();
+            pb.q_start = e->pf_start.data();
+            pb.q_len = e->pf_len.data();
+            DBK_TRY(dbk_prefill_step(p, &pb, qd + static_cast<size_t>(n) * qrow, od + static_cast<size_t>(n) * orow,
+                                     e->cfg.out_dtype, s));
+        }
         if (e2e && n > 0 && bufs->host_out) {  // layer l's output goes back while l+1 computes
             DBK_CUDA(cudaEventRecord(e->ev_o[l], s));
             DBK_CUDA(cudaStreamWaitEvent(e->d2h, e->ev_o[l], 0));
@@ -318,10 +425,24 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     DBK_CUDA(cudaEventRecord(e->ev1, s));
     // S5: statistics record (synchronises the stream) and device-timed step latency
     DBK_TRY(dbk_batch_stats(p, &e->local, s));
+    if (n == 0) {  // no decode launch reduced the record: the empty batch's record (O3)
+        e->local = dbk_stats{};
+        e->local.cap_pages = pc.cap_pages;
+        e->local.free_pages = pc.cap_pages;
+    }
     float ms = 0.f;
     DBK_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     e->local.step_ns = std::llround(static_cast<double>(ms) * 1e6);
-    e->local.n_waiting = static_cast<int64_t>(e->queue.size());
+    e->local.n_waiting = static_cast<int64_t>(e->queue.size() + e->prefilling.size());
+    if (pd) {  // R27: completed prompts join the decode batch from the next step on
+        size_t m = 0;
+        while (m < e->prefilling.size() &&
+               e->prefilling[m].done == e->l_in[e->prefilling[m].r] + e->gen[e->prefilling[m].r]) {
+            e->running.push_back(e->prefilling[m].r);
+            ++m;
+        }
+        e->prefilling.erase(e->prefilling.begin(), e->prefilling.begin() + static_cast<std::ptrdiff_t>(m));
+    }
     if (e->cfg.time_attention && n > 0) {
         for (int l = 0; l < pc.layers; ++l) {
             float a = 0.f;
@@ -384,6 +505,7 @@ dbk_status dbk_engine_step_finish(dbk_engine *e, const dbk_stats *global, dbk_st
         rec->h2d_bytes = e->step_h2d;
         rec->d2h_bytes = e->step_d2h;
         rec->launches = e->step_launches;
+        rec->n_prefill = e->step_prefill;
     }
     e->b = b_next;
     e->prev_known = true;

@@ -107,6 +107,28 @@ __global__ void synth_q_kernel(uint64_t seed, const ReqMeta *req, int n, int lay
     }
 }
 
+// rows of every layer: out[l][row0 + r][h][:] = synth(seed, kind, req[r], pos[r], l, h), layer l at
+// out + l * layer_rows rows (PD fusion: the prefill chunk's q, one launch per step).
+__global__ void synth_rows_layers_kernel(uint64_t seed, int kind, int n_rows, const int64_t *req, const int32_t *pos,
+                                         int layers, int layer_rows, int row0, int n_heads, int d, float scale,
+                                         int dtype, void *out) {
+    const int vpr = d / 8;
+    const long per_layer = static_cast<long>(n_rows) * n_heads * vpr;
+    const long total = per_layer * layers;
+    for (long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; k < total;
+         k += static_cast<long>(gridDim.x) * blockDim.x) {
+        const int l = static_cast<int>(k / per_layer);
+        const long kk = k % per_layer;
+        const int v = static_cast<int>(kk % vpr);
+        const long rh = kk / vpr;
+        const int h = static_cast<int>(rh % n_heads);
+        const int r = static_cast<int>(rh / n_heads);
+        float f[8];
+        synth_vals(synth_key(seed, kind, req[r], pos[r], l, h, v), scale, f);
+        store8(out, ((static_cast<size_t>(l) * layer_rows + row0) * n_heads + rh) * d + v * 8, dtype, f);
+    }
+}
+
 int grid_for(long work, int block) {
     long b = (work + block - 1) / block;
     if (b > 148L * 16) b = 148L * 16;
@@ -141,6 +163,17 @@ cudaError_t launch_synth_rows(uint64_t seed, int kind, int n_rows, const int64_t
     if (work <= 0) return cudaSuccess;
     synth_rows_kernel<<<grid_for(work, 256), 256, 0, s>>>(seed, kind, n_rows, req, pos, layer, n_heads,
                                                           d, ldexpf(1.0f, scale_log2 - 7), dtype, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_synth_rows_layers(uint64_t seed, int kind, int n_rows, const int64_t *req, const int32_t *pos,
+                                    int layers, int layer_rows, int row0, int n_heads, int d, int scale_log2,
+                                    int dtype, void *out, cudaStream_t s) {
+    const long work = static_cast<long>(n_rows) * layers * n_heads * (d / 8);
+    if (work <= 0) return cudaSuccess;
+    synth_rows_layers_kernel<<<grid_for(work, 256), 256, 0, s>>>(seed, kind, n_rows, req, pos, layers, layer_rows,
+                                                                 row0, n_heads, d, ldexpf(1.0f, scale_log2 - 7),
+                                                                 dtype, out);
     return cudaGetLastError();
 }
 

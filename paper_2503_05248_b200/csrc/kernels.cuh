@@ -130,6 +130,10 @@ cudaError_t launch_bt_apply(int32_t *bt, int32_t stride, const BtDelta *d, int32
 cudaError_t launch_synth_rows(uint64_t seed, int kind, int n_rows, const int64_t *req,
                               const int32_t *pos, int layer, int n_heads, int d, int scale_log2,
                               int dtype, void *out, cudaStream_t s);
+// out[l][row0 + r][h][:] = synth(seed, kind, req[r], pos[r], l, h) for all layers (device req/pos).
+cudaError_t launch_synth_rows_layers(uint64_t seed, int kind, int n_rows, const int64_t *req, const int32_t *pos,
+                                    int layers, int layer_rows, int row0, int n_heads, int d, int scale_log2,
+                                    int dtype, void *out, cudaStream_t s);
 // q[l][i][h][:] = synth(seed, q, req_i, ctx_i - 1, l, h) for all layers, layer stride layer_rows rows.
 cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
                            int q_heads, int d, int scale_log2, int dtype, void *q, cudaStream_t s);

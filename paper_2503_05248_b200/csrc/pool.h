@@ -82,4 +82,10 @@ struct dbk_pool {
     dbk::UploadBuffer up_pref;
     std::vector<dbk::PrefTile> pref_tiles;
     int64_t last_prefill_flops = 0;
+    // cached tile list: the L per-layer launches of one step upload once
+    bool pref_valid = false;
+    uint64_t pref_epoch = 0;
+    std::vector<int64_t> pref_ids;
+    std::vector<int32_t> pref_s0, pref_len;
+    int32_t pref_n_tiles = 0;
 };
