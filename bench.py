@@ -132,7 +132,7 @@ def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None)
 
 def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
                  out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1,
-                 trace_override=None, eps_d_ms=None):
+                 trace_override=None, eps_d_ms=None, pd_fusion=False):
     """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
     config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
@@ -160,7 +160,8 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     sched = dbk.Scheduler(**sched_kwargs(c, beta, policy, b_static, sla_ms, eps_d_ms))
     eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap_total, seed=seed,
                      out_dtype=out_dtype, time_attention=time_attention,
-                     rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0)
+                     rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0,
+                     pd_fusion=pd_fusion)
     et = torch.float32 if out_dtype == 2 else torch.float16
     qd = torch.empty(L, max_req, Hq, d, dtype=torch.float16, device=f"cuda:{device}")
     od = torch.empty(L, max_req, Hq, d, dtype=et, device=f"cuda:{device}")

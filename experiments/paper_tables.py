@@ -93,18 +93,21 @@ def _tbt_p99(recs):
     return float(lat[order][np.searchsorted(cum, k)])
 
 
-def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0, policies=("static", "combined"),
-             b_static=None, lo=20.0, hi=640.0, tol=0.05):
-    """Table II / Fig. 5 analog: the largest Poisson rate (qps) at which the p99
-    TBT stays <= D_SLA + eps_D (capacity, Sarathi's definition quoted at P:298), found by
-    bisection on the rate for the static baseline and for Alg. 2 + Alg. 1.  Each probe sends
-    qps x window_s requests (a fixed arrival window, so every probe costs about the same)."""
+def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
+             modes=(("static", False), ("combined", False), ("static", True), ("combined", True)),
+             b_static=None, lo=10.0, hi=640.0, tol=0.05, max_delay_s=2.0):
+    """Table II / Fig. 5 analog: capacity = the largest Poisson rate (qps) at which
+    the p99 TBT stays <= D_SLA + eps_D AND the median scheduling delay (arrival -> first
+    admission, from dbk_engine_request_times) stays <= 2 s -- Sarathi-Serve's definition, which
+    the paper adopts -- found by bisection on the rate, for the static baseline and for
+    Alg. 2 + Alg. 1, without and with PD fusion (Table II row 3 "implemented with PD fusion
+    scenario").  Each probe sends qps x window_s requests (a fixed arrival window)."""
     from synth import configs, trace
     c = configs.CONFIGS[cfg]
     t = c["trace"]
-    out = dict(config=cfg, d_sla_ms=d_sla, eps_d_ms=eps_d, window_s=window_s, rows=[])
+    out = dict(config=cfg, d_sla_ms=d_sla, eps_d_ms=eps_d, window_s=window_s, max_delay_s=max_delay_s, rows=[])
 
-    def ok(policy, qps):
+    def probe(policy, pd, qps):
         n_req = max(100, int(qps * window_s))
         tr = trace.make_trace(n_req, t["mean_in"], t["mean_out"], t["L_max"], t["seed"], dist=t["dist"],
                               arrival="poisson", rate_qps=qps)
@@ -114,30 +117,67 @@ def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0, polici
         gc.collect()
         torch.cuda.empty_cache()
         S = bench.setup_engine(cfg_name=cfg, policy=policy, b_static=b_static or 256, sla_ms=d_sla,
-                               eps_d_ms=eps_d, time_attention=False, trace_override=tr)
+                               eps_d_ms=eps_d, time_attention=False, trace_override=tr, pd_fusion=pd)
         eng = S["eng"]
         bufs = eng.buffers(S["qd"], S["od"])
         recs, ms = bench.run_steps(S, 10 ** 9, bufs, torch.cuda.current_stream())
+        adm, fin = eng.request_times()
+        delay = float(np.median(adm - tr.arrival_ns)) / 1e9
         p99 = _tbt_p99(recs)
-        tok_s = sum(r["n_decode"] for r in recs) / (sum(r["step_ns"] for r in recs) / 1e9)
+        dev_s = sum(r["step_ns"] for r in recs) / 1e9
+        res = dict(qps=qps, p99_tbt_ms=p99, median_sched_delay_s=delay,
+                   decode_tokens_per_s=sum(r["n_decode"] for r in recs) / dev_s,
+                   prefill_tokens_per_s=sum(r.get("n_prefill", 0) for r in recs) / dev_s,
+                   mean_b=float(np.mean([r["b_t"] for r in recs])), steps=len(recs))
+        res["ok"] = bool(p99 <= d_sla + eps_d and delay <= max_delay_s)
         S["eng"].close()
         S["pool"].close()
         S.clear()
-        return p99 <= d_sla + eps_d, p99, tok_s
+        return res
 
-    for pol in policies:
+    for pol, pd in modes:
         a, b = lo, hi
-        best = None
+        best, probes = None, []
         while b - a > tol * a:
             mid = (a * b) ** 0.5
-            good, p99, tok_s = ok(pol, mid)
-            if good:
-                a, best = mid, (mid, p99, tok_s)
+            r = probe(pol, pd, mid)
+            probes.append(r)
+            print(json.dumps(dict(policy=pol, pd=pd, **r)), flush=True)
+            if r["ok"]:
+                a, best = mid, r
             else:
                 b = mid
-        out["rows"].append(dict(policy=pol, capacity_qps=a, p99_ms=best[1] if best else None,
-                                tokens_per_s=best[2] if best else None))
+        out["rows"].append(dict(policy=pol, pd_fusion=pd, capacity_qps=a if best else None, at_capacity=best,
+                                probes=probes))
     return out
+
+
+def pd_table(cfg="llama2-7b", bs=(64, 128, 256)):
+    """PD-fusion whole-trace runs (Table I shape, all-at-once arrivals): static b vs the
+    memory-aware rule deciding the fused iteration's token budget (R25)."""
+    import gc
+
+    import torch
+    rows = []
+    for pol, b in [("static", x) for x in bs] + [("memory", None)]:
+        gc.collect()
+        torch.cuda.empty_cache()
+        S = bench.setup_engine(cfg_name=cfg, policy=pol, b_static=b or 256, time_attention=False, pd_fusion=True)
+        eng = S["eng"]
+        bufs = eng.buffers(S["qd"], S["od"])
+        t0 = time.time()
+        recs, ms = bench.run_steps(S, 10 ** 9, bufs, torch.cuda.current_stream())
+        dev_s = ms / 1e3
+        rows.append(dict(policy=pol, b_static=b, steps=len(recs), device_s=dev_s,
+                         decode_tokens_per_s=sum(r["n_decode"] for r in recs) / dev_s,
+                         prefill_tokens_per_s=sum(r["n_prefill"] for r in recs) / dev_s,
+                         mean_b=float(np.mean([r["b_t"] for r in recs])),
+                         preemptions=int(sum(r["n_preempted"] for r in recs)), wall_s=time.time() - t0))
+        print(json.dumps(rows[-1]), flush=True)
+        S["eng"].close()
+        S["pool"].close()
+        S.clear()
+    return dict(config=cfg, rows=rows)
 
 
 def main():
@@ -146,6 +186,7 @@ def main():
     ap.add_argument("--table1", action="store_true")
     ap.add_argument("--sla", action="store_true")
     ap.add_argument("--capacity", action="store_true")
+    ap.add_argument("--pd", action="store_true")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
     a = ap.parse_args()
     import torch
@@ -163,6 +204,9 @@ def main():
         save()
     if a.table1:
         res["table1"] = table1()
+        save()
+    if a.pd:
+        res["pd_table"] = pd_table()
         save()
     if a.sla or a.capacity:
         res["fig3_13b"] = fig3("llama2-13b-sla", bs=(32, 64, 128, 256))

@@ -233,6 +233,15 @@ class Engine:
         _lib.dbk_engine_attn_timing(self.h, C.byref(ms), C.byref(la), C.byref(by), 1 if reset else 0)
         return ms.value, la.value, by.value
 
+    def request_times(self):
+        """(first_admit_ns, finish_ns) per trace index, -1 = not yet / another rank."""
+        n = len(self._arr)
+        a = np.full(n, -1, np.int64)
+        f = np.full(n, -1, np.int64)
+        _lib.dbk_engine_request_times(self.h, n, a.ctypes.data_as(C.POINTER(C.c_int64)),
+                                      f.ctypes.data_as(C.POINTER(C.c_int64)))
+        return a, f
+
 
 def stats_reduce(records, mode=0):
     arr = (dbk_stats * len(records))(*[dbk_stats(*[int(r.get(f, 0)) for f in _lib.STATS_FIELDS])

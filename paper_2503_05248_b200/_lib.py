@@ -142,6 +142,7 @@ SIGNATURES = {
     "dbk_engine_done": [P, PI32],
     "dbk_engine_last_batch": [P, PI32, PI64, PI32, I32],
     "dbk_engine_attn_timing": [P, C.POINTER(C.c_double), PI64, PI64, I32],
+    "dbk_engine_request_times": [P, I32, PI64, PI64],
     "dbk_comm_unique_id": [P],
     "dbk_comm_create": [I32, I32, P, I32, C.POINTER(P)],
     "dbk_comm_destroy": [P],

@@ -21,6 +21,7 @@ struct dbk_engine {
     // full (global) trace; this rank serves indices i with i % world == rank
     std::vector<int64_t> arrival, ids;
     std::vector<int32_t> l_in, l_out, gen;
+    std::vector<int64_t> admit_ns, finish_ns;  // per trace index, -1 = not yet
     std::vector<int32_t> mine;        // local trace indices in arrival order
     size_t next_local = 0;            // next local index to release
     size_t next_global = 0;           // first global index with arrival > clock
@@ -139,6 +140,8 @@ dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_
     e->l_in.assign(c.l_in, c.l_in + c.n_requests);
     e->l_out.assign(c.l_out, c.l_out + c.n_requests);
     e->gen.assign(c.n_requests, 0);
+    e->admit_ns.assign(c.n_requests, -1);
+    e->finish_ns.assign(c.n_requests, -1);
     e->ids.resize(c.n_requests);
     for (int i = 0; i < c.n_requests; ++i) e->ids[i] = c.req_ids ? c.req_ids[i] : i;
     for (int i = c.rank; i < c.n_requests; i += c.world) e->mine.push_back(i);
@@ -232,6 +235,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         adm_ids.push_back(e->ids[r]);
         adm_tok.push_back(static_cast<int32_t>(T));
         e->running.push_back(r);
+        if (e->admit_ns[r] < 0) e->admit_ns[r] = e->clock;
         ++adm;
     }
     if (!adm_ids.empty())
@@ -329,6 +333,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
                 e->queue.pop_front();
                 DBK_TRY(dbk_request_begin(p, e->ids[r], e->l_in[r], e->l_out[r]));
                 e->prefilling.push_back({r, 0});
+                if (e->admit_ns[r] < 0) e->admit_ns[r] = e->clock;
                 ++adm;
                 k = std::min<int64_t>(T, budget);
                 freep -= ceil_div(k, P);
@@ -469,8 +474,12 @@ dbk_status dbk_engine_step_finish(dbk_engine *e, const dbk_stats *global, dbk_st
     std::vector<int64_t> done_ids;
     keep.reserve(e->running.size());
     for (int32_t r : e->running) {
-        if (e->gen[r] == e->l_out[r]) done_ids.push_back(e->ids[r]);
-        else keep.push_back(r);
+        if (e->gen[r] == e->l_out[r]) {
+            done_ids.push_back(e->ids[r]);
+            e->finish_ns[r] = e->clock + global->step_ns;
+        } else {
+            keep.push_back(r);
+        }
     }
     if (!done_ids.empty()) DBK_TRY(dbk_release(p, static_cast<int32_t>(done_ids.size()), done_ids.data()));
     e->running.swap(keep);
@@ -536,6 +545,16 @@ dbk_status dbk_engine_last_batch(dbk_engine *e, int32_t *n, int64_t *ids, int32_
     for (int32_t x = 0; x < cap && x < *n; ++x) {
         if (ids) ids[x] = e->batch_ids[x];
         if (ctx) ctx[x] = e->batch_ctx[x];
+    }
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_request_times(dbk_engine *e, int32_t n, int64_t *first_admit_ns, int64_t *finish_ns) {
+    if (!e || n < 0) return fail(DBK_EINVAL, "engine_request_times: bad argument");
+    for (int32_t i = 0; i < n; ++i) {
+        const bool have = static_cast<size_t>(i) < e->admit_ns.size();
+        if (first_admit_ns) first_admit_ns[i] = have ? e->admit_ns[i] : -1;
+        if (finish_ns) finish_ns[i] = have ? e->finish_ns[i] : -1;
     }
     return DBK_OK;
 }

@@ -87,6 +87,11 @@ def _pd_vs_replay(dbk, tr, L, Hq, Hkv, d, cap_pages, policy, b_max, dtype="bf16"
     assert rp.done()
     assert sum(r["n_finished"] for r in recs) == len(tr)
     assert sum(r["n_decode"] for r in recs) == int(tr.l_out.sum())
+    # per-request timeline: admitted after arrival, FCFS first admissions, finished afterwards
+    adm, fin = eng.request_times()
+    assert (adm >= tr.arrival_ns).all() and (fin > adm).all()
+    assert (np.diff(adm) >= 0).all()
+    assert fin.max() == recs[-1]["clock_ns"] + recs[-1]["step_ns"]
     pool.close()
     return recs, checked
 
