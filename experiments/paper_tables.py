@@ -177,6 +177,7 @@ def pd_table(cfg="llama2-7b", bs=(64, 128, 256)):
         S["eng"].close()
         S["pool"].close()
         S.clear()
+        del eng, bufs  # the engine holds the pool, the pool holds the KV allocation
     return dict(config=cfg, rows=rows)
 
 

@@ -131,7 +131,10 @@ typedef struct dbk_batch {
     int32_t n;             /* active requests (0 = no-op)                        */
     int32_t layer;         /* 0 .. layers-1                                       */
     int32_t fuse_stats;    /* 1: also produce the dbk_stats record (S4)           */
-    int32_t _reserved;
+    int32_t chain;         /* 1: the previous operation on `stream` is this pool's *
+                            * dbk_decode_step (same batch, another layer): launch  *
+                            * as a programmatic dependent so it fills that launch's *
+                            * tail (ignored with fuse_stats); 0: plain stream order */
     const int64_t *req_ids;/* host [n], batch order                               */
 } dbk_batch;
 

@@ -109,9 +109,9 @@ class KVPool:
         _lib.dbk_block_table_d2h(self.h, out.ctypes.data_as(C.POINTER(C.c_int32)), _stream(stream))
         return out
 
-    def decode_step(self, req_ids, layer, q, out, out_dtype=2, fuse_stats=False, stream=None):
+    def decode_step(self, req_ids, layer, q, out, out_dtype=2, fuse_stats=False, stream=None, chain=False):
         ids, pids = _i64(req_ids)
-        b = dbk_batch(len(ids), int(layer), 1 if fuse_stats else 0, 0, pids)
+        b = dbk_batch(len(ids), int(layer), 1 if fuse_stats else 0, 1 if chain else 0, pids)
         _lib.dbk_decode_step(self.h, C.byref(b), _ptr(q), _ptr(out), int(out_dtype), _stream(stream))
 
     def prefill_step(self, req_ids, q_start, q_len, layer, q, out, out_dtype=2, stream=None):

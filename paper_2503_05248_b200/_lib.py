@@ -41,7 +41,7 @@ class dbk_pool_info(C.Structure):
 
 class dbk_batch(C.Structure):
     _fields_ = [("n", C.c_int32), ("layer", C.c_int32), ("fuse_stats", C.c_int32),
-                ("_reserved", C.c_int32), ("req_ids", C.POINTER(C.c_int64))]
+                ("chain", C.c_int32), ("req_ids", C.POINTER(C.c_int64))]
 
 
 class dbk_prefill_batch(C.Structure):

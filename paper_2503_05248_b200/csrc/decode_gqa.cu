@@ -292,8 +292,7 @@ cudaError_t launch_gqa_t(const DecodeParams &p, int ctas, const CUtensorMap &tma
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    kern<<<ctas, kWarps * 32, smem, s>>>(p, tmap);
-    return cudaGetLastError();
+    return launch_kernel(kern, dim3(ctas), dim3(kWarps * 32), smem, s, p.pdl != 0, p, tmap);
 }
 
 template <typename T, int D, int GQ>
@@ -323,8 +322,7 @@ cudaError_t launch_gqa_v(const DecodeParams &p, const CUtensorMap &tmap, cudaStr
         occ = n;
     }
     const int ctas = std::max(1, std::min(sms * occ, (p.n_tasks + W - 1) / W));
-    kern<<<ctas, W * 32, smem, s>>>(p, tmap);
-    return cudaGetLastError();
+    return launch_kernel(kern, dim3(ctas), dim3(W * 32), smem, s, p.pdl != 0, p, tmap);
 }
 
 int gqa_variant() {

@@ -258,8 +258,7 @@ cudaError_t launch_t(const DecodeParams &p, int ctas, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    kern<<<ctas, kWarps * 32, smem, s>>>(p);
-    return cudaGetLastError();
+    return launch_kernel(kern, dim3(ctas), dim3(kWarps * 32), smem, s, p.pdl != 0, p);
 }
 
 template <typename T, int D, int GQ>

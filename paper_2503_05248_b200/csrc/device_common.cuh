@@ -229,7 +229,13 @@ __device__ __forceinline__ int task_fetch(const DecodeParams &p, int lane) {
 }
 
 // A warp with no task left: the last one resets the counters for the next launch.
+// Programmatic dependent launch: the warp first waits for the PREVIOUS decode grid to complete
+// (a no-op without the launch attribute), then lets the NEXT one launch.  So when the next
+// grid starts (its own parity of scratch), the grid before this one -- the last user of that
+// parity -- has completed, and the next grid's CTAs fill the SMs this grid's tail leaves idle.
 __device__ __forceinline__ void task_exit(const DecodeParams &p, int lane, int total_warps) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (lane == 0) {
         __threadfence();
         const int e = atomicAdd(p.task_counter + 1, 1);

@@ -395,15 +395,21 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
                                 pc.head_dim, e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
         ++p->n_launches;
     }
+    // device-resident decode-only steps chain the layer launches (programmatic dependent
+    // launch: layer l+1's CTAs fill layer l's tail); then the attention time is one window
+    const bool chained = !e2e && n_pf_rows == 0 && n > 0;
+    const bool per_layer_ev = e->cfg.time_attention && n > 0 && !chained;
+    if (e->cfg.time_attention && chained) DBK_CUDA(cudaEventRecord(e->att0[0], s));
     for (int l = 0; l < pc.layers; ++l) {
         uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
         uint8_t *od = static_cast<uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;
         bt.layer = l;
         bt.fuse_stats = l == 0 ? 1 : 0;
+        bt.chain = (chained && l > 0) ? 1 : 0;
         if (e2e && n > 0) DBK_CUDA(cudaStreamWaitEvent(s, e->ev_q[l], 0));
-        if (e->cfg.time_attention && n > 0) DBK_CUDA(cudaEventRecord(e->att0[l], s));
+        if (per_layer_ev) DBK_CUDA(cudaEventRecord(e->att0[l], s));
         DBK_TRY(dbk_decode_step(p, &bt, qd, od, e->cfg.out_dtype, s));
-        if (e->cfg.time_attention && n > 0) DBK_CUDA(cudaEventRecord(e->att1[l], s));
+        if (per_layer_ev) DBK_CUDA(cudaEventRecord(e->att1[l], s));
         e->layer_bytes[l] = p->last_decode_bytes;
         if (n_pf_rows > 0) {  // causal attention of the prefill chunk (K7, tensor cores)
             dbk_prefill_batch pb;
@@ -422,6 +428,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             DBK_CUDA(cudaMemcpyAsync(oh, od, n * orow, cudaMemcpyDeviceToHost, e->d2h));
         }
     }
+    if (e->cfg.time_attention && chained) DBK_CUDA(cudaEventRecord(e->att1[0], s));
     if (e2e && n > 0) {
         if (bufs->host_out) e->step_d2h += static_cast<int64_t>(pc.layers) * n * orow;
         DBK_CUDA(cudaEventRecord(e->ev_d2h, e->d2h));
@@ -451,7 +458,8 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     if (e->cfg.time_attention && n > 0) {
         for (int l = 0; l < pc.layers; ++l) {
             float a = 0.f;
-            DBK_CUDA(cudaEventElapsedTime(&a, e->att0[l], e->att1[l]));
+            if (per_layer_ev) DBK_CUDA(cudaEventElapsedTime(&a, e->att0[l], e->att1[l]));
+            else if (l == 0) DBK_CUDA(cudaEventElapsedTime(&a, e->att0[0], e->att1[0]));
             e->att_ms += a;
             e->att_bytes += e->layer_bytes[l];
             ++e->att_launches;

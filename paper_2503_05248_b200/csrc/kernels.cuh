@@ -67,8 +67,27 @@ struct DecodeParams {
     int32_t n_tasks;
     int32_t *task_counter;
     int32_t tma_rank;            // K2: 5 = one 5-D box per tile, 2 = 2-D boxes of 16 x 64
-    int32_t _pad;
+    // 1: programmatic dependent launch after the previous decode launch on the stream (its
+    // scratch -- split-K workspace, arrival and task counters -- is the other parity's)
+    int32_t pdl;
 };
+
+// Launch with (pdl) or without the programmatic-stream-serialization attribute.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                          Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<Args &&>(args)...);
+}
 
 struct AppendJob {
     int64_t req_id;

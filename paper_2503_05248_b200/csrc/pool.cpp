@@ -194,8 +194,8 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     };
     if (cudaMalloc(&p->d_bt, bt_n * sizeof(int32_t)) != cudaSuccess ||
         cudaMemset(p->d_bt, 0xFF, bt_n * sizeof(int32_t)) != cudaSuccess ||
-        cudaMalloc(&p->d_counters, static_cast<size_t>(cfg->max_requests) * cfg->kv_heads * sizeof(int32_t)) != cudaSuccess ||
-        cudaMemset(p->d_counters, 0, static_cast<size_t>(cfg->max_requests) * cfg->kv_heads * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&p->d_counters, 2 * static_cast<size_t>(cfg->max_requests) * cfg->kv_heads * sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(p->d_counters, 0, 2 * static_cast<size_t>(cfg->max_requests) * cfg->kv_heads * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&p->d_stats, 128 + 64) != cudaSuccess ||
         cudaMemset(p->d_stats, 0, 128 + 64) != cudaSuccess ||
         cudaMallocHost(&p->h_stats, sizeof(dbk_stats)) != cudaSuccess ||
@@ -216,6 +216,7 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     p->has_ptmap = make_pool_tmap(p, true, &p->ptmap, &prank);
     p->ctas_per_sm = p->has_tmap ? decode_gqa_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group)
                                  : decode_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group);
+    if (const char *e = std::getenv("DBK_NO_PDL")) p->pdl_enabled = !(e[0] == '1');  // A/B runs
     if (const char *e = std::getenv("DBK_CHUNK_PAGES")) {  // tuning override (multiple of 4, <= 64)
         const long long v = std::atoll(e);
         if (v >= 4 && v <= 64 && v % 4 == 0) p->force_chunk_pages = v;
@@ -538,8 +539,8 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
         p->d_ws_o = nullptr;
         p->d_ws_ml = nullptr;
         p->ws_cap = 0;
-        DBK_CUDA(cudaMalloc(&p->d_ws_o, c * p->cfg.head_dim * sizeof(float)));
-        DBK_CUDA(cudaMalloc(&p->d_ws_ml, c * sizeof(float2)));
+        DBK_CUDA(cudaMalloc(&p->d_ws_o, 2 * c * p->cfg.head_dim * sizeof(float)));  // two parities
+        DBK_CUDA(cudaMalloc(&p->d_ws_ml, 2 * c * sizeof(float2)));
         p->ws_cap = c;
     }
     p->meta_ids.assign(ids, ids + n);
@@ -594,9 +595,12 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     dp.out_dtype = out_dtype;
     dp.q_heads = p->cfg.q_heads;
     dp.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(p->cfg.head_dim)));
-    dp.ws_o = p->d_ws_o;
-    dp.ws_ml = p->d_ws_ml;
-    dp.counters = p->d_counters;
+    // consecutive launches alternate two copies of their scratch (programmatic dependent launch:
+    // a chained launch may start while the previous one drains; kernels.cuh DecodeParams::pdl)
+    const int par = p->launch_parity;
+    dp.ws_o = p->d_ws_o + static_cast<size_t>(par) * p->ws_cap * p->cfg.head_dim;
+    dp.ws_ml = p->d_ws_ml + static_cast<size_t>(par) * p->ws_cap;
+    dp.counters = p->d_counters + static_cast<size_t>(par) * p->cfg.max_requests * p->cfg.kv_heads;
     dp.fuse_stats = b->fuse_stats ? 1 : 0;
     dp.max_pages_per_req = p->cfg.max_pages_per_req;
     dp.stats = reinterpret_cast<unsigned long long *>(p->d_stats);
@@ -605,14 +609,15 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     dp.layer = b->layer;
     dp.kv_heads = p->cfg.kv_heads;
     dp.n_tasks = p->meta_items * p->cfg.kv_heads;
-    dp.task_counter = p->d_task_counter;
+    dp.task_counter = p->d_task_counter + 2 * par;
     dp.tma_rank = p->tma_rank;
-    dp._pad = 0;
+    dp.pdl = (b->chain && !b->fuse_stats && p->pdl_enabled) ? 1 : 0;
     // persistent grid: every resident CTA slot (4 warps each), or fewer for small batches
     const int ctas = std::max(1, std::min(p->num_sms * p->ctas_per_sm, (dp.n_tasks + 3) / 4));
     DBK_CUDA(launch_decode(dp, p->cfg.kv_dtype, p->cfg.head_dim, p->cfg.q_heads / p->cfg.kv_heads, ctas,
                            p->has_tmap ? &p->tmap : nullptr, s));
     ++p->n_launches;
+    p->launch_parity ^= 1;
     p->last_decode_bytes = decode_bytes(p, out_dtype);
     return DBK_OK;
 }

@@ -72,6 +72,8 @@ struct dbk_pool {
     int64_t max_chunk_pages = 32, force_chunk_pages = 0;
     int64_t last_decode_bytes = 0;
     int64_t n_launches = 0;                   // kernels launched by this pool (gpu_launches)
+    int launch_parity = 0;                    // scratch copy of the next decode launch
+    bool pdl_enabled = true;
     // pool-wide 2-D tensor map (rows of head_dim elements, 16 x 64 boxes, 128B swizzle) for K2
     alignas(64) CUtensorMap tmap;
     bool has_tmap = false;
