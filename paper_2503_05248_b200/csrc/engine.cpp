@@ -62,7 +62,7 @@ struct dbk_engine {
     int32_t comm_mode = DBK_MODE_DP;
     // end-to-end mode: host<->device copies on their own streams, ordered by events
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t ev_kv = nullptr, ev_d2h = nullptr;
+    cudaEvent_t ev_d2h = nullptr;
     std::vector<cudaEvent_t> ev_q, ev_o;
     ~dbk_engine() {
         up_pf.release();
@@ -73,7 +73,6 @@ struct dbk_engine {
         for (auto e : att1) cudaEventDestroy(e);
         for (auto e : ev_q) cudaEventDestroy(e);
         for (auto e : ev_o) cudaEventDestroy(e);
-        if (ev_kv) cudaEventDestroy(ev_kv);
         if (ev_d2h) cudaEventDestroy(ev_d2h);
         if (h2d) cudaStreamDestroy(h2d);
         if (d2h) cudaStreamDestroy(d2h);
@@ -99,7 +98,6 @@ dbk_status ensure_copy_streams(dbk_engine *e) {
     const int L = e->pool->cfg.layers;
     DBK_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
     DBK_CUDA(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
-    DBK_CUDA(cudaEventCreateWithFlags(&e->ev_kv, cudaEventDisableTiming));
     DBK_CUDA(cudaEventCreateWithFlags(&e->ev_d2h, cudaEventDisableTiming));
     e->ev_q.assign(L, nullptr);
     e->ev_o.assign(L, nullptr);
@@ -274,26 +272,28 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     const size_t orow = static_cast<size_t>(pc.q_heads) * pc.head_dim * (e->cfg.out_dtype == 2 ? 4 : 2);
     if (n > 0) {
         if (e2e) {
-            // end-to-end: this step's new K/V rows and every layer's q come from pinned host
-            // memory on a copy stream (inside the timed region: it waits on ev0); layer l's
-            // attention waits only for q[l], so the PCIe transfers overlap the attention
+            // end-to-end: this step's new K/V rows and q come from pinned host memory on a copy
+            // stream (inside the timed region: it waits on ev0), layer by layer: layer l's KV
+            // append and attention wait only for layer l's K, V and q, so the PCIe transfers of
+            // later layers overlap the attention of earlier ones
             DBK_TRY(ensure_copy_streams(e));
             uint8_t *kd = static_cast<uint8_t *>(bufs->kv_dev);
             uint8_t *vd = kd + static_cast<size_t>(pc.max_requests) * kvrow;
+            const size_t lrow = kvrow / pc.layers;  // one layer's K (or V) row of a request
             DBK_CUDA(cudaStreamWaitEvent(e->h2d, e->ev0, 0));
-            DBK_CUDA(cudaMemcpyAsync(kd, bufs->host_k, n * kvrow, cudaMemcpyHostToDevice, e->h2d));
-            DBK_CUDA(cudaMemcpyAsync(vd, bufs->host_v, n * kvrow, cudaMemcpyHostToDevice, e->h2d));
-            DBK_CUDA(cudaEventRecord(e->ev_kv, e->h2d));
-            e->step_h2d += 2 * static_cast<int64_t>(n * kvrow);
             for (int l = 0; l < pc.layers; ++l) {
+                const size_t off = static_cast<size_t>(l) * lrow;
+                DBK_CUDA(cudaMemcpy2DAsync(kd + off, kvrow, static_cast<const uint8_t *>(bufs->host_k) + off, kvrow,
+                                           lrow, n, cudaMemcpyHostToDevice, e->h2d));
+                DBK_CUDA(cudaMemcpy2DAsync(vd + off, kvrow, static_cast<const uint8_t *>(bufs->host_v) + off, kvrow,
+                                           lrow, n, cudaMemcpyHostToDevice, e->h2d));
                 uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
                 const uint8_t *qh = static_cast<const uint8_t *>(bufs->host_q) + static_cast<size_t>(l) * n * qrow;
                 DBK_CUDA(cudaMemcpyAsync(qd, qh, n * qrow, cudaMemcpyHostToDevice, e->h2d));
                 DBK_CUDA(cudaEventRecord(e->ev_q[l], e->h2d));
             }
-            e->step_h2d += static_cast<int64_t>(pc.layers) * n * qrow;
-            DBK_CUDA(cudaStreamWaitEvent(s, e->ev_kv, 0));
-            DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), kd, vd, 0, s));
+            e->step_h2d += 2 * static_cast<int64_t>(n * kvrow) + static_cast<int64_t>(pc.layers) * n * qrow;
+            DBK_TRY(append_plan(p, n, e->batch_ids.data(), ones.data(), true, s));  // layers appended below
         } else {
             DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), nullptr, nullptr, e->cfg.synth_seed, s));
         }
@@ -406,7 +406,12 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         bt.layer = l;
         bt.fuse_stats = l == 0 ? 1 : 0;
         bt.chain = (chained && l > 0) ? 1 : 0;
-        if (e2e && n > 0) DBK_CUDA(cudaStreamWaitEvent(s, e->ev_q[l], 0));
+        if (e2e && n > 0) {
+            DBK_CUDA(cudaStreamWaitEvent(s, e->ev_q[l], 0));
+            DBK_TRY(append_launch(p, bufs->kv_dev,
+                                  static_cast<const uint8_t *>(bufs->kv_dev) + static_cast<size_t>(pc.max_requests) * kvrow,
+                                  0, l, 1, s));
+        }
         if (per_layer_ev) DBK_CUDA(cudaEventRecord(e->att0[l], s));
         DBK_TRY(dbk_decode_step(p, &bt, qd, od, e->cfg.out_dtype, s));
         if (per_layer_ev) DBK_CUDA(cudaEventRecord(e->att1[l], s));

@@ -18,7 +18,7 @@ template <typename T, int D>
 __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
     constexpr int VPR = D / 8;  // 16-byte vectors per row
     const AppendJob job = p.jobs[blockIdx.x];
-    const int layer = blockIdx.y;
+    const int layer = p.layer0 + blockIdx.y;
     const int rows_per_block = job.ntok;  // rows of one (head, K|V) tile this job writes
     const int total = p.kv_heads * 2 * rows_per_block * VPR;
     uint8_t *page = p.kv + static_cast<size_t>(layer) * p.layer_stride +
@@ -139,7 +139,7 @@ int grid_for(long work, int block) {
 
 cudaError_t launch_append(const AppendParams &p, int kv_dtype, int head_dim, cudaStream_t s) {
     if (p.n_jobs <= 0) return cudaSuccess;
-    dim3 grid(p.n_jobs, p.layers);
+    dim3 grid(p.n_jobs, p.n_launch_layers > 0 ? p.n_launch_layers : p.layers);
     if (kv_dtype == 0) {
         if (head_dim == 128) append_kernel<__half, 128><<<grid, 256, 0, s>>>(p);
         else append_kernel<__half, 64><<<grid, 256, 0, s>>>(p);

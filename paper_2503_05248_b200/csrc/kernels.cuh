@@ -105,6 +105,8 @@ struct AppendParams {
     int32_t n_jobs, layers, kv_heads;
     const void *k_src, *v_src;   // [rows][layers][kv_heads][D] or null (synthetic)
     uint64_t seed;
+    int32_t layer0 = 0;          // this launch writes layers [layer0, layer0 + n_launch_layers)
+    int32_t n_launch_layers = 0; // 0 = all layers
 };
 
 struct BtDelta {

@@ -299,15 +299,12 @@ dbk_status flush_deltas(dbk_pool *p, cudaStream_t s) {
     p->pending.clear();
     return DBK_OK;
 }
-}  // namespace dbk
-
-extern "C" {
-
-dbk_status dbk_append_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok,
-                             const void *k, const void *v, uint64_t seed, void *stream) {
+// Validates and performs the bookkeeping of an append (pages lowest-free-first, all-or-nothing,
+// R7/R8), flushes the block-table deltas and uploads the job list; no KV is written yet.
+dbk_status append_plan(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok, bool explicit_rows,
+                       cudaStream_t s) {
     if (!p) return fail(DBK_EINVAL, "null pool");
     if (n < 0 || (n > 0 && (!ids || !n_tok))) return fail(DBK_EINVAL, "append_tokens: bad arrays");
-    if ((k == nullptr) != (v == nullptr)) return fail(DBK_EINVAL, "append_tokens: k and v must both be given or both NULL");
     const int64_t P = p->cfg.page_size;
     // validate and count pages first: all-or-nothing (R8)
     std::vector<Request *> rs(n);
@@ -333,7 +330,6 @@ dbk_status dbk_append_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const i
         return fail(DBK_ECAP, "append_tokens: needs %lld pages, %lld free", static_cast<long long>(need),
                     static_cast<long long>(p->pages.free_count));
     DBK_CUDA(cudaSetDevice(p->cfg.device));
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     p->jobs.clear();
     int32_t src_row = 0;
     for (int i = 0; i < n; ++i) {
@@ -354,7 +350,7 @@ dbk_status dbk_append_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const i
             j.pos0 = pos;
             j.ntok = cnt;
             j.phys = r.pages[pos / P];
-            j.src_row = k ? src_row + (pos - c0) : -1;
+            j.src_row = explicit_rows ? src_row + (pos - c0) : -1;
             p->jobs.push_back(j);
             pos += cnt;
         }
@@ -363,24 +359,46 @@ dbk_status dbk_append_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const i
     }
     ++p->epoch;
     DBK_TRY(flush_deltas(p, s));
-    if (!p->jobs.empty()) {
+    if (!p->jobs.empty())
         DBK_TRY(p->up_append.upload(p->jobs.data(), p->jobs.size() * sizeof(AppendJob), s));
-        AppendParams ap;
-        ap.kv = p->kv;
-        ap.layer_stride = p->layer_stride;
-        ap.page_stride = p->page_stride;
-        ap.tile_bytes = p->tile_bytes;
-        ap.jobs = static_cast<const AppendJob *>(p->up_append.dev);
-        ap.n_jobs = static_cast<int32_t>(p->jobs.size());
-        ap.layers = p->cfg.layers;
-        ap.kv_heads = p->cfg.kv_heads;
-        ap.k_src = k;
-        ap.v_src = v;
-        ap.seed = seed;
-        DBK_CUDA(launch_append(ap, p->cfg.kv_dtype, p->cfg.head_dim, s));
-        ++p->n_launches;
-    }
     return DBK_OK;
+}
+
+// Writes layers [layer0, layer0 + nl) of the jobs planned by the last append_plan (whose job
+// list is still in up_append's device buffer).
+dbk_status append_launch(dbk_pool *p, const void *k, const void *v, uint64_t seed, int32_t layer0, int32_t nl,
+                         cudaStream_t s) {
+    if (p->jobs.empty() || nl <= 0) return DBK_OK;
+    AppendParams ap;
+    ap.kv = p->kv;
+    ap.layer_stride = p->layer_stride;
+    ap.page_stride = p->page_stride;
+    ap.tile_bytes = p->tile_bytes;
+    ap.jobs = static_cast<const AppendJob *>(p->up_append.dev);
+    ap.n_jobs = static_cast<int32_t>(p->jobs.size());
+    ap.layers = p->cfg.layers;
+    ap.kv_heads = p->cfg.kv_heads;
+    ap.k_src = k;
+    ap.v_src = v;
+    ap.seed = seed;
+    ap.layer0 = layer0;
+    ap.n_launch_layers = nl;
+    DBK_CUDA(launch_append(ap, p->cfg.kv_dtype, p->cfg.head_dim, s));
+    ++p->n_launches;
+    return DBK_OK;
+}
+
+}  // namespace dbk
+
+extern "C" {
+
+dbk_status dbk_append_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok,
+                             const void *k, const void *v, uint64_t seed, void *stream) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if ((k == nullptr) != (v == nullptr)) return fail(DBK_EINVAL, "append_tokens: k and v must both be given or both NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DBK_TRY(dbk::append_plan(p, n, ids, n_tok, k != nullptr, s));
+    return dbk::append_launch(p, k, v, seed, 0, p->cfg.layers, s);
 }
 
 dbk_status dbk_release(dbk_pool *p, int32_t n, const int64_t *ids) {
