@@ -132,7 +132,7 @@ def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None)
 
 def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
                  out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1,
-                 trace_override=None, eps_d_ms=None, pd_fusion=False):
+                 trace_override=None, eps_d_ms=None, pd_fusion=False, swap_bytes=0):
     """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
     config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
@@ -155,13 +155,15 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     cap_pages = int(cap_bytes // (P * beta))
     maxp = -(-c["trace"]["L_max"] // P)
     pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, "f16", device=device)
+    if swap_bytes:  # swap preemption (R29-R31): pinned host swap space
+        pool.swap_space_attach(torch.empty(int(swap_bytes), dtype=torch.uint8, pin_memory=True))
     # M_max of the whole job: DP shards add their pools; TP ranks hold the same tokens
     mem_cap_total = cap_pages * P * beta * (world if tp == 1 else 1)
     sched = dbk.Scheduler(**sched_kwargs(c, beta, policy, b_static, sla_ms, eps_d_ms))
     eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap_total, seed=seed,
                      out_dtype=out_dtype, time_attention=time_attention,
                      rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0,
-                     pd_fusion=pd_fusion)
+                     pd_fusion=pd_fusion, preempt_mode=1 if swap_bytes else 0)
     et = torch.float32 if out_dtype == 2 else torch.float16
     qd = torch.empty(L, max_req, Hq, d, dtype=torch.float16, device=f"cuda:{device}")
     od = torch.empty(L, max_req, Hq, d, dtype=et, device=f"cuda:{device}")

@@ -11,6 +11,9 @@
              the shape of Table I row 3 -- attention-only.
 * --sla    : the SLA feedback (Alg. 2 + min with Alg. 1) on the 13B shape with a binding
              D_SLA = tau(b_mem / 2) from the sweep's fit, and the literal 50 ms.
+* --swap   : preemption by swapping vs recomputation (NEXT row 4) on the 7B shape with a
+             40 GB KV cap: static b = 256 over-commits it (recompute / swap to a 16 GB pinned
+             host space) vs the memory-aware rule, which keeps the batch under the cap.
 Every run goes through the C-ABI engine; numbers are device-timed (CUDA events).
 """
 from __future__ import annotations
@@ -181,6 +184,44 @@ def pd_table(cfg="llama2-7b", bs=(64, 128, 256)):
     return dict(config=cfg, rows=rows)
 
 
+def swap_table(cfg="llama2-7b", kv_gb=40.0, swap_gb=16.0, n_req=1500, b=256):
+    """Whole trace (all-at-once) near the KV cap: recompute vs swap preemption (static b) and
+    the memory-aware rule.  In this attention-only engine a recompute is the KV fill of the
+    request's T tokens (no weights), i.e. a lower bound of the real re-prefill cost."""
+    import gc
+
+    import torch
+    rows = []
+    for pol, swap in (("static", 0), ("static", swap_gb), ("memory", 0)):
+        gc.collect()
+        torch.cuda.empty_cache()
+        S = bench.setup_engine(cfg_name=cfg, policy=pol, b_static=b, time_attention=False, n_req=n_req,
+                               cap_bytes=int(kv_gb * bench.GB), swap_bytes=int(swap * bench.GB))
+        eng = S["eng"]
+        bufs = eng.buffers(S["qd"], S["od"])
+        t0 = time.time()
+        recs, ms = bench.run_steps(S, 10 ** 9, bufs, torch.cuda.current_stream())
+        dev_s = ms / 1e3
+        sw = [r for r in recs if r["n_swap_out"] or r["n_swap_in"]]
+        rows.append(dict(policy=pol, b_static=b if pol == "static" else None, preempt="swap" if swap else "recompute",
+                         swap_gb=swap, kv_cap_pages=S["cap_pages"], steps=len(recs), device_s=dev_s,
+                         tokens_per_s=sum(r["n_decode"] for r in recs) / dev_s,
+                         mean_b=float(np.mean([r["n_decode"] for r in recs])),
+                         preemptions=int(sum(r["n_preempted"] for r in recs)),
+                         swapped_out=int(sum(r["n_swap_out"] for r in recs)),
+                         swapped_in=int(sum(r["n_swap_in"] for r in recs)),
+                         swap_gb_moved=sum(r["swap_bytes"] for r in recs) / bench.GB,
+                         mean_step_ms=float(np.mean([r["step_ns"] for r in recs]) / 1e6),
+                         mean_step_ms_with_swap=float(np.mean([r["step_ns"] for r in sw]) / 1e6) if sw else None,
+                         wall_s=time.time() - t0))
+        print(json.dumps(rows[-1]), flush=True)
+        S["eng"].close()
+        S["pool"].close()
+        S.clear()
+        del eng, bufs
+    return dict(config=cfg, kv_gb=kv_gb, n_requests=n_req, rows=rows)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--fig3", action="store_true")
@@ -188,6 +229,7 @@ def main():
     ap.add_argument("--sla", action="store_true")
     ap.add_argument("--capacity", action="store_true")
     ap.add_argument("--pd", action="store_true")
+    ap.add_argument("--swap", action="store_true")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
     a = ap.parse_args()
     import torch
@@ -208,6 +250,9 @@ def main():
         save()
     if a.pd:
         res["pd_table"] = pd_table()
+        save()
+    if a.swap:
+        res["swap"] = swap_table()
         save()
     if a.sla or a.capacity:
         res["fig3_13b"] = fig3("llama2-13b-sla", bs=(32, 64, 128, 256))

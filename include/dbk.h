@@ -101,6 +101,36 @@ dbk_status dbk_append_tokens(dbk_pool *pool, int32_t n_req, const int64_t *req_i
  * next launch.  ENOENT on an unknown id (earlier ids are released). */
 dbk_status dbk_release(dbk_pool *pool, int32_t n_req, const int64_t *req_ids);
 
+/* Swap space ("The swapping method involves
+ * temporarily moving data from GPU memory to CPU memory when capacity is
+ * exceeded.  The data are moved back to the GPU when space becomes
+ * available").  host_mem: caller-owned PINNED host memory (cudaHostAlloc /
+ * torch pin_memory; EINVAL otherwise) that outlives the pool; it holds
+ * floor(bytes / (layers * kv_heads * 2*P*d*2)) swap pages laid out
+ * [layer][swap_page][kv_head][2][P][head_dim] (layer-major, like the pool).
+ * NULL detaches.  EINVAL while requests are swapped out. */
+dbk_status dbk_swap_space_attach(dbk_pool *pool, void *host_mem, size_t bytes, int64_t *swap_pages_out);
+
+/* Move each request's KV (all its pages, all layers) into swap pages taken
+ * lowest-free-first in batch order, then release its device pages and slot
+ * (as dbk_release); the request keeps its id, l_in, l_out and ctx.
+ * All-or-nothing: ECAP if the swap space lacks pages, ENOENT on an unknown
+ * or already swapped id (state unchanged).  The device-to-host copies are
+ * copy-engine 2-D copies (one per run of consecutive pages) async on
+ * `stream`, ordered before any later write to the released pages on it. */
+dbk_status dbk_swap_out(dbk_pool *pool, int32_t n_req, const int64_t *req_ids, void *stream);
+
+/* Bring swapped requests back: each gets a slot and ceil(ctx/P) device pages
+ * lowest-free-first in batch order (exactly the pages an append of ctx tokens
+ * would take, R7), its KV is copied host-to-device on `stream` and its swap
+ * pages are freed.  All-or-nothing: ECAP if device pages are short, EINVAL if
+ * slots are short, ENOENT if an id is not swapped out.  dbk_release of a
+ * swapped-out id frees its swap pages. */
+dbk_status dbk_swap_in(dbk_pool *pool, int32_t n_req, const int64_t *req_ids, void *stream);
+
+/* Swap pages in use / free, and the bytes moved by swap_out + swap_in so far. */
+dbk_status dbk_swap_usage(dbk_pool *pool, int64_t *used_pages, int64_t *free_pages, int64_t *bytes_moved);
+
 /* Host view of one request: ctx (tokens held), n_pages, slot, and up to
  * pages_cap page ids (logical order) into pages_out (nullable). */
 dbk_status dbk_request_info(dbk_pool *pool, int64_t req_id, int32_t *ctx, int32_t *n_pages,
@@ -274,7 +304,9 @@ typedef struct dbk_engine_config {
     int32_t pd_fusion;              /* 1: PD fusion -- admitted prompts are prefilled in     *
                                      * chunks of c_t = max(0, b_t - N^d) tokens inside the    *
                                      * decode iteration (R25-R28; device-resident mode only)  */
-    int32_t _reserved;
+    int32_t preempt_mode;           /* 0: recompute (R18); 1: swap a victim to the pool's   *
+                                     * swap space when it has room, else recompute (R29-R31;*
+                                     * needs dbk_swap_space_attach; not with pd_fusion)      */
 } dbk_engine_config;
 
 typedef struct dbk_engine dbk_engine;
@@ -301,6 +333,8 @@ typedef struct dbk_step_record {
     int64_t h2d_bytes, d2h_bytes;
     int32_t launches;
     int32_t n_prefill;              /* PD fusion: prompt tokens prefilled this step (this rank) */
+    int32_t n_swap_out, n_swap_in;  /* swap preemption: victims swapped out / readmitted by swap-in */
+    int64_t swap_bytes;             /* bytes the swaps of this step moved (both directions)   */
 } dbk_step_record;
 
 dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_config *cfg,

@@ -39,6 +39,18 @@ Admitted requests first PREFILL in chunks, then decode.  Step order (replaces 2-
  e. requests whose prompt is complete join the running batch at the END of the step (they
     emit their first token in the next step).
 N^p (n_waiting) = released requests not in this step's decode batch = queue + prefilling.
+
+Swap preemption ("temporarily moving data from GPU memory
+to CPU memory when capacity is exceeded.  The data are moved back to the GPU when space
+becomes available"; readings R29-R31 of DESIGN.md), non-PD steps only:
+ 3'. a victim of step 3 whose pages fit the free swap pages (swap_cap_pages in total) is
+     swapped out: its device pages are released exactly as on recompute and it goes to the
+     queue head, but it keeps its KV (ctx = l_in + generated) in swap pages; otherwise it is
+     preempted for recompute as before;
+ 2'. admitting a swapped-out head needs the same ceil((T + 1) / P) free pages; it gets
+     ceil(T / P) pages lowest-free-first (the pages a prefill of T tokens would take) and its
+     swap pages are freed -- the page tables are identical to recompute; only the KV's origin
+     (copied back instead of recomputed) and the step latency differ.
 """
 from __future__ import annotations
 
@@ -64,8 +76,14 @@ class RankEngine:
     """One GPU's request shard (DP) or the whole batch (G = 1 / TP)."""
 
     def __init__(self, req_ids, arrival_ns, l_in, l_out, cap_pages, page_size, rank=0, world=1,
-                 pd=False, max_rows=None):
+                 pd=False, max_rows=None, swap_cap_pages=0):
         self.pd = bool(pd)
+        if swap_cap_pages and pd:
+            raise ValueError("swap preemption is defined for non-PD steps only")
+        self.swap_cap = int(swap_cap_pages)  # 0: recompute only
+        self.swapped = {}                    # request -> swap pages held
+        self.swap_used = 0
+        self.last_swaps = (0, 0)             # (swapped out, swapped in) of the last step
         self.max_rows = max_rows
         self.prefilling = []          # PD: [req, prompt tokens done], admission order
         self.last_chunks = []         # PD: (req, q_start, q_len) of the last step
@@ -101,13 +119,16 @@ class RankEngine:
         return self.arrival[self.next] if self.next < len(self.req_ids) else None
 
     def admit_and_grow(self, b_share):
-        admitted = preempted = 0
+        admitted = preempted = swap_out = swap_in = 0
         while self.queue and len(self.running) < b_share:           # step 2
             r = self.queue[0]
             T = self.l_in[r] + self.gen[r]
             if self.kv.alloc.free < -(-(T + 1) // self.P):
                 break
             self.queue.popleft()
+            if r in self.swapped:                                      # step 2'
+                self.swap_used -= self.swapped.pop(r)
+                swap_in += 1
             self.kv.begin(r)
             self.kv.append([r], [T])
             self.running.append(r)
@@ -117,9 +138,15 @@ class RankEngine:
             if need <= self.kv.alloc.free:
                 break
             victim = self.running.pop()
+            held = len(self.kv.pages[victim])
+            if self.swap_cap and held <= self.swap_cap - self.swap_used:   # step 3'
+                self.swapped[victim] = held
+                self.swap_used += held
+                swap_out += 1
             self.kv.release(victim)
             self.queue.appendleft(victim)
             preempted += 1
+        self.last_swaps = (swap_out, swap_in)
         self.kv.append(self.running, [1] * len(self.running))
         for r in self.running:
             self.gen[r] += 1
@@ -278,7 +305,9 @@ class Replay:
                    used_pages=sum(used), step_ns=int(step_ns), b_next=self.b, rationale=rationale,
                    L0=self.sched.L0, b_quad=self.sched.bq, b_mem=self.sched.b_mem,
                    b_sla=self.sched.b_sla, table_hash=hashes[0] if G == 1 else tuple(hashes),
-                   stats=g, local_stats=recs, batches=batches, n_prefill=n_prefill, chunks=chunks)
+                   stats=g, local_stats=recs, batches=batches, n_prefill=n_prefill, chunks=chunks,
+                   n_swap_out=sum(e.last_swaps[0] for e in self.ranks),
+                   n_swap_in=sum(e.last_swaps[1] for e in self.ranks))
         if any(e.pd for e in self.ranks):
             rec["used_pages"] = g["sum_pages"]   # decode batch pages (prefilling pages excluded)
         self.t += 1

@@ -86,6 +86,27 @@ class KVPool:
         ids, pids = _i64(req_ids)
         _lib.dbk_release(self.h, len(ids), pids)
 
+    def swap_space_attach(self, host_mem):
+        """host_mem: a pinned torch tensor (kept alive by the pool object); returns swap pages."""
+        self._swap_mem = host_mem
+        n = C.c_int64()
+        nbytes = host_mem.numel() * host_mem.element_size() if host_mem is not None else 0
+        _lib.dbk_swap_space_attach(self.h, _ptr(host_mem), nbytes, C.byref(n))
+        return n.value
+
+    def swap_out(self, req_ids, stream=None):
+        ids, pids = _i64(req_ids)
+        _lib.dbk_swap_out(self.h, len(ids), pids, _stream(stream))
+
+    def swap_in(self, req_ids, stream=None):
+        ids, pids = _i64(req_ids)
+        _lib.dbk_swap_in(self.h, len(ids), pids, _stream(stream))
+
+    def swap_usage(self):
+        u, f, b = C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.dbk_swap_usage(self.h, C.byref(u), C.byref(f), C.byref(b))
+        return u.value, f.value, b.value
+
     def request_info(self, req_id):
         ctx, npg, slot = C.c_int32(), C.c_int32(), C.c_int32()
         _lib.dbk_request_info(self.h, int(req_id), C.byref(ctx), C.byref(npg), C.byref(slot), None, 0)
@@ -172,7 +193,7 @@ class Engine:
 
     def __init__(self, pool: KVPool, sched: Scheduler, arrival_ns, l_in, l_out, mem_cap_bytes,
                  sla_ms=0.0, seed=0, out_dtype=2, time_attention=False, rank=0, world=1,
-                 q_scale_log2=0, req_ids=None, pd_fusion=False):
+                 q_scale_log2=0, req_ids=None, pd_fusion=False, preempt_mode=0):
         self.pool, self.sched = pool, sched
         self._arr, pa = _i64(arrival_ns)
         self._li, pli = _i32(l_in)
@@ -182,7 +203,8 @@ class Engine:
             self._ids, pids = _i64(req_ids)
         self.cfg = dbk_engine_config(len(self._arr), q_scale_log2, pa, pli, plo, pids,
                                      int(mem_cap_bytes), float(sla_ms), int(seed), int(out_dtype),
-                                     1 if time_attention else 0, rank, world, 1 if pd_fusion else 0, 0)
+                                     1 if time_attention else 0, rank, world, 1 if pd_fusion else 0,
+                                     int(preempt_mode))
         h = C.c_void_p()
         _lib.dbk_engine_create(pool.h, sched.h, C.byref(self.cfg), C.byref(h))
         self.h = h

@@ -84,7 +84,7 @@ class dbk_engine_config(C.Structure):
                 ("l_out", C.POINTER(C.c_int32)), ("req_ids", C.POINTER(C.c_int64)),
                 ("mem_cap_bytes", C.c_int64), ("sla_ms", C.c_double), ("synth_seed", C.c_uint64),
                 ("out_dtype", C.c_int32), ("time_attention", C.c_int32), ("rank", C.c_int32),
-                ("world", C.c_int32), ("pd_fusion", C.c_int32), ("_reserved", C.c_int32)]
+                ("world", C.c_int32), ("pd_fusion", C.c_int32), ("preempt_mode", C.c_int32)]
 
 
 class dbk_engine_buffers(C.Structure):
@@ -99,7 +99,8 @@ class dbk_step_record(C.Structure):
                 ("b_t", C.c_int32), ("b_next", C.c_int32), ("n_admitted", C.c_int32),
                 ("n_preempted", C.c_int32), ("n_decode", C.c_int32), ("n_finished", C.c_int32),
                 ("rationale", C.c_int32), ("n_waiting", C.c_int32), ("h2d_bytes", C.c_int64),
-                ("d2h_bytes", C.c_int64), ("launches", C.c_int32), ("n_prefill", C.c_int32)]
+                ("d2h_bytes", C.c_int64), ("launches", C.c_int32), ("n_prefill", C.c_int32),
+                ("n_swap_out", C.c_int32), ("n_swap_in", C.c_int32), ("swap_bytes", C.c_int64)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_ if f != "_reserved"}
@@ -119,6 +120,10 @@ SIGNATURES = {
     "dbk_request_begin": [P, I64, I32, I32],
     "dbk_append_tokens": [P, I32, PI64, PI32, P, P, U64, P],
     "dbk_release": [P, I32, PI64],
+    "dbk_swap_space_attach": [P, P, C.c_size_t, PI64],
+    "dbk_swap_out": [P, I32, PI64, P],
+    "dbk_swap_in": [P, I32, PI64, P],
+    "dbk_swap_usage": [P, PI64, PI64, PI64],
     "dbk_request_info": [P, I64, PI32, PI32, PI32, PI32, I32],
     "dbk_pool_usage": [P, PI64, PI64],
     "dbk_block_table_d2h": [P, PI32, P],

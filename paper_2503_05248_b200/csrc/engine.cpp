@@ -22,6 +22,7 @@ struct dbk_engine {
     std::vector<int64_t> arrival, ids;
     std::vector<int32_t> l_in, l_out, gen;
     std::vector<int64_t> admit_ns, finish_ns;  // per trace index, -1 = not yet
+    std::vector<uint8_t> swapped;     // per trace index: KV in the pool's swap space (R29)
     std::vector<int32_t> mine;        // local trace indices in arrival order
     size_t next_local = 0;            // next local index to release
     size_t next_global = 0;           // first global index with arrival > clock
@@ -47,6 +48,8 @@ struct dbk_engine {
     bool in_step = false;
     int64_t step_clock0 = 0;
     int32_t step_b = 0, step_adm = 0, step_pre = 0, step_launches = 0;
+    int32_t step_swap_out = 0, step_swap_in = 0;
+    int64_t step_swap_bytes = 0;
     uint64_t step_hash = 0;
     int64_t step_h2d = 0, step_d2h = 0;
     std::vector<int64_t> batch_ids;
@@ -122,6 +125,9 @@ dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_
     if (c.out_dtype < 0 || c.out_dtype > 2) return fail(DBK_EINVAL, "engine_create: bad out_dtype");
     if (c.pd_fusion != 0 && c.pd_fusion != 1) return fail(DBK_EINVAL, "engine_create: pd_fusion must be 0 or 1");
     if (c.pd_fusion && !pool->has_ptmap) return fail(DBK_EINVAL, "engine_create: PD fusion needs the pool's prefill tensor map");
+    if (c.preempt_mode != 0 && c.preempt_mode != 1) return fail(DBK_EINVAL, "engine_create: preempt_mode must be 0 or 1");
+    if (c.preempt_mode == 1 && (c.pd_fusion || !pool->swap_host))
+        return fail(DBK_EINVAL, "engine_create: swap preemption needs an attached swap space and pd_fusion = 0");
     for (int i = 0; i < c.n_requests; ++i) {
         if (c.l_in[i] < 1 || c.l_out[i] < 1) return fail(DBK_EINVAL, "engine_create: lengths must be >= 1");
         if (i && c.arrival_ns[i] < c.arrival_ns[i - 1]) return fail(DBK_EINVAL, "engine_create: arrivals must be sorted");
@@ -140,6 +146,7 @@ dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_
     e->gen.assign(c.n_requests, 0);
     e->admit_ns.assign(c.n_requests, -1);
     e->finish_ns.assign(c.n_requests, -1);
+    e->swapped.assign(c.n_requests, 0);
     e->ids.resize(c.n_requests);
     for (int i = 0; i < c.n_requests; ++i) e->ids[i] = c.req_ids ? c.req_ids[i] : i;
     for (int i = c.rank; i < c.n_requests; i += c.world) e->mine.push_back(i);
@@ -217,32 +224,50 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     e->step_b = e->b;
     DBK_CUDA(cudaEventRecord(e->ev0, s));
 
-    // S1: FCFS admission with head-of-line blocking (R17); prefill = synthetic fill of T tokens
+    // S1: FCFS admission with head-of-line blocking (R17); prefill = synthetic fill of T tokens,
+    // a swapped-out request is swapped back in instead (R30).  Pages are taken in admission
+    // order: pending fills are flushed before a swap-in.
     const int32_t share = b_share(e->b, e->cfg.rank, e->cfg.world);
     std::vector<int64_t> adm_ids;
     std::vector<int32_t> adm_tok;
     int64_t free_pages = p->pages.free_count;
     int32_t adm = 0, pre = 0;
+    e->step_swap_out = e->step_swap_in = 0;
+    const int64_t swap_bytes0 = p->swap_bytes_moved;
+    auto flush_fills = [&]() -> dbk_status {
+        if (!adm_ids.empty())
+            DBK_TRY(dbk_append_tokens(p, static_cast<int32_t>(adm_ids.size()), adm_ids.data(), adm_tok.data(),
+                                      nullptr, nullptr, e->cfg.synth_seed, s));
+        adm_ids.clear();
+        adm_tok.clear();
+        return DBK_OK;
+    };
     while (!pd && !e->queue.empty() && static_cast<int32_t>(e->running.size()) < share) {
         const int32_t r = e->queue.front();
         const int64_t T = static_cast<int64_t>(e->l_in[r]) + e->gen[r];
         if (free_pages < ceil_div(T + 1, P)) break;
         e->queue.pop_front();
-        DBK_TRY(dbk_request_begin(p, e->ids[r], e->l_in[r], e->l_out[r]));
+        if (e->swapped[r]) {
+            DBK_TRY(flush_fills());
+            DBK_TRY(dbk_swap_in(p, 1, &e->ids[r], s));
+            e->swapped[r] = 0;
+            ++e->step_swap_in;
+        } else {
+            DBK_TRY(dbk_request_begin(p, e->ids[r], e->l_in[r], e->l_out[r]));
+            adm_ids.push_back(e->ids[r]);
+            adm_tok.push_back(static_cast<int32_t>(T));
+        }
         free_pages -= ceil_div(T, P);
-        adm_ids.push_back(e->ids[r]);
-        adm_tok.push_back(static_cast<int32_t>(T));
         e->running.push_back(r);
         if (e->admit_ns[r] < 0) e->admit_ns[r] = e->clock;
         ++adm;
     }
-    if (!adm_ids.empty())
-        DBK_TRY(dbk_append_tokens(p, static_cast<int32_t>(adm_ids.size()), adm_ids.data(), adm_tok.data(),
-                                  nullptr, nullptr, e->cfg.synth_seed, s));
+    DBK_TRY(flush_fills());
 
     // S1/S2: page growth for this step's decode token; LIFO preemption on overflow (R18)
     // a running request holds ctx = l_in + generated tokens; it needs a page iff ctx % P == 0.
     // PD fusion: the admission order is running ++ prefilling, so prefills are evicted first.
+    // Swap mode (R29): a running victim goes to the swap space if it has room, else recompute.
     int64_t need = 0;
     for (int32_t r : e->running)
         if ((static_cast<int64_t>(e->l_in[r]) + e->gen[r]) % P == 0) ++need;
@@ -257,10 +282,18 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             if ((static_cast<int64_t>(e->l_in[victim]) + e->gen[victim]) % P == 0) --need;
         }
         const int64_t vid = e->ids[victim];
-        DBK_TRY(dbk_release(p, 1, &vid));
+        const int64_t vpages = ceil_div(static_cast<int64_t>(e->l_in[victim]) + e->gen[victim], P);
+        if (e->cfg.preempt_mode == 1 && vpages <= p->swap_pages.free_count) {
+            DBK_TRY(dbk_swap_out(p, 1, &vid, s));
+            e->swapped[victim] = 1;
+            ++e->step_swap_out;
+        } else {
+            DBK_TRY(dbk_release(p, 1, &vid));
+        }
         e->queue.push_front(victim);
         ++pre;
     }
+    e->step_swap_bytes = p->swap_bytes_moved - swap_bytes0;
     const int32_t n = static_cast<int32_t>(e->running.size());
     e->batch_ids.resize(n);
     e->batch_ctx.resize(n);
@@ -528,6 +561,9 @@ dbk_status dbk_engine_step_finish(dbk_engine *e, const dbk_stats *global, dbk_st
         rec->d2h_bytes = e->step_d2h;
         rec->launches = e->step_launches;
         rec->n_prefill = e->step_prefill;
+        rec->n_swap_out = e->step_swap_out;
+        rec->n_swap_in = e->step_swap_in;
+        rec->swap_bytes = e->step_swap_bytes;
     }
     e->b = b_next;
     e->prev_known = true;

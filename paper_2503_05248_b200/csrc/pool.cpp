@@ -252,7 +252,8 @@ dbk_status dbk_kv_pool_destroy(dbk_pool *p) {
 dbk_status dbk_request_begin(dbk_pool *p, int64_t id, int32_t l_in, int32_t l_out) {
     if (!p) return fail(DBK_EINVAL, "null pool");
     if (id < 0 || l_in < 1 || l_out < 1) return fail(DBK_EINVAL, "request_begin: need id >= 0, l_in >= 1, l_out >= 1");
-    if (p->reqs.count(id)) return fail(DBK_EINVAL, "request %lld already active", static_cast<long long>(id));
+    if (p->reqs.count(id) || p->swapped.count(id))
+        return fail(DBK_EINVAL, "request %lld already active", static_cast<long long>(id));
     const int64_t P = p->cfg.page_size;
     const int64_t need = (static_cast<int64_t>(l_in) + l_out + P - 1) / P;
     if (need > p->cfg.cap_pages || need > p->cfg.max_pages_per_req)
@@ -405,6 +406,12 @@ dbk_status dbk_release(dbk_pool *p, int32_t n, const int64_t *ids) {
     if (!p) return fail(DBK_EINVAL, "null pool");
     if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "release: bad arrays");
     for (int i = 0; i < n; ++i) {
+        auto sw = p->swapped.find(ids[i]);
+        if (sw != p->swapped.end()) {  // a swapped-out request: its swap pages go back
+            for (int32_t h : sw->second.swap_pages) p->swap_pages.give_back(h);
+            p->swapped.erase(sw);
+            continue;
+        }
         auto it = p->reqs.find(ids[i]);
         if (it == p->reqs.end()) return fail(DBK_ENOENT, "release: unknown request %lld", static_cast<long long>(ids[i]));
         Request &r = it->second;
@@ -417,6 +424,144 @@ dbk_status dbk_release(dbk_pool *p, int32_t n, const int64_t *ids) {
         p->reqs.erase(it);
     }
     ++p->epoch;
+    return DBK_OK;
+}
+
+dbk_status dbk_swap_space_attach(dbk_pool *p, void *host_mem, size_t bytes, int64_t *swap_pages_out) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if (!p->swapped.empty()) return fail(DBK_EINVAL, "swap_space_attach: requests are swapped out");
+    const size_t per_page = static_cast<size_t>(p->cfg.layers) * p->page_stride;
+    const int64_t n = host_mem ? static_cast<int64_t>(bytes / per_page) : 0;
+    if (host_mem) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, host_mem) != cudaSuccess || a.type != cudaMemoryTypeHost) {
+            cudaGetLastError();
+            return fail(DBK_EINVAL, "swap_space_attach: host_mem must be pinned host memory (cudaHostAlloc)");
+        }
+        if (n < 1) return fail(DBK_EINVAL, "swap_space_attach: %zu bytes hold no page (%zu B per page)", bytes, per_page);
+    }
+    p->swap_host = static_cast<uint8_t *>(host_mem);
+    p->swap_cap = n;
+    p->swap_pages.init(n);
+    if (swap_pages_out) *swap_pages_out = n;
+    return DBK_OK;
+}
+
+dbk_status dbk_swap_usage(dbk_pool *p, int64_t *used, int64_t *free_pages, int64_t *bytes_moved) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if (used) *used = p->swap_cap - p->swap_pages.free_count;
+    if (free_pages) *free_pages = p->swap_pages.free_count;
+    if (bytes_moved) *bytes_moved = p->swap_bytes_moved;
+    return DBK_OK;
+}
+
+}  // extern "C"
+
+namespace dbk {
+// Copy engine transfers of one request's pages: maximal runs where the device page and the
+// swap page both advance by one become ONE 2-D copy (rows = layers).
+dbk_status swap_copy(dbk_pool *p, const std::vector<int32_t> &dev_pages, const std::vector<int32_t> &host_pages,
+                     bool to_host, cudaStream_t s) {
+    const size_t ps = static_cast<size_t>(p->page_stride);
+    const size_t hpitch = static_cast<size_t>(p->swap_cap) * ps;
+    const size_t dpitch = static_cast<size_t>(p->layer_stride);
+    size_t k = 0;
+    while (k < dev_pages.size()) {
+        size_t run = 1;
+        while (k + run < dev_pages.size() && dev_pages[k + run] == dev_pages[k] + static_cast<int32_t>(run) &&
+               host_pages[k + run] == host_pages[k] + static_cast<int32_t>(run))
+            ++run;
+        uint8_t *dev = p->kv + static_cast<size_t>(dev_pages[k]) * ps;
+        uint8_t *host = p->swap_host + static_cast<size_t>(host_pages[k]) * ps;
+        if (to_host)
+            DBK_CUDA(cudaMemcpy2DAsync(host, hpitch, dev, dpitch, run * ps, p->cfg.layers, cudaMemcpyDeviceToHost, s));
+        else
+            DBK_CUDA(cudaMemcpy2DAsync(dev, dpitch, host, hpitch, run * ps, p->cfg.layers, cudaMemcpyHostToDevice, s));
+        p->swap_bytes_moved += static_cast<int64_t>(run * ps) * p->cfg.layers;
+        k += run;
+    }
+    return DBK_OK;
+}
+}  // namespace dbk
+
+extern "C" {
+
+dbk_status dbk_swap_out(dbk_pool *p, int32_t n, const int64_t *ids, void *stream) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "swap_out: bad arrays");
+    if (!p->swap_host) return fail(DBK_EINVAL, "swap_out: no swap space attached");
+    int64_t need = 0;
+    for (int i = 0; i < n; ++i) {
+        auto it = p->reqs.find(ids[i]);
+        if (it == p->reqs.end()) return fail(DBK_ENOENT, "swap_out: unknown request %lld", static_cast<long long>(ids[i]));
+        need += static_cast<int64_t>(it->second.pages.size());
+    }
+    if (need > p->swap_pages.free_count)
+        return fail(DBK_ECAP, "swap_out: needs %lld swap pages, %lld free", static_cast<long long>(need),
+                    static_cast<long long>(p->swap_pages.free_count));
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int i = 0; i < n; ++i) {
+        auto it = p->reqs.find(ids[i]);
+        Request &r = it->second;
+        SwappedRequest sr;
+        sr.l_in = r.l_in;
+        sr.l_out = r.l_out;
+        sr.ctx = r.ctx;
+        for (size_t x = 0; x < r.pages.size(); ++x) sr.swap_pages.push_back(static_cast<int32_t>(p->swap_pages.take_lowest()));
+        // stream order: the D2H copies precede any later write to the released pages
+        DBK_TRY(swap_copy(p, r.pages, sr.swap_pages, true, s));
+        for (size_t x = 0; x < r.pages.size(); ++x) {
+            p->pages.give_back(r.pages[x]);
+            p->host_bt[static_cast<size_t>(r.slot) * p->cfg.max_pages_per_req + x] = -1;
+            p->pending.push_back({r.slot, static_cast<int32_t>(x), -1});
+        }
+        p->free_slots.push(r.slot);
+        p->swapped.emplace(ids[i], std::move(sr));
+        p->reqs.erase(it);
+    }
+    ++p->epoch;
+    return DBK_OK;
+}
+
+dbk_status dbk_swap_in(dbk_pool *p, int32_t n, const int64_t *ids, void *stream) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "swap_in: bad arrays");
+    int64_t need = 0;
+    for (int i = 0; i < n; ++i) {
+        auto it = p->swapped.find(ids[i]);
+        if (it == p->swapped.end()) return fail(DBK_ENOENT, "swap_in: request %lld is not swapped out", static_cast<long long>(ids[i]));
+        need += static_cast<int64_t>(it->second.swap_pages.size());
+    }
+    if (need > p->pages.free_count)
+        return fail(DBK_ECAP, "swap_in: needs %lld pages, %lld free", static_cast<long long>(need),
+                    static_cast<long long>(p->pages.free_count));
+    if (static_cast<size_t>(n) > p->free_slots.size()) return fail(DBK_EINVAL, "swap_in: no free request slot");
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int i = 0; i < n; ++i) {
+        auto it = p->swapped.find(ids[i]);
+        SwappedRequest &sr = it->second;
+        Request r;
+        r.id = ids[i];
+        r.l_in = sr.l_in;
+        r.l_out = sr.l_out;
+        r.ctx = sr.ctx;
+        r.slot = p->free_slots.top();
+        p->free_slots.pop();
+        for (size_t x = 0; x < sr.swap_pages.size(); ++x) {  // lowest-free-first, like an append (R7)
+            const int32_t pg = static_cast<int32_t>(p->pages.take_lowest());
+            r.pages.push_back(pg);
+            p->host_bt[static_cast<size_t>(r.slot) * p->cfg.max_pages_per_req + x] = pg;
+            p->pending.push_back({r.slot, static_cast<int32_t>(x), pg});
+        }
+        DBK_TRY(swap_copy(p, r.pages, sr.swap_pages, false, s));
+        for (int32_t h : sr.swap_pages) p->swap_pages.give_back(h);
+        p->reqs.emplace(r.id, std::move(r));
+        p->swapped.erase(it);
+    }
+    ++p->epoch;
+    DBK_TRY(flush_deltas(p, s));
     return DBK_OK;
 }
 

@@ -28,6 +28,13 @@ struct Request {
     std::vector<int32_t> pages;   // logical page -> physical page
 };
 
+// A request whose KV lives in the host swap space (swap preemption, NEXT row 4): no device
+// pages and no slot; swap_pages[k] holds its logical page k.
+struct SwappedRequest {
+    int32_t l_in = 0, l_out = 0, ctx = 0;
+    std::vector<int32_t> swap_pages;
+};
+
 dbk_status flush_deltas(dbk_pool *p, cudaStream_t s);
 dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_t s);
 // dbk_append_tokens in two halves: bookkeeping + job upload, then per-layer-range KV writes
@@ -45,6 +52,12 @@ struct dbk_pool {
     int64_t elt = 2, tile_bytes = 0, page_stride = 0, layer_stride = 0;
     dbk::PageBitmap pages;
     std::unordered_map<int64_t, dbk::Request> reqs;
+    // host swap space (caller-owned pinned memory, layout [layer][swap page][page_stride bytes])
+    uint8_t *swap_host = nullptr;
+    int64_t swap_cap = 0;
+    dbk::PageBitmap swap_pages;
+    std::unordered_map<int64_t, dbk::SwappedRequest> swapped;
+    int64_t swap_bytes_moved = 0;             // bytes copied by swap_out + swap_in (counter)
     std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> free_slots;
     std::vector<int32_t> host_bt;             // mirror of the device table
     int32_t *d_bt = nullptr;

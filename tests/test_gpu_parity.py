@@ -193,7 +193,7 @@ def test_append_cap_is_all_or_nothing(dbk):
 
 # ------------------------------------------------------------------ engine replay
 def _engine_vs_replay(dbk, cfgname, n_req=None, policy=None, sla_ms=None, tr=None, cap_pages=None,
-                      layers=None, check_attention_every=0, dtype="f16"):
+                      layers=None, check_attention_every=0, dtype="f16", swap_pages=0):
     c = dict(configs.CONFIGS[cfgname])
     if tr is None:
         t = c["trace"]
@@ -213,14 +213,19 @@ def _engine_vs_replay(dbk, cfgname, n_req=None, policy=None, sla_ms=None, tr=Non
     maxp = -(-c["trace"]["L_max"] // P)
     pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, dtype)
     seed = 31
-    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap, seed=seed, out_dtype=2)
+    if swap_pages:  # swap preemption (R29-R31): pinned host swap space of swap_pages pages
+        assert pool.swap_space_attach(torch.empty(swap_pages * L * Hkv * 2 * P * d * 2, dtype=torch.uint8,
+                                                  pin_memory=True)) == swap_pages
+    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap, seed=seed, out_dtype=2,
+                     preempt_mode=1 if swap_pages else 0)
     et = torch.float16 if dtype == "f16" else torch.bfloat16
     qd = torch.empty(L, max_req, Hq, d, dtype=et, device="cuda")
     od = torch.empty(L, max_req, Hq, d, dtype=torch.float32, device="cuda")
     bufs = eng.buffers(qd, od)
     recs = []
     ids = list(range(len(tr)))
-    rp = oeng.Replay([oeng.RankEngine(ids, tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P)],
+    rp = oeng.Replay([oeng.RankEngine(ids, tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P,
+                                      swap_cap_pages=swap_pages)],
                      opol.SchedConfig(prior=tuple(pr.values()), **kw), mem_cap)
     checked = 0
     while not eng.done():
@@ -228,7 +233,7 @@ def _engine_vs_replay(dbk, cfgname, n_req=None, policy=None, sla_ms=None, tr=Non
         recs.append(g)
         o = rp.step(g["step_ns"])
         for k in ("t", "clock_ns", "b_t", "b_next", "n_admitted", "n_preempted", "n_decode", "n_finished",
-                  "sum_ctx", "used_pages", "rationale"):
+                  "sum_ctx", "used_pages", "rationale", "n_swap_out", "n_swap_in"):
             assert g[k] == o[k], (k, g, {kk: o[kk] for kk in g if kk in o})
         assert (g["table_hash"] & ((1 << 64) - 1)) == o["table_hash"]
         assert g["n_waiting"] == o["stats"]["n_waiting"]
@@ -247,6 +252,8 @@ def _engine_vs_replay(dbk, cfgname, n_req=None, policy=None, sla_ms=None, tr=Non
             checked += 1
     assert rp.done()
     assert sum(r["n_finished"] for r in recs) == len(tr)
+    if swap_pages:
+        assert pool.swap_usage()[0] == 0
     pool.close()
     return recs, checked
 
