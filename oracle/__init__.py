@@ -16,6 +16,7 @@ Modules (each function cites the passage it follows):
 * ``chance``     -- O4 Eqs. 7-11: theta, overflow probability, largest feasible b
 * ``policy``     -- O5 Algorithm 1, O6 Algorithm 2, the min-combination
 * ``engine``     -- O7 continuous-batching replay (S1 -> S7) on logged step times
+* ``model``      -- O8 full decode step of a Llama-2-shaped decoder (NEXT row 3), fp64
 
 Parity status per function is in DESIGN.md "Oracle pins".
 """

@@ -77,3 +77,40 @@ def to_bits(values: np.ndarray, dtype: str) -> np.ndarray:
             raise ValueError("value not exact in bf16")
         return (u >> np.uint32(16)).astype(np.uint16)
     raise ValueError(dtype)
+
+
+# ---------------------------------------------------------------- model inputs (NEXT row 3)
+# Synthetic weights and token ids of the full decode step.  A weight matrix W [rows][K] of
+# kind `kind` (codes below) in layer l: element (n, k) = value(seed, kind, 0, n, l, k // 128,
+# k % 128) * 2**scale_log2, i.e. each row is K/128 "heads" of 128 dims (K % 128 == 0).
+# Token id of (req, pos): (splitmix64 key of (seed, KIND_TOKEN, req, pos, 0, 0, 0) >> 16) % vocab.
+KIND_TOKEN = 7
+KIND_EMBED, KIND_LN1, KIND_WQKV, KIND_WO, KIND_LN2, KIND_WGU, KIND_WDOWN, KIND_LNF, KIND_LM = range(8, 17)
+W_CHUNK = 128
+
+
+def gen_matrix(seed, kind, layer, rows, K, scale_log2=0, row0=0) -> np.ndarray:
+    """float64 [len(rows)][K] synthetic weights (exact in fp16 for scale_log2 >= -14)."""
+    if K % W_CHUNK:
+        raise ValueError("K must be a multiple of 128")
+    rows = np.arange(row0, row0 + rows) if np.isscalar(rows) else np.asarray(rows)
+    v = gen_values(seed, kind, 0, rows[:, None], layer, np.arange(K // W_CHUNK)[None, :], W_CHUNK, scale_log2)
+    return v.reshape(len(rows), K)
+
+
+def gen_norm_weight(seed, kind, layer, H) -> np.ndarray:
+    """RMSNorm gain g = 1 + value * 2**-3, in [0.875, 1.125) (exact in fp16)."""
+    return 1.0 + gen_matrix(seed, kind, layer, 1, H, -3)[0]
+
+
+def gen_token(seed, req, pos, vocab) -> np.ndarray:
+    req = np.asarray(req, dtype=np.uint64)
+    pos = np.asarray(pos, dtype=np.uint64)
+    key1 = splitmix64(np.uint64(seed) ^ (np.uint64(KIND_TOKEN) << np.uint64(56)) ^ req)
+    key2 = splitmix64(key1 ^ (pos << np.uint64(32)))
+    return ((key2 >> np.uint64(16)) % np.uint64(vocab)).astype(np.int64)
+
+
+def weight_scale_log2(K) -> int:
+    """-ceil(log2(K) / 2): keeps X W^T at O(1) for O(1) inputs."""
+    return -int(np.ceil(np.log2(K) / 2))
