@@ -132,7 +132,7 @@ def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None)
 
 def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
                  out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1,
-                 trace_override=None, eps_d_ms=None, pd_fusion=False, swap_bytes=0):
+                 trace_override=None, eps_d_ms=None, pd_fusion=False, swap_bytes=0, full_model=False):
     """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
     config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
@@ -164,11 +164,19 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
                      out_dtype=out_dtype, time_attention=time_attention,
                      rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0,
                      pd_fusion=pd_fusion, preempt_mode=1 if swap_bytes else 0)
+    model = None
+    if full_model:  # NEXT row 3: QKV/O/MLP/LM-head GEMMs with synthetic fp16 weights around the attention
+        if "model" not in c:
+            raise SystemExit(f"--model: no model dimensions for config {cfg_name}")
+        m = c["model"]
+        model = dbk.Model(pool, m["hidden"], m["ffn"], m["vocab"], max_pos=c["trace"]["L_max"] + 16,
+                          weight_seed=seed + 1)
+        eng.attach_model(model)
     et = torch.float32 if out_dtype == 2 else torch.float16
     qd = torch.empty(L, max_req, Hq, d, dtype=torch.float16, device=f"cuda:{device}")
     od = torch.empty(L, max_req, Hq, d, dtype=et, device=f"cuda:{device}")
     kvd = torch.empty(2, max_req, L, Hkv, d, dtype=torch.float16, device=f"cuda:{device}")
-    return dict(dbk=dbk, c=c, tr=tr, pool=pool, sched=sched, eng=eng, qd=qd, od=od, kvd=kvd, tp=tp,
+    return dict(dbk=dbk, c=c, tr=tr, pool=pool, sched=sched, eng=eng, qd=qd, od=od, kvd=kvd, tp=tp, model=model,
                 cap_pages=cap_pages, beta=beta, max_req=max_req, mem_cap_total=mem_cap_total, seed=seed,
                 L=L, Hq=Hq, Hkv=Hkv, d=d)
 
@@ -259,7 +267,7 @@ def run_gpu(args):
     # configs[3] (70B GQA) is sharded by KV heads (TP); the others by requests (DP)
     tp = world if args.config == "llama3-70b-gqa" else 1
     S = setup_engine(device=local, rank=rank, world=world, cfg_name=args.config, policy=args.policy,
-                     b_static=args.b_static, sla_ms=args.sla_ms, tp=tp)
+                     b_static=args.b_static, sla_ms=args.sla_ms, tp=tp, full_model=args.model)
     dbk = S["dbk"]
     eng = S["eng"]
     exchange_kind = None
@@ -301,18 +309,20 @@ def run_gpu(args):
     ms_max, toks = float(ms_t.item()), float(tok_t.item())
     # end-to-end through the same API with pinned host buffers (q, new K/V in; out back)
     L, Hq, Hkv, d, mr = S["L"], S["Hq"], S["Hkv"], S["d"], S["max_req"]
-    hq = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
-    hk = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
-    hv = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
-    ho = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True)
-    ebufs = eng.buffers(S["qd"], S["od"], S["kvd"], hq, hk, hv, ho)
-    run_steps(S, 2, ebufs, stream, dist=dist)
-    erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
-    ems_t = torch.tensor([ems], device="cuda")
-    etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / (world if tp > 1 else 1)], device="cuda")
-    if dist is not None:
-        dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(etok_t)
+    erecs, ems_t, etok_t = [], None, None
+    if not args.model:  # full-model mode is device-resident (its inputs are token ids)
+        hq = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
+        hk = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
+        hv = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
+        ho = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True)
+        ebufs = eng.buffers(S["qd"], S["od"], S["kvd"], hq, hk, hv, ho)
+        run_steps(S, 2, ebufs, stream, dist=dist)
+        erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
+        ems_t = torch.tensor([ems], device="cuda")
+        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / (world if tp > 1 else 1)], device="cuda")
+        if dist is not None:
+            dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
+            dist.all_reduce(etok_t)
     # read-only streaming probe over (part of) the KV pool on this GPU: the achievable
     # read bandwidth beside which the attention kernel's is reported
     import ctypes
@@ -336,7 +346,9 @@ def run_gpu(args):
             "steps": n_steps, "warmup": args.warmup, "ms_per_step": round(ms_max / max(n_steps, 1), 4),
             "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None,
             "dtype": "f16",
-            "data": "synthetic (seeded lognormal trace, hash-generated q/K/V; no weights on this path)",
+            "data": ("synthetic (seeded lognormal trace; hash-generated fp16 weights and token ids; prompt KV "
+                     "filled by the generator)") if args.model else
+                    "synthetic (seeded lognormal trace, hash-generated q/K/V; no weights on this path)",
             "config": {"workload": c["name"], "layers": L, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d,
                        "page_size": 16, "kv_dtype": "fp16", "out_dtype": "fp16",
                        "policy": args.policy or c["policy"], "sla_ms": args.sla_ms or c.get("sla_ms"),
@@ -359,10 +371,18 @@ def run_gpu(args):
                          "frac_of_read_probe": round(achieved / probe_gbs, 4)},
             "e2e": {"value": round(float(etok_t.item()) / (float(ems_t.item()) / 1e3), 2), "unit": UNIT,
                     "h2d_bytes_per_step": int(np.mean([r["h2d_bytes"] for r in erecs])) if erecs else 0,
-                    "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in erecs])) if erecs else 0},
+                    "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in erecs])) if erecs else 0}
+            if ems_t is not None else None,
             "gpu_launches": int(sum(r["launches"] for r in recs)),
             "clocks": clk.summary(),
         }
+        if args.model:
+            mc = c["model"]
+            line["config"]["full_model"] = {"hidden": mc["hidden"], "ffn": mc["ffn"], "vocab": mc["vocab"],
+                                            "weights_gb": round(S["model"].weights.numel() / GB, 2),
+                                            "gemms": "cuBLASLt fp16 x fp16 -> fp32 accumulate"}
+            line["config"]["workload"] += " + full decode step (weights)"
+            line["attention_share_of_step"] = line["roofline"]["share_of_step"]
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(S)
         print(json.dumps(line), flush=True)
@@ -439,6 +459,8 @@ def main():
     ap.add_argument("--policy", default=None, choices=[None, "static", "memory", "sla", "combined"])
     ap.add_argument("--b-static", type=int, default=256)
     ap.add_argument("--sla-ms", type=float, default=None)
+    ap.add_argument("--model", action="store_true",
+                    help="full decode step: synthetic-weight QKV/O/MLP/LM-head GEMMs around the attention")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

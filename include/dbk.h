@@ -217,6 +217,71 @@ dbk_status dbk_prefill_step(dbk_pool *pool, const dbk_prefill_batch *batch, cons
                             int32_t out_dtype, void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* Full decode step with synthetic weights           */
+/* ------------------------------------------------------------------------ */
+
+/* A Llama-2-shaped decoder over the pool's heads (readings R32-R35; oracle O8,
+ * oracle/model.py): pre-norm RMSNorm, QKV projection, rotate-half RoPE, paged
+ * decode attention (K1/K2 over the pool), O projection + residual, RMSNorm,
+ * SwiGLU MLP + residual, final RMSNorm and LM head.  The paper does not
+ * define the model; its decode latency is the whole model's ("the enlarged
+ * matrix dimensions in the matrix multiplication operations required for
+ * larger batches").  fp16 pools only. */
+typedef struct dbk_model_config {
+    int32_t hidden;        /* H, multiple of 128                                    */
+    int32_t ffn;           /* F (SwiGLU inner size), multiple of 128                */
+    int32_t vocab;         /* V                                                     */
+    int32_t max_pos;       /* RoPE table rows: positions 0 .. max_pos-1             */
+    double rms_eps;        /* 1e-5 (Llama-2)                                        */
+    double rope_theta;     /* 10000 (Llama-2)                                       */
+    uint64_t weight_seed;  /* synthetic weights (synth/hashgen.py gen_matrix)       */
+    uint64_t token_seed;   /* synthetic input token of (req, pos) (gen_token)       */
+} dbk_model_config;
+
+typedef struct dbk_model dbk_model;
+
+/* Bytes of fp16 weights: V*H (embedding) + L*(2H + (Hq+2Hkv)d*H + H*Hq*d +
+ * 2F*H + H*F) + H + V*H (LM head), each tensor 256-B aligned. */
+size_t dbk_model_weight_bytes(const dbk_pool_config *pool_cfg, const dbk_model_config *cfg);
+
+/* weight_mem: caller-owned device memory of >= dbk_model_weight_bytes bytes,
+ * 256-B aligned; the model fills it with the synthetic weights (device
+ * generator, synchronous).  The model allocates its activation workspace for
+ * the pool's max_requests rows (cudaMalloc) and a cuBLASLt handle.  EINVAL on
+ * bad shapes (kv_dtype must be fp16), ECUDA on CUDA/cuBLAS failures. */
+dbk_status dbk_model_create(dbk_pool *pool, const dbk_model_config *cfg, void *weight_mem, size_t bytes,
+                            dbk_model **out);
+dbk_status dbk_model_destroy(dbk_model *model);
+
+/* Like dbk_append_tokens but without writing KV: allocates the pages of
+ * n_tok[i] more tokens per request (lowest-free-first, all-or-nothing, R7/R8)
+ * and advances ctx; the caller (e.g. dbk_model_step) writes those slots
+ * before any attention reads them. */
+dbk_status dbk_reserve_tokens(dbk_pool *pool, int32_t n_req, const int64_t *req_ids, const int32_t *n_tok,
+                              void *stream);
+
+/* One decode step of the whole model for the batch: request i's decode
+ * token sits at position p_i = ctx_i - 1 (reserved, not yet written), its input
+ * token id is gen_token(token_seed, req_i, p_i).  Writes the token's K/V of
+ * every layer into the pool and, if logits != NULL, logits [n][vocab] fp32
+ * (device).  fuse_stats: layer 0's attention launch also produces the
+ * dbk_stats record (S4).  Async on `stream`. */
+dbk_status dbk_model_step(dbk_model *model, int32_t n, const int64_t *req_ids, int32_t fuse_stats,
+                          void *logits, void *stream);
+
+/* Introspection (tests): device pointers of the activation workspace of the last
+ * step, rows = batch order: [0] x fp32 [n][H] (residual stream), [1] h fp16 [n][H]
+ * (last norm output), [2] qkv fp16 [n][(Hq+2Hkv)d], [3] q fp16 [n][Hq][d] (after RoPE),
+ * [4] attention out fp16 [n][Hq*d], [5] gate|up fp16 [n][2F], [6] act fp16 [n][F]
+ * -- all of the LAST layer; [7] logits fp32 [n][V] (internal buffer). */
+dbk_status dbk_model_buffers(dbk_model *model, void **ptrs_out_8);
+
+/* Time split of the model steps since the last reset (CUDA events on the
+ * step's stream): attention launches vs everything else (GEMMs, norms, RoPE). */
+dbk_status dbk_model_timing(dbk_model *model, double *attn_ms, double *total_ms, int64_t *steps,
+                            int32_t reset);
+
+/* ------------------------------------------------------------------------ */
 /* Synthetic input generator (input side only; none of the method's math)  */
 /* ------------------------------------------------------------------------ */
 
@@ -356,6 +421,11 @@ dbk_status dbk_engine_done(dbk_engine *e, int32_t *done);
 /* The last step's decode batch: n, then req_ids[n], ctx[n] (host, cap entries). */
 dbk_status dbk_engine_last_batch(dbk_engine *e, int32_t *n, int64_t *req_ids, int32_t *ctx,
                                  int32_t cap);
+/* Full-model mode (NEXT row 3): every decode step runs dbk_model_step (QKV / O /
+ * MLP / LM-head GEMMs + the attention) instead of the synthetic-q attention; the
+ * decode token's KV is written by the model (dbk_reserve_tokens + RoPE epilogue).
+ * Device-resident, non-PD engines only; NULL detaches. */
+dbk_status dbk_engine_attach_model(dbk_engine *e, dbk_model *model);
 /* Attention timing accumulated with time_attention = 1: total ms of the
  * attention launches (CUDA events on the launching stream), their count and
  * the algorithmic bytes they moved. */

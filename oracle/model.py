@@ -66,9 +66,10 @@ def embed_rows(seed, s: ModelShape, tokens):
 
 
 def head_weights(seed, s: ModelShape):
-    return dict(g_f=hashgen.gen_norm_weight(seed, hashgen.KIND_LNF, 0, s.hidden),
-                w_lm=hashgen.gen_matrix(seed, hashgen.KIND_LM, 0, s.vocab, s.hidden,
-                                        hashgen.weight_scale_log2(s.hidden)))
+    sl = hashgen.weight_scale_log2(s.hidden)
+    rows = [hashgen.gen_matrix(seed, hashgen.KIND_LM, 0, min(4096, s.vocab - r0), s.hidden, sl, row0=r0)
+            for r0 in range(0, s.vocab, 4096)]
+    return dict(g_f=hashgen.gen_norm_weight(seed, hashgen.KIND_LNF, 0, s.hidden), w_lm=np.concatenate(rows))
 
 
 def rmsnorm(x, g, eps):
@@ -106,10 +107,11 @@ def attention(q, K, V):
 
 
 def decode_step(s: ModelShape, weight_seed, kv_seed, req_ids, ctx, token_seed=None, layer_weights=None,
-                head=None):
+                head=None, kv_written=None):
     """The decode step of every request (module docstring).  Returns (logits [n][V],
     new_k [L][n][Hkv][d], new_v, x_final [n][H]).  layer_weights / head: optional cached
-    results of weights() / head_weights()."""
+    results of weights() / head_weights().  kv_written: {(req, pos, layer): (k [Hkv][d], v)}
+    -- history positions written by earlier model steps (instead of the synthetic fill)."""
     n = len(req_ids)
     d, Hkv = s.head_dim, s.kv_heads
     token_seed = weight_seed if token_seed is None else token_seed
@@ -134,6 +136,9 @@ def decode_step(s: ModelShape, weight_seed, kv_seed, req_ids, ctx, token_seed=No
                                                    np.arange(Hkv)[None, :], d), k[None]], axis=0)
             V = np.concatenate([hashgen.gen_values(kv_seed, hashgen.KIND_V, int(r), hist, lay,
                                                    np.arange(Hkv)[None, :], d), v[None]], axis=0)
+            for (wr, wp, wl), (kk, vv) in (kv_written or {}).items():
+                if wr == int(r) and wl == lay and wp < p:
+                    K[wp], V[wp] = kk, vv
             a[i] = attention(q, K, V).reshape(-1)
         x = x + a @ W["w_o"].T
         h = rmsnorm(x, W["g2"], s.rms_eps)

@@ -18,8 +18,8 @@ import numpy as np
 
 from . import _lib
 from ._lib import (DbkError, dbk_batch, dbk_engine_buffers, dbk_engine_config,  # noqa: F401
-                   dbk_pool_config, dbk_prefill_batch, dbk_sched_config, dbk_sched_state, dbk_stats,
-                   dbk_step_record)
+                   dbk_model_config, dbk_pool_config, dbk_prefill_batch, dbk_sched_config, dbk_sched_state,
+                   dbk_stats, dbk_step_record)
 
 _lib.lib()  # load now: no silent fallback
 
@@ -85,6 +85,11 @@ class KVPool:
     def release(self, req_ids):
         ids, pids = _i64(req_ids)
         _lib.dbk_release(self.h, len(ids), pids)
+
+    def reserve_tokens(self, req_ids, n_tok, stream=None):
+        ids, pids = _i64(req_ids)
+        nt, pnt = _i32(n_tok)
+        _lib.dbk_reserve_tokens(self.h, len(ids), pids, pnt, _stream(stream))
 
     def swap_space_attach(self, host_mem):
         """host_mem: a pinned torch tensor (kept alive by the pool object); returns swap pages."""
@@ -188,6 +193,41 @@ class Scheduler:
         return {f: getattr(s, f) for f, _ in s._fields_}
 
 
+class Model:
+    """dbk_model: full decode step with synthetic fp16 weights over a KVPool (NEXT row 3)."""
+
+    def __init__(self, pool: KVPool, hidden, ffn, vocab, max_pos=4096, rms_eps=1e-5, rope_theta=10000.0,
+                 weight_seed=0, token_seed=None):
+        import torch
+        self.pool = pool
+        self.cfg = dbk_model_config(int(hidden), int(ffn), int(vocab), int(max_pos), float(rms_eps),
+                                    float(rope_theta), int(weight_seed),
+                                    int(weight_seed if token_seed is None else token_seed))
+        nbytes = _lib.dbk_model_weight_bytes(C.byref(pool.cfg), C.byref(self.cfg))
+        if nbytes == 0:
+            raise DbkError(1, "dbk_model_weight_bytes", "invalid model config")
+        self.weights = torch.empty(nbytes, dtype=torch.uint8, device=pool.kv.device)
+        h = C.c_void_p()
+        _lib.dbk_model_create(pool.h, C.byref(self.cfg), self.weights.data_ptr(), nbytes, C.byref(h))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.dbk_model_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def step(self, req_ids, logits=None, fuse_stats=True, stream=None):
+        ids, pids = _i64(req_ids)
+        _lib.dbk_model_step(self.h, len(ids), pids, 1 if fuse_stats else 0, _ptr(logits), _stream(stream))
+
+    def timing(self, reset=False):
+        a, t, n = C.c_double(), C.c_double(), C.c_int64()
+        _lib.dbk_model_timing(self.h, C.byref(a), C.byref(t), C.byref(n), 1 if reset else 0)
+        return a.value, t.value, n.value
+
+
 class Engine:
     """dbk_engine over a KVPool and a Scheduler; trace arrays are copied."""
 
@@ -215,6 +255,10 @@ class Engine:
             self.h = None
 
     __del__ = close
+
+    def attach_model(self, model):
+        self.model = model
+        _lib.dbk_engine_attach_model(self.h, model.h if model is not None else None)
 
     @staticmethod
     def buffers(q_dev, out_dev, kv_dev=None, host_q=None, host_k=None, host_v=None, host_out=None):

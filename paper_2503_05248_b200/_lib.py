@@ -93,6 +93,12 @@ class dbk_engine_buffers(C.Structure):
                 ("host_out", C.c_void_p)]
 
 
+class dbk_model_config(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("ffn", C.c_int32), ("vocab", C.c_int32), ("max_pos", C.c_int32),
+                ("rms_eps", C.c_double), ("rope_theta", C.c_double), ("weight_seed", C.c_uint64),
+                ("token_seed", C.c_uint64)]
+
+
 class dbk_step_record(C.Structure):
     _fields_ = [("t", C.c_int64), ("clock_ns", C.c_int64), ("step_ns", C.c_int64),
                 ("sum_ctx", C.c_int64), ("used_pages", C.c_int64), ("table_hash", C.c_int64),
@@ -120,6 +126,14 @@ SIGNATURES = {
     "dbk_request_begin": [P, I64, I32, I32],
     "dbk_append_tokens": [P, I32, PI64, PI32, P, P, U64, P],
     "dbk_release": [P, I32, PI64],
+    "dbk_reserve_tokens": [P, I32, PI64, PI32, P],
+    "dbk_model_weight_bytes": [C.POINTER(dbk_pool_config), C.POINTER(dbk_model_config)],
+    "dbk_model_create": [P, C.POINTER(dbk_model_config), P, C.c_size_t, C.POINTER(P)],
+    "dbk_model_destroy": [P],
+    "dbk_model_step": [P, I32, PI64, I32, P, P],
+    "dbk_model_timing": [P, C.POINTER(C.c_double), C.POINTER(C.c_double), PI64, I32],
+    "dbk_engine_attach_model": [P, P],
+    "dbk_model_buffers": [P, C.POINTER(C.c_void_p)],
     "dbk_swap_space_attach": [P, P, C.c_size_t, PI64],
     "dbk_swap_out": [P, I32, PI64, P],
     "dbk_swap_in": [P, I32, PI64, P],
@@ -155,7 +169,8 @@ SIGNATURES = {
     "dbk_stats_reduce": [C.POINTER(dbk_stats), I32, I32, C.POINTER(dbk_stats)],
     "dbk_engine_attach_comm": [P, P, I32],
 }
-_RESTYPE = {"dbk_last_error": C.c_char_p, "dbk_version": C.c_char_p, "dbk_kv_pool_bytes": C.c_size_t}
+_RESTYPE = {"dbk_last_error": C.c_char_p, "dbk_version": C.c_char_p, "dbk_kv_pool_bytes": C.c_size_t,
+            "dbk_model_weight_bytes": C.c_size_t}
 
 _lib = None
 

@@ -63,6 +63,7 @@ struct dbk_engine {
     std::vector<int64_t> layer_bytes;
     dbk_comm *comm = nullptr;
     int32_t comm_mode = DBK_MODE_DP;
+    dbk_model *model = nullptr;       // full-model mode (NEXT row 3)
     // end-to-end mode: host<->device copies on their own streams, ordered by events
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_d2h = nullptr;
@@ -187,6 +188,13 @@ dbk_status dbk_engine_done(dbk_engine *e, int32_t *done) {
     return DBK_OK;
 }
 
+dbk_status dbk_engine_attach_model(dbk_engine *e, dbk_model *m) {
+    if (!e) return fail(DBK_EINVAL, "attach_model: null engine");
+    if (m && e->cfg.pd_fusion) return fail(DBK_EINVAL, "attach_model: full-model mode is not combined with PD fusion");
+    e->model = m;
+    return DBK_OK;
+}
+
 dbk_status dbk_engine_attach_comm(dbk_engine *e, dbk_comm *c, int32_t mode) {
     if (!e || (mode != DBK_MODE_DP && mode != DBK_MODE_TP)) return fail(DBK_EINVAL, "attach_comm: bad argument");
     e->comm = c;
@@ -207,6 +215,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         return fail(DBK_EINVAL, "engine_step_launch: end-to-end mode needs host_q, host_k, host_v and kv_dev");
     const bool pd = e->cfg.pd_fusion != 0;
     if (pd && e2e) return fail(DBK_EINVAL, "engine_step_launch: PD fusion runs in device-resident mode only");
+    if (e->model && e2e) return fail(DBK_EINVAL, "engine_step_launch: full-model mode is device-resident");
     DBK_CUDA(cudaSetDevice(pc.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t P = pc.page_size;
@@ -327,6 +336,8 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             }
             e->step_h2d += 2 * static_cast<int64_t>(n * kvrow) + static_cast<int64_t>(pc.layers) * n * qrow;
             DBK_TRY(append_plan(p, n, e->batch_ids.data(), ones.data(), true, s));  // layers appended below
+        } else if (e->model) {  // the model's QKV epilogue writes the decode token's K/V
+            DBK_TRY(dbk_reserve_tokens(p, n, e->batch_ids.data(), ones.data(), s));
         } else {
             DBK_TRY(dbk_append_tokens(p, n, e->batch_ids.data(), ones.data(), nullptr, nullptr, e->cfg.synth_seed, s));
         }
@@ -423,17 +434,18 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     bt.n = n;
     bt.req_ids = e->batch_ids.data();
     if (n > 0) DBK_TRY(prepare_batch(p, n, e->batch_ids.data(), s));
-    if (n > 0 && !e2e) {  // synthetic q of all layers (stands in for the QKV projection), one launch
+    if (n > 0 && !e2e && !e->model) {  // synthetic q of all layers (stands in for the QKV projection), one launch
         DBK_CUDA(launch_synth_q(e->cfg.synth_seed, p->d_req, n, pc.layers, pc.max_requests, pc.q_heads,
                                 pc.head_dim, e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
         ++p->n_launches;
     }
     // device-resident decode-only steps chain the layer launches (programmatic dependent
     // launch: layer l+1's CTAs fill layer l's tail); then the attention time is one window
-    const bool chained = !e2e && n_pf_rows == 0 && n > 0;
-    const bool per_layer_ev = e->cfg.time_attention && n > 0 && !chained;
+    const bool chained = !e2e && n_pf_rows == 0 && n > 0 && !e->model;
+    const bool per_layer_ev = e->cfg.time_attention && n > 0 && !chained && !e->model;
     if (e->cfg.time_attention && chained) DBK_CUDA(cudaEventRecord(e->att0[0], s));
-    for (int l = 0; l < pc.layers; ++l) {
+    if (e->model) DBK_TRY(dbk_model_step(e->model, n, e->batch_ids.data(), 1, nullptr, s));
+    for (int l = 0; l < (e->model ? 0 : pc.layers); ++l) {
         uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
         uint8_t *od = static_cast<uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;
         bt.layer = l;
@@ -493,7 +505,14 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         }
         e->prefilling.erase(e->prefilling.begin(), e->prefilling.begin() + static_cast<std::ptrdiff_t>(m));
     }
-    if (e->cfg.time_attention && n > 0) {
+    if (e->cfg.time_attention && n > 0 && e->model) {  // the model's per-layer attention events
+        double a = 0;
+        DBK_TRY(dbk_model_timing(e->model, &a, nullptr, nullptr, 1));
+        e->att_ms += a;
+        e->att_bytes += static_cast<int64_t>(pc.layers) * p->last_decode_bytes;
+        e->att_launches += pc.layers;
+    }
+    if (e->cfg.time_attention && n > 0 && !e->model) {
         for (int l = 0; l < pc.layers; ++l) {
             float a = 0.f;
             if (per_layer_ev) DBK_CUDA(cudaEventElapsedTime(&a, e->att0[l], e->att1[l]));

@@ -1,0 +1,483 @@
+// Full decode step with synthetic weights (R32-R35):
+// a Llama-2-shaped decoder whose attention is the pool's paged decode attention (K1/K2).
+//   - plain GEMMs (QKV, O, gate|up, down, LM head): cuBLASLt, fp16 operands, fp32
+//     accumulation; the O and down projections accumulate into the fp32 residual stream
+//     in place (beta = 1, C = D);
+//   - our kernels: synthetic weight fill, embedding + RMSNorm, RMSNorm, RoPE + KV write
+//     straight into the decode token's page slot (the QKV GEMM's epilogue), SiLU * up.
+#include <cublasLt.h>
+#include <cuda_fp16.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <new>
+#include <tuple>
+#include <vector>
+
+#include "common.h"
+#include "device_common.cuh"
+#include "kernels.cuh"
+#include "pool.h"
+
+using namespace dbk;
+
+namespace {
+using namespace dbk::dev;
+
+constexpr int kWChunk = 128;  // synthetic weight rows are K/128 "heads" of 128 dims (hashgen)
+constexpr int kKindToken = 7, kKindEmbed = 8, kKindLn1 = 9, kKindWqkv = 10, kKindWo = 11, kKindLn2 = 12,
+              kKindWgu = 13, kKindWdown = 14, kKindLnf = 15, kKindLm = 16;
+
+// ------------------------------------------------------------------ kernels
+// W[row][k] = (byte - 128) * scale (+1 for norm gains), byte of (seed, kind, 0, row, layer, k / 128,
+// k % 128): the host passes scale = 2^(scale_log2 - 7), i.e. value * 2^scale_log2 of synth/hashgen.py
+__global__ void fill_weights_kernel(__half *w, int64_t rows, int K, int layer, int kind, uint64_t seed, float scale,
+                                    int norm) {
+    const int64_t per_row = K / 8;
+    const int64_t total = rows * per_row;
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < total;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t row = c / per_row;
+        const int k = static_cast<int>(c % per_row) * 8;
+        float f[8];
+        synth_vals(synth_key(seed, kind, 0, static_cast<int>(row), layer, k / kWChunk, (k % kWChunk) / 8), scale, f);
+        if (norm)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] += 1.0f;
+        *reinterpret_cast<uint4 *>(w + row * K + k) = pack8<__half>(f);
+    }
+}
+
+__device__ __forceinline__ float block_sum(float v, float *red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float t = 0.f;
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+// h[i] = RMSNorm(x[i]) * g (fp16); with embed != nullptr, x[i] = E[token(req_i, ctx_i - 1)] first.
+// One CTA per row; H % 8 == 0 and H / 8 <= 4 * blockDim.x.
+__global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, float eps, int H, __half *h,
+                                                   const ReqMeta *req, const __half *embed, uint64_t tok_seed,
+                                                   int vocab) {
+    __shared__ float red[8];
+    const int i = blockIdx.x;
+    float *xr = x + static_cast<size_t>(i) * H;
+    const int nv = H / 8;
+    float v[4][8];
+    float ss = 0.f;
+    const __half *er = nullptr;
+    if (embed) {
+        const ReqMeta rm = req[i];
+        const uint64_t key = synth_key(tok_seed, kKindToken, rm.req_id, rm.ctx - 1, 0, 0, 0);
+        er = embed + static_cast<size_t>((key >> 16) % static_cast<uint64_t>(vocab)) * H;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int j = threadIdx.x + c * blockDim.x;
+        if (j < nv) {
+            if (er) {
+                unpack8<__half>(*reinterpret_cast<const uint4 *>(er + j * 8), v[c]);
+                *reinterpret_cast<float4 *>(xr + j * 8) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+                *reinterpret_cast<float4 *>(xr + j * 8 + 4) = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
+            } else {
+                const float4 a = *reinterpret_cast<const float4 *>(xr + j * 8);
+                const float4 b = *reinterpret_cast<const float4 *>(xr + j * 8 + 4);
+                v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
+                v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) ss += v[c][e] * v[c][e];
+        }
+    }
+    const float r = rsqrtf(block_sum(ss, red) / static_cast<float>(H) + eps);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int j = threadIdx.x + c * blockDim.x;
+        if (j < nv) {
+            float gg[8], o[8];
+            unpack8<__half>(*reinterpret_cast<const uint4 *>(g + j * 8), gg);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = v[c][e] * r * gg[e];
+            *reinterpret_cast<uint4 *>(h + static_cast<size_t>(i) * H + j * 8) = pack8<__half>(o);
+        }
+    }
+}
+
+// RoPE (rotate-half pairs (j, j + d/2), angle table cs[pos][j] = (cos, sin)) on the q and k
+// heads of the QKV GEMM output; q -> q_out [n][Hq][d], k and v -> the decode token's slot
+// (position ctx - 1) of this layer's page tile.  One CTA per token.
+__global__ void __launch_bounds__(256) rope_kv_kernel(const __half *qkv, const ReqMeta *req, const int32_t *bt,
+                                                      int bt_stride, uint8_t *kv_layer, int64_t page_stride,
+                                                      int64_t tile_bytes, const float2 *cs, int Hq, int Hkv, int d,
+                                                      __half *q_out) {
+    const int i = blockIdx.x;
+    const ReqMeta rm = req[i];
+    const int p = rm.ctx - 1;
+    const int32_t page = bt[static_cast<size_t>(rm.slot) * bt_stride + p / kP];
+    const int half_d = d / 2;
+    const int nqkv = (Hq + 2 * Hkv) * d;
+    const __half *row = qkv + static_cast<size_t>(i) * nqkv;
+    const float2 *csr = cs + static_cast<size_t>(p) * half_d;
+    uint8_t *pg = kv_layer + static_cast<int64_t>(page) * page_stride;
+    // rotated heads: Hq q heads then Hkv k heads, two pairs per thread-iteration
+    const int rot_items = (Hq + Hkv) * half_d / 2;
+    for (int t = threadIdx.x; t < rot_items; t += blockDim.x) {
+        const int hh = (2 * t) / half_d, j = (2 * t) % half_d;
+        const __half *src = row + hh * d;
+        const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(src + j));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(src + j + half_d));
+        const float2 c0 = csr[j], c1 = csr[j + 1];
+        const __half2 lo = __floats2half2_rn(a.x * c0.x - b.x * c0.y, a.y * c1.x - b.y * c1.y);
+        const __half2 hi = __floats2half2_rn(b.x * c0.x + a.x * c0.y, b.y * c1.x + a.y * c1.y);
+        __half *dst;
+        if (hh < Hq) {
+            dst = q_out + (static_cast<size_t>(i) * Hq + hh) * d;
+        } else {
+            dst = reinterpret_cast<__half *>(pg + (hh - Hq) * tile_bytes) + (p % kP) * d;  // K row
+        }
+        *reinterpret_cast<__half2 *>(dst + j) = lo;
+        *reinterpret_cast<__half2 *>(dst + j + half_d) = hi;
+    }
+    // v heads: plain copy into the V rows, 16 B per thread
+    const int vv = Hkv * d / 8;
+    for (int t = threadIdx.x; t < vv; t += blockDim.x) {
+        const int g = (t * 8) / d, e = (t * 8) % d;
+        const uint4 val = *reinterpret_cast<const uint4 *>(row + (Hq + Hkv + g) * d + e);
+        __half *dst = reinterpret_cast<__half *>(pg + g * tile_bytes) + (kP + p % kP) * d + e;
+        *reinterpret_cast<uint4 *>(dst) = val;
+    }
+}
+
+// act[i][j] = silu(gu[i][j]) * gu[i][F + j]
+__global__ void silu_mul_kernel(const __half *gu, int n, int F, __half *act) {
+    const int64_t per_row = F / 8;
+    const int64_t total = static_cast<int64_t>(n) * per_row;
+    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < total;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = c / per_row;
+        const int j = static_cast<int>(c % per_row) * 8;
+        float g[8], u[8], o[8];
+        unpack8<__half>(*reinterpret_cast<const uint4 *>(gu + i * 2 * F + j), g);
+        unpack8<__half>(*reinterpret_cast<const uint4 *>(gu + i * 2 * F + F + j), u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = g[e] / (1.0f + __expf(-g[e])) * u[e];
+        *reinterpret_cast<uint4 *>(act + i * F + j) = pack8<__half>(o);
+    }
+}
+
+int grid_of(int64_t work, int block, int sms) {
+    int64_t b = (work + block - 1) / block;
+    const int64_t cap = static_cast<int64_t>(sms) * 8;
+    return static_cast<int>(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+struct LayerW {
+    __half *ln1, *wqkv, *wo, *ln2, *wgu, *wdown;
+};
+
+struct GemmPlan {
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+    cublasLtMatmulAlgo_t algo{};
+    bool has_algo = false;
+};
+
+}  // namespace
+
+struct dbk_model {
+    dbk_pool *pool = nullptr;
+    int device = 0;
+    dbk_model_config cfg{};
+    int L = 0, Hq = 0, Hkv = 0, d = 0, H = 0, F = 0, V = 0, nqkv = 0, rows = 0;
+    __half *embed = nullptr, *lnf = nullptr, *lm = nullptr;
+    std::vector<LayerW> lw;
+    float2 *cs = nullptr;
+    float *x = nullptr, *logits = nullptr;
+    __half *h = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *gu = nullptr, *act = nullptr;
+    cublasLtHandle_t lt = nullptr;
+    void *lt_ws = nullptr;
+    size_t lt_ws_bytes = 32u << 20;
+    std::map<std::tuple<int, int, int, int>, GemmPlan> plans;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> a0, a1;
+    bool pending = false;
+    double attn_ms = 0, total_ms = 0;
+    int64_t steps = 0;
+    ~dbk_model() {
+        for (auto &kv : plans) {
+            if (kv.second.op) cublasLtMatmulDescDestroy(kv.second.op);
+            if (kv.second.a) cublasLtMatrixLayoutDestroy(kv.second.a);
+            if (kv.second.b) cublasLtMatrixLayoutDestroy(kv.second.b);
+            if (kv.second.c) cublasLtMatrixLayoutDestroy(kv.second.c);
+        }
+        if (lt) cublasLtDestroy(lt);
+        for (void *ptr : {static_cast<void *>(cs), static_cast<void *>(x), static_cast<void *>(logits),
+                          static_cast<void *>(h), static_cast<void *>(qkv), static_cast<void *>(q),
+                          static_cast<void *>(attn), static_cast<void *>(gu), static_cast<void *>(act), lt_ws})
+            if (ptr) cudaFree(ptr);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        for (auto e : a0) cudaEventDestroy(e);
+        for (auto e : a1) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+#define DBK_LT(call)                                                                                 \
+    do {                                                                                             \
+        cublasStatus_t st_ = (call);                                                                 \
+        if (st_ != CUBLAS_STATUS_SUCCESS) return fail(DBK_ECUDA, "%s: cublas status %d", #call, st_); \
+    } while (0)
+
+// Y[M][N] (+)= X[M][K] W[N][K]^T, row-major: in cuBLASLt's column-major terms
+// Y^T (N x M, ld N) = op_T(W as K x N, ld K) * (X as K x M, ld K).
+dbk_status gemm(dbk_model *m, int M, int N, int K, const __half *X, const __half *W, void *Y, bool y_f32,
+                bool accumulate, cudaStream_t s) {
+    if (M == 0) return DBK_OK;
+    auto key = std::make_tuple(M, N, K, (y_f32 ? 1 : 0) | (accumulate ? 2 : 0));
+    GemmPlan &g = m->plans[key];
+    if (!g.op) {
+        DBK_LT(cublasLtMatmulDescCreate(&g.op, CUBLAS_COMPUTE_32F, CUDA_R_32F));
+        const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
+        DBK_LT(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof tA));
+        DBK_LT(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof tB));
+        DBK_LT(cublasLtMatrixLayoutCreate(&g.a, CUDA_R_16F, K, N, K));
+        DBK_LT(cublasLtMatrixLayoutCreate(&g.b, CUDA_R_16F, K, M, K));
+        DBK_LT(cublasLtMatrixLayoutCreate(&g.c, y_f32 ? CUDA_R_32F : CUDA_R_16F, N, M, N));
+        cublasLtMatmulPreference_t pref;
+        DBK_LT(cublasLtMatmulPreferenceCreate(&pref));
+        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &m->lt_ws_bytes,
+                                             sizeof m->lt_ws_bytes);
+        cublasLtMatmulHeuristicResult_t res{};
+        int found = 0;
+        const cublasStatus_t st =
+            cublasLtMatmulAlgoGetHeuristic(m->lt, g.op, g.a, g.b, g.c, g.c, pref, 1, &res, &found);
+        cublasLtMatmulPreferenceDestroy(pref);
+        if (st != CUBLAS_STATUS_SUCCESS || found < 1)
+            return fail(DBK_ECUDA, "cuBLASLt: no algorithm for %d x %d x %d", M, N, K);
+        g.algo = res.algo;
+        g.has_algo = true;
+    }
+    const float alpha = 1.0f, beta = accumulate ? 1.0f : 0.0f;
+    DBK_LT(cublasLtMatmul(m->lt, g.op, &alpha, W, g.a, X, g.b, &beta, Y, g.c, Y, g.c, &g.algo, m->lt_ws,
+                          m->lt_ws_bytes, s));
+    return DBK_OK;
+}
+
+dbk_status collect_timing(dbk_model *m) {
+    if (!m->pending) return DBK_OK;
+    DBK_CUDA(cudaEventSynchronize(m->ev1));
+    float t = 0.f;
+    DBK_CUDA(cudaEventElapsedTime(&t, m->ev0, m->ev1));
+    m->total_ms += t;
+    for (int l = 0; l < m->L; ++l) {
+        DBK_CUDA(cudaEventElapsedTime(&t, m->a0[l], m->a1[l]));
+        m->attn_ms += t;
+    }
+    ++m->steps;
+    m->pending = false;
+    return DBK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dbk_model_weight_bytes(const dbk_pool_config *pc, const dbk_model_config *c) {
+    if (!pc || !c || c->hidden <= 0 || c->ffn <= 0 || c->vocab <= 0) return 0;
+    const size_t H = c->hidden, F = c->ffn, V = c->vocab, d = pc->head_dim;
+    const size_t nqkv = (static_cast<size_t>(pc->q_heads) + 2 * pc->kv_heads) * d;
+    size_t per_layer = align256(H * 2) * 2 + align256(nqkv * H * 2) + align256(H * pc->q_heads * d * 2) +
+                       align256(2 * F * H * 2) + align256(H * F * 2);
+    return align256(V * H * 2) + pc->layers * per_layer + align256(H * 2) + align256(V * H * 2);
+}
+
+dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, size_t bytes, dbk_model **out) {
+    if (!p || !c || !out) return fail(DBK_EINVAL, "model_create: null argument");
+    const dbk_pool_config &pc = p->cfg;
+    if (pc.kv_dtype != 0) return fail(DBK_EINVAL, "model_create: the model path is fp16 (kv_dtype 0)");
+    if (c->hidden % kWChunk || c->ffn % kWChunk || c->hidden > 8 * 4 * 256 || c->vocab < 1 || c->max_pos < 1 ||
+        (pc.q_heads * pc.head_dim) % kWChunk || c->rms_eps <= 0 || c->rope_theta <= 0)
+        return fail(DBK_EINVAL, "model_create: hidden, ffn, q_heads*head_dim multiples of 128, hidden <= 8192");
+    const size_t need = dbk_model_weight_bytes(&pc, c);
+    if (!wmem || bytes < need || (reinterpret_cast<uintptr_t>(wmem) & 255))
+        return fail(DBK_EINVAL, "model_create: weight_mem must be 256-B aligned and >= %zu bytes", need);
+    DBK_CUDA(cudaSetDevice(pc.device));
+    dbk_model *m = new (std::nothrow) dbk_model();
+    if (!m) return fail(DBK_EINVAL, "out of host memory");
+    m->pool = p;
+    m->device = pc.device;
+    m->cfg = *c;
+    m->L = pc.layers;
+    m->Hq = pc.q_heads;
+    m->Hkv = pc.kv_heads;
+    m->d = pc.head_dim;
+    m->H = c->hidden;
+    m->F = c->ffn;
+    m->V = c->vocab;
+    m->nqkv = (m->Hq + 2 * m->Hkv) * m->d;
+    m->rows = pc.max_requests;
+    auto bail = [&](dbk_status st) {
+        delete m;
+        return st;
+    };
+    // weights: carve the caller's memory, fill with the generator
+    uint8_t *w = static_cast<uint8_t *>(wmem);
+    auto take = [&](size_t elems) {
+        __half *r = reinterpret_cast<__half *>(w);
+        w += align256(elems * 2);
+        return r;
+    };
+    const int sms = p->num_sms;
+    auto fill = [&](__half *dst, int64_t rows_, int K, int layer, int kind, int scale_log2, int norm) {
+        fill_weights_kernel<<<grid_of(rows_ * K / 8, 256, sms), 256>>>(dst, rows_, K, layer, kind, c->weight_seed,
+                                                                       std::ldexp(1.0f, scale_log2 - 7), norm);
+    };
+    auto sl2 = [](int K) { return -static_cast<int>(std::ceil(std::log2(static_cast<double>(K)) / 2)); };
+    const int H = m->H, F = m->F, V = m->V, qd = m->Hq * m->d;
+    m->embed = take(static_cast<size_t>(V) * H);
+    fill(m->embed, V, H, 0, kKindEmbed, 0, 0);
+    m->lw.resize(m->L);
+    for (int l = 0; l < m->L; ++l) {
+        LayerW &x = m->lw[l];
+        x.ln1 = take(H);
+        x.wqkv = take(static_cast<size_t>(m->nqkv) * H);
+        x.wo = take(static_cast<size_t>(H) * qd);
+        x.ln2 = take(H);
+        x.wgu = take(static_cast<size_t>(2) * F * H);
+        x.wdown = take(static_cast<size_t>(H) * F);
+        fill(x.ln1, 1, H, l, kKindLn1, -3, 1);
+        fill(x.wqkv, m->nqkv, H, l, kKindWqkv, sl2(H), 0);
+        fill(x.wo, H, qd, l, kKindWo, sl2(qd), 0);
+        fill(x.ln2, 1, H, l, kKindLn2, -3, 1);
+        fill(x.wgu, 2 * F, H, l, kKindWgu, sl2(H), 0);
+        fill(x.wdown, H, F, l, kKindWdown, sl2(F), 0);
+    }
+    m->lnf = take(H);
+    m->lm = take(static_cast<size_t>(V) * H);
+    fill(m->lnf, 1, H, 0, kKindLnf, -3, 1);
+    fill(m->lm, V, H, 0, kKindLm, sl2(H), 0);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+        return bail(fail(DBK_ECUDA, "model_create: weight fill failed"));
+    // RoPE table: angles in double, rounded once to fp32
+    {
+        const int hd = m->d / 2;
+        std::vector<float2> t(static_cast<size_t>(c->max_pos) * hd);
+        for (int pos = 0; pos < c->max_pos; ++pos)
+            for (int j = 0; j < hd; ++j) {
+                const double a = pos * std::pow(c->rope_theta, -2.0 * j / m->d);
+                t[static_cast<size_t>(pos) * hd + j] = make_float2(static_cast<float>(std::cos(a)),
+                                                                   static_cast<float>(std::sin(a)));
+            }
+        if (cudaMalloc(&m->cs, t.size() * sizeof(float2)) != cudaSuccess ||
+            cudaMemcpy(m->cs, t.data(), t.size() * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(fail(DBK_ECUDA, "model_create: RoPE table"));
+    }
+    const size_t R = m->rows;
+    if (cudaMalloc(&m->x, R * H * 4) != cudaSuccess || cudaMalloc(&m->logits, R * V * 4) != cudaSuccess ||
+        cudaMalloc(&m->h, R * H * 2) != cudaSuccess || cudaMalloc(&m->qkv, R * m->nqkv * 2) != cudaSuccess ||
+        cudaMalloc(&m->q, R * qd * 2) != cudaSuccess || cudaMalloc(&m->attn, R * qd * 2) != cudaSuccess ||
+        cudaMalloc(&m->gu, R * 2 * F * 2) != cudaSuccess || cudaMalloc(&m->act, R * F * 2) != cudaSuccess ||
+        cudaMalloc(&m->lt_ws, m->lt_ws_bytes) != cudaSuccess)
+        return bail(fail(DBK_ECUDA, "model_create: activation workspace"));
+    if (cublasLtCreate(&m->lt) != CUBLAS_STATUS_SUCCESS) return bail(fail(DBK_ECUDA, "model_create: cublasLtCreate"));
+    m->a0.assign(m->L, nullptr);
+    m->a1.assign(m->L, nullptr);
+    if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess)
+        return bail(fail(DBK_ECUDA, "model_create: events"));
+    for (int l = 0; l < m->L; ++l)
+        if (cudaEventCreate(&m->a0[l]) != cudaSuccess || cudaEventCreate(&m->a1[l]) != cudaSuccess)
+            return bail(fail(DBK_ECUDA, "model_create: events"));
+    *out = m;
+    return DBK_OK;
+}
+
+dbk_status dbk_model_destroy(dbk_model *m) {
+    if (!m) return DBK_OK;
+    cudaSetDevice(m->device);  // the pool may already be gone
+    cudaDeviceSynchronize();
+    delete m;
+    return DBK_OK;
+}
+
+dbk_status dbk_model_step(dbk_model *m, int32_t n, const int64_t *ids, int32_t fuse_stats, void *logits,
+                          void *stream) {
+    if (!m) return fail(DBK_EINVAL, "model_step: null model");
+    if (n < 0 || n > m->rows || (n > 0 && !ids)) return fail(DBK_EINVAL, "model_step: bad batch (n <= max_requests)");
+    if (n == 0) return DBK_OK;
+    dbk_pool *p = m->pool;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    DBK_TRY(collect_timing(m));
+    DBK_TRY(prepare_batch(p, n, ids, s));  // ReqMeta (ctx incl. the reserved decode token) + block table
+    for (int32_t i = 0; i < n; ++i)
+        if (p->reqs.at(ids[i]).ctx > m->cfg.max_pos) return fail(DBK_EINVAL, "model_step: position beyond max_pos");
+    const int H = m->H, F = m->F, qd = m->Hq * m->d;
+    const float eps = static_cast<float>(m->cfg.rms_eps);
+    DBK_CUDA(cudaEventRecord(m->ev0, s));
+    norm_kernel<<<n, 256, 0, s>>>(m->x, m->lw[0].ln1, eps, H, m->h, p->d_req, m->embed, m->cfg.token_seed, m->V);
+    DBK_CUDA(cudaGetLastError());
+    dbk_batch bt{};
+    bt.n = n;
+    bt.req_ids = ids;
+    for (int l = 0; l < m->L; ++l) {
+        const LayerW &w = m->lw[l];
+        DBK_TRY(gemm(m, n, m->nqkv, H, m->h, w.wqkv, m->qkv, false, false, s));
+        rope_kv_kernel<<<n, 256, 0, s>>>(m->qkv, p->d_req, p->d_bt, p->cfg.max_pages_per_req,
+                                         p->kv + static_cast<size_t>(l) * p->layer_stride, p->page_stride,
+                                         p->tile_bytes, m->cs, m->Hq, m->Hkv, m->d, m->q);
+        DBK_CUDA(cudaGetLastError());
+        bt.layer = l;
+        bt.fuse_stats = (fuse_stats && l == 0) ? 1 : 0;
+        DBK_CUDA(cudaEventRecord(m->a0[l], s));
+        DBK_TRY(dbk_decode_step(p, &bt, m->q, m->attn, 0, s));
+        DBK_CUDA(cudaEventRecord(m->a1[l], s));
+        DBK_TRY(gemm(m, n, H, qd, m->attn, w.wo, m->x, true, true, s));       // x += attn W_o^T
+        norm_kernel<<<n, 256, 0, s>>>(m->x, w.ln2, eps, H, m->h, nullptr, nullptr, 0, 0);
+        DBK_TRY(gemm(m, n, 2 * F, H, m->h, w.wgu, m->gu, false, false, s));
+        silu_mul_kernel<<<grid_of(static_cast<int64_t>(n) * F / 8, 256, p->num_sms), 256, 0, s>>>(m->gu, n, F,
+                                                                                                 m->act);
+        DBK_TRY(gemm(m, n, H, F, m->act, w.wdown, m->x, true, true, s));      // x += act W_down^T
+        const __half *g_next = l + 1 < m->L ? m->lw[l + 1].ln1 : m->lnf;
+        norm_kernel<<<n, 256, 0, s>>>(m->x, g_next, eps, H, m->h, nullptr, nullptr, 0, 0);
+        DBK_CUDA(cudaGetLastError());
+        p->n_launches += 4;  // ours: RoPE/KV, 2 norms, SiLU (attention counts itself; GEMMs are cuBLASLt's)
+    }
+    DBK_TRY(gemm(m, n, m->V, H, m->h, m->lm, logits ? logits : m->logits, true, false, s));
+    DBK_CUDA(cudaEventRecord(m->ev1, s));
+    m->pending = true;
+    p->n_launches += 1;  // the embedding + first norm
+    return DBK_OK;
+}
+
+dbk_status dbk_model_buffers(dbk_model *m, void **p) {
+    if (!m || !p) return fail(DBK_EINVAL, "model_buffers: null argument");
+    void *b[8] = {m->x, m->h, m->qkv, m->q, m->attn, m->gu, m->act, m->logits};
+    for (int k = 0; k < 8; ++k) p[k] = b[k];
+    return DBK_OK;
+}
+
+dbk_status dbk_model_timing(dbk_model *m, double *attn_ms, double *total_ms, int64_t *steps, int32_t reset) {
+    if (!m) return fail(DBK_EINVAL, "model_timing: null model");
+    DBK_TRY(collect_timing(m));
+    if (attn_ms) *attn_ms = m->attn_ms;
+    if (total_ms) *total_ms = m->total_ms;
+    if (steps) *steps = m->steps;
+    if (reset) {
+        m->attn_ms = m->total_ms = 0;
+        m->steps = 0;
+    }
+    return DBK_OK;
+}
+
+}  // extern "C"

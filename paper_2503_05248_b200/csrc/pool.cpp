@@ -303,7 +303,7 @@ dbk_status flush_deltas(dbk_pool *p, cudaStream_t s) {
 // Validates and performs the bookkeeping of an append (pages lowest-free-first, all-or-nothing,
 // R7/R8), flushes the block-table deltas and uploads the job list; no KV is written yet.
 dbk_status append_plan(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok, bool explicit_rows,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool upload_jobs) {
     if (!p) return fail(DBK_EINVAL, "null pool");
     if (n < 0 || (n > 0 && (!ids || !n_tok))) return fail(DBK_EINVAL, "append_tokens: bad arrays");
     const int64_t P = p->cfg.page_size;
@@ -360,6 +360,10 @@ dbk_status append_plan(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t
     }
     ++p->epoch;
     DBK_TRY(flush_deltas(p, s));
+    if (!upload_jobs) {
+        p->jobs.clear();  // reserve only: nothing for append_launch to write
+        return DBK_OK;
+    }
     if (!p->jobs.empty())
         DBK_TRY(p->up_append.upload(p->jobs.data(), p->jobs.size() * sizeof(AppendJob), s));
     return DBK_OK;
@@ -400,6 +404,11 @@ dbk_status dbk_append_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const i
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     DBK_TRY(dbk::append_plan(p, n, ids, n_tok, k != nullptr, s));
     return dbk::append_launch(p, k, v, seed, 0, p->cfg.layers, s);
+}
+
+dbk_status dbk_reserve_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok, void *stream) {
+    if (!p) return fail(DBK_EINVAL, "null pool");
+    return dbk::append_plan(p, n, ids, n_tok, false, static_cast<cudaStream_t>(stream), false);
 }
 
 dbk_status dbk_release(dbk_pool *p, int32_t n, const int64_t *ids) {

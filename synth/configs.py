@@ -29,6 +29,7 @@ CONFIGS = {
         trace=dict(dist="lognormal", mean_in=191.0, mean_out=381.9, L_max=4096, seed=2),
         policy="memory", eps_m=0.02, b_min=1, b_max=512,
         weights_bytes=13_500_000_000, reserve_bytes=10 * GB,
+        model=dict(hidden=4096, ffn=11008, vocab=32000),  # full-model mode (NEXT row 3)
         prior=dict(n=256, mean_in=191.0, mean_out=381.9),
     ),
     # configs[2]
@@ -38,6 +39,7 @@ CONFIGS = {
         trace=dict(dist="lognormal", mean_in=237.7, mean_out=416.2, L_max=4096, seed=3),
         policy="combined", eps_m=0.02, b_min=1, b_max=512, sla_ms=50.0, eps_d_ms=2.0,
         alpha=8, delta=2, weights_bytes=26_000_000_000, reserve_bytes=10 * GB,
+        model=dict(hidden=5120, ffn=13824, vocab=32000),
         prior=dict(n=256, mean_in=237.7, mean_out=416.2),
     ),
     # configs[3] (per GPU: kv_heads / G)

@@ -1,0 +1,161 @@
+"""GPU parity of the full decode step (NEXT row 3; dbk_model_*, R32-R35) against the
+fp64 oracle O8 (oracle/model.py).
+
+Bar (R35): fp16 weights and fp16 activations at every GEMM boundary with fp32 accumulation
+and an fp32 residual stream vs the fp64 oracle on the same (exactly representable) weights:
+per row relative L2 error <= MODEL_TOL for the logits, and for the K/V rows the model
+writes into the pool.  Block tables / ctx after dbk_reserve_tokens are bit-exact."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import model as om  # noqa: E402
+from oracle import policy as opol  # noqa: E402
+from oracle import engine as oeng  # noqa: E402
+from oracle.allocator import PagedKV  # noqa: E402
+from synth import configs, trace  # noqa: E402
+from test_gpu_parity import dbk  # noqa: E402,F401
+
+MODEL_TOL = 1e-2
+P = 16
+
+
+def rel_l2(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    return (np.linalg.norm(got - want, axis=-1) / np.maximum(np.linalg.norm(want, axis=-1), 1e-30)).max()
+
+
+def _read_kv(pool, s, req, pos, layer):
+    """The K and V rows [Hkv][d] of (req, pos, layer) straight from the pool's memory."""
+    _, _, pages = pool.request_info(req)
+    cap = pool.cfg.cap_pages
+    t = pool.kv.view(torch.float16).view(s.layers, cap, s.kv_heads, 2, P, s.head_dim)
+    tile = t[layer, pages[pos // P], :, :, pos % P, :].float().cpu().numpy()
+    return tile[:, 0, :], tile[:, 1, :]
+
+
+def _setup(dbk, s, ctx, kv_seed, wseed, cap=None):
+    n = len(ctx)
+    maxp = max(-(-(c + 4) // P) for c in ctx) + 1
+    cap = cap or sum(-(-(c + 1) // P) for c in ctx) + 4
+    pool = dbk.KVPool(s.layers, s.q_heads, s.kv_heads, s.head_dim, cap, n + 2, maxp, "f16")
+    model = dbk.Model(pool, s.hidden, s.ffn, s.vocab, max_pos=maxp * P, weight_seed=wseed)
+    ids = [int(i) * 131 + 7 for i in range(n)]
+    ref = PagedKV(cap, P)
+    for r, c in zip(ids, ctx):
+        pool.request_begin(r, max(1, c - 1), 4)
+        ref.begin(r)
+    pool.append_tokens(ids, [c - 1 for c in ctx], seed=kv_seed)   # the synthetic history
+    ref.append(ids, [c - 1 for c in ctx])
+    return pool, model, ids, ref
+
+
+@pytest.mark.parametrize("shape", [
+    om.ModelShape(layers=2, q_heads=4, kv_heads=4, head_dim=64, hidden=256, ffn=384, vocab=300),
+    om.ModelShape(layers=3, q_heads=8, kv_heads=2, head_dim=128, hidden=512, ffn=640, vocab=1000),
+    om.ModelShape(layers=1, q_heads=16, kv_heads=2, head_dim=128, hidden=2048, ffn=1408, vocab=512),
+])
+def test_model_step_parity(dbk, shape):
+    s = shape
+    kv_seed, wseed = 5, 11
+    ctx = [1, 2, 16, 17, 33, 100, 257]
+    pool, model, ids, ref = _setup(dbk, s, ctx, kv_seed, wseed)
+    pool.reserve_tokens(ids, [1] * len(ids))
+    ref.append(ids, [1] * len(ids))
+    for r in ids:
+        c, _, pages = pool.request_info(r)
+        assert c == ref.ctx[r] and pages == ref.pages[r]
+    logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
+    model.step(ids, logits)
+    st = pool.batch_stats()
+    assert st["n_active"] == len(ids) and st["sum_ctx"] == sum(ctx) and st["table_mismatch"] == 0
+    want, nk, nv, _ = om.decode_step(s, wseed, kv_seed, ids, ctx)
+    assert rel_l2(logits.cpu().numpy(), want) <= MODEL_TOL
+    for lay in range(s.layers):
+        for i, (r, c) in enumerate(zip(ids, ctx)):
+            k, v = _read_kv(pool, s, r, c - 1, lay)
+            assert rel_l2(k, nk[lay, i]) <= MODEL_TOL and rel_l2(v, nv[lay, i]) <= MODEL_TOL
+    model.close()
+    pool.close()
+
+
+def test_model_two_steps_attend_to_model_written_kv(dbk):
+    """Step 2 attends over the K/V step 1 wrote (oracle: kv_written from its own step 1)."""
+    s = om.ModelShape(layers=2, q_heads=8, kv_heads=4, head_dim=64, hidden=512, ffn=512, vocab=400)
+    kv_seed, wseed = 3, 4
+    ctx = [5, 16, 31, 64]
+    pool, model, ids, ref = _setup(dbk, s, ctx, kv_seed, wseed)
+    pool.reserve_tokens(ids, [1] * len(ids))
+    model.step(ids)
+    _, k1, v1, _ = om.decode_step(s, wseed, kv_seed, ids, ctx)
+    written = {(r, c - 1, lay): (k1[lay, i], v1[lay, i]) for i, (r, c) in enumerate(zip(ids, ctx))
+               for lay in range(s.layers)}
+    pool.reserve_tokens(ids, [1] * len(ids))
+    logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
+    model.step(ids, logits)
+    want, _, _, _ = om.decode_step(s, wseed, kv_seed, ids, [c + 1 for c in ctx], kv_written=written)
+    assert rel_l2(logits.cpu().numpy(), want) <= MODEL_TOL
+    model.close()
+    pool.close()
+
+
+def test_model_llama2_7b_layer_full_size(dbk):
+    """One Llama-2-7B-shaped layer (H 4096, 32 x 128 heads, F 11008, V 32000), 4 requests."""
+    s = om.ModelShape(layers=1, q_heads=32, kv_heads=32, head_dim=128, hidden=4096, ffn=11008, vocab=32000)
+    kv_seed, wseed = 21, 22
+    ctx = [3, 190, 573, 1100]
+    pool, model, ids, ref = _setup(dbk, s, ctx, kv_seed, wseed)
+    pool.reserve_tokens(ids, [1] * len(ids))
+    logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
+    model.step(ids, logits)
+    want, nk, nv, _ = om.decode_step(s, wseed, kv_seed, ids, ctx)
+    assert rel_l2(logits.cpu().numpy(), want) <= MODEL_TOL
+    for i, (r, c) in enumerate(zip(ids, ctx)):
+        k, v = _read_kv(pool, s, r, c - 1, 0)
+        assert rel_l2(k, nk[0, i]) <= MODEL_TOL and rel_l2(v, nv[0, i]) <= MODEL_TOL
+    model.close()
+    pool.close()
+
+
+def test_engine_full_model_mode_replays(dbk):
+    """The engine with the model attached: every decision bit-exact against the oracle's
+    replay of the logged step times; the K/V the model writes is what later steps read
+    (checked per step above); here the batch bookkeeping and telemetry."""
+    c = configs.CONFIGS["toy-tight"]
+    tr = trace.make_trace(30, 128, 128, 256, seed=1, dist="uniform")
+    L, Hq, Hkv, d = 2, 8, 8, 64
+    cap_pages = c["cap_tokens"] // P
+    beta = 2 * L * Hkv * d * 2
+    mem_cap = cap_pages * P * beta
+    pr = configs.prior_record(c)
+    kw = dict(policy=opol.MEMORY, b_static=c["b_max"], b_min=c["b_min"], b_max=c["b_max"], b0=c["b_min"],
+              eps_m=c["eps_m"], bytes_per_token=beta, page_size=P, refresh_steps=5, w_len=16, w_sla=4,
+              alpha=4, delta=1, d_sla_ms=50.0, eps_d_ms=0.01)
+    sched = dbk.Scheduler(prior=tuple(pr.values()), **kw)
+    max_req = c["b_max"] + 2
+    pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, 16, "f16")
+    model = dbk.Model(pool, 512, 768, 500, max_pos=256, weight_seed=9)
+    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap, seed=31, out_dtype=2)
+    eng.attach_model(model)
+    qd = torch.empty(L, max_req, Hq, d, dtype=torch.float16, device="cuda")
+    od = torch.empty(L, max_req, Hq, d, dtype=torch.float32, device="cuda")
+    bufs = eng.buffers(qd, od)
+    rp = oeng.Replay([oeng.RankEngine(list(range(len(tr))), tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P)],
+                     opol.SchedConfig(prior=tuple(pr.values()), **kw), mem_cap)
+    n = 0
+    while not eng.done():
+        g = eng.step(bufs)
+        o = rp.step(g["step_ns"])
+        for k in ("b_t", "b_next", "n_admitted", "n_preempted", "n_decode", "n_finished", "sum_ctx", "used_pages",
+                  "rationale"):
+            assert g[k] == o[k], (k, g[k], o[k])
+        assert (g["table_hash"] & ((1 << 64) - 1)) == o["table_hash"]
+        n += 1
+    assert rp.done() and n > 10
+    a_ms, t_ms, steps = model.timing()
+    assert steps > 0 and 0 < a_ms < t_ms
+    eng.close()
+    model.close()
+    pool.close()
