@@ -18,7 +18,7 @@ from oracle.allocator import PagedKV  # noqa: E402
 from synth import configs, trace  # noqa: E402
 from test_gpu_parity import dbk  # noqa: E402,F401
 
-MODEL_TOL = 1e-2
+MODEL_TOL = 2e-3  # R35: >= 4x the observed 2.3e-4 .. 4.6e-4 (profiles/r01_model_err.json)
 P = 16
 
 
