@@ -66,7 +66,7 @@ struct dbk_engine {
     dbk_model *model = nullptr;       // full-model mode (NEXT row 3)
     // end-to-end mode: host<->device copies on their own streams, ordered by events
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t ev_d2h = nullptr;
+    cudaEvent_t ev_d2h = nullptr, ev_up = nullptr;
     std::vector<cudaEvent_t> ev_q, ev_o;
     ~dbk_engine() {
         up_pf.release();
@@ -78,6 +78,7 @@ struct dbk_engine {
         for (auto e : ev_q) cudaEventDestroy(e);
         for (auto e : ev_o) cudaEventDestroy(e);
         if (ev_d2h) cudaEventDestroy(ev_d2h);
+        if (ev_up) cudaEventDestroy(ev_up);
         if (h2d) cudaStreamDestroy(h2d);
         if (d2h) cudaStreamDestroy(d2h);
     }
@@ -103,6 +104,7 @@ dbk_status ensure_copy_streams(dbk_engine *e) {
     DBK_CUDA(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
     DBK_CUDA(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
     DBK_CUDA(cudaEventCreateWithFlags(&e->ev_d2h, cudaEventDisableTiming));
+    DBK_CUDA(cudaEventCreateWithFlags(&e->ev_up, cudaEventDisableTiming));
     e->ev_q.assign(L, nullptr);
     e->ev_o.assign(L, nullptr);
     for (int l = 0; l < L; ++l) {
@@ -313,29 +315,8 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     const size_t kvrow = static_cast<size_t>(pc.layers) * pc.kv_heads * pc.head_dim * 2;
     const size_t orow = static_cast<size_t>(pc.q_heads) * pc.head_dim * (e->cfg.out_dtype == 2 ? 4 : 2);
     if (n > 0) {
-        if (e2e) {
-            // end-to-end: this step's new K/V rows and q come from pinned host memory on a copy
-            // stream (inside the timed region: it waits on ev0), layer by layer: layer l's KV
-            // append and attention wait only for layer l's K, V and q, so the PCIe transfers of
-            // later layers overlap the attention of earlier ones
-            DBK_TRY(ensure_copy_streams(e));
-            uint8_t *kd = static_cast<uint8_t *>(bufs->kv_dev);
-            uint8_t *vd = kd + static_cast<size_t>(pc.max_requests) * kvrow;
-            const size_t lrow = kvrow / pc.layers;  // one layer's K (or V) row of a request
-            DBK_CUDA(cudaStreamWaitEvent(e->h2d, e->ev0, 0));
-            for (int l = 0; l < pc.layers; ++l) {
-                const size_t off = static_cast<size_t>(l) * lrow;
-                DBK_CUDA(cudaMemcpy2DAsync(kd + off, kvrow, static_cast<const uint8_t *>(bufs->host_k) + off, kvrow,
-                                           lrow, n, cudaMemcpyHostToDevice, e->h2d));
-                DBK_CUDA(cudaMemcpy2DAsync(vd + off, kvrow, static_cast<const uint8_t *>(bufs->host_v) + off, kvrow,
-                                           lrow, n, cudaMemcpyHostToDevice, e->h2d));
-                uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
-                const uint8_t *qh = static_cast<const uint8_t *>(bufs->host_q) + static_cast<size_t>(l) * n * qrow;
-                DBK_CUDA(cudaMemcpyAsync(qd, qh, n * qrow, cudaMemcpyHostToDevice, e->h2d));
-                DBK_CUDA(cudaEventRecord(e->ev_q[l], e->h2d));
-            }
-            e->step_h2d += 2 * static_cast<int64_t>(n * kvrow) + static_cast<int64_t>(pc.layers) * n * qrow;
-            DBK_TRY(append_plan(p, n, e->batch_ids.data(), ones.data(), true, s));  // layers appended below
+        if (e2e) {  // the K/V rows arrive over PCIe below (after every small upload of this step)
+            DBK_TRY(append_plan(p, n, e->batch_ids.data(), ones.data(), true, s));  // layers appended per layer
         } else if (e->model) {  // the model's QKV epilogue writes the decode token's K/V
             DBK_TRY(dbk_reserve_tokens(p, n, e->batch_ids.data(), ones.data(), s));
         } else {
@@ -438,6 +419,32 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         DBK_CUDA(launch_synth_q(e->cfg.synth_seed, p->d_req, n, pc.layers, pc.max_requests, pc.q_heads,
                                 pc.head_dim, e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
         ++p->n_launches;
+    }
+    if (e2e && n > 0) {
+        // end-to-end: this step's new K/V rows and q come from pinned host memory on a copy
+        // stream (inside the timed region: it waits on ev0), layer by layer: layer l's KV
+        // append and attention wait only for layer l's K, V and q, so the PCIe transfers of
+        // later layers overlap the attention of earlier ones.  Issued after this step's small
+        // metadata uploads on `s`: host-to-device copies share the copy engine in issue order,
+        // so an upload queued behind 400 MB of inputs would hold layer 0 back until they land.
+        DBK_TRY(ensure_copy_streams(e));
+        uint8_t *kd = static_cast<uint8_t *>(bufs->kv_dev);
+        uint8_t *vd = kd + static_cast<size_t>(pc.max_requests) * kvrow;
+        const size_t lrow = kvrow / pc.layers;  // one layer's K (or V) row of a request
+        DBK_CUDA(cudaEventRecord(e->ev_up, s));
+        DBK_CUDA(cudaStreamWaitEvent(e->h2d, e->ev_up, 0));
+        for (int l = 0; l < pc.layers; ++l) {
+            const size_t off = static_cast<size_t>(l) * lrow;
+            DBK_CUDA(cudaMemcpy2DAsync(kd + off, kvrow, static_cast<const uint8_t *>(bufs->host_k) + off, kvrow,
+                                       lrow, n, cudaMemcpyHostToDevice, e->h2d));
+            DBK_CUDA(cudaMemcpy2DAsync(vd + off, kvrow, static_cast<const uint8_t *>(bufs->host_v) + off, kvrow,
+                                       lrow, n, cudaMemcpyHostToDevice, e->h2d));
+            uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
+            const uint8_t *qh = static_cast<const uint8_t *>(bufs->host_q) + static_cast<size_t>(l) * n * qrow;
+            DBK_CUDA(cudaMemcpyAsync(qd, qh, n * qrow, cudaMemcpyHostToDevice, e->h2d));
+            DBK_CUDA(cudaEventRecord(e->ev_q[l], e->h2d));
+        }
+        e->step_h2d += 2 * static_cast<int64_t>(n * kvrow) + static_cast<int64_t>(pc.layers) * n * qrow;
     }
     // device-resident decode-only steps chain the layer launches (programmatic dependent
     // launch: layer l+1's CTAs fill layer l's tail); then the attention time is one window
