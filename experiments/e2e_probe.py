@@ -1,5 +1,6 @@
 import sys, json, torch
-sys.path.insert(0, ".")
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
 S = bench.setup_engine(cfg_name="llama2-7b")
 eng = S["eng"]; stream = torch.cuda.current_stream()

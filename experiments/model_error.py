@@ -1,6 +1,8 @@
 """Observed model-step errors vs the fp64 oracle (for the R35 tolerance record)."""
 import sys, json, numpy as np, torch
-sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+import os
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tests")); sys.path.insert(0, ROOT)
 import paper_2503_05248_b200 as dbk
 from oracle import model as om
 from test_gpu_model import _setup, _read_kv, rel_l2

@@ -22,9 +22,26 @@ MODEL_TOL = 2e-3  # R35: >= 4x the observed 2.3e-4 .. 4.6e-4 (profiles/r01_model
 P = 16
 
 
-def rel_l2(got, want):
+OBSERVED = {}  # largest error seen per quantity (written to gpurun_out/model_err.json if that exists)
+
+
+def rel_l2(got, want, what=None):
     got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
-    return (np.linalg.norm(got - want, axis=-1) / np.maximum(np.linalg.norm(want, axis=-1), 1e-30)).max()
+    e = float((np.linalg.norm(got - want, axis=-1) / np.maximum(np.linalg.norm(want, axis=-1), 1e-30)).max())
+    if what:
+        OBSERVED[what] = max(OBSERVED.get(what, 0.0), e)
+    return e
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _record_errors():
+    yield
+    import json
+    import os
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if OBSERVED and os.path.isdir(out):
+        with open(os.path.join(out, "model_err.json"), "w") as f:
+            json.dump({"bar": MODEL_TOL, "observed_max_rel_l2": OBSERVED}, f, indent=1)
 
 
 def _read_kv(pool, s, req, pos, layer):
@@ -72,11 +89,11 @@ def test_model_step_parity(dbk, shape):
     st = pool.batch_stats()
     assert st["n_active"] == len(ids) and st["sum_ctx"] == sum(ctx) and st["table_mismatch"] == 0
     want, nk, nv, _ = om.decode_step(s, wseed, kv_seed, ids, ctx)
-    assert rel_l2(logits.cpu().numpy(), want) <= MODEL_TOL
+    assert rel_l2(logits.cpu().numpy(), want, "logits") <= MODEL_TOL
     for lay in range(s.layers):
         for i, (r, c) in enumerate(zip(ids, ctx)):
             k, v = _read_kv(pool, s, r, c - 1, lay)
-            assert rel_l2(k, nk[lay, i]) <= MODEL_TOL and rel_l2(v, nv[lay, i]) <= MODEL_TOL
+            assert rel_l2(k, nk[lay, i], "k") <= MODEL_TOL and rel_l2(v, nv[lay, i], "v") <= MODEL_TOL
     model.close()
     pool.close()
 
@@ -96,7 +113,7 @@ def test_model_two_steps_attend_to_model_written_kv(dbk):
     logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
     model.step(ids, logits)
     want, _, _, _ = om.decode_step(s, wseed, kv_seed, ids, [c + 1 for c in ctx], kv_written=written)
-    assert rel_l2(logits.cpu().numpy(), want) <= MODEL_TOL
+    assert rel_l2(logits.cpu().numpy(), want, "logits_step2") <= MODEL_TOL
     model.close()
     pool.close()
 
@@ -111,10 +128,10 @@ def test_model_llama2_7b_layer_full_size(dbk):
     logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
     model.step(ids, logits)
     want, nk, nv, _ = om.decode_step(s, wseed, kv_seed, ids, ctx)
-    assert rel_l2(logits.cpu().numpy(), want) <= MODEL_TOL
+    assert rel_l2(logits.cpu().numpy(), want, "logits_7b") <= MODEL_TOL
     for i, (r, c) in enumerate(zip(ids, ctx)):
         k, v = _read_kv(pool, s, r, c - 1, 0)
-        assert rel_l2(k, nk[0, i]) <= MODEL_TOL and rel_l2(v, nv[0, i]) <= MODEL_TOL
+        assert rel_l2(k, nk[0, i], "k_7b") <= MODEL_TOL and rel_l2(v, nv[0, i], "v_7b") <= MODEL_TOL
     model.close()
     pool.close()
 
