@@ -269,6 +269,16 @@ dbk_status dbk_reserve_tokens(dbk_pool *pool, int32_t n_req, const int64_t *req_
 dbk_status dbk_model_step(dbk_model *model, int32_t n, const int64_t *req_ids, int32_t fuse_stats,
                           void *logits, void *stream);
 
+/* PD fusion through the model: the decode tokens of req_ids[0..n) (as dbk_model_step)
+ * plus every token of each prefill chunk (chunks->req_ids[c], positions q_start[c] ..
+ * q_start[c] + q_len[c] - 1, already reserved; chunks->layer is ignored) run as ONE batch
+ * of n + sum(q_len) rows through the GEMMs; decode rows attend with K1/K2, chunk rows
+ * causally with K7 (R24).  Token ids gen_token(token_seed, req, pos) for every row.
+ * logits (nullable): device [n + sum(q_len)][vocab] fp32, rows in that order.  EINVAL if
+ * the rows exceed max_requests or a chunk lies outside the reserved tokens. */
+dbk_status dbk_model_step_pd(dbk_model *model, int32_t n, const int64_t *req_ids, const dbk_prefill_batch *chunks,
+                             int32_t fuse_stats, void *logits, void *stream);
+
 /* Introspection (tests): device pointers of the activation workspace of the last
  * step, rows = batch order: [0] x fp32 [n][H] (residual stream), [1] h fp16 [n][H]
  * (last norm output), [2] qkv fp16 [n][(Hq+2Hkv)d], [3] q fp16 [n][Hq][d] (after RoPE),

@@ -106,44 +106,63 @@ def attention(q, K, V):
     return out
 
 
-def decode_step(s: ModelShape, weight_seed, kv_seed, req_ids, ctx, token_seed=None, layer_weights=None,
-                head=None, kv_written=None):
-    """The decode step of every request (module docstring).  Returns (logits [n][V],
-    new_k [L][n][Hkv][d], new_v, x_final [n][H]).  layer_weights / head: optional cached
-    results of weights() / head_weights().  kv_written: {(req, pos, layer): (k [Hkv][d], v)}
-    -- history positions written by earlier model steps (instead of the synthetic fill)."""
-    n = len(req_ids)
+def forward_rows(s: ModelShape, weight_seed, kv_seed, rows, token_seed=None, layer_weights=None, head=None,
+                 kv_written=None):
+    """One model step over activation rows [(req, pos)] -- decode tokens (pos = ctx - 1) and
+    prefill-chunk tokens (PD fusion, R24: a chunk token at position p attends causally to
+    positions 0..p of its request).  Layer by layer: every row's (k, v) is computed first,
+    then each row attends over its request's positions 0..p, taking a position's K/V from
+    (in order) this step's rows, kv_written {(req, pos, layer): (k, v)} of earlier steps, or
+    the pool's synthetic fill (generator kinds K/V).  Returns (logits [R][V],
+    written {(req, pos, layer): (k, v)} of this step, x_final [R][H])."""
+    R = len(rows)
     d, Hkv = s.head_dim, s.kv_heads
     token_seed = weight_seed if token_seed is None else token_seed
-    pos = [int(c) - 1 for c in ctx]
-    toks = [int(hashgen.gen_token(token_seed, int(r), p, s.vocab)) for r, p in zip(req_ids, pos)]
+    toks = [int(hashgen.gen_token(token_seed, int(r), int(p), s.vocab)) for r, p in rows]
     x = embed_rows(weight_seed, s, toks)
-    new_k = np.zeros((s.layers, n, Hkv, d))
-    new_v = np.zeros_like(new_k)
+    written = {}
     for lay in range(s.layers):
         W = layer_weights[lay] if layer_weights is not None else weights(weight_seed, s, lay)
         h = rmsnorm(x, W["g1"], s.rms_eps)
         qkv = h @ W["w_qkv"].T
-        a = np.zeros((n, s.q_heads * d))
-        for i, (r, p) in enumerate(zip(req_ids, pos)):
+        qs = []
+        for i, (r, p) in enumerate(rows):
             q = qkv[i, : s.q_heads * d].reshape(s.q_heads, d)
             k = qkv[i, s.q_heads * d:(s.q_heads + Hkv) * d].reshape(Hkv, d)
             v = qkv[i, (s.q_heads + Hkv) * d:].reshape(Hkv, d)
-            q, k = rope(q, p, s.rope_theta), rope(k, p, s.rope_theta)
-            new_k[lay, i], new_v[lay, i] = k, v
-            hist = np.arange(p)[:, None]
-            K = np.concatenate([hashgen.gen_values(kv_seed, hashgen.KIND_K, int(r), hist, lay,
-                                                   np.arange(Hkv)[None, :], d), k[None]], axis=0)
-            V = np.concatenate([hashgen.gen_values(kv_seed, hashgen.KIND_V, int(r), hist, lay,
-                                                   np.arange(Hkv)[None, :], d), v[None]], axis=0)
-            for (wr, wp, wl), (kk, vv) in (kv_written or {}).items():
-                if wr == int(r) and wl == lay and wp < p:
-                    K[wp], V[wp] = kk, vv
-            a[i] = attention(q, K, V).reshape(-1)
+            qs.append(rope(q, p, s.rope_theta))
+            written[(int(r), int(p), lay)] = (rope(k, p, s.rope_theta), v)
+        a = np.zeros((R, s.q_heads * d))
+        for i, (r, p) in enumerate(rows):
+            pos = np.arange(p + 1)[:, None]
+            K = hashgen.gen_values(kv_seed, hashgen.KIND_K, int(r), pos, lay, np.arange(Hkv)[None, :], d)
+            V = hashgen.gen_values(kv_seed, hashgen.KIND_V, int(r), pos, lay, np.arange(Hkv)[None, :], d)
+            for j in range(p + 1):
+                src = written.get((int(r), j, lay))
+                if src is None and kv_written is not None:
+                    src = kv_written.get((int(r), j, lay))
+                if src is not None:
+                    K[j], V[j] = src
+            a[i] = attention(qs[i], K, V).reshape(-1)
         x = x + a @ W["w_o"].T
         h = rmsnorm(x, W["g2"], s.rms_eps)
         gu = h @ W["w_gu"].T
         x = x + (silu(gu[:, : s.ffn]) * gu[:, s.ffn:]) @ W["w_down"].T
     hw = head if head is not None else head_weights(weight_seed, s)
     logits = rmsnorm(x, hw["g_f"], s.rms_eps) @ hw["w_lm"].T
+    return logits, written, x
+
+
+def decode_step(s: ModelShape, weight_seed, kv_seed, req_ids, ctx, token_seed=None, layer_weights=None,
+                head=None, kv_written=None):
+    """The decode step of every request (module docstring): forward_rows over the rows
+    (req_i, ctx_i - 1).  Returns (logits [n][V], new_k [L][n][Hkv][d], new_v, x_final [n][H])."""
+    rows = [(int(r), int(c) - 1) for r, c in zip(req_ids, ctx)]
+    logits, written, x = forward_rows(s, weight_seed, kv_seed, rows, token_seed, layer_weights, head, kv_written)
+    n = len(rows)
+    new_k = np.zeros((s.layers, n, s.kv_heads, s.head_dim))
+    new_v = np.zeros_like(new_k)
+    for lay in range(s.layers):
+        for i, (r, p) in enumerate(rows):
+            new_k[lay, i], new_v[lay, i] = written[(r, p, lay)]
     return logits, new_k, new_v, x

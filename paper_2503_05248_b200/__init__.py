@@ -222,6 +222,15 @@ class Model:
         ids, pids = _i64(req_ids)
         _lib.dbk_model_step(self.h, len(ids), pids, 1 if fuse_stats else 0, _ptr(logits), _stream(stream))
 
+    def step_pd(self, req_ids, chunk_ids, q_start, q_len, logits=None, fuse_stats=True, stream=None):
+        ids, pids = _i64(req_ids)
+        cid, pcid = _i64(chunk_ids)
+        s0, ps0 = _i32(q_start)
+        ln, pln = _i32(q_len)
+        b = dbk_prefill_batch(len(cid), 0, pcid, ps0, pln)
+        _lib.dbk_model_step_pd(self.h, len(ids), pids, C.byref(b), 1 if fuse_stats else 0, _ptr(logits),
+                               _stream(stream))
+
     def timing(self, reset=False):
         a, t, n = C.c_double(), C.c_double(), C.c_int64()
         _lib.dbk_model_timing(self.h, C.byref(a), C.byref(t), C.byref(n), 1 if reset else 0)

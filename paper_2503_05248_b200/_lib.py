@@ -131,6 +131,7 @@ SIGNATURES = {
     "dbk_model_create": [P, C.POINTER(dbk_model_config), P, C.c_size_t, C.POINTER(P)],
     "dbk_model_destroy": [P],
     "dbk_model_step": [P, I32, PI64, I32, P, P],
+    "dbk_model_step_pd": [P, I32, PI64, C.POINTER(dbk_prefill_batch), I32, P, P],
     "dbk_model_timing": [P, C.POINTER(C.c_double), C.POINTER(C.c_double), PI64, I32],
     "dbk_engine_attach_model": [P, P],
     "dbk_model_buffers": [P, C.POINTER(C.c_void_p)],

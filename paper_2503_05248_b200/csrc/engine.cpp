@@ -192,7 +192,6 @@ dbk_status dbk_engine_done(dbk_engine *e, int32_t *done) {
 
 dbk_status dbk_engine_attach_model(dbk_engine *e, dbk_model *m) {
     if (!e) return fail(DBK_EINVAL, "attach_model: null engine");
-    if (m && e->cfg.pd_fusion) return fail(DBK_EINVAL, "attach_model: full-model mode is not combined with PD fusion");
     e->model = m;
     return DBK_OK;
 }
@@ -374,7 +373,9 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             ++i;
             if (cut) break;
         }
-        if (!e->pf_ids.empty()) {
+        if (!e->pf_ids.empty() && e->model) {  // the model writes the chunk's K/V (real prefill)
+            DBK_TRY(dbk_reserve_tokens(p, static_cast<int32_t>(e->pf_ids.size()), e->pf_ids.data(), e->pf_len.data(), s));
+        } else if (!e->pf_ids.empty()) {
             DBK_TRY(dbk_append_tokens(p, static_cast<int32_t>(e->pf_ids.size()), e->pf_ids.data(), e->pf_len.data(),
                                       nullptr, nullptr, e->cfg.synth_seed, s));
             // the chunk's q rows (synthetic, all layers) follow the decode rows: (req, position)
@@ -451,7 +452,14 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     const bool chained = !e2e && n_pf_rows == 0 && n > 0 && !e->model;
     const bool per_layer_ev = e->cfg.time_attention && n > 0 && !chained && !e->model;
     if (e->cfg.time_attention && chained) DBK_CUDA(cudaEventRecord(e->att0[0], s));
-    if (e->model) DBK_TRY(dbk_model_step(e->model, n, e->batch_ids.data(), 1, nullptr, s));
+    if (e->model) {
+        dbk_prefill_batch pb{};
+        pb.n = static_cast<int32_t>(e->pf_ids.size());
+        pb.req_ids = e->pf_ids.data();
+        pb.q_start = e->pf_start.data();
+        pb.q_len = e->pf_len.data();
+        DBK_TRY(dbk_model_step_pd(e->model, n, e->batch_ids.data(), pb.n > 0 ? &pb : nullptr, 1, nullptr, s));
+    }
     for (int l = 0; l < (e->model ? 0 : pc.layers); ++l) {
         uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
         uint8_t *od = static_cast<uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;

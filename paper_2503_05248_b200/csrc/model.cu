@@ -25,6 +25,14 @@ using namespace dbk;
 namespace {
 using namespace dbk::dev;
 
+// One activation row of a model step: a decode token (pos = ctx - 1) or a prefill-chunk token.
+struct RowMeta {
+    int64_t req_id;
+    int32_t slot;  // block-table row
+    int32_t pos;   // token position
+};
+static_assert(sizeof(RowMeta) == 16, "RowMeta layout");
+
 constexpr int kWChunk = 128;  // synthetic weight rows are K/128 "heads" of 128 dims (hashgen)
 constexpr int kKindToken = 7, kKindEmbed = 8, kKindLn1 = 9, kKindWqkv = 10, kKindWo = 11, kKindLn2 = 12,
               kKindWgu = 13, kKindWdown = 14, kKindLnf = 15, kKindLm = 16;
@@ -61,10 +69,10 @@ __device__ __forceinline__ float block_sum(float v, float *red) {
     return t;
 }
 
-// h[i] = RMSNorm(x[i]) * g (fp16); with embed != nullptr, x[i] = E[token(req_i, ctx_i - 1)] first.
+// h[i] = RMSNorm(x[i]) * g (fp16); with embed != nullptr, x[i] = E[token(req_i, pos_i)] first.
 // One CTA per row; H % 8 == 0 and H / 8 <= 4 * blockDim.x.
 __global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, float eps, int H, __half *h,
-                                                   const ReqMeta *req, const __half *embed, uint64_t tok_seed,
+                                                   const RowMeta *rows, const __half *embed, uint64_t tok_seed,
                                                    int vocab) {
     __shared__ float red[8];
     const int i = blockIdx.x;
@@ -74,8 +82,8 @@ __global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, fl
     float ss = 0.f;
     const __half *er = nullptr;
     if (embed) {
-        const ReqMeta rm = req[i];
-        const uint64_t key = synth_key(tok_seed, kKindToken, rm.req_id, rm.ctx - 1, 0, 0, 0);
+        const RowMeta rm = rows[i];
+        const uint64_t key = synth_key(tok_seed, kKindToken, rm.req_id, rm.pos, 0, 0, 0);
         er = embed + static_cast<size_t>((key >> 16) % static_cast<uint64_t>(vocab)) * H;
     }
 #pragma unroll
@@ -111,15 +119,15 @@ __global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, fl
 }
 
 // RoPE (rotate-half pairs (j, j + d/2), angle table cs[pos][j] = (cos, sin)) on the q and k
-// heads of the QKV GEMM output; q -> q_out [n][Hq][d], k and v -> the decode token's slot
-// (position ctx - 1) of this layer's page tile.  One CTA per token.
-__global__ void __launch_bounds__(256) rope_kv_kernel(const __half *qkv, const ReqMeta *req, const int32_t *bt,
+// heads of the QKV GEMM output; q -> q_out [rows][Hq][d], k and v -> the token's slot of this
+// layer's page tile.  One CTA per row (token).
+__global__ void __launch_bounds__(256) rope_kv_kernel(const __half *qkv, const RowMeta *rows, const int32_t *bt,
                                                       int bt_stride, uint8_t *kv_layer, int64_t page_stride,
                                                       int64_t tile_bytes, const float2 *cs, int Hq, int Hkv, int d,
                                                       __half *q_out) {
     const int i = blockIdx.x;
-    const ReqMeta rm = req[i];
-    const int p = rm.ctx - 1;
+    const RowMeta rm = rows[i];
+    const int p = rm.pos;
     const int32_t page = bt[static_cast<size_t>(rm.slot) * bt_stride + p / kP];
     const int half_d = d / 2;
     const int nqkv = (Hq + 2 * Hkv) * d;
@@ -207,6 +215,8 @@ struct dbk_model {
     void *lt_ws = nullptr;
     size_t lt_ws_bytes = 32u << 20;
     std::map<std::tuple<int, int, int, int>, GemmPlan> plans;
+    UploadBuffer up_rows;
+    std::vector<RowMeta> rows_h;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> a0, a1;
     bool pending = false;
@@ -220,6 +230,8 @@ struct dbk_model {
             if (kv.second.c) cublasLtMatrixLayoutDestroy(kv.second.c);
         }
         if (lt) cublasLtDestroy(lt);
+        up_rows.release();
+        if (up_rows.done) cudaEventDestroy(up_rows.done);
         for (void *ptr : {static_cast<void *>(cs), static_cast<void *>(x), static_cast<void *>(logits),
                           static_cast<void *>(h), static_cast<void *>(qkv), static_cast<void *>(q),
                           static_cast<void *>(attn), static_cast<void *>(gu), static_cast<void *>(act), lt_ws})
@@ -412,51 +424,93 @@ dbk_status dbk_model_destroy(dbk_model *m) {
 
 dbk_status dbk_model_step(dbk_model *m, int32_t n, const int64_t *ids, int32_t fuse_stats, void *logits,
                           void *stream) {
+    return dbk_model_step_pd(m, n, ids, nullptr, fuse_stats, logits, stream);
+}
+
+dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const dbk_prefill_batch *chunks,
+                             int32_t fuse_stats, void *logits, void *stream) {
     if (!m) return fail(DBK_EINVAL, "model_step: null model");
-    if (n < 0 || n > m->rows || (n > 0 && !ids)) return fail(DBK_EINVAL, "model_step: bad batch (n <= max_requests)");
-    if (n == 0) return DBK_OK;
+    if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "model_step: bad batch");
+    const int32_t nch = chunks ? chunks->n : 0;
+    if (nch < 0 || (nch > 0 && (!chunks->req_ids || !chunks->q_start || !chunks->q_len)))
+        return fail(DBK_EINVAL, "model_step: bad chunk arrays");
     dbk_pool *p = m->pool;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     DBK_CUDA(cudaSetDevice(p->cfg.device));
     DBK_TRY(collect_timing(m));
-    DBK_TRY(prepare_batch(p, n, ids, s));  // ReqMeta (ctx incl. the reserved decode token) + block table
-    for (int32_t i = 0; i < n; ++i)
-        if (p->reqs.at(ids[i]).ctx > m->cfg.max_pos) return fail(DBK_EINVAL, "model_step: position beyond max_pos");
+    // activation rows: the decode tokens (batch order), then every chunk's tokens
+    m->rows_h.clear();
+    for (int32_t i = 0; i < n; ++i) {
+        auto it = p->reqs.find(ids[i]);
+        if (it == p->reqs.end()) return fail(DBK_ENOENT, "model_step: unknown request %lld", static_cast<long long>(ids[i]));
+        if (it->second.ctx < 1) return fail(DBK_EINVAL, "model_step: request without a reserved decode token");
+        m->rows_h.push_back({ids[i], it->second.slot, it->second.ctx - 1});
+    }
+    int64_t chunk_rows = 0;
+    for (int32_t c = 0; c < nch; ++c) {
+        auto it = p->reqs.find(chunks->req_ids[c]);
+        if (it == p->reqs.end())
+            return fail(DBK_ENOENT, "model_step: unknown request %lld", static_cast<long long>(chunks->req_ids[c]));
+        const int32_t s0 = chunks->q_start[c], len = chunks->q_len[c];
+        if (s0 < 0 || len < 1 || static_cast<int64_t>(s0) + len > it->second.ctx)
+            return fail(DBK_EINVAL, "model_step: chunk %d outside the reserved tokens", c);
+        for (int32_t j = 0; j < len; ++j) m->rows_h.push_back({chunks->req_ids[c], it->second.slot, s0 + j});
+        chunk_rows += len;
+    }
+    const int R = static_cast<int>(m->rows_h.size());
+    if (R == 0) return DBK_OK;
+    if (R > m->rows) return fail(DBK_EINVAL, "model_step: %d rows > max_requests (%d)", R, m->rows);
+    for (const RowMeta &r : m->rows_h)
+        if (r.pos >= m->cfg.max_pos) return fail(DBK_EINVAL, "model_step: position beyond max_pos");
+    DBK_TRY(flush_deltas(p, s));
+    if (n > 0) DBK_TRY(prepare_batch(p, n, ids, s));
+    DBK_TRY(m->up_rows.upload(m->rows_h.data(), m->rows_h.size() * sizeof(RowMeta), s));
+    const RowMeta *rows = static_cast<const RowMeta *>(m->up_rows.dev);
     const int H = m->H, F = m->F, qd = m->Hq * m->d;
     const float eps = static_cast<float>(m->cfg.rms_eps);
     DBK_CUDA(cudaEventRecord(m->ev0, s));
-    norm_kernel<<<n, 256, 0, s>>>(m->x, m->lw[0].ln1, eps, H, m->h, p->d_req, m->embed, m->cfg.token_seed, m->V);
+    norm_kernel<<<R, 256, 0, s>>>(m->x, m->lw[0].ln1, eps, H, m->h, rows, m->embed, m->cfg.token_seed, m->V);
     DBK_CUDA(cudaGetLastError());
     dbk_batch bt{};
     bt.n = n;
     bt.req_ids = ids;
+    dbk_prefill_batch pb{};
+    if (nch > 0) pb = *chunks;
     for (int l = 0; l < m->L; ++l) {
         const LayerW &w = m->lw[l];
-        DBK_TRY(gemm(m, n, m->nqkv, H, m->h, w.wqkv, m->qkv, false, false, s));
-        rope_kv_kernel<<<n, 256, 0, s>>>(m->qkv, p->d_req, p->d_bt, p->cfg.max_pages_per_req,
+        DBK_TRY(gemm(m, R, m->nqkv, H, m->h, w.wqkv, m->qkv, false, false, s));
+        rope_kv_kernel<<<R, 256, 0, s>>>(m->qkv, rows, p->d_bt, p->cfg.max_pages_per_req,
                                          p->kv + static_cast<size_t>(l) * p->layer_stride, p->page_stride,
                                          p->tile_bytes, m->cs, m->Hq, m->Hkv, m->d, m->q);
         DBK_CUDA(cudaGetLastError());
-        bt.layer = l;
-        bt.fuse_stats = (fuse_stats && l == 0) ? 1 : 0;
         DBK_CUDA(cudaEventRecord(m->a0[l], s));
-        DBK_TRY(dbk_decode_step(p, &bt, m->q, m->attn, 0, s));
+        if (n > 0 || (fuse_stats && l == 0)) {
+            bt.layer = l;
+            bt.fuse_stats = (fuse_stats && l == 0) ? 1 : 0;
+            DBK_TRY(dbk_decode_step(p, &bt, m->q, m->attn, 0, s));
+        }
+        if (nch > 0) {  // the chunk rows' causal attention (K7, tensor cores)
+            pb.layer = l;
+            DBK_TRY(dbk_prefill_step(p, &pb, m->q + static_cast<size_t>(n) * qd, m->attn + static_cast<size_t>(n) * qd,
+                                     0, s));
+        }
         DBK_CUDA(cudaEventRecord(m->a1[l], s));
-        DBK_TRY(gemm(m, n, H, qd, m->attn, w.wo, m->x, true, true, s));       // x += attn W_o^T
-        norm_kernel<<<n, 256, 0, s>>>(m->x, w.ln2, eps, H, m->h, nullptr, nullptr, 0, 0);
-        DBK_TRY(gemm(m, n, 2 * F, H, m->h, w.wgu, m->gu, false, false, s));
-        silu_mul_kernel<<<grid_of(static_cast<int64_t>(n) * F / 8, 256, p->num_sms), 256, 0, s>>>(m->gu, n, F,
+        DBK_TRY(gemm(m, R, H, qd, m->attn, w.wo, m->x, true, true, s));       // x += attn W_o^T
+        norm_kernel<<<R, 256, 0, s>>>(m->x, w.ln2, eps, H, m->h, nullptr, nullptr, 0, 0);
+        DBK_TRY(gemm(m, R, 2 * F, H, m->h, w.wgu, m->gu, false, false, s));
+        silu_mul_kernel<<<grid_of(static_cast<int64_t>(R) * F / 8, 256, p->num_sms), 256, 0, s>>>(m->gu, R, F,
                                                                                                  m->act);
-        DBK_TRY(gemm(m, n, H, F, m->act, w.wdown, m->x, true, true, s));      // x += act W_down^T
+        DBK_TRY(gemm(m, R, H, F, m->act, w.wdown, m->x, true, true, s));      // x += act W_down^T
         const __half *g_next = l + 1 < m->L ? m->lw[l + 1].ln1 : m->lnf;
-        norm_kernel<<<n, 256, 0, s>>>(m->x, g_next, eps, H, m->h, nullptr, nullptr, 0, 0);
+        norm_kernel<<<R, 256, 0, s>>>(m->x, g_next, eps, H, m->h, nullptr, nullptr, 0, 0);
         DBK_CUDA(cudaGetLastError());
         p->n_launches += 4;  // ours: RoPE/KV, 2 norms, SiLU (attention counts itself; GEMMs are cuBLASLt's)
     }
-    DBK_TRY(gemm(m, n, m->V, H, m->h, m->lm, logits ? logits : m->logits, true, false, s));
+    DBK_TRY(gemm(m, R, m->V, H, m->h, m->lm, logits ? logits : m->logits, true, false, s));
     DBK_CUDA(cudaEventRecord(m->ev1, s));
     m->pending = true;
     p->n_launches += 1;  // the embedding + first norm
+    (void)chunk_rows;
     return DBK_OK;
 }
 

@@ -53,11 +53,11 @@ def _read_kv(pool, s, req, pos, layer):
     return tile[:, 0, :], tile[:, 1, :]
 
 
-def _setup(dbk, s, ctx, kv_seed, wseed, cap=None):
+def _setup(dbk, s, ctx, kv_seed, wseed, cap=None, max_req=None):
     n = len(ctx)
     maxp = max(-(-(c + 4) // P) for c in ctx) + 1
     cap = cap or sum(-(-(c + 1) // P) for c in ctx) + 4
-    pool = dbk.KVPool(s.layers, s.q_heads, s.kv_heads, s.head_dim, cap, n + 2, maxp, "f16")
+    pool = dbk.KVPool(s.layers, s.q_heads, s.kv_heads, s.head_dim, cap, max_req or n + 2, maxp, "f16")
     model = dbk.Model(pool, s.hidden, s.ffn, s.vocab, max_pos=maxp * P, weight_seed=wseed)
     ids = [int(i) * 131 + 7 for i in range(n)]
     ref = PagedKV(cap, P)
@@ -173,6 +173,86 @@ def test_engine_full_model_mode_replays(dbk):
     assert rp.done() and n > 10
     a_ms, t_ms, steps = model.timing()
     assert steps > 0 and 0 < a_ms < t_ms
+    eng.close()
+    model.close()
+    pool.close()
+
+
+def test_model_step_pd_chunks_and_decode_rows(dbk):
+    """PD fusion through the model (dbk_model_step_pd): decode rows of two requests with a
+    synthetic history + a 40-token prompt prefilled in two chunks (24 + 16 tokens) over two
+    steps; step 2's chunk attends over step 1's model-written K/V.  Oracle: forward_rows with
+    the K/V of its own step 1 (R24)."""
+    s = om.ModelShape(layers=2, q_heads=8, kv_heads=2, head_dim=128, hidden=512, ffn=640, vocab=700)
+    kv_seed, wseed = 8, 9
+    pool, model, ids, ref = _setup(dbk, s, [20, 45], kv_seed, wseed, cap=40, max_req=32)
+    C = 999
+    pool.request_begin(C, 40, 4)
+    written = {}
+    ctx = {ids[0]: 19, ids[1]: 44}
+    for s0, k in ((0, 24), (24, 16)):
+        pool.reserve_tokens(ids, [1, 1])
+        pool.reserve_tokens([C], [k])
+        for r in ids:
+            ctx[r] += 1
+        R = 2 + k
+        logits = torch.empty(R, s.vocab, dtype=torch.float32, device="cuda")
+        model.step_pd(ids, [C], [s0], [k], logits)
+        st = pool.batch_stats()
+        assert st["n_active"] == 2 and st["sum_ctx"] == ctx[ids[0]] + ctx[ids[1]]
+        rows = [(r, ctx[r] - 1) for r in ids] + [(C, s0 + j) for j in range(k)]
+        want, w, _ = om.forward_rows(s, wseed, kv_seed, rows, kv_written=written)
+        written.update(w)
+        assert rel_l2(logits.cpu().numpy(), want, "logits_pd") <= MODEL_TOL
+        for lay in range(s.layers):
+            for (r, p) in rows:
+                kk, vv = _read_kv(pool, s, r, p, lay)
+                assert rel_l2(kk, w[(r, p, lay)][0], "k_pd") <= MODEL_TOL
+                assert rel_l2(vv, w[(r, p, lay)][1], "v_pd") <= MODEL_TOL
+    with pytest.raises(dbk.DbkError):  # a chunk beyond the reserved tokens
+        model.step_pd(ids, [C], [38], [4])
+    model.close()
+    pool.close()
+
+
+def test_engine_pd_fusion_with_model_replays(dbk):
+    """PD fusion + the full model in the engine: prompts are prefilled THROUGH the model in
+    chunks of c_t = max(0, b_t - N^d) tokens (R25-R27, R34 no longer applies); every record
+    incl. the chunk size and every decision bit-exact against the oracle's PD replay."""
+    tr = trace.make_trace(30, 200, 80, 512, seed=6, dist="uniform")
+    L, Hq, Hkv, d, P = 2, 8, 2, 128, 16
+    cap_pages = 60
+    beta = 2 * L * Hkv * d * 2
+    mem_cap = cap_pages * P * beta
+    pr = configs.prior_record(dict(prior=dict(n=8, mean_in=100.0, mean_out=40.0), trace=dict(dist="uniform")))
+    b_max = 64
+    # static b = 64 over-commits the 60-page cap: LIFO preemption and recompute through the model
+    kw = dict(policy=opol.STATIC, b_static=b_max, b_min=1, b_max=b_max, b0=8, eps_m=0.02, bytes_per_token=beta,
+              page_size=P, refresh_steps=5, w_len=16, w_sla=4, alpha=4, delta=1, d_sla_ms=50.0, eps_d_ms=0.01)
+    sched = dbk.Scheduler(prior=tuple(pr.values()), **kw)
+    max_req = b_max + 2
+    maxp = -(-int((tr.l_in + tr.l_out).max()) // P) + 1
+    pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, "f16")
+    model = dbk.Model(pool, 512, 512, 300, max_pos=maxp * P, weight_seed=5)
+    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap, seed=17, out_dtype=2, pd_fusion=True)
+    eng.attach_model(model)
+    qd = torch.empty(L, max_req, Hq, d, dtype=torch.float16, device="cuda")
+    od = torch.empty(L, max_req, Hq, d, dtype=torch.float32, device="cuda")
+    bufs = eng.buffers(qd, od)
+    rp = oeng.Replay([oeng.RankEngine(list(range(len(tr))), tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P, pd=True,
+                                      max_rows=max_req)], opol.SchedConfig(prior=tuple(pr.values()), **kw), mem_cap)
+    recs = []
+    while not eng.done():
+        g = eng.step(bufs)
+        recs.append(g)
+        o = rp.step(g["step_ns"])
+        for k in ("b_t", "b_next", "n_admitted", "n_preempted", "n_decode", "n_finished", "sum_ctx", "used_pages",
+                  "rationale", "n_prefill"):
+            assert g[k] == o[k], (k, g[k], o[k])
+        assert (g["table_hash"] & ((1 << 64) - 1)) == o["table_hash"]
+    assert rp.done()
+    assert sum(r["n_prefill"] for r in recs) >= int(tr.l_in.sum())
+    assert sum(r["n_preempted"] for r in recs) > 0      # the 60-page cap forces recompute through the model
     eng.close()
     model.close()
     pool.close()

@@ -110,3 +110,46 @@ def test_synthetic_weights_are_exact_in_fp16():
     s = om.ModelShape(layers=1, q_heads=4, kv_heads=2, head_dim=128, hidden=512, ffn=1024, vocab=64)
     for v in list(om.weights(3, s, 0).values()) + list(om.head_weights(3, s).values()):
         hashgen.to_bits(v, "f16")  # raises if any value is not exact
+
+
+def test_chunked_prefill_equals_token_by_token_decode():
+    """R24 causal semantics: a whole prompt in one step (rows (r, 0..P-1)), the same prompt in
+    two chunks, and P single-token steps (each attending over the K/V the earlier steps
+    wrote) give the same logits and K/V."""
+    s = om.ModelShape(layers=2, q_heads=8, kv_heads=2, head_dim=64, hidden=256, ffn=256, vocab=120)
+    r, P = 42, 9
+    full, wf, _ = om.forward_rows(s, 1, 2, [(r, p) for p in range(P)])
+    a, wa, _ = om.forward_rows(s, 1, 2, [(r, p) for p in range(4)])
+    b, wb, _ = om.forward_rows(s, 1, 2, [(r, p) for p in range(4, P)], kv_written=wa)
+    assert np.allclose(np.concatenate([a, b]), full, rtol=1e-12, atol=1e-12)
+    seq, kv = [], {}
+    for p in range(P):
+        lg, w, _ = om.forward_rows(s, 1, 2, [(r, p)], kv_written=kv)
+        kv.update(w)
+        seq.append(lg[0])
+    assert np.allclose(np.stack(seq), full, rtol=1e-12, atol=1e-12)
+    for key, (k, v) in wf.items():
+        assert np.allclose(kv[key][0], k, rtol=1e-12, atol=1e-12) and np.allclose(kv[key][1], v, rtol=1e-12, atol=1e-12)
+
+
+def test_prefill_matches_torch_causal_attention():
+    """A whole prompt through one layer vs torch (F.scaled_dot_product_attention is_causal)."""
+    import torch.nn.functional as F
+    s = om.ModelShape(layers=1, q_heads=4, kv_heads=4, head_dim=64, hidden=256, ffn=256, vocab=50)
+    r, P, d = 7, 6, 64
+    _, written, x = om.forward_rows(s, 3, 4, [(r, p) for p in range(P)])
+    W = om.weights(3, s, 0)
+    toks = [int(hashgen.gen_token(3, r, p, s.vocab)) for p in range(P)]
+    T = lambda a: torch.from_numpy(np.asarray(a, np.float64))  # noqa: E731
+    x0 = T(om.embed_rows(3, s, toks))
+    h = F.rms_norm(x0, (s.hidden,), T(W["g1"]), s.rms_eps)
+    qkv = F.linear(h, T(W["w_qkv"]))
+    q = torch.stack([T(om.rope(qkv[p, :256].view(4, d).numpy(), p, s.rope_theta)) for p in range(P)])
+    k = torch.stack([T(written[(r, p, 0)][0]) for p in range(P)])
+    v = qkv[:, 512:].view(P, 4, d)
+    o = F.scaled_dot_product_attention(q.transpose(0, 1), k.transpose(0, 1), v.transpose(0, 1), is_causal=True)
+    x1 = x0 + F.linear(o.transpose(0, 1).reshape(P, -1), T(W["w_o"]))
+    h2 = F.rms_norm(x1, (s.hidden,), T(W["g2"]), s.rms_eps)
+    g, u = F.linear(h2, T(W["w_gu"])).split(s.ffn, dim=-1)
+    x2 = x1 + F.linear(F.silu(g) * u, T(W["w_down"]))
+    assert np.allclose(x, x2.numpy(), rtol=1e-12, atol=1e-12)
