@@ -11,6 +11,7 @@
              the shape of Table I row 3 -- attention-only.
 * --sla    : the SLA feedback (Alg. 2 + min with Alg. 1) on the 13B shape with a binding
              D_SLA = tau(b_mem / 2) from the sweep's fit, and the literal 50 ms.
+* --pd-model: the PD table with the full model: prompts prefilled through the weights.
 * --swap   : preemption by swapping vs recomputation (NEXT row 4) on the 7B shape with a
              40 GB KV cap: static b = 256 over-commits it (recompute / swap to a 16 GB pinned
              host space) vs the memory-aware rule, which keeps the batch under the cap.
@@ -155,9 +156,10 @@ def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
     return out
 
 
-def pd_table(cfg="llama2-7b", bs=(64, 128, 256)):
+def pd_table(cfg="llama2-7b", bs=(64, 128, 256), full_model=False):
     """PD-fusion whole-trace runs (Table I shape, all-at-once arrivals): static b vs the
-    memory-aware rule deciding the fused iteration's token budget (R25)."""
+    memory-aware rule deciding the fused iteration's token budget (R25).  full_model: prompts
+    are prefilled through the weights (QKV/O/MLP GEMMs + K7) instead of the KV fill."""
     import gc
 
     import torch
@@ -165,23 +167,26 @@ def pd_table(cfg="llama2-7b", bs=(64, 128, 256)):
     for pol, b in [("static", x) for x in bs] + [("memory", None)]:
         gc.collect()
         torch.cuda.empty_cache()
-        S = bench.setup_engine(cfg_name=cfg, policy=pol, b_static=b or 256, time_attention=False, pd_fusion=True)
+        S = bench.setup_engine(cfg_name=cfg, policy=pol, b_static=b or 256, time_attention=False, pd_fusion=True,
+                               full_model=full_model)
         eng = S["eng"]
         bufs = eng.buffers(S["qd"], S["od"])
         t0 = time.time()
         recs, ms = bench.run_steps(S, 10 ** 9, bufs, torch.cuda.current_stream())
         dev_s = ms / 1e3
-        rows.append(dict(policy=pol, b_static=b, steps=len(recs), device_s=dev_s,
+        rows.append(dict(policy=pol, b_static=b, full_model=full_model, steps=len(recs), device_s=dev_s,
                          decode_tokens_per_s=sum(r["n_decode"] for r in recs) / dev_s,
                          prefill_tokens_per_s=sum(r["n_prefill"] for r in recs) / dev_s,
                          mean_b=float(np.mean([r["b_t"] for r in recs])),
                          preemptions=int(sum(r["n_preempted"] for r in recs)), wall_s=time.time() - t0))
         print(json.dumps(rows[-1]), flush=True)
         S["eng"].close()
+        if S.get("model") is not None:
+            S["model"].close()
         S["pool"].close()
         S.clear()
         del eng, bufs  # the engine holds the pool, the pool holds the KV allocation
-    return dict(config=cfg, rows=rows)
+    return dict(config=cfg, full_model=full_model, rows=rows)
 
 
 def swap_table(cfg="llama2-7b", kv_gb=40.0, swap_gb=16.0, n_req=1500, b=256):
@@ -230,6 +235,7 @@ def main():
     ap.add_argument("--capacity", action="store_true")
     ap.add_argument("--pd", action="store_true")
     ap.add_argument("--swap", action="store_true")
+    ap.add_argument("--pd-model", action="store_true", help="PD table with prefill through the full model")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
     a = ap.parse_args()
     import torch
@@ -250,6 +256,9 @@ def main():
         save()
     if a.pd:
         res["pd_table"] = pd_table()
+        save()
+    if a.pd_model:
+        res["pd_table_model"] = pd_table(full_model=True)
         save()
     if a.swap:
         res["swap"] = swap_table()
