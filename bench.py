@@ -266,6 +266,10 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # configs[3] (70B GQA) is sharded by KV heads (TP); the others by requests (DP)
     tp = world if args.config == "llama3-70b-gqa" else 1
+    if args.tp_shard:  # one GPU runs exactly rank 0's share of a KV-head TP run of that width
+        if world != 1 or args.config != "llama3-70b-gqa":
+            raise SystemExit("--tp-shard: single-GPU emulation of the 70B KV-head TP shard only")
+        tp = args.tp_shard
     S = setup_engine(device=local, rank=rank, world=world, cfg_name=args.config, policy=args.policy,
                      b_static=args.b_static, sla_ms=args.sla_ms, tp=tp, full_model=args.model)
     dbk = S["dbk"]
@@ -359,7 +363,8 @@ def run_gpu(args):
                        "mean_batch": round(float(np.mean([r["n_decode"] for r in recs])), 1) if recs else 0,
                        "mean_ctx": round(float(np.mean([r["sum_ctx"] / max(r["n_decode"], 1) for r in recs])), 1) if recs else 0,
                        "fast_forward_steps": args.ff,
-                       "parallelism": f"tp{world} (KV-head shards)" if tp > 1 else f"dp{world} (request shards)",
+                       "parallelism": (f"rank 0 of tp{tp} (KV-head shard on one GPU; no exchange)" if args.tp_shard else
+                                       f"tp{world} (KV-head shards)" if tp > 1 else f"dp{world} (request shards)"),
                        "stats_exchange": exchange_kind,
                        "l2": "inputs > L2 (~1e2 GB of KV read per step vs 126 MB L2)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -459,6 +464,8 @@ def main():
     ap.add_argument("--policy", default=None, choices=[None, "static", "memory", "sla", "combined"])
     ap.add_argument("--b-static", type=int, default=256)
     ap.add_argument("--sla-ms", type=float, default=None)
+    ap.add_argument("--tp-shard", type=int, default=0, choices=[0, 2, 4, 8],
+                    help="70B GQA: run rank 0's KV-head shard of a TP-G job on this one GPU (per-GPU kernel rate)")
     ap.add_argument("--model", action="store_true",
                     help="full decode step: synthetic-weight QKV/O/MLP/LM-head GEMMs around the attention")
     args = ap.parse_args()

@@ -217,6 +217,10 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     p->ctas_per_sm = p->has_tmap ? decode_gqa_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group)
                                  : decode_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group);
     if (const char *e = std::getenv("DBK_NO_PDL")) p->pdl_enabled = !(e[0] == '1');  // A/B runs
+    if (const char *e = std::getenv("DBK_TASKS_PER_WARP")) {  // tuning override
+        const long long v = std::atoll(e);
+        if (v >= 1 && v <= 16) p->tasks_per_warp = v;
+    }
     if (const char *e = std::getenv("DBK_CHUNK_PAGES")) {  // tuning override (multiple of 4, <= 64)
         const long long v = std::atoll(e);
         if (v >= 4 && v <= 64 && v % 4 == 0) p->force_chunk_pages = v;
@@ -646,10 +650,16 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
         m.l_out = r.l_out;
         total_pages += (r.ctx + P - 1) / P;
     }
-    // chunk size (pages per warp task, <= 32): at least ~4 tasks per resident warp, so the
-    // dynamic task queue balances; otherwise as large as possible (fewer split-K merges)
+    // chunk size (pages per warp task, 4..32): ~tasks_per_warp (3) tasks per resident warp so
+    // the dynamic queue balances, but not below 12 pages while every warp still gets a task:
+    // each task pays fixed costs (metadata, q, split-K partial + merge) -- measured on the
+    // per-GPU shards of 70B KV-head TP (profiles/r01_tune_chunks.txt): 12 pages beat 6 by 13 %
+    // at TP8, 15 beat 12 by 4 % at TP4
     const int64_t warps = static_cast<int64_t>(p->num_sms) * p->ctas_per_sm * 4;
-    int64_t cp = (total_pages * p->cfg.kv_heads + 4 * warps - 1) / (4 * warps);
+    const int64_t tpw = p->tasks_per_warp;
+    const int64_t work = total_pages * p->cfg.kv_heads;
+    int64_t cp = (work + tpw * warps - 1) / (tpw * warps);
+    cp = std::max<int64_t>(cp, std::min<int64_t>(12, (work + warps - 1) / warps));
     cp = std::max<int64_t>(4, std::min<int64_t>(p->max_chunk_pages, cp));
     if (p->force_chunk_pages > 0) cp = std::min<int64_t>(p->force_chunk_pages, p->max_chunk_pages);
     p->meta_work.clear();

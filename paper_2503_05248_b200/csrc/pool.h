@@ -88,6 +88,7 @@ struct dbk_pool {
     int num_sms = 148, ctas_per_sm = 1;
     // pages per warp task: <= 64 (two page ids per lane); 32 measured best (profiles/r01_tune.txt)
     int64_t max_chunk_pages = 32, force_chunk_pages = 0;
+    int64_t tasks_per_warp = 3;               // chunk size target: total tasks ~ tasks_per_warp x warps
     int64_t last_decode_bytes = 0;
     int64_t n_launches = 0;                   // kernels launched by this pool (gpu_launches)
     int launch_parity = 0;                    // scratch copy of the next decode launch
