@@ -152,10 +152,15 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
     uint32_t qa[KSTEPS][2];
     load_q(cur, qa);
 
+    bool released = false;
     while (cur.task < p.n_tasks) {
         // one task ahead: the metadata of the task after `nxt` and the q of `nxt`
         const Task nnx = load_task(p, __shfl_sync(kFull, pend, 0), lane);
         pend = task_fetch(p, lane);
+        if (!released && nnx.task >= p.n_tasks) {  // queue drained: only cur and nxt remain
+            pdl_release();
+            released = true;
+        }
         uint32_t qn[KSTEPS][2];
         load_q(nxt, qn);
         const int i = cur.it.i, c = cur.it.c, g = cur.g;

@@ -86,11 +86,16 @@ decode_kernel(const DecodeParams p) {
     uint4 qraw[GQ];
     load_q(cur, qraw);
 
+    bool released = false;
     while (cur.task < p.n_tasks) {
         // one task ahead: metadata of the task after `nxt` and the q of `nxt` are requested
         // now and used when they become current, so their latency hides behind this task
         const Task nnx = load_task(p, __shfl_sync(kFull, pend, 0), lane);
         pend = task_fetch(p, lane);
+        if (!released && nnx.task >= p.n_tasks) {  // queue drained: only cur and nxt remain
+            pdl_release();
+            released = true;
+        }
         uint4 qnext[GQ];
         load_q(nxt, qnext);
         const int i = cur.it.i, c = cur.it.c, g = cur.g;

@@ -228,6 +228,17 @@ __device__ __forceinline__ int task_fetch(const DecodeParams &p, int lane) {
     return lane == 0 ? atomicAdd(p.task_counter, 1) : 0;
 }
 
+// Programmatic dependent launch, released early: once a warp has fetched past the end of the
+// task queue (only the tasks it holds remain), it waits for the PREVIOUS decode grid to
+// complete and lets the NEXT one launch.  Every CTA reaches this point as the queue drains, so
+// the next grid's CTAs take each SM as soon as one of this grid's CTAs exits -- they fill this
+// grid's tail instead of starting after it.  The next grid uses the other parity of scratch,
+// whose last user (the grid before this one) has completed by then.
+__device__ __forceinline__ void pdl_release() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // A warp with no task left: the last one resets the counters for the next launch.
 // Programmatic dependent launch: the warp first waits for the PREVIOUS decode grid to complete
 // (a no-op without the launch attribute), then lets the NEXT one launch.  So when the next
