@@ -33,6 +33,9 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 
+FULL_MODEL = False  # --model: every run is the whole decode step with synthetic weights (NEXT row 3)
+
+
 def _run(cfg, policy, b_static=256, sla_ms=None, ff=300, steps=40, full=False, n_req=None):
     import gc
 
@@ -40,7 +43,7 @@ def _run(cfg, policy, b_static=256, sla_ms=None, ff=300, steps=40, full=False, n
     gc.collect()
     torch.cuda.empty_cache()
     S = bench.setup_engine(cfg_name=cfg, policy=policy, b_static=b_static, sla_ms=sla_ms, time_attention=False,
-                           n_req=n_req)
+                           n_req=n_req, full_model=FULL_MODEL)
     eng = S["eng"]
     bufs = eng.buffers(S["qd"], S["od"])
     stream = torch.cuda.current_stream()
@@ -58,7 +61,10 @@ def _run(cfg, policy, b_static=256, sla_ms=None, ff=300, steps=40, full=False, n
     out["tokens_per_s"] = out["tokens"] / (ms / 1e3)
     if not full:
         out["b_trace_tail"] = [r["b_next"] for r in recs[-10:]]
+    out["full_model"] = FULL_MODEL
     S["eng"].close()
+    if S.get("model") is not None:
+        S["model"].close()
     S["pool"].close()
     S.clear()
     return out
@@ -121,7 +127,8 @@ def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
         gc.collect()
         torch.cuda.empty_cache()
         S = bench.setup_engine(cfg_name=cfg, policy=policy, b_static=b_static or 256, sla_ms=d_sla,
-                               eps_d_ms=eps_d, time_attention=False, trace_override=tr, pd_fusion=pd)
+                               eps_d_ms=eps_d, time_attention=False, trace_override=tr, pd_fusion=pd,
+                               full_model=FULL_MODEL)
         eng = S["eng"]
         bufs = eng.buffers(S["qd"], S["od"])
         recs, ms = bench.run_steps(S, 10 ** 9, bufs, torch.cuda.current_stream())
@@ -135,6 +142,8 @@ def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
                    mean_b=float(np.mean([r["b_t"] for r in recs])), steps=len(recs))
         res["ok"] = bool(p99 <= d_sla + eps_d and delay <= max_delay_s)
         S["eng"].close()
+        if S.get("model") is not None:
+            S["model"].close()
         S["pool"].close()
         S.clear()
         return res
@@ -236,8 +245,11 @@ def main():
     ap.add_argument("--pd", action="store_true")
     ap.add_argument("--swap", action="store_true")
     ap.add_argument("--pd-model", action="store_true", help="PD table with prefill through the full model")
+    ap.add_argument("--model", action="store_true", help="--fig3/--table1/--sla with the full decode step")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
     a = ap.parse_args()
+    global FULL_MODEL
+    FULL_MODEL = a.model
     import torch
     torch.cuda.set_device(0)
     res = {}
