@@ -246,6 +246,8 @@ def main():
     ap.add_argument("--swap", action="store_true")
     ap.add_argument("--pd-model", action="store_true", help="PD table with prefill through the full model")
     ap.add_argument("--model", action="store_true", help="--fig3/--table1/--sla with the full decode step")
+    ap.add_argument("--cap-lo", type=float, default=10.0, help="capacity bisection: lowest rate (qps)")
+    ap.add_argument("--cap-hi", type=float, default=640.0, help="capacity bisection: highest rate (qps)")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
     a = ap.parse_args()
     global FULL_MODEL
@@ -285,7 +287,8 @@ def main():
             res["sla"] = sla(fit=d)
             save()
         if a.capacity:
-            res["capacity"] = capacity(d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem))
+            res["capacity"] = capacity(d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem), lo=a.cap_lo,
+                                       hi=a.cap_hi)
             save()
     print(json.dumps({k: (v.get("fit") if isinstance(v, dict) else None) for k, v in res.items()}))
 
