@@ -314,12 +314,22 @@ def run_gpu(args):
     # end-to-end through the same API with pinned host buffers (q, new K/V in; out back)
     L, Hq, Hkv, d, mr = S["L"], S["Hq"], S["Hkv"], S["d"], S["max_req"]
     erecs, ems_t, etok_t = [], None, None
-    if not args.model:  # full-model mode is device-resident (its inputs are token ids)
+    if not args.model:  # attention-only: q and the new K/V rows in, every layer's output back
         hq = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
         hk = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
         hv = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
         ho = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True)
         ebufs = eng.buffers(S["qd"], S["od"], S["kvd"], hq, hk, hv, ho)
+        run_steps(S, 2, ebufs, stream, dist=dist)
+        erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
+        ems_t = torch.tensor([ems], device="cuda")
+        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / (world if tp > 1 else 1)], device="cuda")
+        if dist is not None:
+            dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
+            dist.all_reduce(etok_t)
+    else:  # full model end to end: each step's input token ids in, greedy samples out (4 B per row each way)
+        host_tok = torch.zeros(len(S["tr"]), dtype=torch.int32).pin_memory()
+        ebufs = eng.buffers(S["qd"], S["od"], host_tokens=host_tok)
         run_steps(S, 2, ebufs, stream, dist=dist)
         erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
         ems_t = torch.tensor([ems], device="cuda")

@@ -274,10 +274,14 @@ dbk_status dbk_model_step(dbk_model *model, int32_t n, const int64_t *req_ids, i
  * q_start[c] + q_len[c] - 1, already reserved; chunks->layer is ignored) run as ONE batch
  * of n + sum(q_len) rows through the GEMMs; decode rows attend with K1/K2, chunk rows
  * causally with K7 (R24).  Token ids gen_token(token_seed, req, pos) for every row.
- * logits (nullable): device [n + sum(q_len)][vocab] fp32, rows in that order.  EINVAL if
- * the rows exceed max_requests or a chunk lies outside the reserved tokens. */
+ * logits (nullable): device [n + sum(q_len)][vocab] fp32, rows in that order.  tokens
+ * (nullable): device int32 [n], the decode rows' input token ids (e.g. the previous step's
+ * samples; clamped into [0, vocab)) instead of gen_token.  sampled (nullable): device int32
+ * [n + sum(q_len)], greedy sampling -- the lowest index of each row's largest logit.  EINVAL
+ * if the rows exceed max_requests or a chunk lies outside the reserved tokens. */
 dbk_status dbk_model_step_pd(dbk_model *model, int32_t n, const int64_t *req_ids, const dbk_prefill_batch *chunks,
-                             int32_t fuse_stats, void *logits, void *stream);
+                             int32_t fuse_stats, void *logits, const int32_t *tokens, int32_t *sampled,
+                             void *stream);
 
 /* Introspection (tests): device pointers of the activation workspace of the last
  * step, rows = batch order: [0] x fp32 [n][H] (residual stream), [1] h fp16 [n][H]
@@ -400,6 +404,9 @@ typedef struct dbk_engine_buffers {
     void *q_dev, *out_dev, *kv_dev;
     const void *host_q, *host_k, *host_v;
     void *host_out;
+    int32_t *host_tokens;  /* full-model mode, end to end: pinned host int32 [n_requests] indexed
+                            * by trace index; each step reads the decode rows' input tokens
+                            * from it (H2D) and writes their greedy samples back (D2H) */
 } dbk_engine_buffers;
 
 typedef struct dbk_step_record {

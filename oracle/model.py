@@ -93,6 +93,14 @@ def silu(x):
     return x / (1.0 + np.exp(-x))
 
 
+def greedy_ok(logits_row, token, tol):
+    """Greedy sampling (argmax) has several right answers when logits tie within the rounding
+    of a lower-precision path: token is valid iff its logit is within tol * max|logit| of the
+    row's maximum."""
+    row = np.asarray(logits_row, np.float64)
+    return 0 <= token < len(row) and row[token] >= row.max() - tol * np.abs(row).max()
+
+
 def attention(q, K, V):
     """q [Hq][d], K, V [ctx][Hkv][d]: O1 for one request (full softmax, scale 1/sqrt(d))."""
     Hq, d = q.shape
@@ -107,18 +115,21 @@ def attention(q, K, V):
 
 
 def forward_rows(s: ModelShape, weight_seed, kv_seed, rows, token_seed=None, layer_weights=None, head=None,
-                 kv_written=None):
+                 kv_written=None, tokens=None):
     """One model step over activation rows [(req, pos)] -- decode tokens (pos = ctx - 1) and
     prefill-chunk tokens (PD fusion, R24: a chunk token at position p attends causally to
     positions 0..p of its request).  Layer by layer: every row's (k, v) is computed first,
     then each row attends over its request's positions 0..p, taking a position's K/V from
     (in order) this step's rows, kv_written {(req, pos, layer): (k, v)} of earlier steps, or
-    the pool's synthetic fill (generator kinds K/V).  Returns (logits [R][V],
+    the pool's synthetic fill (generator kinds K/V).  tokens: optional input token ids of the
+    first len(tokens) rows (instead of gen_token).  Returns (logits [R][V],
     written {(req, pos, layer): (k, v)} of this step, x_final [R][H])."""
     R = len(rows)
     d, Hkv = s.head_dim, s.kv_heads
     token_seed = weight_seed if token_seed is None else token_seed
     toks = [int(hashgen.gen_token(token_seed, int(r), int(p), s.vocab)) for r, p in rows]
+    for i, t in enumerate(tokens or []):
+        toks[i] = int(t)
     x = embed_rows(weight_seed, s, toks)
     written = {}
     for lay in range(s.layers):
@@ -154,11 +165,12 @@ def forward_rows(s: ModelShape, weight_seed, kv_seed, rows, token_seed=None, lay
 
 
 def decode_step(s: ModelShape, weight_seed, kv_seed, req_ids, ctx, token_seed=None, layer_weights=None,
-                head=None, kv_written=None):
+                head=None, kv_written=None, tokens=None):
     """The decode step of every request (module docstring): forward_rows over the rows
     (req_i, ctx_i - 1).  Returns (logits [n][V], new_k [L][n][Hkv][d], new_v, x_final [n][H])."""
     rows = [(int(r), int(c) - 1) for r, c in zip(req_ids, ctx)]
-    logits, written, x = forward_rows(s, weight_seed, kv_seed, rows, token_seed, layer_weights, head, kv_written)
+    logits, written, x = forward_rows(s, weight_seed, kv_seed, rows, token_seed, layer_weights, head, kv_written,
+                                      tokens)
     n = len(rows)
     new_k = np.zeros((s.layers, n, s.kv_heads, s.head_dim))
     new_v = np.zeros_like(new_k)

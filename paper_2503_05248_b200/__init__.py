@@ -222,14 +222,15 @@ class Model:
         ids, pids = _i64(req_ids)
         _lib.dbk_model_step(self.h, len(ids), pids, 1 if fuse_stats else 0, _ptr(logits), _stream(stream))
 
-    def step_pd(self, req_ids, chunk_ids, q_start, q_len, logits=None, fuse_stats=True, stream=None):
+    def step_pd(self, req_ids, chunk_ids, q_start, q_len, logits=None, fuse_stats=True, stream=None,
+                tokens=None, sampled=None):
         ids, pids = _i64(req_ids)
         cid, pcid = _i64(chunk_ids)
         s0, ps0 = _i32(q_start)
         ln, pln = _i32(q_len)
         b = dbk_prefill_batch(len(cid), 0, pcid, ps0, pln)
         _lib.dbk_model_step_pd(self.h, len(ids), pids, C.byref(b), 1 if fuse_stats else 0, _ptr(logits),
-                               _stream(stream))
+                               _ptr(tokens), _ptr(sampled), _stream(stream))
 
     def timing(self, reset=False):
         a, t, n = C.c_double(), C.c_double(), C.c_int64()
@@ -270,9 +271,10 @@ class Engine:
         _lib.dbk_engine_attach_model(self.h, model.h if model is not None else None)
 
     @staticmethod
-    def buffers(q_dev, out_dev, kv_dev=None, host_q=None, host_k=None, host_v=None, host_out=None):
+    def buffers(q_dev, out_dev, kv_dev=None, host_q=None, host_k=None, host_v=None, host_out=None,
+                host_tokens=None):
         return dbk_engine_buffers(_ptr(q_dev), _ptr(out_dev), _ptr(kv_dev), _ptr(host_q),
-                                  _ptr(host_k), _ptr(host_v), _ptr(host_out))
+                                  _ptr(host_k), _ptr(host_v), _ptr(host_out), _ptr(host_tokens))
 
     def step(self, bufs, stream=None):
         rec = dbk_step_record()

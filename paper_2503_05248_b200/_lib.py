@@ -90,7 +90,7 @@ class dbk_engine_config(C.Structure):
 class dbk_engine_buffers(C.Structure):
     _fields_ = [("q_dev", C.c_void_p), ("out_dev", C.c_void_p), ("kv_dev", C.c_void_p),
                 ("host_q", C.c_void_p), ("host_k", C.c_void_p), ("host_v", C.c_void_p),
-                ("host_out", C.c_void_p)]
+                ("host_out", C.c_void_p), ("host_tokens", C.c_void_p)]
 
 
 class dbk_model_config(C.Structure):
@@ -131,7 +131,7 @@ SIGNATURES = {
     "dbk_model_create": [P, C.POINTER(dbk_model_config), P, C.c_size_t, C.POINTER(P)],
     "dbk_model_destroy": [P],
     "dbk_model_step": [P, I32, PI64, I32, P, P],
-    "dbk_model_step_pd": [P, I32, PI64, C.POINTER(dbk_prefill_batch), I32, P, P],
+    "dbk_model_step_pd": [P, I32, PI64, C.POINTER(dbk_prefill_batch), I32, P, P, P, P],
     "dbk_model_timing": [P, C.POINTER(C.c_double), C.POINTER(C.c_double), PI64, I32],
     "dbk_engine_attach_model": [P, P],
     "dbk_model_buffers": [P, C.POINTER(C.c_void_p)],

@@ -38,6 +38,7 @@ struct dbk_engine {
     std::vector<int32_t> pf_start, pf_len;
     std::vector<uint8_t> pf_rows;     // per chunk row: req id (int64) | position (int32)
     UploadBuffer up_pf;
+    UploadBuffer tok_in, tok_out;     // full-model e2e: token ids (pinned staging + device)
     int32_t step_prefill = 0;
     int64_t clock = 0, t = 0;
     int32_t b = 1;
@@ -71,6 +72,10 @@ struct dbk_engine {
     ~dbk_engine() {
         up_pf.release();
         if (up_pf.done) cudaEventDestroy(up_pf.done);
+        tok_in.release();
+        tok_out.release();
+        if (tok_in.done) cudaEventDestroy(tok_in.done);
+        if (tok_out.done) cudaEventDestroy(tok_out.done);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (auto e : att0) cudaEventDestroy(e);
@@ -211,12 +216,14 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     dbk_pool *p = e->pool;
     const dbk_pool_config &pc = p->cfg;
     const bool e2e = bufs->host_q != nullptr;
+    const bool tok_io = bufs->host_tokens != nullptr;  // full-model end to end: token ids in, samples out
     if (!bufs->q_dev || !bufs->out_dev) return fail(DBK_EINVAL, "engine_step_launch: q_dev and out_dev are required");
     if (e2e && (!bufs->host_k || !bufs->host_v || !bufs->kv_dev))
         return fail(DBK_EINVAL, "engine_step_launch: end-to-end mode needs host_q, host_k, host_v and kv_dev");
     const bool pd = e->cfg.pd_fusion != 0;
     if (pd && e2e) return fail(DBK_EINVAL, "engine_step_launch: PD fusion runs in device-resident mode only");
-    if (e->model && e2e) return fail(DBK_EINVAL, "engine_step_launch: full-model mode is device-resident");
+    if (e->model && e2e) return fail(DBK_EINVAL, "engine_step_launch: full-model mode takes token ids (host_tokens), not q/K/V");
+    if (tok_io && !e->model) return fail(DBK_EINVAL, "engine_step_launch: host_tokens needs an attached model");
     DBK_CUDA(cudaSetDevice(pc.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t P = pc.page_size;
@@ -458,7 +465,26 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         pb.req_ids = e->pf_ids.data();
         pb.q_start = e->pf_start.data();
         pb.q_len = e->pf_len.data();
-        DBK_TRY(dbk_model_step_pd(e->model, n, e->batch_ids.data(), pb.n > 0 ? &pb : nullptr, 1, nullptr, s));
+        int32_t *tok_dev = nullptr, *smp_dev = nullptr;
+        if (tok_io && n > 0) {  // this step's input tokens from the caller's array (pinned), H2D
+            DBK_TRY(e->tok_in.reserve(static_cast<size_t>(n) * 4));
+            int32_t *th = static_cast<int32_t *>(e->tok_in.host);
+            if (e->tok_in.pending) DBK_CUDA(cudaEventSynchronize(e->tok_in.done));
+            for (int32_t x = 0; x < n; ++x) th[x] = bufs->host_tokens[e->running[x]];
+            DBK_CUDA(cudaMemcpyAsync(e->tok_in.dev, th, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, s));
+            DBK_CUDA(cudaEventRecord(e->tok_in.done, s));
+            e->tok_in.pending = true;
+            tok_dev = static_cast<int32_t *>(e->tok_in.dev);
+            DBK_TRY(e->tok_out.reserve(static_cast<size_t>(pc.max_requests) * 4));
+            smp_dev = static_cast<int32_t *>(e->tok_out.dev);
+            e->step_h2d += static_cast<int64_t>(n) * 4;
+        }
+        DBK_TRY(dbk_model_step_pd(e->model, n, e->batch_ids.data(), pb.n > 0 ? &pb : nullptr, 1, nullptr, tok_dev,
+                                  smp_dev, s));
+        if (smp_dev) {  // the decode rows' samples back to pinned memory (scattered after the sync)
+            DBK_CUDA(cudaMemcpyAsync(e->tok_out.host, smp_dev, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, s));
+            e->step_d2h += static_cast<int64_t>(n) * 4;
+        }
     }
     for (int l = 0; l < (e->model ? 0 : pc.layers); ++l) {
         uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
@@ -510,6 +536,10 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     float ms = 0.f;
     DBK_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     e->local.step_ns = std::llround(static_cast<double>(ms) * 1e6);
+    if (tok_io && n > 0) {  // the stream is synchronised: each decode row's sample -> its request's slot
+        const int32_t *sh = static_cast<const int32_t *>(e->tok_out.host);
+        for (int32_t x = 0; x < n; ++x) bufs->host_tokens[e->running[x]] = sh[x];
+    }
     e->local.n_waiting = static_cast<int64_t>(e->queue.size() + e->prefilling.size());
     if (pd) {  // R27: completed prompts join the decode batch from the next step on
         size_t m = 0;

@@ -73,7 +73,7 @@ __device__ __forceinline__ float block_sum(float v, float *red) {
 // One CTA per row; H % 8 == 0 and H / 8 <= 4 * blockDim.x.
 __global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, float eps, int H, __half *h,
                                                    const RowMeta *rows, const __half *embed, uint64_t tok_seed,
-                                                   int vocab) {
+                                                   int vocab, const int32_t *tokens = nullptr, int n_tok = 0) {
     __shared__ float red[8];
     const int i = blockIdx.x;
     float *xr = x + static_cast<size_t>(i) * H;
@@ -83,8 +83,14 @@ __global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, fl
     const __half *er = nullptr;
     if (embed) {
         const RowMeta rm = rows[i];
-        const uint64_t key = synth_key(tok_seed, kKindToken, rm.req_id, rm.pos, 0, 0, 0);
-        er = embed + static_cast<size_t>((key >> 16) % static_cast<uint64_t>(vocab)) * H;
+        uint64_t tok;
+        if (i < n_tok) {  // caller-provided token id (e.g. the previous step's sample)
+            const int32_t t = tokens[i];
+            tok = static_cast<uint64_t>(t < 0 ? 0 : (t >= vocab ? vocab - 1 : t));
+        } else {
+            tok = (synth_key(tok_seed, kKindToken, rm.req_id, rm.pos, 0, 0, 0) >> 16) % static_cast<uint64_t>(vocab);
+        }
+        er = embed + static_cast<size_t>(tok) * H;
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -177,6 +183,45 @@ __global__ void silu_mul_kernel(const __half *gu, int n, int F, __half *act) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] = g[e] / (1.0f + __expf(-g[e])) * u[e];
         *reinterpret_cast<uint4 *>(act + i * F + j) = pack8<__half>(o);
+    }
+}
+
+// Greedy sampling: out[i] = the lowest index of the largest logit of row i (NaN rows -> 0).
+__global__ void __launch_bounds__(256) argmax_kernel(const float *logits, int V, int32_t *out) {
+    __shared__ float bv[8];
+    __shared__ int bi[8];
+    const float *row = logits + static_cast<size_t>(blockIdx.x) * V;
+    float best = -INFINITY;
+    int idx = 0x7fffffff;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) {
+        const float v = row[j];
+        if (v > best) {  // strided scan: the first hit of a value is its lowest index in this thread
+            best = v;
+            idx = j;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(kFull, best, o);
+        const int oi = __shfl_xor_sync(kFull, idx, o);
+        if (ov > best || (ov == best && oi < idx)) {
+            best = ov;
+            idx = oi;
+        }
+    }
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (lane == 0) {
+        bv[warp] = best;
+        bi[warp] = idx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w)
+            if (bv[w] > best || (bv[w] == best && bi[w] < idx)) {
+                best = bv[w];
+                idx = bi[w];
+            }
+        out[blockIdx.x] = idx == 0x7fffffff ? 0 : idx;
     }
 }
 
@@ -424,11 +469,12 @@ dbk_status dbk_model_destroy(dbk_model *m) {
 
 dbk_status dbk_model_step(dbk_model *m, int32_t n, const int64_t *ids, int32_t fuse_stats, void *logits,
                           void *stream) {
-    return dbk_model_step_pd(m, n, ids, nullptr, fuse_stats, logits, stream);
+    return dbk_model_step_pd(m, n, ids, nullptr, fuse_stats, logits, nullptr, nullptr, stream);
 }
 
 dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const dbk_prefill_batch *chunks,
-                             int32_t fuse_stats, void *logits, void *stream) {
+                             int32_t fuse_stats, void *logits, const int32_t *tokens, int32_t *sampled,
+                             void *stream) {
     if (!m) return fail(DBK_EINVAL, "model_step: null model");
     if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "model_step: bad batch");
     const int32_t nch = chunks ? chunks->n : 0;
@@ -469,7 +515,8 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
     const int H = m->H, F = m->F, qd = m->Hq * m->d;
     const float eps = static_cast<float>(m->cfg.rms_eps);
     DBK_CUDA(cudaEventRecord(m->ev0, s));
-    norm_kernel<<<R, 256, 0, s>>>(m->x, m->lw[0].ln1, eps, H, m->h, rows, m->embed, m->cfg.token_seed, m->V);
+    norm_kernel<<<R, 256, 0, s>>>(m->x, m->lw[0].ln1, eps, H, m->h, rows, m->embed, m->cfg.token_seed, m->V,
+                                  tokens, tokens ? n : 0);
     DBK_CUDA(cudaGetLastError());
     dbk_batch bt{};
     bt.n = n;
@@ -506,7 +553,13 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
         DBK_CUDA(cudaGetLastError());
         p->n_launches += 4;  // ours: RoPE/KV, 2 norms, SiLU (attention counts itself; GEMMs are cuBLASLt's)
     }
-    DBK_TRY(gemm(m, R, m->V, H, m->h, m->lm, logits ? logits : m->logits, true, false, s));
+    float *lg = logits ? static_cast<float *>(logits) : m->logits;
+    DBK_TRY(gemm(m, R, m->V, H, m->h, m->lm, lg, true, false, s));
+    if (sampled) {
+        argmax_kernel<<<R, 256, 0, s>>>(lg, m->V, sampled);
+        DBK_CUDA(cudaGetLastError());
+        ++p->n_launches;
+    }
     DBK_CUDA(cudaEventRecord(m->ev1, s));
     m->pending = true;
     p->n_launches += 1;  // the embedding + first norm

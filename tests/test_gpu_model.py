@@ -256,3 +256,80 @@ def test_engine_pd_fusion_with_model_replays(dbk):
     eng.close()
     model.close()
     pool.close()
+
+
+def test_model_explicit_tokens_and_greedy_sampling(dbk):
+    """Caller-provided input tokens for the decode rows (dbk_model_step_pd tokens) and greedy
+    sampling (sampled): logits vs O8 with the same token ids; every sample is a valid argmax
+    of the oracle's logits (ties within the fp16 path's rounding, R35) and, bit for bit, the
+    lowest-index argmax of the returned logits."""
+    s = om.ModelShape(layers=2, q_heads=8, kv_heads=4, head_dim=64, hidden=512, ffn=512, vocab=32000)
+    kv_seed, wseed = 12, 13
+    ctx = [3, 40, 111]
+    pool, model, ids, ref = _setup(dbk, s, ctx, kv_seed, wseed)
+    pool.reserve_tokens(ids, [1] * len(ids))
+    toks = [31999, 0, 12345]
+    tk = torch.tensor(toks, dtype=torch.int32, device="cuda")
+    smp = torch.full((len(ids),), -1, dtype=torch.int32, device="cuda")
+    logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
+    model.step_pd(ids, [], [], [], logits, tokens=tk, sampled=smp)
+    want, _, _, _ = om.decode_step(s, wseed, kv_seed, ids, ctx, tokens=toks)
+    got = logits.cpu().numpy()
+    assert rel_l2(got, want, "logits_tokens") <= MODEL_TOL
+    sm = smp.cpu().numpy()
+    for i in range(len(ids)):
+        assert sm[i] == int(np.argmax(got[i]))
+        assert om.greedy_ok(want[i], int(sm[i]), MODEL_TOL)
+    model.close()
+    pool.close()
+
+
+def test_engine_model_end_to_end_tokens(dbk):
+    """The engine in full-model mode with host_tokens: each step reads the decode rows' token
+    ids from the caller's pinned array and writes their greedy samples back (4 B per row each
+    way).  The first decode step (synthetic history only) is checked against O8 with the
+    caller's initial tokens; every decision replays bit-exactly."""
+    c = configs.CONFIGS["toy"]
+    tr = trace.make_trace(8, 40, 20, 128, seed=2, dist="uniform")
+    L, Hq, Hkv, d, V = 2, 8, 8, 64, 700
+    s = om.ModelShape(layers=L, q_heads=Hq, kv_heads=Hkv, head_dim=d, hidden=512, ffn=512, vocab=V)
+    cap_pages = 256
+    beta = 2 * L * Hkv * d * 2
+    mem_cap = cap_pages * P * beta
+    pr = configs.prior_record(c)
+    kw = dict(policy=opol.STATIC, b_static=8, b_min=1, b_max=8, b0=8, eps_m=0.02, bytes_per_token=beta,
+              page_size=P, refresh_steps=5, w_len=16, w_sla=4, alpha=4, delta=1, d_sla_ms=50.0, eps_d_ms=0.01)
+    sched = dbk.Scheduler(prior=tuple(pr.values()), **kw)
+    pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, 10, 16, "f16")
+    model = dbk.Model(pool, 512, 512, V, max_pos=256, weight_seed=9)
+    seed = 31
+    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap, seed=seed, out_dtype=2)
+    eng.attach_model(model)
+    qd = torch.empty(L, 10, Hq, d, dtype=torch.float16, device="cuda")
+    od = torch.empty(L, 10, Hq, d, dtype=torch.float32, device="cuda")
+    host_tok = torch.tensor([(7 * i + 3) % V for i in range(len(tr))], dtype=torch.int32).pin_memory()
+    init = host_tok.clone().numpy()
+    bufs = eng.buffers(qd, od, host_tokens=host_tok)
+    rp = oeng.Replay([oeng.RankEngine(list(range(len(tr))), tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P)],
+                     opol.SchedConfig(prior=tuple(pr.values()), **kw), mem_cap)
+    first = True
+    while not eng.done():
+        g = eng.step(bufs)
+        o = rp.step(g["step_ns"])
+        for k in ("b_t", "b_next", "n_admitted", "n_preempted", "n_decode", "n_finished", "sum_ctx", "used_pages"):
+            assert g[k] == o[k], (k, g[k], o[k])
+        assert g["h2d_bytes"] == 4 * g["n_decode"] and g["d2h_bytes"] == 4 * g["n_decode"]
+        if first and g["n_decode"]:
+            bid, bctx = eng.last_batch()
+            # the step's logits are in the model's internal buffer; recompute the samples' validity
+            want, _, _, _ = om.decode_step(s, 9, seed, [int(r) for r in bid], [int(x) for x in bctx],
+                                           tokens=[int(init[int(r)]) for r in bid])
+            samples = host_tok.numpy()[[int(r) for r in bid]]
+            for i in range(len(bid)):
+                assert om.greedy_ok(want[i], int(samples[i]), MODEL_TOL)
+            first = False
+    assert rp.done() and not first
+    assert np.all((host_tok.numpy() >= 0) & (host_tok.numpy() < V))
+    eng.close()
+    model.close()
+    pool.close()
