@@ -206,8 +206,9 @@ def run_steps(S, k, bufs, stream, comm_world=1, dist=None):
     return recs, e0.elapsed_time(e1)
 
 
-def cpu_baseline(S, budget_s=15.0, threads=None):
-    """The oracle (plain C, fp64) on a bounded sample of the current decode batch."""
+def cpu_baseline(S, budget_s=15.0, threads=None, single_budget_s=5.0):
+    """The oracle (plain C, fp64) on a bounded sample of the current decode batch: all host
+    cores, and one thread (SURVEY.md §8(d) "1 thread and nproc threads")."""
     from oracle import attention as oatt
     c = S["c"]
     L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
@@ -225,17 +226,25 @@ def cpu_baseline(S, budget_s=15.0, threads=None):
         nxt += np_
     bt, pk, pv, qq = oatt.synth_paged_batch(S["seed"], [int(x) for x in ids[sel]], ctx[sel], pages, 0,
                                             Hq, Hkv, d, P, "f16")
-    secs, reps = 0.0, 0
-    while secs < budget_s:
-        t0 = time.perf_counter()
-        oatt.paged_decode_attention(ctx[sel], bt, pk, pv, qq, "f16", nthreads=threads)
-        secs += time.perf_counter() - t0
-        reps += 1
+
+    def timed(nth, budget):
+        secs, reps = 0.0, 0
+        while secs < budget:
+            t0 = time.perf_counter()
+            oatt.paged_decode_attention(ctx[sel], bt, pk, pv, qq, "f16", nthreads=nth)
+            secs += time.perf_counter() - t0
+            reps += 1
+        return secs, reps
+    secs, reps = timed(threads, budget_s)
+    s1, r1 = timed(1, single_budget_s)
+    kv_bytes = float(np.sum(ctx[sel])) * 2 * Hkv * d * 2   # the KV the sample reads, per repetition
     tok_s = k * reps / L / secs
     return {"value": round(tok_s, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "single_thread_value": round(k * r1 / L / s1, 3),
+            "kv_gbs_processed": round(kv_bytes * reps / secs / 1e9, 3),
             "sample": f"{k} random requests of the timed batch (mean ctx {float(np.mean(ctx[sel])):.0f}) x "
-                      f"1 layer, fp64 paged attention, {reps} repetitions in {secs:.1f} s; tokens/s = "
-                      f"request-layers / L / time"}
+                      f"1 layer, fp64 paged attention, {reps} repetitions in {secs:.1f} s on {threads} threads "
+                      f"({r1} in {s1:.1f} s on 1 thread); tokens/s = request-layers / L / time"}
 
 
 def _make_comm(dbk, dist, world, rank, local):
