@@ -87,6 +87,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/prefill_bench.json")
     ap.add_argument("--shape", type=int, default=-1, help="run only this shape index")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--dtypes", default="f16,bf16", help="KV / q dtypes (the bench configs are fp16)")
     a = ap.parse_args()
     import torch
 
@@ -103,11 +104,13 @@ def main():
     rows = []
     if a.shape >= 0:
         shapes = [shapes[a.shape]]
-    for s in shapes:
-        r = run_shape(dbk, torch, *s, reps=a.reps)
-        r["frac_of_peak"] = r["tflops"] / peak
-        rows.append(r)
-        print(json.dumps(r), flush=True)
+    for dt in a.dtypes.split(","):
+        for s in shapes:
+            r = run_shape(dbk, torch, *s, reps=a.reps, dtype=dt)
+            r["dtype"] = dt
+            r["frac_of_peak"] = r["tflops"] / peak
+            rows.append(r)
+            print(json.dumps(r), flush=True)
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(dict(peak_tflops=peak, peak_source=src, rows=rows), f, indent=1)
