@@ -198,6 +198,60 @@ def pd_table(cfg="llama2-7b", bs=(64, 128, 256), full_model=False):
     return dict(config=cfg, full_model=full_model, rows=rows)
 
 
+def surge_table(cfg="surge-7b-dp", lam0=None, bs=(64, 128, 256), policies=("memory", "combined"),
+                d_sla=20.0, eps_d=0.8):
+    """BASELINE configs[4] analog on one GPU (one DP rank's share, its own 40 GB KV cap): a
+    piecewise-Poisson surge -- lambda0 for 60 s, 2.5 lambda0 for 30 s, lambda0 for 60 s,
+    lambda0 sized so the steady state holds ~60 % of the cap (Little: N = 0.6 eta / E[ctx],
+    lifetime = l_out steps of tau(N) from the Fig. 3 fit) -- through static b vs the dynamic
+    rules.  Reports tokens/s, preemptions, peak KV occupancy, p99 TBT and scheduling delay."""
+    import gc
+
+    import torch
+    from synth import configs, trace
+    c = configs.CONFIGS[cfg]
+    t = c["trace"]
+    beta = configs.kv_bytes_per_token(c)
+    eta = c["cap_bytes_per_gpu"] // beta
+    e_ctx = t["mean_in"] + t["mean_out"] / 2
+    n_conc = 0.6 * eta / e_ctx
+    if lam0 is None:
+        tau_ms = 0.63 + 0.0305 * n_conc          # attention-only Fig. 3 fit (7B), profiles/r01_paper_tables.json
+        lam0 = n_conc / (t["mean_out"] * tau_ms / 1e3)
+    segs = [(0, lam0), (60000, 2.5 * lam0), (90000, lam0)]
+    n = int(lam0 * 60 + 2.5 * lam0 * 30 + lam0 * 60)
+    tr = trace.make_trace(n, t["mean_in"], t["mean_out"], t["L_max"], t["seed"], dist=t["dist"],
+                          arrival="piecewise", segments=segs)
+    rows = []
+    runs = [("static", b) for b in bs] + [(p, None) for p in policies]
+    for pol, b in runs:
+        gc.collect()
+        torch.cuda.empty_cache()
+        S = bench.setup_engine(cfg_name=cfg, policy=pol, b_static=b or 256, time_attention=False,
+                               trace_override=tr, sla_ms=d_sla, eps_d_ms=eps_d)
+        eng = S["eng"]
+        bufs = eng.buffers(S["qd"], S["od"])
+        t0 = time.time()
+        recs, ms = bench.run_steps(S, 10 ** 9, bufs, torch.cuda.current_stream())
+        adm, fin = eng.request_times()
+        dev_s = sum(r["step_ns"] for r in recs) / 1e9
+        clock_s = (recs[-1]["clock_ns"] + recs[-1]["step_ns"]) / 1e9
+        rows.append(dict(policy=pol, b_static=b, steps=len(recs), tokens=int(sum(r["n_decode"] for r in recs)),
+                         tokens_per_s_device=sum(r["n_decode"] for r in recs) / dev_s,
+                         makespan_s=clock_s, preemptions=int(sum(r["n_preempted"] for r in recs)),
+                         peak_pages=int(max(r["used_pages"] for r in recs)), cap_pages=S["cap_pages"],
+                         p99_tbt_ms=_tbt_p99(recs), median_sched_delay_s=float(np.median(adm - tr.arrival_ns)) / 1e9,
+                         p99_sched_delay_s=float(np.percentile(adm - tr.arrival_ns, 99)) / 1e9,
+                         mean_b=float(np.mean([r["b_t"] for r in recs])), wall_s=time.time() - t0))
+        print(json.dumps(rows[-1]), flush=True)
+        S["eng"].close()
+        S["pool"].close()
+        S.clear()
+        del eng, bufs
+    return dict(config=cfg, lambda0_qps=lam0, segments=segs, n_requests=n, d_sla_ms=d_sla, eps_d_ms=eps_d,
+                rows=rows)
+
+
 def swap_table(cfg="llama2-7b", kv_gb=40.0, swap_gb=16.0, n_req=1500, b=256):
     """Whole trace (all-at-once) near the KV cap: recompute vs swap preemption (static b) and
     the memory-aware rule.  In this attention-only engine a recompute is the KV fill of the
@@ -244,6 +298,7 @@ def main():
     ap.add_argument("--capacity", action="store_true")
     ap.add_argument("--pd", action="store_true")
     ap.add_argument("--swap", action="store_true")
+    ap.add_argument("--surge", action="store_true", help="configs[4]: traffic surge near the KV cap")
     ap.add_argument("--pd-model", action="store_true", help="PD table with prefill through the full model")
     ap.add_argument("--model", action="store_true", help="--fig3/--table1/--sla with the full decode step")
     ap.add_argument("--cap-lo", type=float, default=10.0, help="capacity bisection: lowest rate (qps)")
@@ -276,6 +331,9 @@ def main():
         save()
     if a.swap:
         res["swap"] = swap_table()
+        save()
+    if a.surge:
+        res["surge"] = surge_table()
         save()
     if a.sla or a.capacity:
         res["fig3_13b"] = fig3("llama2-13b-sla", bs=(32, 64, 128, 256))
