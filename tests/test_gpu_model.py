@@ -333,3 +333,34 @@ def test_engine_model_end_to_end_tokens(dbk):
     eng.close()
     model.close()
     pool.close()
+
+
+def test_model_edge_cases(dbk):
+    """Empty step, too many rows, positions past the RoPE table, unsupported configs."""
+    s = om.ModelShape(layers=1, q_heads=4, kv_heads=4, head_dim=64, hidden=256, ffn=256, vocab=100)
+    pool, model, ids, ref = _setup(dbk, s, [5, 9], 1, 2)
+    model.step([])                                     # n = 0: no-op
+    pool.reserve_tokens(ids, [1, 1])
+    with pytest.raises(dbk.DbkError):                  # a chunk of 3 rows + 2 decode rows > 4 slots
+        pool.request_begin(77, 3, 1)
+        pool.reserve_tokens([77], [3])
+        model.step_pd(ids, [77], [0], [3])
+    model.close()
+    pool.close()
+    pool = dbk.KVPool(1, 4, 4, 64, 16, 4, 8, "f16")
+    small = dbk.Model(pool, 256, 256, 100, max_pos=8, weight_seed=1)
+    pool.request_begin(1, 8, 8)
+    pool.append_tokens([1], [8], seed=1)
+    pool.reserve_tokens([1], [1])                      # position 8 >= max_pos
+    with pytest.raises(dbk.DbkError):
+        small.step([1])
+    small.close()
+    pool.close()
+    bpool = dbk.KVPool(1, 4, 4, 64, 16, 4, 8, "bf16")
+    with pytest.raises(dbk.DbkError):                  # the model path is fp16
+        dbk.Model(bpool, 256, 256, 100)
+    bpool.close()
+    fpool = dbk.KVPool(1, 4, 4, 64, 16, 4, 8, "f16")
+    with pytest.raises(dbk.DbkError):                  # hidden must be a multiple of 128
+        dbk.Model(fpool, 200, 256, 100)
+    fpool.close()
