@@ -299,6 +299,7 @@ def main():
     ap.add_argument("--pd", action="store_true")
     ap.add_argument("--swap", action="store_true")
     ap.add_argument("--surge", action="store_true", help="configs[4]: traffic surge near the KV cap")
+    ap.add_argument("--surge-lam0", type=float, default=None, help="base rate (qps); default from Little's law")
     ap.add_argument("--pd-model", action="store_true", help="PD table with prefill through the full model")
     ap.add_argument("--model", action="store_true", help="--fig3/--table1/--sla with the full decode step")
     ap.add_argument("--cap-lo", type=float, default=10.0, help="capacity bisection: lowest rate (qps)")
@@ -333,7 +334,7 @@ def main():
         res["swap"] = swap_table()
         save()
     if a.surge:
-        res["surge"] = surge_table()
+        res["surge"] = surge_table(lam0=a.surge_lam0)
         save()
     if a.sla or a.capacity:
         res["fig3_13b"] = fig3("llama2-13b-sla", bs=(32, 64, 128, 256))

@@ -104,6 +104,30 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): one instruction for two lanes of work.
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t r, float &a, float &b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // one {64 elements x 16 tokens} box (2 KiB) of the (page, kv head) tile: d-half h of K or V
@@ -279,21 +303,18 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
             tmem_ld32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
             tmem_ld_wait();
             float s[64];
-            float bmax = -INFINITY;
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
             const int vis = row_ok ? p_row - b * kBK : -1;  // keys k <= vis of this block are visible
             if (vis >= kBK - 1) {
 #pragma unroll
-                for (int k = 0; k < 64; ++k) {
-                    s[k] = __uint_as_float(u[k]);
-                    bmax = fmaxf(bmax, s[k]);
-                }
+                for (int k = 0; k < 64; ++k) s[k] = __uint_as_float(u[k]);
             } else {
 #pragma unroll
-                for (int k = 0; k < 64; ++k) {
-                    s[k] = k <= vis ? __uint_as_float(u[k]) : -INFINITY;
-                    bmax = fmaxf(bmax, s[k]);
-                }
+                for (int k = 0; k < 64; ++k) s[k] = k <= vis ? __uint_as_float(u[k]) : -INFINITY;
             }
+#pragma unroll
+            for (int k = 0; k < 64; k += 2) mx[(k >> 1) & 3] = fmax3(mx[(k >> 1) & 3], s[k], s[k + 1]);
+            const float bmax = fmaxf(fmax3(mx[0], mx[1], mx[2]), mx[3]);
             const float m_new = fmaxf(M, bmax * c_log2);
             const bool grow = m_new > M + 8.f;  // rescale only when the max grows by > 2^8
             if (b > 0 && __any_sync(kFull, grow)) {
@@ -318,21 +339,26 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
             // 32..63.  bf16: hi = P truncated to its top 16 bits (one byte permute per pair),
             // lo = the exact fp32 remainder rounded to bf16 -- ~17 significant bits in all.
             const float nm = (M == -INFINITY) ? 0.f : -M;
-            float La = 0.f, Lb = 0.f;
+            const uint64_t c2 = f2_pack(c_log2, c_log2), nm2 = f2_pack(nm, nm);
+            uint64_t L2 = f2_pack(0.f, 0.f);
 #pragma unroll
             for (int k0 = 0; k0 < 64; k0 += 32) {
                 uint32_t hi[16], lo[16];
 #pragma unroll
                 for (int k = 0; k < 32; k += 2) {
-                    const float p0 = ex2_approx(fmaf(s[k0 + k], c_log2, nm));
-                    const float p1 = ex2_approx(fmaf(s[k0 + k + 1], c_log2, nm));
-                    La += p0;
-                    Lb += p1;
+                    float x0, x1, p0, p1;
+                    f2_unpack(ffma2(f2_pack(s[k0 + k], s[k0 + k + 1]), c2, nm2), x0, x1);
+                    p0 = ex2_approx(x0);
+                    p1 = ex2_approx(x1);
+                    const uint64_t pp = f2_pack(p0, p1);
+                    L2 = fadd2(L2, pp);
                     if constexpr (kBF16) {
                         const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);
                         hi[k >> 1] = __byte_perm(u0, u1, 0x7632);
-                        lo[k >> 1] = Elt<T>::from_f2(p0 - __uint_as_float(u0 & 0xFFFF0000u),
-                                                     p1 - __uint_as_float(u1 & 0xFFFF0000u));
+                        float r0, r1;
+                        f2_unpack(fadd2(pp, f2_pack(-__uint_as_float(u0 & 0xFFFF0000u), -__uint_as_float(u1 & 0xFFFF0000u))),
+                                  r0, r1);
+                        lo[k >> 1] = Elt<T>::from_f2(r0, r1);
                     } else {
                         hi[k >> 1] = Elt<T>::from_f2(p0, p1);
                     }
@@ -340,6 +366,8 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
                 tmem_st16(ts + (k0 >> 1), hi);
                 if constexpr (kBF16) tmem_st16(ts + 32 + (k0 >> 1), lo);
             }
+            float La, Lb;
+            f2_unpack(L2, La, Lb);
             if (zero_tail && b == n_blk - 1) {
                 uint8_t *vt = ring + (b % STG) * STAGE + NBOX * HALF;
                 const int v0 = n_keys & (kBK - 1);
