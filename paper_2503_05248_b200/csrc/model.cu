@@ -492,7 +492,6 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
         if (it->second.ctx < 1) return fail(DBK_EINVAL, "model_step: request without a reserved decode token");
         m->rows_h.push_back({ids[i], it->second.slot, it->second.ctx - 1});
     }
-    int64_t chunk_rows = 0;
     for (int32_t c = 0; c < nch; ++c) {
         auto it = p->reqs.find(chunks->req_ids[c]);
         if (it == p->reqs.end())
@@ -501,7 +500,6 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
         if (s0 < 0 || len < 1 || static_cast<int64_t>(s0) + len > it->second.ctx)
             return fail(DBK_EINVAL, "model_step: chunk %d outside the reserved tokens", c);
         for (int32_t j = 0; j < len; ++j) m->rows_h.push_back({chunks->req_ids[c], it->second.slot, s0 + j});
-        chunk_rows += len;
     }
     const int R = static_cast<int>(m->rows_h.size());
     if (R == 0) return DBK_OK;
@@ -563,7 +561,6 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
     DBK_CUDA(cudaEventRecord(m->ev1, s));
     m->pending = true;
     p->n_launches += 1;  // the embedding + first norm
-    (void)chunk_rows;
     return DBK_OK;
 }
 
