@@ -312,10 +312,11 @@ def run_gpu(args):
         recs, ms = run_steps(S, args.steps, bufs, stream, dist=dist)
     att_ms, att_launches, att_bytes = eng.attn_timing(reset=True)
     info = S["pool"].info()
-    # decode tokens of the whole job: DP shards are disjoint (sum over ranks); TP ranks
-    # serve the same requests (count once)
+    # decode tokens of the whole job: every rank's step record carries the GLOBAL counts (the
+    # exchanged, reduced record: DP sums the disjoint shards, TP ranks serve the same requests),
+    # so each rank contributes 1/world of it to the all-reduce
     ms_t = torch.tensor([ms], device="cuda")
-    tok_t = torch.tensor([float(sum(r["n_decode"] for r in recs)) / (world if tp > 1 else 1)], device="cuda")
+    tok_t = torch.tensor([float(sum(r["n_decode"] for r in recs)) / world], device="cuda")
     if dist is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tok_t)
@@ -332,7 +333,7 @@ def run_gpu(args):
         run_steps(S, 2, ebufs, stream, dist=dist)
         erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
         ems_t = torch.tensor([ems], device="cuda")
-        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / (world if tp > 1 else 1)], device="cuda")
+        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / world], device="cuda")
         if dist is not None:
             dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
             dist.all_reduce(etok_t)
@@ -342,7 +343,7 @@ def run_gpu(args):
         run_steps(S, 2, ebufs, stream, dist=dist)
         erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
         ems_t = torch.tensor([ems], device="cuda")
-        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / (world if tp > 1 else 1)], device="cuda")
+        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / world], device="cuda")
         if dist is not None:
             dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
             dist.all_reduce(etok_t)
@@ -362,6 +363,9 @@ def run_gpu(args):
             traffic, _ = ncu_traffic()
         c = S["c"]
         n_steps = len(recs)
+        # the decode tokens these steps could emit if every step only streamed its KV at `peak`
+        kv_s = sum(r["sum_ctx"] for r in recs) * S["beta"] / (world if tp == 1 else 1) / (peak * 1e9)
+        tok_roof = (toks / kv_s) if kv_s > 0 else 0.0
         kname = "decode_gqa_kernel (K2, tensor cores)" if info["decode_path"] == 2 else \
             "decode_kernel (K1, paged decode attention)"
         line = {
@@ -392,7 +396,10 @@ def run_gpu(args):
                          "ms_per_launch": round(att_ms / max(att_launches, 1), 4), "peak_source": peak_src,
                          "share_of_step": round(att_ms / max(ms, 1e-9), 4), "ctas_per_sm": info["ctas_per_sm"],
                          "chunk_pages": info["chunk_pages"], "read_probe_gbs": round(probe_gbs, 1),
-                         "frac_of_read_probe": round(achieved / probe_gbs, 4)},
+                         "frac_of_read_probe": round(achieved / probe_gbs, 4),
+                         # tokens/s roofline = BW * n / (sum_i ctx_i * beta) per step
+                         "tokens_per_s_at_peak": round(tok_roof, 1),
+                         "tokens_frac_of_roofline": round(toks / (ms_max / 1e3) / tok_roof, 4) if tok_roof else None},
             "e2e": {"value": round(float(etok_t.item()) / (float(ems_t.item()) / 1e3), 2), "unit": UNIT,
                     "h2d_bytes_per_step": int(np.mean([r["h2d_bytes"] for r in erecs])) if erecs else 0,
                     "d2h_bytes_per_step": int(np.mean([r["d2h_bytes"] for r in erecs])) if erecs else 0}
