@@ -140,24 +140,31 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const __half *qkv, const R
     const __half *row = qkv + static_cast<size_t>(i) * nqkv;
     const float2 *csr = cs + static_cast<size_t>(p) * half_d;
     uint8_t *pg = kv_layer + static_cast<int64_t>(page) * page_stride;
-    // rotated heads: Hq q heads then Hkv k heads, two pairs per thread-iteration
-    const int rot_items = (Hq + Hkv) * half_d / 2;
+    // rotated heads: Hq q heads then Hkv k heads, eight pairs (16-byte loads/stores) per item
+    const int rot_items = (Hq + Hkv) * half_d / 8;
     for (int t = threadIdx.x; t < rot_items; t += blockDim.x) {
-        const int hh = (2 * t) / half_d, j = (2 * t) % half_d;
+        const int hh = (8 * t) / half_d, j = (8 * t) % half_d;
         const __half *src = row + hh * d;
-        const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(src + j));
-        const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(src + j + half_d));
-        const float2 c0 = csr[j], c1 = csr[j + 1];
-        const __half2 lo = __floats2half2_rn(a.x * c0.x - b.x * c0.y, a.y * c1.x - b.y * c1.y);
-        const __half2 hi = __floats2half2_rn(b.x * c0.x + a.x * c0.y, b.y * c1.x + a.y * c1.y);
+        float a[8], b[8], o_lo[8], o_hi[8];
+        unpack8<__half>(*reinterpret_cast<const uint4 *>(src + j), a);
+        unpack8<__half>(*reinterpret_cast<const uint4 *>(src + j + half_d), b);
+        const float4 *c4 = reinterpret_cast<const float4 *>(csr + j);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float4 c = c4[e];  // (cos, sin) of pairs j + 2e and j + 2e + 1
+            o_lo[2 * e] = a[2 * e] * c.x - b[2 * e] * c.y;
+            o_hi[2 * e] = b[2 * e] * c.x + a[2 * e] * c.y;
+            o_lo[2 * e + 1] = a[2 * e + 1] * c.z - b[2 * e + 1] * c.w;
+            o_hi[2 * e + 1] = b[2 * e + 1] * c.z + a[2 * e + 1] * c.w;
+        }
         __half *dst;
         if (hh < Hq) {
             dst = q_out + (static_cast<size_t>(i) * Hq + hh) * d;
         } else {
             dst = reinterpret_cast<__half *>(pg + (hh - Hq) * tile_bytes) + (p % kP) * d;  // K row
         }
-        *reinterpret_cast<__half2 *>(dst + j) = lo;
-        *reinterpret_cast<__half2 *>(dst + j + half_d) = hi;
+        *reinterpret_cast<uint4 *>(dst + j) = pack8<__half>(o_lo);
+        *reinterpret_cast<uint4 *>(dst + j + half_d) = pack8<__half>(o_hi);
     }
     // v heads: plain copy into the V rows, 16 B per thread
     const int vv = Hkv * d / 8;

@@ -404,3 +404,42 @@ def test_sla_binding_full_size_replay(dbk):
     # (running requests are never evicted by the SLA rule -- Alg. 2 line 16 clamps b >= N^d --
     # so the step time only falls as they finish; the replay above checks every decision)
     _free(S)
+
+
+@pytest.mark.parametrize("tp", [1, 8])
+def test_gqa_bench_config_sampled_parity(dbk, tp):
+    """The 70B GQA bench launch configuration (K2 on tensor cores, 120 GB per-GPU cap, batch
+    up to 1024; tp = 8: rank 0's KV-head shard, 8 q-heads of 1 kv head): decisions replayed
+    bit-exactly, then sampled (request, layer) outputs of the last step vs the oracle from
+    logical coordinates."""
+    import gc
+
+    import bench
+    gc.collect()
+    torch.cuda.empty_cache()
+    S = bench.setup_engine(device=0, cfg_name="llama3-70b-gqa", time_attention=True, out_dtype=2, n_req=2000,
+                           tp=tp)
+    assert S["pool"].info()["decode_path"] == 2
+    eng = S["eng"]
+    bufs = eng.buffers(S["qd"], S["od"])
+    stream = torch.cuda.current_stream()
+    recs = [eng.step(bufs, stream) for _ in range(30)]
+    torch.cuda.synchronize()
+    _replay_full_size(S, recs)
+    L, Hq, Hkv, d, P = S["L"], S["Hq"], S["Hkv"], S["d"], 16
+    ids, ctx = eng.last_batch()
+    assert recs[-1]["n_decode"] == len(ids) and len(ids) > 500
+    rng = np.random.default_rng(7)
+    sel = rng.choice(len(ids), size=8, replace=False)
+    for lay in (0, L - 1):
+        pages, nxt = [], 0
+        for cx in ctx[sel]:
+            m = -(-int(cx) // P)
+            pages.append(list(range(nxt, nxt + m)))
+            nxt += m
+        bt, pk, pv, qq = oatt.synth_paged_batch(S["seed"], [int(x) for x in ids[sel]], ctx[sel], pages, lay,
+                                                Hq, Hkv, d, P, "f16")
+        want = oatt.paged_decode_attention(ctx[sel], bt, pk, pv, qq, "f16", nthreads=8)
+        got = S["od"][lay, torch.as_tensor(sel, device="cuda")].cpu().numpy().astype(np.float64)
+        assert row_err(got, want) <= TOL
+    _free(S)
