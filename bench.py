@@ -177,6 +177,7 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     od = torch.empty(L, max_req, Hq, d, dtype=et, device=f"cuda:{device}")
     kvd = torch.empty(2, max_req, L, Hkv, d, dtype=torch.float16, device=f"cuda:{device}")
     return dict(dbk=dbk, c=c, tr=tr, pool=pool, sched=sched, eng=eng, qd=qd, od=od, kvd=kvd, tp=tp, model=model,
+                policy=policy, b_static=b_static, sla_ms=sla_ms, eps_d_ms=eps_d_ms,
                 cap_pages=cap_pages, beta=beta, max_req=max_req, mem_cap_total=mem_cap_total, seed=seed,
                 L=L, Hq=Hq, Hkv=Hkv, d=d)
 
@@ -204,6 +205,29 @@ def run_steps(S, k, bufs, stream, comm_world=1, dist=None):
     if dist is not None:
         dist.barrier()
     return recs, e0.elapsed_time(e1)
+
+
+def oracle_sched_replay(S, recs):
+    """The oracle's scheduler replay (O7: allocator + Alg. 1 / Alg. 2, Python) of the first
+    steps of this very run from their logged step times: host time per step at full scale
+    (SURVEY.md §8(d)), and whether every decision agreed bit for bit."""
+    from oracle import engine as oeng
+    from oracle import policy as opol
+    if not recs or S.get("tp", 1) != 1:
+        return {}
+    c, tr, P = S["c"], S["tr"], S["c"]["page_size"]
+    kw = sched_kwargs(c, S["beta"], S.get("policy"), S.get("b_static", 256), S.get("sla_ms"), S.get("eps_d_ms"))
+    rp = oeng.Replay([oeng.RankEngine(list(range(len(tr))), tr.arrival_ns, tr.l_in, tr.l_out, S["cap_pages"], P)],
+                     opol.SchedConfig(**kw), S["mem_cap_total"])
+    agree = True
+    t0 = time.perf_counter()
+    for g in recs:
+        o = rp.step(g["step_ns"])
+        agree &= all(g[k] == o[k] for k in ("b_t", "b_next", "n_admitted", "n_preempted", "n_decode", "sum_ctx",
+                                            "used_pages"))
+    dt = time.perf_counter() - t0
+    return {"sched_replay_ms_per_step": round(dt / len(recs) * 1e3, 3), "sched_replay_steps": len(recs),
+            "sched_replay_bit_exact": bool(agree)}
 
 
 def cpu_baseline(S, budget_s=15.0, threads=None, single_budget_s=5.0):
@@ -305,7 +329,7 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     bufs = eng.buffers(S["qd"], S["od"])
     # fast-forward to the steady state (untimed), then W warm-up steps (untimed)
-    run_steps(S, args.ff, bufs, stream, dist=dist)
+    ff_recs, _ = run_steps(S, args.ff, bufs, stream, dist=dist)
     run_steps(S, args.warmup, bufs, stream, dist=dist)
     eng.attn_timing(reset=True)
     with ClockSampler(local) as clk:
@@ -416,6 +440,7 @@ def run_gpu(args):
             line["attention_share_of_step"] = line["roofline"]["share_of_step"]
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(S)
+            line["cpu_baseline"].update(oracle_sched_replay(S, ff_recs[:60]))
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
