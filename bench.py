@@ -292,11 +292,20 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # test harness only (tests/test_gpu_bench_multirank.py): every rank on cuda:0 with a gloo
+    # process group, so the N > 1 bookkeeping of this script runs on a one-GPU box
+    gloo_test = os.environ.get("DBK_BENCH_TEST_GLOO") == "1"
+    if gloo_test:
+        local = 0
+    red = "cpu" if gloo_test else "cuda"  # device of the timing / token all-reduces
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # configs[3] (70B GQA) is sharded by KV heads (TP); the others by requests (DP)
     tp = world if args.config == "llama3-70b-gqa" else 1
     if args.tp_shard:  # one GPU runs exactly rank 0's share of a KV-head TP run of that width
@@ -311,6 +320,8 @@ def run_gpu(args):
     if world > 1:
         mode = dbk._lib.MODE_TP if tp > 1 else dbk._lib.MODE_DP
         try:  # libdbk's own NCCL communicator (ncclAllGather of the records inside the engine step)
+            if gloo_test:
+                raise RuntimeError("gloo test harness: no NCCL between ranks sharing one GPU")
             comm = _make_comm(dbk, dist, world, rank, local)
             dbk._lib.dbk_engine_attach_comm(eng.h, comm, mode)
             exchange_kind = "libdbk NCCL all-gather"
@@ -320,12 +331,13 @@ def run_gpu(args):
             fields = dbk._lib.STATS_FIELDS
 
             def exchange(local_rec):
-                t = torch.tensor([local_rec[f] for f in fields], dtype=torch.int64, device="cuda")
+                t = torch.tensor([local_rec[f] for f in fields], dtype=torch.int64, device=red)
                 out = [torch.zeros_like(t) for _ in range(world)]
                 dist.all_gather(out, t)
                 return dbk.stats_reduce([dict(zip(fields, o.tolist())) for o in out], mode)
             S["exchange"] = exchange
-            exchange_kind = "torch.distributed NCCL all-gather"
+            exchange_kind = "torch.distributed gloo all-gather (test harness)" if gloo_test else \
+                "torch.distributed NCCL all-gather"
     stream = torch.cuda.current_stream()
     bufs = eng.buffers(S["qd"], S["od"])
     # fast-forward to the steady state (untimed), then W warm-up steps (untimed)
@@ -339,8 +351,8 @@ def run_gpu(args):
     # decode tokens of the whole job: every rank's step record carries the GLOBAL counts (the
     # exchanged, reduced record: DP sums the disjoint shards, TP ranks serve the same requests),
     # so each rank contributes 1/world of it to the all-reduce
-    ms_t = torch.tensor([ms], device="cuda")
-    tok_t = torch.tensor([float(sum(r["n_decode"] for r in recs)) / world], device="cuda")
+    ms_t = torch.tensor([ms], device=red)
+    tok_t = torch.tensor([float(sum(r["n_decode"] for r in recs)) / world], device=red)
     if dist is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tok_t)
@@ -356,8 +368,8 @@ def run_gpu(args):
         ebufs = eng.buffers(S["qd"], S["od"], S["kvd"], hq, hk, hv, ho)
         run_steps(S, 2, ebufs, stream, dist=dist)
         erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
-        ems_t = torch.tensor([ems], device="cuda")
-        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / world], device="cuda")
+        ems_t = torch.tensor([ems], device=red)
+        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / world], device=red)
         if dist is not None:
             dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
             dist.all_reduce(etok_t)
@@ -366,8 +378,8 @@ def run_gpu(args):
         ebufs = eng.buffers(S["qd"], S["od"], host_tokens=host_tok)
         run_steps(S, 2, ebufs, stream, dist=dist)
         erecs, ems = run_steps(S, args.steps, ebufs, stream, dist=dist)
-        ems_t = torch.tensor([ems], device="cuda")
-        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / world], device="cuda")
+        ems_t = torch.tensor([ems], device=red)
+        etok_t = torch.tensor([float(sum(r["n_decode"] for r in erecs)) / world], device=red)
         if dist is not None:
             dist.all_reduce(ems_t, op=dist.ReduceOp.MAX)
             dist.all_reduce(etok_t)
