@@ -153,3 +153,11 @@ def test_prefill_matches_torch_causal_attention():
     g, u = F.linear(h2, T(W["w_gu"])).split(s.ffn, dim=-1)
     x2 = x1 + F.linear(F.silu(g) * u, T(W["w_down"]))
     assert np.allclose(x, x2.numpy(), rtol=1e-12, atol=1e-12)
+
+
+def test_greedy_ok_rule():
+    row = np.array([0.5, 2.0, 1.999, -3.0])
+    assert om.greedy_ok(row, 1, 2e-3)                 # the argmax
+    assert om.greedy_ok(row, 2, 2e-3)                 # within 2e-3 * max|logit| = 6e-3 of it
+    assert not om.greedy_ok(row, 0, 2e-3)
+    assert not om.greedy_ok(row, 4, 2e-3) and not om.greedy_ok(row, -1, 2e-3)
