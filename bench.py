@@ -175,7 +175,7 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     et = torch.float32 if out_dtype == 2 else torch.float16
     qd = torch.empty(L, max_req, Hq, d, dtype=torch.float16, device=f"cuda:{device}")
     od = torch.empty(L, max_req, Hq, d, dtype=et, device=f"cuda:{device}")
-    kvd = torch.empty(2, max_req, L, Hkv, d, dtype=torch.float16, device=f"cuda:{device}")
+    kvd = torch.empty(2, L, max_req, Hkv, d, dtype=torch.float16, device=f"cuda:{device}")
     return dict(dbk=dbk, c=c, tr=tr, pool=pool, sched=sched, eng=eng, qd=qd, od=od, kvd=kvd, tp=tp, model=model,
                 policy=policy, b_static=b_static, sla_ms=sla_ms, eps_d_ms=eps_d_ms,
                 cap_pages=cap_pages, beta=beta, max_req=max_req, mem_cap_total=mem_cap_total, seed=seed,

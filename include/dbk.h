@@ -395,11 +395,12 @@ typedef struct dbk_engine dbk_engine;
  * token's K/V with the synthetic generator.  With PD fusion the prefill
  * chunk's rows follow the decode rows in q_dev / out_dev: decode rows
  * [0, N^d), chunk rows [N^d, N^d + c_t) (c_t is clamped to max_requests - N^d).  End-to-end mode: host_q
- * [layers][n][q_heads][d], host_k / host_v [n][layers][kv_heads][d] (pinned
- * host, kv_dtype) are copied H2D into q_dev / kv_dev each step and out is
- * copied D2H into host_out [layers][n][q_heads][d] (out_dtype).
+ * [layers][n][q_heads][d], host_k / host_v [layers][n][kv_heads][d] (pinned
+ * host, kv_dtype; layer-major, as a model produces them) are copied H2D into
+ * q_dev / kv_dev layer by layer each step and out is copied D2H into host_out
+ * [layers][n][q_heads][d] (out_dtype).
  * q_dev: [layers][max_requests][q_heads][d]; out_dev: same shape, out_dtype;
- * kv_dev: [2][max_requests][layers][kv_heads][d] (e2e only). */
+ * kv_dev: [2][layers][max_requests][kv_heads][d] (e2e only). */
 typedef struct dbk_engine_buffers {
     void *q_dev, *out_dev, *kv_dev;
     const void *host_q, *host_k, *host_v;

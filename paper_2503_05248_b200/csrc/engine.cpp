@@ -436,17 +436,19 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         // metadata uploads on `s`: host-to-device copies share the copy engine in issue order,
         // so an upload queued behind 400 MB of inputs would hold layer 0 back until they land.
         DBK_TRY(ensure_copy_streams(e));
+        // K/V rows are layer-major on both sides ([layers][rows][kv_heads][d]): one contiguous
+        // copy per layer (2-D copies of 2 KiB rows -- 70B shards -- ran far below PCIe speed)
         uint8_t *kd = static_cast<uint8_t *>(bufs->kv_dev);
         uint8_t *vd = kd + static_cast<size_t>(pc.max_requests) * kvrow;
         const size_t lrow = kvrow / pc.layers;  // one layer's K (or V) row of a request
         DBK_CUDA(cudaEventRecord(e->ev_up, s));
         DBK_CUDA(cudaStreamWaitEvent(e->h2d, e->ev_up, 0));
         for (int l = 0; l < pc.layers; ++l) {
-            const size_t off = static_cast<size_t>(l) * lrow;
-            DBK_CUDA(cudaMemcpy2DAsync(kd + off, kvrow, static_cast<const uint8_t *>(bufs->host_k) + off, kvrow,
-                                       lrow, n, cudaMemcpyHostToDevice, e->h2d));
-            DBK_CUDA(cudaMemcpy2DAsync(vd + off, kvrow, static_cast<const uint8_t *>(bufs->host_v) + off, kvrow,
-                                       lrow, n, cudaMemcpyHostToDevice, e->h2d));
+            const size_t doff = static_cast<size_t>(l) * pc.max_requests * lrow, hoff = static_cast<size_t>(l) * n * lrow;
+            DBK_CUDA(cudaMemcpyAsync(kd + doff, static_cast<const uint8_t *>(bufs->host_k) + hoff, n * lrow,
+                                     cudaMemcpyHostToDevice, e->h2d));
+            DBK_CUDA(cudaMemcpyAsync(vd + doff, static_cast<const uint8_t *>(bufs->host_v) + hoff, n * lrow,
+                                     cudaMemcpyHostToDevice, e->h2d));
             uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
             const uint8_t *qh = static_cast<const uint8_t *>(bufs->host_q) + static_cast<size_t>(l) * n * qrow;
             DBK_CUDA(cudaMemcpyAsync(qd, qh, n * qrow, cudaMemcpyHostToDevice, e->h2d));
@@ -496,7 +498,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             DBK_CUDA(cudaStreamWaitEvent(s, e->ev_q[l], 0));
             DBK_TRY(append_launch(p, bufs->kv_dev,
                                   static_cast<const uint8_t *>(bufs->kv_dev) + static_cast<size_t>(pc.max_requests) * kvrow,
-                                  0, l, 1, s));
+                                  0, l, 1, s, pc.max_requests));
         }
         if (per_layer_ev) DBK_CUDA(cudaEventRecord(e->att0[l], s));
         DBK_TRY(dbk_decode_step(p, &bt, qd, od, e->cfg.out_dtype, s));

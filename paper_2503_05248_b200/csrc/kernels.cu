@@ -39,8 +39,11 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
             synth_vals(synth_key(p.seed, 1 + kv, job.req_id, pos, layer, head, v), scale, f);
             val = pack8<T>(f);
         } else {
+            const size_t srow = p.src_layer_rows > 0
+                                    ? static_cast<size_t>(layer) * p.src_layer_rows + job.src_row + tok
+                                    : static_cast<size_t>(job.src_row + tok) * p.layers + layer;
             const T *src = reinterpret_cast<const T *>(kv ? p.v_src : p.k_src) +
-                           ((static_cast<size_t>(job.src_row + tok) * p.layers + layer) * p.kv_heads + head) * D +
+                           (srow * p.kv_heads + head) * D +
                            v * 8;
             val = __ldg(reinterpret_cast<const uint4 *>(src));
         }

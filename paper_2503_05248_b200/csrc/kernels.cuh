@@ -103,7 +103,9 @@ struct AppendParams {
     int64_t layer_stride, page_stride, tile_bytes;
     const AppendJob *jobs;
     int32_t n_jobs, layers, kv_heads;
-    const void *k_src, *v_src;   // [rows][layers][kv_heads][D] or null (synthetic)
+    const void *k_src, *v_src;   // [rows][layers][kv_heads][D] or null (synthetic); with
+                                 // src_layer_rows > 0: [layers][src_layer_rows][kv_heads][D]
+    int32_t src_layer_rows = 0;
     uint64_t seed;
     int32_t layer0 = 0;          // this launch writes layers [layer0, layer0 + n_launch_layers)
     int32_t n_launch_layers = 0; // 0 = all layers

@@ -376,7 +376,7 @@ dbk_status append_plan(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t
 // Writes layers [layer0, layer0 + nl) of the jobs planned by the last append_plan (whose job
 // list is still in up_append's device buffer).
 dbk_status append_launch(dbk_pool *p, const void *k, const void *v, uint64_t seed, int32_t layer0, int32_t nl,
-                         cudaStream_t s) {
+                         cudaStream_t s, int32_t src_layer_rows) {
     if (p->jobs.empty() || nl <= 0) return DBK_OK;
     AppendParams ap;
     ap.kv = p->kv;
@@ -392,6 +392,7 @@ dbk_status append_launch(dbk_pool *p, const void *k, const void *v, uint64_t see
     ap.seed = seed;
     ap.layer0 = layer0;
     ap.n_launch_layers = nl;
+    ap.src_layer_rows = src_layer_rows;
     DBK_CUDA(launch_append(ap, p->cfg.kv_dtype, p->cfg.head_dim, s));
     ++p->n_launches;
     return DBK_OK;

@@ -41,7 +41,7 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
 dbk_status append_plan(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok, bool explicit_rows,
                        cudaStream_t s, bool upload_jobs = true);
 dbk_status append_launch(dbk_pool *p, const void *k, const void *v, uint64_t seed, int32_t layer0, int32_t nl,
-                         cudaStream_t s);
+                         cudaStream_t s, int32_t src_layer_rows = 0);
 
 }  // namespace dbk
 

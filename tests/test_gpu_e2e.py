@@ -1,5 +1,5 @@
 """GPU parity of the engine's end-to-end mode (bench.py `e2e`): q and the step's new K/V rows
-come from pinned host memory layer by layer (per-layer 2-D copies on a copy stream, per-layer
+come from pinned host memory layer by layer (layer-major rows, one copy per layer on a copy stream, per-layer
 KV append), and every layer's output goes back to pinned host memory.
 
 The oracle side: K/V of prefilled positions from the synthetic generator, K/V of decode
@@ -87,10 +87,10 @@ def test_engine_end_to_end_mode_parity(dbk, L, Hq, Hkv, d, dtype):
         n = len(ids)
         assert g["h2d_bytes"] == n * (L * Hq * d * 2 + 2 * L * Hkv * d * 2)
         assert g["d2h_bytes"] == n * L * Hq * d * 4
-        kv_k = kb[:n * L * Hkv].reshape(n, L, Hkv, d)
-        kv_v = vb[:n * L * Hkv].reshape(n, L, Hkv, d)
+        kv_k = kb[:L * n * Hkv].reshape(L, n, Hkv, d)   # layer-major host rows
+        kv_v = vb[:L * n * Hkv].reshape(L, n, Hkv, d)
         for x in range(n):
-            over[(int(ids[x]), int(ctx[x]) - 1)] = (kv_k[x], kv_v[x])
+            over[(int(ids[x]), int(ctx[x]) - 1)] = (kv_k[:, x], kv_v[:, x])
         if n and t % 2 == 0:
             pages = [[x * maxp + p for p in range(-(-int(cx) // P))] for x, cx in enumerate(ctx)]
             got_all = ho.numpy()[:L * n * Hq * d].reshape(L, n, Hq, d).astype(np.float64)
