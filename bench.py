@@ -132,7 +132,8 @@ def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None)
 
 def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
                  out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1,
-                 trace_override=None, eps_d_ms=None, pd_fusion=False, swap_bytes=0, full_model=False):
+                 trace_override=None, eps_d_ms=None, pd_fusion=False, swap_bytes=0, full_model=False,
+                 free_bytes=None):
     """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
     config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
@@ -145,7 +146,9 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     beta = configs.kv_bytes_per_token(c, tp=tp)
     max_req = c["b_max"] + 8
     io_bytes = 2 * L * max_req * Hq * d * 4 + 2 * max_req * L * Hkv * d * 2
-    free, _ = torch.cuda.mem_get_info(device)
+    # free HBM: this GPU's, or the minimum over the ranks (every rank then derives the same cap,
+    # eta and therefore the same b_t decisions)
+    free = free_bytes if free_bytes is not None else torch.cuda.mem_get_info(device)[0]
     if cap_bytes is None and os.environ.get("DBK_BENCH_KV_GB"):  # profiling runs only (smaller pool)
         cap_bytes = int(float(os.environ["DBK_BENCH_KV_GB"]) * GB)
     if cap_bytes is None and "cap_bytes_per_gpu" in c:
@@ -312,8 +315,14 @@ def run_gpu(args):
         if world != 1 or args.config != "llama3-70b-gqa":
             raise SystemExit("--tp-shard: single-GPU emulation of the 70B KV-head TP shard only")
         tp = args.tp_shard
+    free_bytes = None
+    if dist is not None:  # the same pool size on every rank (MIN of the ranks' free HBM)
+        f_t = torch.tensor([float(torch.cuda.mem_get_info(local)[0])], dtype=torch.float64, device=red)
+        dist.all_reduce(f_t, op=dist.ReduceOp.MIN)
+        free_bytes = int(f_t.item())
     S = setup_engine(device=local, rank=rank, world=world, cfg_name=args.config, policy=args.policy,
-                     b_static=args.b_static, sla_ms=args.sla_ms, tp=tp, full_model=args.model)
+                     b_static=args.b_static, sla_ms=args.sla_ms, tp=tp, full_model=args.model,
+                     free_bytes=free_bytes)
     dbk = S["dbk"]
     eng = S["eng"]
     exchange_kind = None
