@@ -68,7 +68,7 @@ class KVPool:
         self.h = h
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:  # _lib is None during interpreter teardown
             _lib.dbk_kv_pool_destroy(self.h)
             self.h = None
 
@@ -174,7 +174,7 @@ class Scheduler:
         self.h = h
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:  # _lib is None during interpreter teardown
             _lib.dbk_sched_destroy(self.h)
             self.h = None
 
@@ -212,7 +212,7 @@ class Model:
         self.h = h
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:  # _lib is None during interpreter teardown
             _lib.dbk_model_destroy(self.h)
             self.h = None
 
@@ -260,7 +260,7 @@ class Engine:
         self.h = h
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:  # _lib is None during interpreter teardown
             _lib.dbk_engine_destroy(self.h)
             self.h = None
 
