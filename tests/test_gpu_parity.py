@@ -443,3 +443,26 @@ def test_gqa_bench_config_sampled_parity(dbk, tp):
         got = S["od"][lay, torch.as_tensor(sel, device="cuda")].cpu().numpy().astype(np.float64)
         assert row_err(got, want) <= TOL
     _free(S)
+
+
+def test_bench_config_whole_trace_replay(dbk):
+    """The bench's 7B launch configuration run to completion (3 000 requests all at once,
+    memory-aware rule, pool sized from free HBM): every one of its ~2 000 steps replayed by the
+    oracle from the logged step times, bit for bit (admissions, preemptions, tokens, pages,
+    block-table checksums, b_t), and every request finished."""
+    import gc
+
+    import bench
+    gc.collect()
+    torch.cuda.empty_cache()
+    S = bench.setup_engine(device=0, time_attention=False, out_dtype=0)
+    eng = S["eng"]
+    bufs = eng.buffers(S["qd"], S["od"])
+    stream = torch.cuda.current_stream()
+    recs = []
+    while not eng.done():
+        recs.append(eng.step(bufs, stream))
+    assert sum(r["n_finished"] for r in recs) == len(S["tr"])
+    assert sum(r["n_decode"] for r in recs) == int(S["tr"].l_out.sum())
+    _replay_full_size(S, recs)
+    _free(S)
