@@ -133,7 +133,7 @@ def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None)
 def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
                  out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1,
                  trace_override=None, eps_d_ms=None, pd_fusion=False, swap_bytes=0, full_model=False,
-                 free_bytes=None):
+                 free_bytes=None, pd_token_budget=0):
     """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
     config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
@@ -166,7 +166,7 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap_total, seed=seed,
                      out_dtype=out_dtype, time_attention=time_attention,
                      rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0,
-                     pd_fusion=pd_fusion, preempt_mode=1 if swap_bytes else 0)
+                     pd_fusion=pd_fusion, preempt_mode=1 if swap_bytes else 0, pd_token_budget=pd_token_budget)
     model = None
     if full_model:  # NEXT row 3: QKV/O/MLP/LM-head GEMMs with synthetic fp16 weights around the attention
         if "model" not in c:

@@ -105,7 +105,7 @@ def _tbt_p99(recs):
 
 def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
              modes=(("static", False), ("combined", False), ("static", True), ("combined", True)),
-             b_static=None, lo=10.0, hi=640.0, tol=0.05, max_delay_s=2.0, ctrl_margin_ms=0.0):
+             b_static=None, lo=10.0, hi=640.0, tol=0.05, max_delay_s=2.0, ctrl_margin_ms=0.0, pd_token_budget=0):
     """Table II / Fig. 5 analog: capacity = the largest Poisson rate (qps) at which
     the p99 TBT stays <= D_SLA + eps_D AND the median scheduling delay (arrival -> first
     admission, from dbk_engine_request_times) stays <= 2 s -- Sarathi-Serve's definition, which
@@ -116,7 +116,7 @@ def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
     c = configs.CONFIGS[cfg]
     t = c["trace"]
     out = dict(config=cfg, d_sla_ms=d_sla, eps_d_ms=eps_d, window_s=window_s, max_delay_s=max_delay_s,
-               ctrl_margin_ms=ctrl_margin_ms, rows=[])
+               ctrl_margin_ms=ctrl_margin_ms, pd_token_budget=pd_token_budget, rows=[])
 
     def probe(policy, pd, qps):
         n_req = max(100, int(qps * window_s))
@@ -129,7 +129,7 @@ def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
         torch.cuda.empty_cache()
         S = bench.setup_engine(cfg_name=cfg, policy=policy, b_static=b_static or 256, sla_ms=d_sla - ctrl_margin_ms,
                                eps_d_ms=eps_d, time_attention=False, trace_override=tr, pd_fusion=pd,
-                               full_model=FULL_MODEL)
+                               full_model=FULL_MODEL, pd_token_budget=pd_token_budget if pd else 0)
         eng = S["eng"]
         bufs = eng.buffers(S["qd"], S["od"])
         recs, ms = bench.run_steps(S, 10 ** 9, bufs, torch.cuda.current_stream())
@@ -308,6 +308,8 @@ def main():
     ap.add_argument("--cap-margin", type=float, default=0.0,
                     help="Alg. 2 steers to D_SLA - margin while capacity is judged at D_SLA (p99)")
     ap.add_argument("--cap-pd-only", action="store_true", help="capacity: the combined rule with PD fusion only")
+    ap.add_argument("--pd-token-budget", type=int, default=0,
+                    help="PD fusion: fixed iteration token budget (R36) instead of b_t (R25)")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
     a = ap.parse_args()
     global FULL_MODEL
@@ -353,7 +355,8 @@ def main():
             modes = (("combined", True),) if a.cap_pd_only else \
                 (("static", False), ("combined", False), ("static", True), ("combined", True))
             res["capacity"] = capacity(d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem), lo=a.cap_lo,
-                                       hi=a.cap_hi, ctrl_margin_ms=a.cap_margin, modes=modes)
+                                       hi=a.cap_hi, ctrl_margin_ms=a.cap_margin, modes=modes,
+                                       pd_token_budget=a.pd_token_budget)
             save()
     print(json.dumps({k: (v.get("fit") if isinstance(v, dict) else None) for k, v in res.items()}))
 

@@ -386,6 +386,11 @@ typedef struct dbk_engine_config {
     int32_t preempt_mode;           /* 0: recompute (R18); 1: swap a victim to the pool's   *
                                      * swap space when it has room, else recompute (R29-R31;*
                                      * needs dbk_swap_space_attach; not with pd_fusion)      */
+    int32_t pd_token_budget;        /* PD fusion only.  0: the iteration's token budget is b_t *
+                                     * (R25: c_t = b_t - N^d).  > 0: a fixed token budget per *
+                                     * iteration (R36: c_t = budget - N^d) while b_t still     *
+                                     * bounds running + prefilling requests                    */
+    int32_t _reserved;
 } dbk_engine_config;
 
 typedef struct dbk_engine dbk_engine;

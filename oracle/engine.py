@@ -30,7 +30,9 @@ chunk size"; readings R25-R28 of DESIGN.md): prefill shares the
 Admitted requests first PREFILL in chunks, then decode.  Step order (replaces 2-3):
  a. decode growth of the running (fully prefilled) requests, LIFO preemption over the
     admission order running ++ prefilling (a victim's prefill progress is discarded);
- b. chunk budget c_t = max(0, min(b_share, max_rows) - N^d), N^d = |running|;
+ b. chunk budget c_t = max(0, min(b_share, max_rows) - N^d), N^d = |running| (R25); with a
+    fixed iteration token budget B (R36): c_t = max(0, min(B, max_rows) - N^d) while b_share
+    still bounds |running| + |prefilling| in step c;
  c. FCFS chunk: prefilling requests in admission order, then new admissions from the queue
     head (while |running| + |prefilling| < b_share and the whole prompt + 1 fits the free
     pages, head-of-line blocking), each taking min(remaining prompt, budget left) tokens;
@@ -76,8 +78,9 @@ class RankEngine:
     """One GPU's request shard (DP) or the whole batch (G = 1 / TP)."""
 
     def __init__(self, req_ids, arrival_ns, l_in, l_out, cap_pages, page_size, rank=0, world=1,
-                 pd=False, max_rows=None, swap_cap_pages=0):
+                 pd=False, max_rows=None, swap_cap_pages=0, pd_token_budget=0):
         self.pd = bool(pd)
+        self.pd_token_budget = int(pd_token_budget)  # R36: fixed iteration token budget (0: R25, b_t)
         if swap_cap_pages and pd:
             raise ValueError("swap preemption is defined for non-PD steps only")
         self.swap_cap = int(swap_cap_pages)  # 0: recompute only
@@ -167,7 +170,8 @@ class RankEngine:
         self.kv.append(self.running, [1] * len(self.running))
         for r in self.running:
             self.gen[r] += 1
-        rows = b_share if self.max_rows is None else min(b_share, self.max_rows)
+        tokens = self.pd_token_budget if self.pd_token_budget > 0 else b_share
+        rows = tokens if self.max_rows is None else min(tokens, self.max_rows)
         budget = max(0, rows - len(self.running))                     # b
         chunks, adm, i = [], 0, 0
         while budget > 0:                                              # c

@@ -243,7 +243,7 @@ class Engine:
 
     def __init__(self, pool: KVPool, sched: Scheduler, arrival_ns, l_in, l_out, mem_cap_bytes,
                  sla_ms=0.0, seed=0, out_dtype=2, time_attention=False, rank=0, world=1,
-                 q_scale_log2=0, req_ids=None, pd_fusion=False, preempt_mode=0):
+                 q_scale_log2=0, req_ids=None, pd_fusion=False, preempt_mode=0, pd_token_budget=0):
         self.pool, self.sched = pool, sched
         self._arr, pa = _i64(arrival_ns)
         self._li, pli = _i32(l_in)
@@ -254,7 +254,7 @@ class Engine:
         self.cfg = dbk_engine_config(len(self._arr), q_scale_log2, pa, pli, plo, pids,
                                      int(mem_cap_bytes), float(sla_ms), int(seed), int(out_dtype),
                                      1 if time_attention else 0, rank, world, 1 if pd_fusion else 0,
-                                     int(preempt_mode))
+                                     int(preempt_mode), int(pd_token_budget), 0)
         h = C.c_void_p()
         _lib.dbk_engine_create(pool.h, sched.h, C.byref(self.cfg), C.byref(h))
         self.h = h

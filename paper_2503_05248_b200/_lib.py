@@ -84,7 +84,8 @@ class dbk_engine_config(C.Structure):
                 ("l_out", C.POINTER(C.c_int32)), ("req_ids", C.POINTER(C.c_int64)),
                 ("mem_cap_bytes", C.c_int64), ("sla_ms", C.c_double), ("synth_seed", C.c_uint64),
                 ("out_dtype", C.c_int32), ("time_attention", C.c_int32), ("rank", C.c_int32),
-                ("world", C.c_int32), ("pd_fusion", C.c_int32), ("preempt_mode", C.c_int32)]
+                ("world", C.c_int32), ("pd_fusion", C.c_int32), ("preempt_mode", C.c_int32),
+                ("pd_token_budget", C.c_int32), ("_reserved", C.c_int32)]
 
 
 class dbk_engine_buffers(C.Structure):

@@ -134,6 +134,8 @@ dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_
     if (c.pd_fusion != 0 && c.pd_fusion != 1) return fail(DBK_EINVAL, "engine_create: pd_fusion must be 0 or 1");
     if (c.pd_fusion && !pool->has_ptmap) return fail(DBK_EINVAL, "engine_create: PD fusion needs the pool's prefill tensor map");
     if (c.preempt_mode != 0 && c.preempt_mode != 1) return fail(DBK_EINVAL, "engine_create: preempt_mode must be 0 or 1");
+    if (c.pd_token_budget < 0 || (c.pd_token_budget > 0 && !c.pd_fusion))
+        return fail(DBK_EINVAL, "engine_create: pd_token_budget needs pd_fusion and must be >= 0");
     if (c.preempt_mode == 1 && (c.pd_fusion || !pool->swap_host))
         return fail(DBK_EINVAL, "engine_create: swap preemption needs an attached swap space and pd_fusion = 0");
     for (int i = 0; i < c.n_requests; ++i) {
@@ -336,7 +338,9 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     e->pf_len.clear();
     int32_t n_pf_rows = 0;
     if (pd) {
-        int64_t budget = std::max<int64_t>(0, std::min<int64_t>(share, pc.max_requests) - n);
+        // R25: the token budget is this rank's b_t; R36: a fixed budget, b_t bounding requests only
+        const int64_t tokens = e->cfg.pd_token_budget > 0 ? e->cfg.pd_token_budget : share;
+        int64_t budget = std::max<int64_t>(0, std::min<int64_t>(tokens, pc.max_requests) - n);
         int64_t freep = p->pages.free_count;
         size_t i = 0;
         while (budget > 0) {

@@ -32,7 +32,8 @@ def row_err(got, want):
     return (np.abs(got - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)).max()
 
 
-def _pd_vs_replay(dbk, tr, L, Hq, Hkv, d, cap_pages, policy, b_max, dtype="bf16", check_every=5, sla_ms=50.0):
+def _pd_vs_replay(dbk, tr, L, Hq, Hkv, d, cap_pages, policy, b_max, dtype="bf16", check_every=5, sla_ms=50.0,
+                  pd_token_budget=0):
     P = 16
     beta = 2 * L * Hkv * d * 2
     mem_cap = cap_pages * P * beta
@@ -46,14 +47,16 @@ def _pd_vs_replay(dbk, tr, L, Hq, Hkv, d, cap_pages, policy, b_max, dtype="bf16"
     maxp = -(-int((tr.l_in + tr.l_out).max()) // P) + 1
     pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, dtype)
     seed = 17
-    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap, seed=seed, out_dtype=2, pd_fusion=True)
+    eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap, seed=seed, out_dtype=2, pd_fusion=True,
+                     pd_token_budget=pd_token_budget)
     et = torch.float16 if dtype == "f16" else torch.bfloat16
     qd = torch.empty(L, max_req, Hq, d, dtype=et, device="cuda")
     od = torch.empty(L, max_req, Hq, d, dtype=torch.float32, device="cuda")
     bufs = eng.buffers(qd, od)
     ids = list(range(len(tr)))
     rp = oeng.Replay([oeng.RankEngine(ids, tr.arrival_ns, tr.l_in, tr.l_out, cap_pages, P, pd=True,
-                                      max_rows=max_req)], opol.SchedConfig(prior=tuple(pr.values()), **kw), mem_cap)
+                                      max_rows=max_req, pd_token_budget=pd_token_budget)],
+                     opol.SchedConfig(prior=tuple(pr.values()), **kw), mem_cap)
     recs, checked = [], 0
     while not eng.done():
         g = eng.step(bufs)
@@ -118,3 +121,13 @@ def test_pd_engine_sla_policy(dbk):
     recs, _ = _pd_vs_replay(dbk, tr, 2, 8, 8, 128, 600, opol.COMBINED, 64, dtype="f16", check_every=7,
                             sla_ms=0.05)
     assert len({r["b_t"] for r in recs}) > 1
+
+
+def test_pd_fixed_token_budget_replays(dbk):
+    """R36: a fixed iteration token budget (here 48 tokens) under the combined policy; every
+    record incl. the chunk size replayed bit-exactly, chunk attention checked."""
+    tr = trace.make_trace(40, 100, 60, 300, seed=8, dist="uniform", arrival="poisson", rate_qps=800.0)
+    recs, checked = _pd_vs_replay(dbk, tr, 2, 8, 8, 128, 600, opol.COMBINED, 64, dtype="f16", check_every=4,
+                                  sla_ms=0.3, pd_token_budget=48)
+    assert checked > 0
+    assert max(r["n_prefill"] + r["n_decode"] for r in recs) <= 66

@@ -110,3 +110,32 @@ def test_pd_dp_two_ranks_shares():
     for r in recs:   # rank k's budget is its share of b minus its own decode count
         for k, (ch, loc) in enumerate(zip(r["chunks"], r["local_stats"])):
             assert sum(q for _, _, q in ch) <= max(0, oeng.b_share(r["b_t"], k, 2) - loc["n_active"])
+
+
+def test_pd_fixed_token_budget_reading():
+    """R36: with a fixed iteration token budget B the chunk is c_t = B - N^d while b_t still
+    bounds running + prefilling; B = b_t reproduces R25 step for step."""
+    import numpy as np
+    from oracle import engine as oeng
+    from oracle import policy
+    from synth import trace
+    tr = trace.make_trace(30, 150, 40, 400, seed=4, dist="uniform")
+    ids = list(range(len(tr)))
+
+    def run(budget, b):
+        e = oeng.RankEngine(ids, tr.arrival_ns, tr.l_in, tr.l_out, 400, 16, pd=True, max_rows=512,
+                            pd_token_budget=budget)
+        rp = oeng.Replay([e], policy.SchedConfig(policy=policy.STATIC, b_static=b), 0)
+        recs = []
+        while not rp.done():
+            recs.append(rp.step(1_000_000))
+            assert len(e.running) + len(e.prefilling) <= b          # b_t bounds the requests
+            assert recs[-1]["n_prefill"] + recs[-1]["n_decode"] <= max(budget or b, recs[-1]["n_decode"])
+        return recs
+    a, same = run(0, 16), run(16, 16)
+    keys = ("n_admitted", "n_preempted", "n_decode", "n_prefill", "sum_ctx", "table_hash")
+    assert [[r[k] for k in keys] for r in a] == [[r[k] for k in keys] for r in same]
+    big = run(96, 16)                                   # more prefill per step, same request bound
+    assert max(r["n_prefill"] for r in big) > max(r["n_prefill"] for r in a)
+    assert len(big) < len(a)                            # prompts finish in fewer iterations
+    assert sum(r["n_decode"] for r in big) == int(np.sum(tr.l_out))
