@@ -308,6 +308,8 @@ def main():
     ap.add_argument("--cap-margin", type=float, default=0.0,
                     help="Alg. 2 steers to D_SLA - margin while capacity is judged at D_SLA (p99)")
     ap.add_argument("--cap-pd-only", action="store_true", help="capacity: the combined rule with PD fusion only")
+    ap.add_argument("--cap-d", type=float, default=None, help="capacity: pin D_SLA (ms) instead of tau(b_mem/2)")
+    ap.add_argument("--cap-modes", default=None, help="capacity modes, e.g. static:pd,combined:pd,combined:nopd")
     ap.add_argument("--pd-token-budget", type=int, default=0,
                     help="PD fusion: fixed iteration token budget (R36) instead of b_t (R25)")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
@@ -354,6 +356,10 @@ def main():
         if a.capacity:
             modes = (("combined", True),) if a.cap_pd_only else \
                 (("static", False), ("combined", False), ("static", True), ("combined", True))
+            if a.cap_modes:
+                modes = tuple((m.split(":")[0], m.split(":")[1] == "pd") for m in a.cap_modes.split(","))
+            if a.cap_d:
+                d = a.cap_d
             res["capacity"] = capacity(d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem), lo=a.cap_lo,
                                        hi=a.cap_hi, ctrl_margin_ms=a.cap_margin, modes=modes,
                                        pd_token_budget=a.pd_token_budget)
