@@ -118,3 +118,36 @@ def test_scheduler_matches_oracle_decision_for_decision(dbk, policy):
             assert (s["b_low"], s["b_high"]) == (os_.sla.low, os_.sla.high)
         if policy in (1, 3):
             assert (s["win_n"], s["win_S"], s["win_V2"]) == os_.moments()
+
+
+def test_ctypes_struct_layouts_match_the_header(tmp_path):
+    """Every ctypes mirror of a dbk.h struct has the C size and the C offset of every field
+    (compiled with the host C compiler against include/dbk.h)."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    from paper_2503_05248_b200 import _lib
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = [getattr(_lib, n) for n in dir(_lib) if n.startswith("dbk_") and isinstance(getattr(_lib, n), type)
+               and issubclass(getattr(_lib, n), ctypes.Structure)]
+    assert len(structs) >= 10
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "dbk.h"', "int main(void) {"]
+    for st in structs:
+        lines.append(f'printf("{st.__name__} %zu\\n", sizeof({st.__name__}));')
+        for f, _ in st._fields_:
+            lines.append(f'printf("{st.__name__}.{f} %zu\\n", offsetof({st.__name__}, {f}));')
+    lines += ["return 0; }"]
+    src = tmp_path / "layouts.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layouts"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([cc, "-std=c11", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    out = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for st in structs:
+        assert int(out[st.__name__]) == ctypes.sizeof(st), st.__name__
+        for f, _ in st._fields_:
+            assert int(out[f"{st.__name__}.{f}"]) == getattr(st, f).offset, (st.__name__, f)
