@@ -166,7 +166,7 @@ def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
     return out
 
 
-def pd_table(cfg="llama2-7b", bs=(64, 128, 256), full_model=False):
+def pd_table(cfg="llama2-7b", bs=(64, 128, 256), full_model=False, pd_token_budget=0):
     """PD-fusion whole-trace runs (Table I shape, all-at-once arrivals): static b vs the
     memory-aware rule deciding the fused iteration's token budget (R25).  full_model: prompts
     are prefilled through the weights (QKV/O/MLP GEMMs + K7) instead of the KV fill."""
@@ -178,7 +178,7 @@ def pd_table(cfg="llama2-7b", bs=(64, 128, 256), full_model=False):
         gc.collect()
         torch.cuda.empty_cache()
         S = bench.setup_engine(cfg_name=cfg, policy=pol, b_static=b or 256, time_attention=False, pd_fusion=True,
-                               full_model=full_model)
+                               full_model=full_model, pd_token_budget=pd_token_budget)
         eng = S["eng"]
         bufs = eng.buffers(S["qd"], S["od"])
         t0 = time.time()
@@ -196,7 +196,7 @@ def pd_table(cfg="llama2-7b", bs=(64, 128, 256), full_model=False):
         S["pool"].close()
         S.clear()
         del eng, bufs  # the engine holds the pool, the pool holds the KV allocation
-    return dict(config=cfg, full_model=full_model, rows=rows)
+    return dict(config=cfg, full_model=full_model, pd_token_budget=pd_token_budget, rows=rows)
 
 
 def surge_table(cfg="surge-7b-dp", lam0=None, bs=(64, 128, 256), policies=("memory", "combined"),
@@ -336,7 +336,7 @@ def main():
         res["pd_table"] = pd_table()
         save()
     if a.pd_model:
-        res["pd_table_model"] = pd_table(full_model=True)
+        res["pd_table_model"] = pd_table(full_model=True, pd_token_budget=a.pd_token_budget)
         save()
     if a.swap:
         res["swap"] = swap_table()
