@@ -309,6 +309,7 @@ def main():
                     help="Alg. 2 steers to D_SLA - margin while capacity is judged at D_SLA (p99)")
     ap.add_argument("--cap-pd-only", action="store_true", help="capacity: the combined rule with PD fusion only")
     ap.add_argument("--cap-d", type=float, default=None, help="capacity: pin D_SLA (ms) instead of tau(b_mem/2)")
+    ap.add_argument("--cap-config", default="llama2-13b-sla", help="capacity / SLA config (e.g. llama2-7b)")
     ap.add_argument("--cap-modes", default=None, help="capacity modes, e.g. static:pd,combined:pd,combined:nopd")
     ap.add_argument("--pd-token-budget", type=int, default=0,
                     help="PD fusion: fixed iteration token budget (R36) instead of b_t (R25)")
@@ -345,7 +346,7 @@ def main():
         res["surge"] = surge_table(lam0=a.surge_lam0)
         save()
     if a.sla or a.capacity:
-        res["fig3_13b"] = fig3("llama2-13b-sla", bs=(32, 64, 128, 256))
+        res["fig3_13b"] = fig3(a.cap_config, bs=(32, 64, 128, 256))
         save()
         # binding SLA: the step latency at half the largest static batch; eps_D = 4 % of D
         b_mem = max(r["mean_batch"] for r in res["fig3_13b"]["rows"])
@@ -360,7 +361,7 @@ def main():
                 modes = tuple((m.split(":")[0], m.split(":")[1] == "pd") for m in a.cap_modes.split(","))
             if a.cap_d:
                 d = a.cap_d
-            res["capacity"] = capacity(d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem), lo=a.cap_lo,
+            res["capacity"] = capacity(cfg=a.cap_config, d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem), lo=a.cap_lo,
                                        hi=a.cap_hi, ctrl_margin_ms=a.cap_margin, modes=modes,
                                        pd_token_budget=a.pd_token_budget)
             save()
