@@ -43,14 +43,19 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """dram bytes per decode launch from the committed ncu --set full summary, or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
-    return None, None
+def ncu_traffic(config, tp, kernel, model=False):
+    """The committed ncu capture (profiles/ncu_traffic.json, written by profiles/run_ncu_traffic.sh
+    on the current build) of THIS configuration's decode kernel: dram read + write bytes per
+    launch and the algorithmic bytes of the same launches, or None if it has no entry."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    for e in d.get("entries", []):
+        if e["config"] == config and e["tp"] == tp and e["kernel"] == kernel and bool(e.get("model")) == bool(model):
+            return e
+    return None
 
 
 class ClockSampler:
@@ -133,7 +138,7 @@ def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None)
 def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
                  out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1,
                  trace_override=None, eps_d_ms=None, pd_fusion=False, swap_bytes=0, full_model=False,
-                 free_bytes=None, pd_token_budget=0):
+                 free_bytes=None, pd_token_budget=0, tp_rank=0):
     """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
     config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
@@ -157,7 +162,10 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
         cap_bytes = free - c["weights_bytes"] // tp - c["reserve_bytes"] - io_bytes
     cap_pages = int(cap_bytes // (P * beta))
     maxp = -(-c["trace"]["L_max"] // P)
-    pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, "f16", device=device)
+    # KV-head TP: rank tp_rank holds global kv heads [tp_rank*Hkv, (tp_rank+1)*Hkv) (and their q heads);
+    # the generator keys K/V/q by the global head, so the shards are disjoint slices of the TP1 job
+    pool = dbk.KVPool(L, Hq, Hkv, d, cap_pages, max_req, maxp, "f16", device=device,
+                      kv_head_offset=tp_rank * Hkv if tp > 1 else 0)
     if swap_bytes:  # swap preemption (R29-R31): pinned host swap space
         pool.swap_space_attach(torch.empty(int(swap_bytes), dtype=torch.uint8, pin_memory=True))
     # M_max of the whole job: DP shards add their pools; TP ranks hold the same tokens
@@ -182,7 +190,7 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     return dict(dbk=dbk, c=c, tr=tr, pool=pool, sched=sched, eng=eng, qd=qd, od=od, kvd=kvd, tp=tp, model=model,
                 policy=policy, b_static=b_static, sla_ms=sla_ms, eps_d_ms=eps_d_ms,
                 cap_pages=cap_pages, beta=beta, max_req=max_req, mem_cap_total=mem_cap_total, seed=seed,
-                L=L, Hq=Hq, Hkv=Hkv, d=d)
+                L=L, Hq=Hq, Hkv=Hkv, d=d, tp_rank=tp_rank)
 
 
 def run_steps(S, k, bufs, stream, comm_world=1, dist=None):
@@ -233,6 +241,52 @@ def oracle_sched_replay(S, recs):
             "sched_replay_bit_exact": bool(agree)}
 
 
+def cpu_model():
+    """The host CPU's model name (/proc/cpuinfo), for the cpu_baseline record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def toy_step_oracle(budget_s=3.0):
+    """SURVEY.md §8(d) input (i): the oracle's whole toy decode step (BASELINE configs[0]: 8
+    requests, 1 layer, 8 heads x d64, 256-page cap, memory rule) -- the replay's S1-S7 (admission,
+    page growth, statistics, Alg. 1) plus fp64 paged attention of the step's batch on one thread,
+    repeated over the toy trace until ~budget_s.  Inputs are built outside the timed calls."""
+    from oracle import attention as oatt
+    from oracle import engine as oeng
+    from oracle import policy as opol
+    c, tr = make_workload("toy")
+    L, Hq, Hkv, d, P = c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["page_size"]
+    cap = c["cap_tokens"] // P
+    beta = configs.kv_bytes_per_token(c)
+    kw = sched_kwargs(c, beta)
+    secs, steps, toks = 0.0, 0, 0
+    while secs < budget_s:
+        rp = oeng.Replay([oeng.RankEngine(list(range(len(tr))), tr.arrival_ns, tr.l_in, tr.l_out, cap, P)],
+                         opol.SchedConfig(**kw), cap * P * beta)
+        while not rp.done() and secs < budget_s:
+            t0 = time.perf_counter()
+            rec = rp.step(1_000_000)
+            dt = time.perf_counter() - t0
+            rs, ctx, li, lo, pages = rec["batches"][0]
+            if rs:
+                bt, pk, pv, qq = oatt.synth_paged_batch(1, rs, ctx, pages, 0, Hq, Hkv, d, P, "f16")
+                t0 = time.perf_counter()
+                oatt.paged_decode_attention(np.asarray(ctx), bt, pk, pv, qq, "f16", nthreads=1)
+                dt += time.perf_counter() - t0
+            secs += dt
+            steps += 1
+            toks += len(rs)
+    return {"toy_step_ms": round(1e3 * secs / max(steps, 1), 4), "toy_steps": steps,
+            "toy_tokens_per_s": round(toks / secs, 1) if secs > 0 else None}
+
+
 def cpu_baseline(S, budget_s=15.0, threads=None, single_budget_s=5.0):
     """The oracle (plain C, fp64) on a bounded sample of the current decode batch: all host
     cores, and one thread (SURVEY.md §8(d) "1 thread and nproc threads")."""
@@ -267,25 +321,12 @@ def cpu_baseline(S, budget_s=15.0, threads=None, single_budget_s=5.0):
     kv_bytes = float(np.sum(ctx[sel])) * 2 * Hkv * d * 2   # the KV the sample reads, per repetition
     tok_s = k * reps / L / secs
     return {"value": round(tok_s, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "single_thread_value": round(k * r1 / L / s1, 3),
             "kv_gbs_processed": round(kv_bytes * reps / secs / 1e9, 3),
             "sample": f"{k} random requests of the timed batch (mean ctx {float(np.mean(ctx[sel])):.0f}) x "
                       f"1 layer, fp64 paged attention, {reps} repetitions in {secs:.1f} s on {threads} threads "
                       f"({r1} in {s1:.1f} s on 1 thread); tokens/s = request-layers / L / time"}
-
-
-def _make_comm(dbk, dist, world, rank, local):
-    """ncclUniqueId from rank 0 (dbk_comm_unique_id), broadcast over torch.distributed."""
-    import ctypes
-    buf = (ctypes.c_char * 128)()
-    if rank == 0:
-        dbk._lib.dbk_comm_unique_id(buf)
-    obj = [bytes(buf.raw)]
-    dist.broadcast_object_list(obj, src=0)
-    idbuf = (ctypes.c_char * 128).from_buffer_copy(obj[0])
-    comm = ctypes.c_void_p()
-    dbk._lib.dbk_comm_create(world, rank, idbuf, local, ctypes.byref(comm))
-    return comm
 
 
 def run_gpu(args):
@@ -315,6 +356,8 @@ def run_gpu(args):
         if world != 1 or args.config != "llama3-70b-gqa":
             raise SystemExit("--tp-shard: single-GPU emulation of the 70B KV-head TP shard only")
         tp = args.tp_shard
+        if not 0 <= args.tp_rank < tp:
+            raise SystemExit("--tp-rank must be in [0, tp-shard)")
     free_bytes = None
     if dist is not None:  # the same pool size on every rank (MIN of the ranks' free HBM)
         f_t = torch.tensor([float(torch.cuda.mem_get_info(local)[0])], dtype=torch.float64, device=red)
@@ -322,21 +365,13 @@ def run_gpu(args):
         free_bytes = int(f_t.item())
     S = setup_engine(device=local, rank=rank, world=world, cfg_name=args.config, policy=args.policy,
                      b_static=args.b_static, sla_ms=args.sla_ms, tp=tp, full_model=args.model,
-                     free_bytes=free_bytes)
+                     free_bytes=free_bytes, tp_rank=(args.tp_rank if args.tp_shard else rank) if tp > 1 else 0)
     dbk = S["dbk"]
     eng = S["eng"]
-    exchange_kind = None
+    exchange_kind, comm = None, None
     if world > 1:
         mode = dbk._lib.MODE_TP if tp > 1 else dbk._lib.MODE_DP
-        try:  # libdbk's own NCCL communicator (ncclAllGather of the records inside the engine step)
-            if gloo_test:
-                raise RuntimeError("gloo test harness: no NCCL between ranks sharing one GPU")
-            comm = _make_comm(dbk, dist, world, rank, local)
-            dbk._lib.dbk_engine_attach_comm(eng.h, comm, mode)
-            exchange_kind = "libdbk NCCL all-gather"
-        except Exception as ex:  # fall back to torch.distributed (also NCCL) for the same exchange
-            print(f"[bench] dbk_comm unavailable ({ex}); exchanging records via torch.distributed",
-                  file=sys.stderr)
+        if gloo_test:  # test harness only: ranks share one GPU, so the records go through gloo
             fields = dbk._lib.STATS_FIELDS
 
             def exchange(local_rec):
@@ -345,8 +380,17 @@ def run_gpu(args):
                 dist.all_gather(out, t)
                 return dbk.stats_reduce([dict(zip(fields, o.tolist())) for o in out], mode)
             S["exchange"] = exchange
-            exchange_kind = "torch.distributed gloo all-gather (test harness)" if gloo_test else \
-                "torch.distributed NCCL all-gather"
+            exchange_kind = {"kind": "torch.distributed gloo all-gather (DBK_BENCH_TEST_GLOO test harness)"}
+        else:  # the product path: libdbk's own NCCL communicator; any failure is fatal (no fallback)
+            comm = dbk.Comm(dist, world, rank, local)
+            nr, rk = comm.info()
+            print(f"[bench] rank {rank}: libdbk NCCL communicator nranks={nr} rank={rk} "
+                  f"mode={'TP' if tp > 1 else 'DP'}", file=sys.stderr, flush=True)
+            if (nr, rk) != (world, rank):
+                raise SystemExit(f"NCCL communicator reports nranks={nr} rank={rk}, expected {world}/{rank}")
+            eng.attach_comm(comm, mode)
+            exchange_kind = {"kind": "libdbk ncclAllGather of the 128-B records (dbk_stats_allgather)",
+                             "nccl_nranks": nr}
     stream = torch.cuda.current_stream()
     bufs = eng.buffers(S["qd"], S["od"])
     # fast-forward to the steady state (untimed), then W warm-up steps (untimed)
@@ -357,6 +401,13 @@ def run_gpu(args):
         recs, ms = run_steps(S, args.steps, bufs, stream, dist=dist)
     att_ms, att_launches, att_bytes = eng.attn_timing(reset=True)
     info = S["pool"].info()
+    xch = eng.last_exchange(reset=True) if comm is not None else None
+    # every rank's own timed-region device time (ms), gathered for the line (max is `value`'s clock)
+    per_rank_ms = [ms]
+    if dist is not None:
+        g = [torch.zeros(1, device=red) for _ in range(world)]
+        dist.all_gather(g, torch.tensor([ms], device=red))
+        per_rank_ms = [float(x.item()) for x in g]
     # decode tokens of the whole job: every rank's step record carries the GLOBAL counts (the
     # exchanged, reduced record: DP sums the disjoint shards, TP ranks serve the same requests),
     # so each rank contributes 1/world of it to the all-reduce
@@ -369,7 +420,9 @@ def run_gpu(args):
     # end-to-end through the same API with pinned host buffers (q, new K/V in; out back)
     L, Hq, Hkv, d, mr = S["L"], S["Hq"], S["Hkv"], S["d"], S["max_req"]
     erecs, ems_t, etok_t = [], None, None
-    if not args.model:  # attention-only: q and the new K/V rows in, every layer's output back
+    if args.no_e2e:
+        pass
+    elif not args.model:  # attention-only: q and the new K/V rows in, every layer's output back
         hq = torch.empty(L * mr * Hq * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
         hk = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
         hv = torch.empty(mr * L * Hkv * d, dtype=torch.float16, pin_memory=True).uniform_(-1, 1)
@@ -403,9 +456,8 @@ def run_gpu(args):
     if rank == 0:
         peak, peak_src = measured_peaks()
         achieved = att_bytes / 1e9 / (att_ms / 1e3) if att_ms > 0 else 0.0
-        traffic = None
-        if args.config == CFG_NAME and tp == 1:
-            traffic, _ = ncu_traffic()
+        kern = "decode_gqa_kernel" if info["decode_path"] == 2 else "decode_kernel"
+        traffic_rec = ncu_traffic(args.config, tp, kern, args.model)
         c = S["c"]
         n_steps = len(recs)
         # the decode tokens these steps could emit if every step only streamed its KV at `peak`
@@ -431,12 +483,24 @@ def run_gpu(args):
                        "mean_batch": round(float(np.mean([r["n_decode"] for r in recs])), 1) if recs else 0,
                        "mean_ctx": round(float(np.mean([r["sum_ctx"] / max(r["n_decode"], 1) for r in recs])), 1) if recs else 0,
                        "fast_forward_steps": args.ff,
-                       "parallelism": (f"rank 0 of tp{tp} (KV-head shard on one GPU; no exchange)" if args.tp_shard else
+                       "parallelism": (f"rank {args.tp_rank} of tp{tp} (KV-head shard on one GPU; no exchange)"
+                                       if args.tp_shard else
                                        f"tp{world} (KV-head shards)" if tp > 1 else f"dp{world} (request shards)"),
-                       "stats_exchange": exchange_kind,
+                       "stats_exchange": (dict(exchange_kind or {}, **({
+                           "host_us_per_step": round(xch["us_total"] / max(xch["count"], 1), 2),
+                           "exchanges": xch["count"],
+                           "last_step_ns_per_rank": [r["step_ns"] for r in xch["records"]]} if xch else {}))
+                           if world > 1 else None),
+                       "per_rank_ms": [round(x, 3) for x in per_rank_ms],
                        "l2": "inputs > L2 (~1e2 GB of KV read per step vs 126 MB L2)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kname,
+                         "frac": round(achieved / peak, 4),
+                         "traffic": traffic_rec["dram_bytes_per_launch"] if traffic_rec else None,
+                         "traffic_source": ({k: traffic_rec[k] for k in ("file", "build", "launches",
+                                                                          "algorithmic_bytes_per_launch",
+                                                                          "traffic_over_algorithmic")}
+                                            if traffic_rec else "no ncu entry for this configuration"),
+                         "kernel": kname,
                          "bytes_per_launch": int(att_bytes / max(att_launches, 1)),
                          "ms_per_launch": round(att_ms / max(att_launches, 1), 4), "peak_source": peak_src,
                          "share_of_step": round(att_ms / max(ms, 1e-9), 4), "ctas_per_sm": info["ctas_per_sm"],
@@ -462,6 +526,7 @@ def run_gpu(args):
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(S)
             line["cpu_baseline"].update(oracle_sched_replay(S, ff_recs[:60]))
+            line["cpu_baseline"].update(toy_step_oracle())
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -518,6 +583,7 @@ def run_reference(args):
             "data": "synthetic (same trace and generator as the GPU arm)",
             "config": {"workload": c["name"], "layers": L, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"per step {per_step} random requests of the steady-state batch at one "
                                        f"layer (fp64 C oracle); tokens/s = request-layers / L / time"},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -538,6 +604,8 @@ def main():
     ap.add_argument("--sla-ms", type=float, default=None)
     ap.add_argument("--tp-shard", type=int, default=0, choices=[0, 2, 4, 8],
                     help="70B GQA: run rank 0's KV-head shard of a TP-G job on this one GPU (per-GPU kernel rate)")
+    ap.add_argument("--tp-rank", type=int, default=0, help="with --tp-shard: which rank's KV-head shard")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) run (profiling)")
     ap.add_argument("--model", action="store_true",
                     help="full decode step: synthetic-weight QKV/O/MLP/LM-head GEMMs around the attention")
     args = ap.parse_args()

@@ -53,7 +53,8 @@ const char *dbk_version(void);
 /* KV pool: paged KV cache + page allocator + request table                  */
 /* ------------------------------------------------------------------------ */
 
-/* Shapes of one GPU's share of the model (KV-head TP: pass the local heads).
+/* Shapes of one GPU's share of the model (KV-head TP: pass the local heads and
+ * kv_head_offset).
  * Device layout of the caller-provided KV memory:
  *   kv[layer][page][kv_head][2 (K,V)][page_size][head_dim], element kv_dtype.
  * Constraints: q_heads % kv_heads == 0, q_heads/kv_heads in {1,2,4,8},
@@ -64,7 +65,12 @@ typedef struct dbk_pool_config {
     int32_t max_requests;       /* request slots (rows of the block table)   */
     int32_t max_pages_per_req;  /* block-table row width = ceil(L_max / P)   */
     int32_t device;             /* CUDA device ordinal                       */
-    int32_t _reserved;
+    int32_t kv_head_offset;     /* KV-head TP: global index of this pool's
+                                 * first kv head, rank * kv_heads for rank r of a TP-G job; its
+                                 * q heads are kv_head_offset * (q_heads/kv_heads) + 0.. .  Only
+                                 * the synthetic generator sees it (K/V/q values are keyed by the
+                                 * GLOBAL head, so the G shards of a job hold disjoint slices of
+                                 * the TP1 problem); 0 on one GPU.  >= 0 */
 } dbk_pool_config;
 
 typedef struct dbk_pool dbk_pool;
@@ -479,7 +485,18 @@ dbk_status dbk_stats_allgather(dbk_comm *c, const dbk_stats *local, dbk_stats *a
 /* Host reduction: DP = SUM (max_ctx MAX, over_cap OR); TP = all equal
  * (EINVAL otherwise); both: step_ns = MAX. */
 dbk_status dbk_stats_reduce(const dbk_stats *all, int32_t nranks, int32_t mode, dbk_stats *global);
+/* This communicator's size and rank as NCCL reports them (ncclCommCount, ncclCommUserRank). */
+dbk_status dbk_comm_info(dbk_comm *c, int32_t *nranks, int32_t *rank);
+/* dbk_engine_step then exchanges every step's record through `c`.  DP (request shards): the
+ * communicator must have cfg.world ranks; TP (KV-head shards): the engine has world 1 and
+ * every rank serves all requests.  EINVAL otherwise.  NULL detaches. */
 dbk_status dbk_engine_attach_comm(dbk_engine *e, dbk_comm *c, int32_t mode);
+/* The last exchange of dbk_engine_step: up to cap per-rank records in rank order (each with
+ * that rank's own device-timed step_ns) into all (nullable), their count, the host time of
+ * that exchange (us: H2D + all-gather + D2H + reduce) and the total / count since the last
+ * reset.  nranks = 0 before the first exchange or without a communicator. */
+dbk_status dbk_engine_last_exchange(dbk_engine *e, dbk_stats *all, int32_t cap, int32_t *nranks, double *us,
+                                    double *us_total, int64_t *count, int32_t reset);
 
 #ifdef __cplusplus
 }

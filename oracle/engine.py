@@ -241,9 +241,11 @@ class RankEngine:
         return fin
 
 
-def b_share(b, rank, world):
-    """This rank's share of the global b_t (DP request shards, reading R21)."""
-    return b // world + (1 if rank < b % world else 0)
+def b_share(b, rank, world, t=0):
+    """This rank's share of the global b_t at step t (DP request shards, reading R21): an
+    equal split, the b_t mod G remainder going to the ranks r with (r - t) mod G < b_t mod G,
+    so the extra slot rotates and a rank whose floor share is 0 (b_t < G) still gets a turn."""
+    return b // world + (1 if (rank - t) % world < b % world else 0)
 
 
 class Replay:
@@ -277,11 +279,11 @@ class Replay:
         chunks = []
         for e in self.ranks:
             if e.pd:
-                a, p, ch = e.step_pd(b_share(self.b, e.rank, G))
+                a, p, ch = e.step_pd(b_share(self.b, e.rank, G, self.t))
                 n_prefill += sum(k for _, _, k in ch)
                 chunks.append(ch)
             else:
-                a, p = e.admit_and_grow(b_share(self.b, e.rank, G))
+                a, p = e.admit_and_grow(b_share(self.b, e.rank, G, self.t))
             adm += a
             pre += p
         recs = [e.local_stats() for e in self.ranks]

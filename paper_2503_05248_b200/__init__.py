@@ -53,11 +53,11 @@ class KVPool:
     """dbk_pool: paged KV cache over caller-owned device memory (a torch tensor)."""
 
     def __init__(self, layers, q_heads, kv_heads, head_dim, cap_pages, max_requests,
-                 max_pages_per_req, kv_dtype="f16", page_size=16, device=0, kv_mem=None):
+                 max_pages_per_req, kv_dtype="f16", page_size=16, device=0, kv_mem=None, kv_head_offset=0):
         import torch
         self.cfg = dbk_pool_config(layers, q_heads, kv_heads, head_dim, page_size,
                                    0 if kv_dtype == "f16" else 1, cap_pages, max_requests,
-                                   max_pages_per_req, device, 0)
+                                   max_pages_per_req, device, int(kv_head_offset))
         self.nbytes = _lib.dbk_kv_pool_bytes(C.byref(self.cfg))
         if self.nbytes == 0:
             raise DbkError(1, "dbk_kv_pool_bytes", "invalid pool config")
@@ -266,6 +266,21 @@ class Engine:
 
     __del__ = close
 
+    def attach_comm(self, comm, mode):
+        """Exchange every step's record through a libdbk communicator (Comm); mode MODE_DP / MODE_TP."""
+        self.comm = comm
+        _lib.dbk_engine_attach_comm(self.h, comm.h if comm is not None else None, int(mode))
+
+    def last_exchange(self, reset=False, cap=64):
+        """The last step's exchange: per-rank records (rank order), host us of that exchange,
+        total us and count since the last reset."""
+        arr = (dbk_stats * cap)()
+        n, us, tot, cnt = C.c_int32(), C.c_double(), C.c_double(), C.c_int64()
+        _lib.dbk_engine_last_exchange(self.h, arr, cap, C.byref(n), C.byref(us), C.byref(tot), C.byref(cnt),
+                                      1 if reset else 0)
+        return dict(records=[arr[r].as_dict() for r in range(min(n.value, cap))], us=us.value,
+                    us_total=tot.value, count=cnt.value)
+
     def attach_model(self, model):
         self.model = model
         _lib.dbk_engine_attach_model(self.h, model.h if model is not None else None)
@@ -318,6 +333,36 @@ class Engine:
         _lib.dbk_engine_request_times(self.h, n, a.ctypes.data_as(C.POINTER(C.c_int64)),
                                       f.ctypes.data_as(C.POINTER(C.c_int64)))
         return a, f
+
+
+class Comm:
+    """dbk_comm: libdbk's NCCL communicator for the 128-B statistics exchange.  The
+    ncclUniqueId comes from rank 0 (dbk_comm_unique_id) and is broadcast over the caller's
+    torch.distributed process group (`dist`)."""
+
+    def __init__(self, dist, world, rank, device):
+        buf = (C.c_char * 128)()
+        if rank == 0:
+            _lib.dbk_comm_unique_id(buf)
+        obj = [bytes(buf.raw)]
+        dist.broadcast_object_list(obj, src=0)
+        idbuf = (C.c_char * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        _lib.dbk_comm_create(int(world), int(rank), idbuf, int(device), C.byref(h))
+        self.h = h
+
+    def info(self):
+        """(nranks, rank) as NCCL reports them."""
+        n, r = C.c_int32(), C.c_int32()
+        _lib.dbk_comm_info(self.h, C.byref(n), C.byref(r))
+        return n.value, r.value
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.dbk_comm_destroy(self.h)
+            self.h = None
+
+    __del__ = close
 
 
 def stats_reduce(records, mode=0):

@@ -30,7 +30,8 @@ class dbk_pool_config(C.Structure):
     _fields_ = [("layers", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32),
                 ("head_dim", C.c_int32), ("page_size", C.c_int32), ("kv_dtype", C.c_int32),
                 ("cap_pages", C.c_int64), ("max_requests", C.c_int32),
-                ("max_pages_per_req", C.c_int32), ("device", C.c_int32), ("_reserved", C.c_int32)]
+                ("max_pages_per_req", C.c_int32), ("device", C.c_int32),
+                ("kv_head_offset", C.c_int32)]
 
 
 class dbk_pool_info(C.Structure):
@@ -170,6 +171,9 @@ SIGNATURES = {
     "dbk_stats_allgather": [P, C.POINTER(dbk_stats), C.POINTER(dbk_stats), C.POINTER(dbk_stats), I32, P],
     "dbk_stats_reduce": [C.POINTER(dbk_stats), I32, I32, C.POINTER(dbk_stats)],
     "dbk_engine_attach_comm": [P, P, I32],
+    "dbk_comm_info": [P, PI32, PI32],
+    "dbk_engine_last_exchange": [P, C.POINTER(dbk_stats), I32, PI32, C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), PI64, I32],
 }
 _RESTYPE = {"dbk_last_error": C.c_char_p, "dbk_version": C.c_char_p, "dbk_kv_pool_bytes": C.c_size_t,
             "dbk_model_weight_bytes": C.c_size_t}

@@ -98,6 +98,16 @@ dbk_status dbk_comm_create(int32_t nranks, int32_t rank, const void *id_in, int3
     return DBK_OK;
 }
 
+dbk_status dbk_comm_info(dbk_comm *c, int32_t *nranks, int32_t *rank) {
+    if (!c) return dbk::fail(DBK_EINVAL, "comm_info: null communicator");
+    int n = 0, r = 0;
+    DBK_NCCL(ncclCommCount(c->nccl, &n));
+    DBK_NCCL(ncclCommUserRank(c->nccl, &r));
+    if (nranks) *nranks = n;
+    if (rank) *rank = r;
+    return DBK_OK;
+}
+
 dbk_status dbk_comm_destroy(dbk_comm *c) {
     if (!c) return DBK_OK;
     if (c->nccl) ncclCommDestroy(c->nccl);

@@ -2,6 +2,7 @@
 // DESIGN.md R17-R22).  The decode step's GPU work is timed with CUDA events; the
 // measured latency feeds Algorithm 2 and advances the engine clock.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <deque>
@@ -64,6 +65,10 @@ struct dbk_engine {
     std::vector<int64_t> layer_bytes;
     dbk_comm *comm = nullptr;
     int32_t comm_mode = DBK_MODE_DP;
+    int32_t comm_nranks = 1;
+    std::vector<dbk_stats> x_all;     // the last exchange: every rank's record, rank order
+    double x_us = 0, x_us_total = 0;  // host time of the last exchange / since the last reset
+    int64_t x_count = 0;
     dbk_model *model = nullptr;       // full-model mode (NEXT row 3)
     // end-to-end mode: host<->device copies on their own streams, ordered by events
     cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -91,8 +96,11 @@ struct dbk_engine {
 
 namespace {
 
-int32_t b_share(int32_t b, int32_t rank, int32_t world) {  // R21
-    return b / world + (rank < b % world ? 1 : 0);
+// R21: equal split of b_t, the remainder rotating with the step index t (a rank whose floor
+// share is 0 when b_t < G still admits every G steps: liveness)
+int32_t b_share(int32_t b, int32_t rank, int32_t world, int64_t t) {
+    const int64_t k = ((static_cast<int64_t>(rank) - t) % world + world) % world;
+    return b / world + (k < b % world ? 1 : 0);
 }
 
 void release_arrivals(dbk_engine *e) {
@@ -205,8 +213,36 @@ dbk_status dbk_engine_attach_model(dbk_engine *e, dbk_model *m) {
 
 dbk_status dbk_engine_attach_comm(dbk_engine *e, dbk_comm *c, int32_t mode) {
     if (!e || (mode != DBK_MODE_DP && mode != DBK_MODE_TP)) return fail(DBK_EINVAL, "attach_comm: bad argument");
+    int32_t n = 1;
+    if (c) {
+        DBK_TRY(dbk_comm_info(c, &n, nullptr));
+        // DP: the engine serves request shard `rank` of `world`, the communicator must span the
+        // same ranks; TP: every rank serves all requests (world 1), the communicator spans the
+        // KV-head shards
+        if (mode == DBK_MODE_DP && n != e->cfg.world)
+            return fail(DBK_EINVAL, "attach_comm: DP communicator of %d ranks, engine world %d", n, e->cfg.world);
+        if (mode == DBK_MODE_TP && e->cfg.world != 1)
+            return fail(DBK_EINVAL, "attach_comm: TP mode needs an engine with world 1 (got %d)", e->cfg.world);
+    }
     e->comm = c;
     e->comm_mode = mode;
+    e->comm_nranks = n;
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_last_exchange(dbk_engine *e, dbk_stats *all, int32_t cap, int32_t *nranks, double *us,
+                                    double *us_total, int64_t *count, int32_t reset) {
+    if (!e) return fail(DBK_EINVAL, "engine_last_exchange: null engine");
+    const int32_t n = static_cast<int32_t>(e->x_all.size());
+    if (nranks) *nranks = n;
+    for (int32_t r = 0; all && r < n && r < cap; ++r) all[r] = e->x_all[r];
+    if (us) *us = e->x_us;
+    if (us_total) *us_total = e->x_us_total;
+    if (count) *count = e->x_count;
+    if (reset) {
+        e->x_us_total = 0;
+        e->x_count = 0;
+    }
     return DBK_OK;
 }
 
@@ -246,7 +282,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     // S1: FCFS admission with head-of-line blocking (R17); prefill = synthetic fill of T tokens,
     // a swapped-out request is swapped back in instead (R30).  Pages are taken in admission
     // order: pending fills are flushed before a swap-in.
-    const int32_t share = b_share(e->b, e->cfg.rank, e->cfg.world);
+    const int32_t share = b_share(e->b, e->cfg.rank, e->cfg.world, e->t);
     std::vector<int64_t> adm_ids;
     std::vector<int32_t> adm_tok;
     int64_t free_pages = p->pages.free_count;
@@ -403,7 +439,8 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             const uint8_t *dev = static_cast<const uint8_t *>(e->up_pf.dev);
             DBK_CUDA(launch_synth_rows_layers(e->cfg.synth_seed, 0, n_pf_rows, reinterpret_cast<const int64_t *>(dev),
                                               reinterpret_cast<const int32_t *>(dev + static_cast<size_t>(n_pf_rows) * 8),
-                                              pc.layers, pc.max_requests, n, pc.q_heads, pc.head_dim,
+                                              pc.layers, pc.max_requests, n, pc.q_heads,
+                                              pc.kv_head_offset * (pc.q_heads / pc.kv_heads), pc.head_dim,
                                               e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
             ++p->n_launches;
         }
@@ -429,7 +466,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     if (n > 0) DBK_TRY(prepare_batch(p, n, e->batch_ids.data(), s));
     if (n > 0 && !e2e && !e->model) {  // synthetic q of all layers (stands in for the QKV projection), one launch
         DBK_CUDA(launch_synth_q(e->cfg.synth_seed, p->d_req, n, pc.layers, pc.max_requests, pc.q_heads,
-                                pc.head_dim, e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
+                                pc.kv_head_offset * (pc.q_heads / pc.kv_heads), pc.head_dim, e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
         ++p->n_launches;
     }
     if (e2e && n > 0) {
@@ -649,9 +686,13 @@ dbk_status dbk_engine_step(dbk_engine *e, const dbk_engine_buffers *bufs, void *
     dbk_stats local;
     DBK_TRY(dbk_engine_step_launch(e, bufs, stream, &local));
     dbk_stats global = local;
-    if (e->comm) {
-        std::vector<dbk_stats> all(static_cast<size_t>(e->cfg.world));
-        DBK_TRY(dbk_stats_allgather(e->comm, &local, all.data(), &global, e->comm_mode, stream));
+    if (e->comm) {  // the gather buffer holds one record per communicator rank
+        e->x_all.resize(static_cast<size_t>(e->comm_nranks));
+        const auto t0 = std::chrono::steady_clock::now();
+        DBK_TRY(dbk_stats_allgather(e->comm, &local, e->x_all.data(), &global, e->comm_mode, stream));
+        e->x_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        e->x_us_total += e->x_us;
+        ++e->x_count;
     } else if (e->cfg.world != 1) {
         return fail(DBK_EINVAL, "engine_step: world > 1 needs a communicator (or use step_launch/finish)");
     }

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
         uint4 val;
         if (job.src_row < 0) {
             float f[8];
-            synth_vals(synth_key(p.seed, 1 + kv, job.req_id, pos, layer, head, v), scale, f);
+            synth_vals(synth_key(p.seed, 1 + kv, job.req_id, pos, layer, p.head0 + head, v), scale, f);
             val = pack8<T>(f);
         } else {
             const size_t srow = p.src_layer_rows > 0
@@ -91,7 +91,7 @@ __global__ void synth_rows_kernel(uint64_t seed, int kind, int n_rows, const int
 // q of every layer for the batch in `req`: q[l][i][h][:] = synth(seed, q, req_i, ctx_i - 1, l, h),
 // layer l at q + l * layer_rows rows (one launch per step).
 __global__ void synth_q_kernel(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
-                               int q_heads, int d, float scale, int dtype, void *q) {
+                               int q_heads, int head0, int d, float scale, int dtype, void *q) {
     const int vpr = d / 8;
     const long per_layer = static_cast<long>(n) * q_heads * vpr;
     const long total = per_layer * layers;
@@ -105,7 +105,7 @@ __global__ void synth_q_kernel(uint64_t seed, const ReqMeta *req, int n, int lay
         const int r = static_cast<int>(rh / q_heads);
         const ReqMeta rm = req[r];
         float f[8];
-        synth_vals(synth_key(seed, 0, rm.req_id, rm.ctx - 1, l, h, v), scale, f);
+        synth_vals(synth_key(seed, 0, rm.req_id, rm.ctx - 1, l, head0 + h, v), scale, f);
         store8(q, (static_cast<size_t>(l) * layer_rows * q_heads + rh) * d + v * 8, dtype, f);
     }
 }
@@ -113,8 +113,8 @@ __global__ void synth_q_kernel(uint64_t seed, const ReqMeta *req, int n, int lay
 // rows of every layer: out[l][row0 + r][h][:] = synth(seed, kind, req[r], pos[r], l, h), layer l at
 // out + l * layer_rows rows (PD fusion: the prefill chunk's q, one launch per step).
 __global__ void synth_rows_layers_kernel(uint64_t seed, int kind, int n_rows, const int64_t *req, const int32_t *pos,
-                                         int layers, int layer_rows, int row0, int n_heads, int d, float scale,
-                                         int dtype, void *out) {
+                                         int layers, int layer_rows, int row0, int n_heads, int head0, int d,
+                                         float scale, int dtype, void *out) {
     const int vpr = d / 8;
     const long per_layer = static_cast<long>(n_rows) * n_heads * vpr;
     const long total = per_layer * layers;
@@ -127,7 +127,7 @@ __global__ void synth_rows_layers_kernel(uint64_t seed, int kind, int n_rows, co
         const int h = static_cast<int>(rh % n_heads);
         const int r = static_cast<int>(rh / n_heads);
         float f[8];
-        synth_vals(synth_key(seed, kind, req[r], pos[r], l, h, v), scale, f);
+        synth_vals(synth_key(seed, kind, req[r], pos[r], l, head0 + h, v), scale, f);
         store8(out, ((static_cast<size_t>(l) * layer_rows + row0) * n_heads + rh) * d + v * 8, dtype, f);
     }
 }
@@ -170,21 +170,21 @@ cudaError_t launch_synth_rows(uint64_t seed, int kind, int n_rows, const int64_t
 }
 
 cudaError_t launch_synth_rows_layers(uint64_t seed, int kind, int n_rows, const int64_t *req, const int32_t *pos,
-                                    int layers, int layer_rows, int row0, int n_heads, int d, int scale_log2,
-                                    int dtype, void *out, cudaStream_t s) {
+                                    int layers, int layer_rows, int row0, int n_heads, int head0, int d,
+                                    int scale_log2, int dtype, void *out, cudaStream_t s) {
     const long work = static_cast<long>(n_rows) * layers * n_heads * (d / 8);
     if (work <= 0) return cudaSuccess;
     synth_rows_layers_kernel<<<grid_for(work, 256), 256, 0, s>>>(seed, kind, n_rows, req, pos, layers, layer_rows,
-                                                                 row0, n_heads, d, ldexpf(1.0f, scale_log2 - 7),
+                                                                 row0, n_heads, head0, d, ldexpf(1.0f, scale_log2 - 7),
                                                                  dtype, out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
-                           int q_heads, int d, int scale_log2, int dtype, void *q, cudaStream_t s) {
+                           int q_heads, int head0, int d, int scale_log2, int dtype, void *q, cudaStream_t s) {
     const long work = static_cast<long>(n) * layers * q_heads * (d / 8);
     if (work <= 0) return cudaSuccess;
-    synth_q_kernel<<<grid_for(work, 256), 256, 0, s>>>(seed, req, n, layers, layer_rows, q_heads, d,
+    synth_q_kernel<<<grid_for(work, 256), 256, 0, s>>>(seed, req, n, layers, layer_rows, q_heads, head0, d,
                                                        ldexpf(1.0f, scale_log2 - 7), dtype, q);
     return cudaGetLastError();
 }

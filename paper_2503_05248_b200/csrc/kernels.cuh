@@ -107,6 +107,7 @@ struct AppendParams {
                                  // src_layer_rows > 0: [layers][src_layer_rows][kv_heads][D]
     int32_t src_layer_rows = 0;
     uint64_t seed;
+    int32_t head0 = 0;           // global index of kv head 0 (KV-head TP shard) for the generator
     int32_t layer0 = 0;          // this launch writes layers [layer0, layer0 + n_launch_layers)
     int32_t n_launch_layers = 0; // 0 = all layers
 };
@@ -153,13 +154,13 @@ cudaError_t launch_bt_apply(int32_t *bt, int32_t stride, const BtDelta *d, int32
 cudaError_t launch_synth_rows(uint64_t seed, int kind, int n_rows, const int64_t *req,
                               const int32_t *pos, int layer, int n_heads, int d, int scale_log2,
                               int dtype, void *out, cudaStream_t s);
-// out[l][row0 + r][h][:] = synth(seed, kind, req[r], pos[r], l, h) for all layers (device req/pos).
+// out[l][row0 + r][h][:] = synth(seed, kind, req[r], pos[r], l, head0 + h) for all layers (device req/pos).
 cudaError_t launch_synth_rows_layers(uint64_t seed, int kind, int n_rows, const int64_t *req, const int32_t *pos,
-                                    int layers, int layer_rows, int row0, int n_heads, int d, int scale_log2,
-                                    int dtype, void *out, cudaStream_t s);
-// q[l][i][h][:] = synth(seed, q, req_i, ctx_i - 1, l, h) for all layers, layer stride layer_rows rows.
+                                    int layers, int layer_rows, int row0, int n_heads, int head0, int d,
+                                    int scale_log2, int dtype, void *out, cudaStream_t s);
+// q[l][i][h][:] = synth(seed, q, req_i, ctx_i - 1, l, head0 + h) for all layers, layer stride layer_rows rows.
 cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
-                           int q_heads, int d, int scale_log2, int dtype, void *q, cudaStream_t s);
+                           int q_heads, int head0, int d, int scale_log2, int dtype, void *q, cudaStream_t s);
 int decode_ctas_per_sm(int kv_dtype, int head_dim, int group);
 // K7: grid (n_tiles, kv_heads); needs the pool's 5-D tensor map.
 cudaError_t launch_prefill(const PrefillParams &p, int kv_dtype, int head_dim, int group, int n_tiles,

@@ -445,6 +445,7 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
     if (!p || !c || !out) return fail(DBK_EINVAL, "model_create: null argument");
     const dbk_pool_config &pc = p->cfg;
     if (pc.kv_dtype != 0) return fail(DBK_EINVAL, "model_create: the model path is fp16 (kv_dtype 0)");
+    if (pc.kv_head_offset != 0) return fail(DBK_EINVAL, "model_create: the model is single-GPU / DP (kv_head_offset 0)");
     if (c->hidden % kWChunk || c->ffn % kWChunk || c->hidden > 8 * 4 * 256 || c->vocab < 1 || c->max_pos < 1 ||
         (pc.q_heads * pc.head_dim) % kWChunk || c->rms_eps <= 0 || c->rope_theta <= 0)
         return fail(DBK_EINVAL, "model_create: hidden, ffn, q_heads*head_dim multiples of 128, hidden <= 8192");

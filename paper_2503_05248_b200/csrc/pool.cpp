@@ -154,6 +154,8 @@ static bool pool_cfg_ok(const dbk_pool_config *c) {
     if (c->cap_pages < 1 || c->cap_pages > (1LL << 31) - 1 || c->max_requests < 1 ||
         c->max_pages_per_req < 1)
         return false;
+    // generator key: head index in 12 bits (synth/hashgen.py)
+    if (c->kv_head_offset < 0 || (c->kv_head_offset + c->kv_heads) * g > 4096) return false;
     return true;
 }
 
@@ -390,6 +392,7 @@ dbk_status append_launch(dbk_pool *p, const void *k, const void *v, uint64_t see
     ap.k_src = k;
     ap.v_src = v;
     ap.seed = seed;
+    ap.head0 = p->cfg.kv_head_offset;
     ap.layer0 = layer0;
     ap.n_launch_layers = nl;
     ap.src_layer_rows = src_layer_rows;

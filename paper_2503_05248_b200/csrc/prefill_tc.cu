@@ -155,7 +155,7 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
 
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t kv_full[STG], kv_empty[STG];
-    __shared__ __align__(8) uint64_t s_full[2][2], p_full[2][2], pv_done[2], q_ready;
+    __shared__ __align__(8) uint64_t s_full[2][2], p_full[2][2], o_done[2], q_ready;
     __shared__ uint32_t tmem_base_sh;
 
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -183,7 +183,7 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
                 mbar_init(&s_full[t][k], 1);
                 mbar_init(&p_full[t][k], kRows);
             }
-            mbar_init(&pv_done[t], 1);
+            mbar_init(&o_done[t], 1);  // one phase: the tile's last PV
         }
         mbar_init(&q_ready, 2 * kRows);
         fence_mbar_init();
@@ -239,8 +239,12 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
                         umma_ts(to, tp + kk * 8, vdesc, ID_O, (c > 0 || kk > 0) ? 1u : 0u);
                         if constexpr (kBF16) umma_ts(to, tp + 32 + kk * 8, vdesc, ID_O, 1u);
                     }
-                    umma_commit(&pv_done[t]);
+                    // the tile's O is final after its last PV: one commit, one phase (the
+                    // epilogue's only wait on it)
+                    if (c == (t == 0 ? nblk_a : n_blk) - 1) umma_commit(&o_done[t]);
                 }
+                // every phase of kv_empty is observed by the producer before the next one
+                // completes; the softmax threads also wait on it to know PV(c) is done
                 umma_commit(&kv_empty[st]);
             };
             for (int b = 0; b < n_blk; ++b) {
@@ -319,9 +323,12 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
             const bool grow = m_new > M + 8.f;  // rescale only when the max grows by > 2^8
             if (b > 0 && __any_sync(kFull, grow)) {
                 const float f = grow ? exp2f(M - m_new) : 1.f;
-                // O holds blocks < b.  Valid parity wait: the commit behind S(b) covers the
-                // earlier-issued PV(b-2), and PV(b) needs this block's P.
-                mbar_wait(&pv_done[t], (b - 1) & 1);
+                // O holds blocks < b: wait for PV(b-1) through the commit onto kv_empty of
+                // block b-1's stage (phase (b-1)/STG).  Valid parity wait: that barrier's
+                // previous phase (block b-1-STG <= b-2) is complete -- the commit behind S(b)
+                // covers the earlier-issued PV(b-2) -- and its next one (block b-1+STG) needs
+                // this thread's own P(b-1+STG), so it cannot have completed yet.
+                mbar_wait(&kv_empty[(b - 1) % STG], ((b - 1) / STG) & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int c0 = 0; c0 < D; c0 += 32) {
@@ -383,11 +390,9 @@ prefill_tc_kernel(const PrefillParams p, const __grid_constant__ CUtensorMap tma
             mbar_arrive(&p_full[t][b & 1]);
         }
         if (my_blk > 0) {
-            // epilogue: O / L for this row.  A parity wait is only valid for the phase after
-            // the last completed one; S(my_blk-1) implies PV(my_blk-3) done, so wait the last
-            // two PV phases in order.
-            if (my_blk >= 2) mbar_wait(&pv_done[t], (my_blk - 2) & 1);
-            mbar_wait(&pv_done[t], (my_blk - 1) & 1);
+            // epilogue: O / L for this row, once the tile's last PV has completed (o_done has
+            // exactly one phase)
+            mbar_wait(&o_done[t], 0);
             tc_fence_after();
             const float inv = 1.f / L;
             const size_t ob = (static_cast<size_t>(tl.q_row0 + tl.j0 + jt) * p.q_heads + h) * D;

@@ -1,10 +1,12 @@
 """GPU parity of the full decode step (NEXT row 3; dbk_model_*, R32-R35) against the
 fp64 oracle O8 (oracle/model.py).
 
-Bar (R35): fp16 weights and fp16 activations at every GEMM boundary with fp32 accumulation
-and an fp32 residual stream vs the fp64 oracle on the same (exactly representable) weights:
-per row relative L2 error <= MODEL_TOL for the logits, and for the K/V rows the model
-writes into the pool.  Block tables / ctx after dbk_reserve_tokens are bit-exact."""
+Bar (R35, element-wise like R23): fp16 weights and fp16 activations at every GEMM boundary with
+fp32 accumulation and an fp32 residual stream vs the fp64 oracle on the same (exactly
+representable) weights: for every row, max_j |got_j - want_j| <= MODEL_TOL * max_j |want_j| --
+the logits row (one wrong logit among V fails it, which a row L2 norm would dilute by ~1/sqrt(V)),
+and every K / V row [Hkv][d] the model writes into the pool.  Block tables / ctx after
+dbk_reserve_tokens are bit-exact."""
 import numpy as np
 import pytest
 
@@ -18,16 +20,20 @@ from oracle.allocator import PagedKV  # noqa: E402
 from synth import configs, trace  # noqa: E402
 from test_gpu_parity import dbk  # noqa: E402,F401
 
-MODEL_TOL = 2e-3  # R35: >= 4x the observed 2.3e-4 .. 4.6e-4 (profiles/r01_model_err.json)
+MODEL_TOL = 2e-3  # R35 = R23 applied to the model step (observed maxima: profiles/r02_model_err.json)
 P = 16
 
 
 OBSERVED = {}  # largest error seen per quantity (written to gpurun_out/model_err.json if that exists)
 
 
-def rel_l2(got, want, what=None):
+def row_err(got, want, what=None):
+    """max over rows of ||got - want||_inf / ||want||_inf, a row = the last axis (a request's
+    logits; one head's K or V vector of d elements)."""
     got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
-    e = float((np.linalg.norm(got - want, axis=-1) / np.maximum(np.linalg.norm(want, axis=-1), 1e-30)).max())
+    assert got.shape == want.shape, (got.shape, want.shape)
+    got, want = got.reshape(-1, got.shape[-1]), want.reshape(-1, want.shape[-1])
+    e = float((np.abs(got - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)).max())
     if what:
         OBSERVED[what] = max(OBSERVED.get(what, 0.0), e)
     return e
@@ -41,7 +47,7 @@ def _record_errors():
     out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
     if OBSERVED and os.path.isdir(out):
         with open(os.path.join(out, "model_err.json"), "w") as f:
-            json.dump({"bar": MODEL_TOL, "observed_max_rel_l2": OBSERVED}, f, indent=1)
+            json.dump({"bar": MODEL_TOL, "observed_max_row_inf_rel": OBSERVED}, f, indent=1)
 
 
 def _read_kv(pool, s, req, pos, layer):
@@ -89,11 +95,11 @@ def test_model_step_parity(dbk, shape):
     st = pool.batch_stats()
     assert st["n_active"] == len(ids) and st["sum_ctx"] == sum(ctx) and st["table_mismatch"] == 0
     want, nk, nv, _ = om.decode_step(s, wseed, kv_seed, ids, ctx)
-    assert rel_l2(logits.cpu().numpy(), want, "logits") <= MODEL_TOL
+    assert row_err(logits.cpu().numpy(), want, "logits") <= MODEL_TOL
     for lay in range(s.layers):
         for i, (r, c) in enumerate(zip(ids, ctx)):
             k, v = _read_kv(pool, s, r, c - 1, lay)
-            assert rel_l2(k, nk[lay, i], "k") <= MODEL_TOL and rel_l2(v, nv[lay, i], "v") <= MODEL_TOL
+            assert row_err(k, nk[lay, i], "k") <= MODEL_TOL and row_err(v, nv[lay, i], "v") <= MODEL_TOL
     model.close()
     pool.close()
 
@@ -113,7 +119,7 @@ def test_model_two_steps_attend_to_model_written_kv(dbk):
     logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
     model.step(ids, logits)
     want, _, _, _ = om.decode_step(s, wseed, kv_seed, ids, [c + 1 for c in ctx], kv_written=written)
-    assert rel_l2(logits.cpu().numpy(), want, "logits_step2") <= MODEL_TOL
+    assert row_err(logits.cpu().numpy(), want, "logits_step2") <= MODEL_TOL
     model.close()
     pool.close()
 
@@ -128,10 +134,10 @@ def test_model_llama2_7b_layer_full_size(dbk):
     logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
     model.step(ids, logits)
     want, nk, nv, _ = om.decode_step(s, wseed, kv_seed, ids, ctx)
-    assert rel_l2(logits.cpu().numpy(), want, "logits_7b") <= MODEL_TOL
+    assert row_err(logits.cpu().numpy(), want, "logits_7b") <= MODEL_TOL
     for i, (r, c) in enumerate(zip(ids, ctx)):
         k, v = _read_kv(pool, s, r, c - 1, 0)
-        assert rel_l2(k, nk[0, i], "k_7b") <= MODEL_TOL and rel_l2(v, nv[0, i], "v_7b") <= MODEL_TOL
+        assert row_err(k, nk[0, i], "k_7b") <= MODEL_TOL and row_err(v, nv[0, i], "v_7b") <= MODEL_TOL
     model.close()
     pool.close()
 
@@ -203,12 +209,12 @@ def test_model_step_pd_chunks_and_decode_rows(dbk):
         rows = [(r, ctx[r] - 1) for r in ids] + [(C, s0 + j) for j in range(k)]
         want, w, _ = om.forward_rows(s, wseed, kv_seed, rows, kv_written=written)
         written.update(w)
-        assert rel_l2(logits.cpu().numpy(), want, "logits_pd") <= MODEL_TOL
+        assert row_err(logits.cpu().numpy(), want, "logits_pd") <= MODEL_TOL
         for lay in range(s.layers):
             for (r, p) in rows:
                 kk, vv = _read_kv(pool, s, r, p, lay)
-                assert rel_l2(kk, w[(r, p, lay)][0], "k_pd") <= MODEL_TOL
-                assert rel_l2(vv, w[(r, p, lay)][1], "v_pd") <= MODEL_TOL
+                assert row_err(kk, w[(r, p, lay)][0], "k_pd") <= MODEL_TOL
+                assert row_err(vv, w[(r, p, lay)][1], "v_pd") <= MODEL_TOL
     with pytest.raises(dbk.DbkError):  # a chunk beyond the reserved tokens
         model.step_pd(ids, [C], [38], [4])
     model.close()
@@ -275,7 +281,7 @@ def test_model_explicit_tokens_and_greedy_sampling(dbk):
     model.step_pd(ids, [], [], [], logits, tokens=tk, sampled=smp)
     want, _, _, _ = om.decode_step(s, wseed, kv_seed, ids, ctx, tokens=toks)
     got = logits.cpu().numpy()
-    assert rel_l2(got, want, "logits_tokens") <= MODEL_TOL
+    assert row_err(got, want, "logits_tokens") <= MODEL_TOL
     sm = smp.cpu().numpy()
     for i in range(len(ids)):
         assert sm[i] == int(np.argmax(got[i]))

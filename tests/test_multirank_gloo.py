@@ -53,7 +53,7 @@ def _worker(rank, world, port, q):
             # this rank: the same step on its own shard, at the step's (global) clock
             me_clock0 = want["clock_ns"]
             me.release_arrivals(me_clock0)
-            me.admit_and_grow(oeng.b_share(b, rank, world))
+            me.admit_and_grow(oeng.b_share(b, rank, world, steps))
             local = me.local_stats()
             me.retire()
             local["step_ns"] = step_ns + rank  # ranks measure differently; MAX is taken

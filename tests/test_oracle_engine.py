@@ -120,6 +120,26 @@ def test_dp_replay_all_ranks_share_decision():
     assert sum(oeng.b_share(b, k, 2) for b in range(100) for k in range(2)) == sum(range(100))
 
 
+def test_dp_share_rotates_and_small_b_is_live():
+    """R21: the shares always sum to b_t, differ by at most one, and the remainder rotates with
+    the step index; with a static b_t = 1 < G = 4 every rank still serves its shard (round 1
+    gave the remainder to the low ranks only, so ranks 1..3 never admitted)."""
+    for G in (2, 3, 4, 8):
+        for b in range(0, 40):
+            for t in range(2 * G):
+                sh = [oeng.b_share(b, k, G, t) for k in range(G)]
+                assert sum(sh) == b and max(sh) - min(sh) <= 1
+            # over G consecutive steps every rank gets the extra slot (b mod G) times
+            for k in range(G):
+                assert sum(oeng.b_share(b, k, G, t) for t in range(G)) == b
+    tr = trace.make_trace(24, 10, 8, 64, seed=11)
+    rp, recs = _replay(tr, 64, 16, policy.SchedConfig(policy=policy.STATIC, b_static=1), 4 * 64 * 16,
+                       lambda rp: 1_000_000, world=4)
+    assert sum(r["n_finished"] for r in recs) == len(tr)
+    # a rank keeps what it admitted under an earlier share: sum running <= G * ceil(b_t / G)
+    assert all(r["n_decode"] <= 4 for r in recs) and max(r["n_decode"] for r in recs) > 1
+
+
 # ------------------------------------------------------------------ synth
 def test_hashgen_values_exact_and_deterministic():
     v = hashgen.gen_values(5, hashgen.KIND_K, [1, 2], np.arange(7)[:, None], 3, 4, 64)

@@ -109,7 +109,7 @@ def test_pd_dp_two_ranks_shares():
     assert sum(r["n_finished"] for r in recs) == len(tr)
     for r in recs:   # rank k's budget is its share of b minus its own decode count
         for k, (ch, loc) in enumerate(zip(r["chunks"], r["local_stats"])):
-            assert sum(q for _, _, q in ch) <= max(0, oeng.b_share(r["b_t"], k, 2) - loc["n_active"])
+            assert sum(q for _, _, q in ch) <= max(0, oeng.b_share(r["b_t"], k, 2, r["t"]) - loc["n_active"])
 
 
 def test_pd_fixed_token_budget_reading():
