@@ -138,7 +138,7 @@ def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None)
 def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, time_attention=True,
                  out_dtype=0, seed=2024, n_req=None, policy=None, b_static=256, sla_ms=None, tp=1,
                  trace_override=None, eps_d_ms=None, pd_fusion=False, swap_bytes=0, full_model=False,
-                 free_bytes=None, pd_token_budget=0, tp_rank=0):
+                 free_bytes=None, pd_token_budget=0, tp_rank=0, per_layer_launches=False):
     """Pool sized from free HBM (cap = free - modeled fp16 weights of this GPU - reserve), or the
     config's fixed per-GPU cap; DP request shards (world) or KV-head TP (tp)."""
     import torch
@@ -174,7 +174,8 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
     eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap_total, seed=seed,
                      out_dtype=out_dtype, time_attention=time_attention,
                      rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0,
-                     pd_fusion=pd_fusion, preempt_mode=1 if swap_bytes else 0, pd_token_budget=pd_token_budget)
+                     pd_fusion=pd_fusion, preempt_mode=1 if swap_bytes else 0, pd_token_budget=pd_token_budget,
+                     per_layer_launches=per_layer_launches)
     model = None
     if full_model:  # NEXT row 3: QKV/O/MLP/LM-head GEMMs with synthetic fp16 weights around the attention
         if "model" not in c:
@@ -365,7 +366,8 @@ def run_gpu(args):
         free_bytes = int(f_t.item())
     S = setup_engine(device=local, rank=rank, world=world, cfg_name=args.config, policy=args.policy,
                      b_static=args.b_static, sla_ms=args.sla_ms, tp=tp, full_model=args.model,
-                     free_bytes=free_bytes, tp_rank=(args.tp_rank if args.tp_shard else rank) if tp > 1 else 0)
+                     free_bytes=free_bytes, tp_rank=(args.tp_rank if args.tp_shard else rank) if tp > 1 else 0,
+                     per_layer_launches=args.per_layer_launches)
     dbk = S["dbk"]
     eng = S["eng"]
     exchange_kind, comm = None, None
@@ -486,6 +488,9 @@ def run_gpu(args):
                        "parallelism": (f"rank {args.tp_rank} of tp{tp} (KV-head shard on one GPU; no exchange)"
                                        if args.tp_shard else
                                        f"tp{world} (KV-head shards)" if tp > 1 else f"dp{world} (request shards)"),
+                       "decode_launches": ("one PDL-chained launch per layer" if args.per_layer_launches or args.model
+                                           else "multi-layer persistent launches (dbk_decode_step_layers)"),
+                       "decode_launches_per_step": (round(sum(r["launches"] for r in recs) / max(len(recs), 1), 2)),
                        "stats_exchange": (dict(exchange_kind or {}, **({
                            "host_us_per_step": round(xch["us_total"] / max(xch["count"], 1), 2),
                            "exchanges": xch["count"],
@@ -606,6 +611,9 @@ def main():
                     help="70B GQA: run rank 0's KV-head shard of a TP-G job on this one GPU (per-GPU kernel rate)")
     ap.add_argument("--tp-rank", type=int, default=0, help="with --tp-shard: which rank's KV-head shard")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) run (profiling)")
+    ap.add_argument("--per-layer-launches", action="store_true",
+                    help="one PDL-chained decode launch per layer (as a model's step issues them) instead of "
+                         "multi-layer launches")
     ap.add_argument("--model", action="store_true",
                     help="full decode step: synthetic-weight QKV/O/MLP/LM-head GEMMs around the attention")
     args = ap.parse_args()

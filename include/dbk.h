@@ -183,6 +183,19 @@ typedef struct dbk_batch {
 dbk_status dbk_decode_step(dbk_pool *pool, const dbk_batch *batch, const void *q, void *out,
                            int32_t out_dtype, void *stream);
 
+/* The same attention for layers [batch->layer, batch->layer + n_layers) of the batch in as few
+ * persistent launches as the split-K workspace budget allows (all of them when it fits; the
+ * attention-only step, where every layer's q exists before the first launch): a task is
+ * (request chunk, kv head, layer), so the work queue spans the layers and no launch edge,
+ * ramp or tail separates them.  q of layer batch->layer + l at q + l*q_layer_stride
+ * elements, out at out + l*out_layer_stride elements (strides multiples of 8, >= 0).  With
+ * fuse_stats the first launch also reduces the statistics record; chain as above for the
+ * first launch (the later ones always chain).  launches_out (nullable): kernels launched.
+ * Results are identical to n_layers calls of dbk_decode_step.  Async. */
+dbk_status dbk_decode_step_layers(dbk_pool *pool, const dbk_batch *batch, int32_t n_layers, const void *q,
+                                  int64_t q_layer_stride, void *out, int64_t out_layer_stride, int32_t out_dtype,
+                                  void *stream, int32_t *launches_out);
+
 /* Batch statistics of the last fused launch (oracle O3).
  * 16 x int64 = 128 bytes.  step_ns and n_waiting are filled by the host
  * (engine) -- zero from dbk_batch_stats. */
@@ -319,6 +332,13 @@ dbk_status dbk_synth_fill(uint64_t seed, int32_t kind, int32_t n_rows, const int
 dbk_status dbk_probe_read_bandwidth(const void *buf, size_t bytes, int32_t device, void *stream,
                                     double *ms_out);
 
+/* Measurement utility (not part of the method): with DBK_TRACE_TASKS=N set when the pool is
+ * created, every decode warp task (K1/K2) appends a record of 4 x u64 -- start and end
+ * (%globaltimer ns), SM id << 32 | launch sequence, task << 32 | pages -- up to N records.
+ * Copies min(count, cap) records to host (nullable) and their number to n_out (0 without
+ * tracing); reset = 1 restarts the buffer.  Synchronises the device. */
+dbk_status dbk_pool_trace_d2h(dbk_pool *pool, void *host, int64_t cap, int64_t *n_out, int32_t reset);
+
 /* ------------------------------------------------------------------------ */
 /* Scheduler: Algorithm 1 (memory), Algorithm 2 (SLA), min, static          */
 /* ------------------------------------------------------------------------ */
@@ -396,7 +416,10 @@ typedef struct dbk_engine_config {
                                      * (R25: c_t = b_t - N^d).  > 0: a fixed token budget per *
                                      * iteration (R36: c_t = budget - N^d) while b_t still     *
                                      * bounds running + prefilling requests                    */
-    int32_t _reserved;
+    int32_t per_layer_launches;     /* device-resident decode-only steps: 0 = the layers go   *
+                                     * through dbk_decode_step_layers (multi-layer launches); *
+                                     * 1 = one PDL-chained launch per layer (as a model's     *
+                                     * layer-by-layer step would issue them)                  */
 } dbk_engine_config;
 
 typedef struct dbk_engine dbk_engine;

@@ -140,6 +140,16 @@ class KVPool:
         b = dbk_batch(len(ids), int(layer), 1 if fuse_stats else 0, 1 if chain else 0, pids)
         _lib.dbk_decode_step(self.h, C.byref(b), _ptr(q), _ptr(out), int(out_dtype), _stream(stream))
 
+    def decode_step_layers(self, req_ids, layer0, n_layers, q, q_layer_stride, out, out_layer_stride, out_dtype=2,
+                           fuse_stats=False, stream=None, chain=False):
+        """Layers [layer0, layer0 + n_layers) in multi-layer launches; returns the launch count."""
+        ids, pids = _i64(req_ids)
+        b = dbk_batch(len(ids), int(layer0), 1 if fuse_stats else 0, 1 if chain else 0, pids)
+        nl = C.c_int32()
+        _lib.dbk_decode_step_layers(self.h, C.byref(b), int(n_layers), _ptr(q), int(q_layer_stride), _ptr(out),
+                                    int(out_layer_stride), int(out_dtype), _stream(stream), C.byref(nl))
+        return nl.value
+
     def prefill_step(self, req_ids, q_start, q_len, layer, q, out, out_dtype=2, stream=None):
         ids, pids = _i64(req_ids)
         s0, ps0 = _i32(q_start)
@@ -243,7 +253,8 @@ class Engine:
 
     def __init__(self, pool: KVPool, sched: Scheduler, arrival_ns, l_in, l_out, mem_cap_bytes,
                  sla_ms=0.0, seed=0, out_dtype=2, time_attention=False, rank=0, world=1,
-                 q_scale_log2=0, req_ids=None, pd_fusion=False, preempt_mode=0, pd_token_budget=0):
+                 q_scale_log2=0, req_ids=None, pd_fusion=False, preempt_mode=0, pd_token_budget=0,
+                 per_layer_launches=False):
         self.pool, self.sched = pool, sched
         self._arr, pa = _i64(arrival_ns)
         self._li, pli = _i32(l_in)
@@ -254,7 +265,7 @@ class Engine:
         self.cfg = dbk_engine_config(len(self._arr), q_scale_log2, pa, pli, plo, pids,
                                      int(mem_cap_bytes), float(sla_ms), int(seed), int(out_dtype),
                                      1 if time_attention else 0, rank, world, 1 if pd_fusion else 0,
-                                     int(preempt_mode), int(pd_token_budget), 0)
+                                     int(preempt_mode), int(pd_token_budget), 1 if per_layer_launches else 0)
         h = C.c_void_p()
         _lib.dbk_engine_create(pool.h, sched.h, C.byref(self.cfg), C.byref(h))
         self.h = h

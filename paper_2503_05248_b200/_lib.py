@@ -86,7 +86,7 @@ class dbk_engine_config(C.Structure):
                 ("mem_cap_bytes", C.c_int64), ("sla_ms", C.c_double), ("synth_seed", C.c_uint64),
                 ("out_dtype", C.c_int32), ("time_attention", C.c_int32), ("rank", C.c_int32),
                 ("world", C.c_int32), ("pd_fusion", C.c_int32), ("preempt_mode", C.c_int32),
-                ("pd_token_budget", C.c_int32), ("_reserved", C.c_int32)]
+                ("pd_token_budget", C.c_int32), ("per_layer_launches", C.c_int32)]
 
 
 class dbk_engine_buffers(C.Structure):
@@ -172,6 +172,8 @@ SIGNATURES = {
     "dbk_stats_reduce": [C.POINTER(dbk_stats), I32, I32, C.POINTER(dbk_stats)],
     "dbk_engine_attach_comm": [P, P, I32],
     "dbk_comm_info": [P, PI32, PI32],
+    "dbk_pool_trace_d2h": [P, P, I64, PI64, I32],
+    "dbk_decode_step_layers": [P, C.POINTER(dbk_batch), I32, P, I64, P, I64, I32, P, PI32],
     "dbk_engine_last_exchange": [P, C.POINTER(dbk_stats), I32, PI32, C.POINTER(C.c_double),
                                  C.POINTER(C.c_double), PI64, I32],
 }

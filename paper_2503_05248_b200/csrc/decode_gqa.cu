@@ -94,7 +94,6 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
     uint8_t *wbuf = smem + warp * STAGES * STAGE;
     const uint64_t pol = evict_first_policy();
     // row of the pool-wide tensor map: [layer][page][kv_head][K|V][16 tokens] x D elements
-    const int64_t row_layer = static_cast<int64_t>(p.layer) * p.cap_pages;
 
     if (lane == 0) {
 #pragma unroll
@@ -102,21 +101,25 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
         fence_mbar_init();
     }
     __syncwarp();
-    int f0 = task_fetch(p, lane), f1 = task_fetch(p, lane), pend = task_fetch(p, lane);
+    const TaskPlan plan = task_plan(p, static_cast<int>(gridDim.x) * WARPS);
+    int f0 = task_claim(p, plan, lane), f1 = task_claim(p, plan, lane);
     f0 = __shfl_sync(kFull, f0, 0);
     f1 = __shfl_sync(kFull, f1, 0);
     Task cur = load_task(p, f0, lane), nxt = load_task(p, f1, lane);
+    bool released = pdl_try_release(p, lane), drained = false;
     uint32_t seq_iss = 0, cur_start = 0;
     auto top_up = [&](uint32_t seq_cons) {
         while (seq_iss < seq_cons + STAGES) {
             const int j = static_cast<int>(seq_iss - cur_start);
-            int ph, g;
+            int ph, g, lay;
             if (j < cur.it.n) {
                 ph = page_of(cur, j);
                 g = cur.g;
+                lay = cur.l;
             } else if (j - cur.it.n < nxt.it.n) {
                 ph = page_of(nxt, j - cur.it.n);
                 g = nxt.g;
+                lay = nxt.l;
             } else {
                 break;
             }
@@ -124,6 +127,7 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
                 const int s = seq_iss % STAGES;
                 fence_proxy_async();
                 mbar_expect_tx(&bars[warp][s], STAGE);
+                const int64_t row_layer = static_cast<int64_t>(p.layer + lay) * p.cap_pages;
                 const int tile = static_cast<int>((row_layer + ph) * p.kv_heads + g);
                 if (p.tma_rank == 5) {
                     tma_load_tile5(wbuf + s * STAGE, &tmap, tile, &bars[warp][s], pol);
@@ -142,7 +146,8 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
     top_up(0);
     // Q fragments (A operand): row gq = q-head g*GQ+gq, columns = head dims
     auto load_q = [&](const Task &t, uint32_t (&qa)[KSTEPS][2]) {
-        const T *qrow = reinterpret_cast<const T *>(p.q) + (static_cast<size_t>(t.it.i) * p.q_heads + t.g * GQ + gq) * D;
+        const T *qrow = reinterpret_cast<const T *>(p.q) + t.l * p.q_layer_stride +
+                        (static_cast<size_t>(t.it.i) * p.q_heads + t.g * GQ + gq) * D;
 #pragma unroll
         for (int kk = 0; kk < KSTEPS; ++kk) {
             qa[kk][0] = gq < GQ ? __ldg(reinterpret_cast<const uint32_t *>(qrow + 16 * kk + 2 * cq)) : 0u;
@@ -152,25 +157,26 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
     uint32_t qa[KSTEPS][2];
     load_q(cur, qa);
 
-    bool released = false;
     while (cur.task < p.n_tasks) {
-        // one task ahead: the metadata of the task after `nxt` and the q of `nxt`
-        const Task nnx = load_task(p, __shfl_sync(kFull, pend, 0), lane);
-        pend = task_fetch(p, lane);
-        if (!released && nnx.task >= p.n_tasks) {  // queue drained: only cur and nxt remain
-            pdl_release();
-            released = true;
-        }
+        if (!released) released = pdl_try_release(p, lane);
+        // the q of `nxt` (its metadata arrived during the previous task)
         uint32_t qn[KSTEPS][2];
         load_q(nxt, qn);
-        const int i = cur.it.i, c = cur.it.c, g = cur.g;
-        if (p.fuse_stats && c == 0 && g == 0) batch_stats_warp(p, p.req[i], lane);
+        const int i = cur.it.i, c = cur.it.c, g = cur.g, lay = cur.l;
+        const uint64_t t_task0 = p.trace ? globaltimer_ns() : 0;
+        if (p.fuse_stats && c == 0 && g == 0 && lay == 0) batch_stats_warp(p, p.req[i], lane);
         float o[NT][4];
 #pragma unroll
         for (int j = 0; j < NT; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
         float m = -INFINITY, l = 0.f;
 
+        int pend = 0;
+        bool claimed = false;
         for (int k = 0; k < cur.it.n; ++k) {
+            if (!claimed && k + 3 >= cur.it.n) {  // the task after `nxt`, three pages ahead of need
+                if (!drained) pend = task_claim(p, plan, lane);
+                claimed = true;
+            }
             const uint32_t jseq = cur_start + k;
             const int s = jseq % STAGES;
             mbar_wait(&bars[warp][s], (jseq / STAGES) & 1);
@@ -247,24 +253,31 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
         l += __shfl_xor_sync(kFull, l, 1);
         l += __shfl_xor_sync(kFull, l, 2);
         const bool split = cur.it.nchunks > 1;
+        const size_t obase = lay * p.out_layer_stride + static_cast<size_t>(i) * p.q_heads * D;
+        const int wb = lay * p.n_ws_rows + cur.it.chunk_base, ci = (lay * p.n + i) * p.kv_heads + g;
         if (gq < GQ) {
             const int h = g * GQ + gq;
             if (!split) {
                 const float inv = 1.f / l;
-                const size_t base = (static_cast<size_t>(i) * p.q_heads + h) * D + 2 * cq;
+                const size_t base = obase + static_cast<size_t>(h) * D + 2 * cq;
 #pragma unroll
                 for (int j = 0; j < NT; ++j) store2_out(p.out, base + 8 * j, p.out_dtype, o[j][0] * inv, o[j][1] * inv);
             } else {
-                const int wi = cur.it.chunk_base + c;
+                const int wi = wb + c;
                 float *w = p.ws_o + (static_cast<size_t>(wi) * p.q_heads + h) * D + 2 * cq;
 #pragma unroll
                 for (int j = 0; j < NT; ++j) *reinterpret_cast<float2 *>(w + 8 * j) = make_float2(o[j][0], o[j][1]);
                 if (cq == 0) p.ws_ml[static_cast<size_t>(wi) * p.q_heads + h] = make_float2(m, l);
             }
         }
-        if (split && split_arrive_last(p, i, g, cur.it.nchunks, lane))
-            split_merge_warp<GQ, D>(p, cur.it.chunk_base, cur.it.nchunks, i, g, lane);
+        if (split && split_arrive_last(p, ci, cur.it.nchunks, lane))
+            split_merge_warp<GQ, D>(p, wb, cur.it.nchunks, obase, g, ci, lane);
+        trace_task(p, t_task0, cur.task, cur.it.n, lane);
 
+        // the claimed task's metadata: it becomes `nxt` (its pages join the ring behind cur's)
+        const int nn = drained ? p.n_tasks : __shfl_sync(kFull, pend, 0);
+        drained = nn >= p.n_tasks;
+        const Task nnx = load_task(p, nn, lane);
         cur_start += cur.it.n;
         cur = nxt;
         nxt = nnx;
@@ -272,6 +285,11 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
         for (int kk = 0; kk < KSTEPS; ++kk) {
             qa[kk][0] = qn[kk][0];
             qa[kk][1] = qn[kk][1];
+        }
+        if (cur.task >= p.n_tasks && nxt.task < p.n_tasks) {  // no static second task: the claim is next
+            cur = nxt;
+            nxt = load_task(p, p.n_tasks, lane);
+            load_q(cur, qa);
         }
         top_up(cur_start);
     }
@@ -334,7 +352,12 @@ int gqa_variant() {
     static int v = -1;
     if (v < 0) {
         const char *e = std::getenv("DBK_GQA_WS");
-        v = (e && std::strcmp(e, "2x6") == 0) ? 1 : (e && std::strcmp(e, "8x3") == 0) ? 2 : 0;
+        v = 0;
+        if (e && std::strcmp(e, "2x6") == 0) v = 1;
+        if (e && std::strcmp(e, "8x3") == 0) v = 2;
+        if (e && std::strcmp(e, "1x3") == 0) v = 3;
+        if (e && std::strcmp(e, "2x3") == 0) v = 4;
+        if (e && std::strcmp(e, "1x4") == 0) v = 5;
     }
     return v;
 }
@@ -347,6 +370,9 @@ cudaError_t gqa_group(const DecodeParams &p, int group, int ctas, const CUtensor
         case 8:
             if (gqa_variant() == 1) return launch_gqa_v<T, D, 8, 2, 6>(p, tmap, s);
             if (gqa_variant() == 2) return launch_gqa_v<T, D, 8, 8, 3>(p, tmap, s);
+            if (gqa_variant() == 3) return launch_gqa_v<T, D, 8, 1, 3>(p, tmap, s);
+            if (gqa_variant() == 4) return launch_gqa_v<T, D, 8, 2, 3>(p, tmap, s);
+            if (gqa_variant() == 5) return launch_gqa_v<T, D, 8, 1, 4>(p, tmap, s);
             return launch_gqa_t<T, D, 8>(p, ctas, tmap, s);
         default: return cudaErrorInvalidValue;
     }

@@ -45,22 +45,26 @@ decode_kernel(const DecodeParams p) {
         fence_mbar_init();
     }
     __syncwarp();
-    int f0 = task_fetch(p, lane), f1 = task_fetch(p, lane), pend = task_fetch(p, lane);
+    const TaskPlan plan = task_plan(p, static_cast<int>(gridDim.x) * WARPS);
+    int f0 = task_claim(p, plan, lane), f1 = task_claim(p, plan, lane);
     f0 = __shfl_sync(kFull, f0, 0);
     f1 = __shfl_sync(kFull, f1, 0);
     Task cur = load_task(p, f0, lane), nxt = load_task(p, f1, lane);
+    bool released = pdl_try_release(p, lane), drained = false;
     uint32_t seq_iss = 0, cur_start = 0;
     // keep STAGES tiles in flight along this warp's page sequence (current, then next task)
     auto top_up = [&](uint32_t seq_cons) {
         while (seq_iss < seq_cons + STAGES) {
             const int j = static_cast<int>(seq_iss - cur_start);
-            int ph, g;
+            int ph, g, lay;
             if (j < cur.it.n) {
                 ph = page_of(cur, j);
                 g = cur.g;
+                lay = cur.l;
             } else if (j - cur.it.n < nxt.it.n) {
                 ph = page_of(nxt, j - cur.it.n);
                 g = nxt.g;
+                lay = nxt.l;
             } else {
                 break;
             }
@@ -69,7 +73,8 @@ decode_kernel(const DecodeParams p) {
                 fence_proxy_async();
                 mbar_expect_tx(&bars[warp][s], TILE);
                 bulk_g2s(wbuf + s * TILE,
-                         p.kv_layer + static_cast<size_t>(g) * TILE + static_cast<size_t>(ph) * p.page_stride,
+                         p.kv_layer + static_cast<size_t>(lay) * p.layer_stride + static_cast<size_t>(g) * TILE +
+                             static_cast<size_t>(ph) * p.page_stride,
                          TILE, &bars[warp][s], pol);
             }
             ++seq_iss;
@@ -81,25 +86,21 @@ decode_kernel(const DecodeParams p) {
 #pragma unroll
         for (int h = 0; h < GQ; ++h)
             qr[h] = __ldg(reinterpret_cast<const uint4 *>(
-                reinterpret_cast<const T *>(p.q) + (static_cast<size_t>(t.it.i) * p.q_heads + t.g * GQ + h) * D + dl * 8));
+                reinterpret_cast<const T *>(p.q) + t.l * p.q_layer_stride +
+                (static_cast<size_t>(t.it.i) * p.q_heads + t.g * GQ + h) * D + dl * 8));
     };
     uint4 qraw[GQ];
     load_q(cur, qraw);
 
-    bool released = false;
     while (cur.task < p.n_tasks) {
-        // one task ahead: metadata of the task after `nxt` and the q of `nxt` are requested
-        // now and used when they become current, so their latency hides behind this task
-        const Task nnx = load_task(p, __shfl_sync(kFull, pend, 0), lane);
-        pend = task_fetch(p, lane);
-        if (!released && nnx.task >= p.n_tasks) {  // queue drained: only cur and nxt remain
-            pdl_release();
-            released = true;
-        }
+        if (!released) released = pdl_try_release(p, lane);
+        // the q of `nxt` (its metadata arrived during the previous task) is requested now and
+        // used when it becomes current, so its latency hides behind this task
         uint4 qnext[GQ];
         load_q(nxt, qnext);
-        const int i = cur.it.i, c = cur.it.c, g = cur.g;
-        if (p.fuse_stats && c == 0 && g == 0) batch_stats_warp(p, p.req[i], lane);
+        const int i = cur.it.i, c = cur.it.c, g = cur.g, lay = cur.l;
+        const uint64_t t_task0 = p.trace ? globaltimer_ns() : 0;
+        if (p.fuse_stats && c == 0 && g == 0 && lay == 0) batch_stats_warp(p, p.req[i], lane);
 
         float q[GQ][8];  // pre-scaled to log2 units
 #pragma unroll
@@ -117,7 +118,13 @@ decode_kernel(const DecodeParams p) {
             for (int e = 0; e < 8; ++e) acc[t][e] = 0.f;
         }
 
+        int pend = 0;
+        bool claimed = false;
         for (int k = 0; k < cur.it.n; ++k) {
+            if (!claimed && k + 3 >= cur.it.n) {  // the task after `nxt`, three pages ahead of need
+                if (!drained) pend = task_claim(p, plan, lane);
+                claimed = true;
+            }
             const uint32_t jseq = cur_start + k;
             const int s = jseq % STAGES;
             mbar_wait(&bars[warp][s], (jseq / STAGES) & 1);
@@ -200,7 +207,9 @@ decode_kernel(const DecodeParams p) {
 
         // ---- end of task: merge the TG token groups with shuffles, then store or split-K
         const bool split = cur.it.nchunks > 1;
-        const int wi = cur.it.chunk_base + c;
+        const size_t obase = lay * p.out_layer_stride + static_cast<size_t>(i) * p.q_heads * D;
+        const int wb = lay * p.n_ws_rows + cur.it.chunk_base, ci = (lay * p.n + i) * p.kv_heads + g;
+        const int wi = wb + c;
 #pragma unroll
         for (int t = 0; t < GQ; ++t) {
             float M = m[t];
@@ -222,7 +231,7 @@ decode_kernel(const DecodeParams p) {
                     const float inv = 1.f / L;
 #pragma unroll
                     for (int e = 0; e < 8; ++e) a[e] *= inv;
-                    store8_out(p.out, (static_cast<size_t>(i) * p.q_heads + h) * D + dl * 8, p.out_dtype, a);
+                    store8_out(p.out, obase + static_cast<size_t>(h) * D + dl * 8, p.out_dtype, a);
                 } else {
                     float4 *w = reinterpret_cast<float4 *>(p.ws_o + (static_cast<size_t>(wi) * p.q_heads + h) * D + dl * 8);
                     w[0] = make_float4(a[0], a[1], a[2], a[3]);
@@ -231,14 +240,24 @@ decode_kernel(const DecodeParams p) {
                 }
             }
         }
-        if (split && split_arrive_last(p, i, g, cur.it.nchunks, lane))
-            split_merge_warp<GQ, D>(p, cur.it.chunk_base, cur.it.nchunks, i, g, lane);
+        if (split && split_arrive_last(p, ci, cur.it.nchunks, lane))
+            split_merge_warp<GQ, D>(p, wb, cur.it.nchunks, obase, g, ci, lane);
+        trace_task(p, t_task0, cur.task, cur.it.n, lane);
 
+        // the claimed task's metadata: it becomes `nxt` (its pages join the ring behind cur's)
+        const int nn = drained ? p.n_tasks : __shfl_sync(kFull, pend, 0);
+        drained = nn >= p.n_tasks;
+        const Task nnx = load_task(p, nn, lane);
         cur_start += cur.it.n;
         cur = nxt;
         nxt = nnx;
 #pragma unroll
         for (int t = 0; t < GQ; ++t) qraw[t] = qnext[t];
+        if (cur.task >= p.n_tasks && nxt.task < p.n_tasks) {  // no static second task: the claim is next
+            cur = nxt;
+            nxt = load_task(p, p.n_tasks, lane);
+            load_q(cur, qraw);
+        }
         top_up(cur_start);
     }
     task_exit(p, lane, static_cast<int>(gridDim.x) * WARPS);

@@ -190,6 +190,7 @@ __device__ __forceinline__ void batch_stats_warp(const DecodeParams &p, const Re
 struct Task {
     int task;        // >= n_tasks: no task
     int g;           // kv head
+    int l;           // layer within the launch
     ItemMeta it;     // the work item (request chunk)
     int phys_lane;   // physical page of the chunk's k-th page, held by lane k (k < 32)
     int phys_lane2;  // ... of page 32 + k
@@ -200,6 +201,28 @@ __device__ __forceinline__ int page_of(const Task &t, int j) {
     return __shfl_sync(kFull, j < 32 ? t.phys_lane : t.phys_lane2, j & 31);
 }
 
+// ------------------------------------------------------------------ task timeline (measurement)
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// One record per finished task when p.trace is set (DBK_TRACE_TASKS): start / end (globaltimer
+// ns), SM id | launch sequence, task | pages.  Lane 0 only; a no-op in production.
+__device__ __forceinline__ void trace_task(const DecodeParams &p, uint64_t t0, int task, int pages, int lane) {
+    if (p.trace == nullptr || lane != 0) return;
+    const uint64_t t1 = globaltimer_ns();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    const unsigned long long k = atomicAdd(p.trace, 1ull);
+    if (k >= static_cast<unsigned long long>(p.trace_cap)) return;
+    unsigned long long *r = p.trace + 4 * (k + 1);
+    r[0] = t0;
+    r[1] = t1;
+    r[2] = (static_cast<uint64_t>(smid) << 32) | static_cast<uint32_t>(p.trace_seq);
+    r[3] = (static_cast<uint64_t>(static_cast<uint32_t>(task)) << 32) | static_cast<uint32_t>(pages);
+}
+
 // Two independent loads (item record, page ids): issued one task ahead of use.
 __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int lane) {
     Task t;
@@ -207,13 +230,16 @@ __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int l
     t.phys_lane = 0;
     t.phys_lane2 = 0;
     t.g = 0;
+    t.l = 0;
     if (task >= p.n_tasks) {
         t.task = p.n_tasks;
         t.it = ItemMeta{0, 0, 0, 0, 1, 0, 1, 0};
         return t;
     }
-    const int item = task / p.kv_heads;
-    t.g = task - item * p.kv_heads;
+    const int ih = task / p.n_layers;
+    t.l = task - ih * p.n_layers;
+    const int item = ih / p.kv_heads;
+    t.g = ih - item * p.kv_heads;
     const int4 *im = reinterpret_cast<const int4 *>(p.items + item);
     const int4 a = __ldg(im), b = __ldg(im + 1);
     t.it = ItemMeta{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
@@ -222,28 +248,49 @@ __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int l
     return t;
 }
 
-// lane 0 takes the next task index (the caller broadcasts it when it needs it, so the
-// atomic's latency hides behind the current task)
-__device__ __forceinline__ int task_fetch(const DecodeParams &p, int lane) {
+// Task assignment (the host sorts the work list longest-first): tasks are claimed from an
+// atomic counter -- two at the start (the current one and the next, whose pages the ring
+// streams across the boundary), then each further one only when the warp nears the end of its
+// current task.  A warp never holds more than one unstarted task beyond the next: claiming
+// three or four ahead (round 1) left a third of the warps without work when there are ~2
+// tasks per warp (70B TP shards, task trace); static assignment instead stalls on the CTAs
+// that become resident late under programmatic dependent launch.
+struct TaskPlan {
+    int nw;    // warps of the grid
+};
+__device__ __forceinline__ TaskPlan task_plan(const DecodeParams &, int nw) {
+    TaskPlan t;
+    t.nw = nw;
+    return t;
+}
+// lane 0 claims the next task; the value is valid in lane 0 only (broadcast at use, so the
+// atomic's latency hides behind the current task's pages)
+__device__ __forceinline__ int task_claim(const DecodeParams &p, const TaskPlan &, int lane) {
     return lane == 0 ? atomicAdd(p.task_counter, 1) : 0;
 }
 
-// Programmatic dependent launch, released early: once a warp has fetched past the end of the
-// task queue (only the tasks it holds remain), it waits for the PREVIOUS decode grid to
-// complete and lets the NEXT one launch.  Every CTA reaches this point as the queue drains, so
-// the next grid's CTAs take each SM as soon as one of this grid's CTAs exits -- they fill this
-// grid's tail instead of starting after it.  The next grid uses the other parity of scratch,
-// whose last user (the grid before this one) has completed by then.
-__device__ __forceinline__ void pdl_release() {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+// Programmatic dependent launch, released without blocking: the NEXT decode grid reuses the
+// scratch parity (task counter, split-K workspace and arrival counters) of the PREVIOUS one,
+// so this grid lets it launch once the previous grid's last warp has reset that scratch and
+// published its sequence number in done_seq.  Polled at task boundaries (a warp never stalls
+// for the previous grid while it has work); every grid's CTAs trigger or exit, and they exit
+// only after griddepcontrol.wait (task_exit), so the chain is safe either way.
+__device__ __forceinline__ bool pdl_try_release(const DecodeParams &p, int lane) {
+    int ok = 0;
+    if (lane == 0) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.done_seq) : "memory");
+        ok = v >= p.seq - 1;
+    }
+    ok = __shfl_sync(kFull, ok, 0);
+    if (ok) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    return ok != 0;
 }
 
-// A warp with no task left: the last one resets the counters for the next launch.
-// Programmatic dependent launch: the warp first waits for the PREVIOUS decode grid to complete
-// (a no-op without the launch attribute), then lets the NEXT one launch.  So when the next
-// grid starts (its own parity of scratch), the grid before this one -- the last user of that
-// parity -- has completed, and the next grid's CTAs fill the SMs this grid's tail leaves idle.
+// A warp with no task left.  It first waits for the PREVIOUS decode grid to complete (a no-op
+// without the launch attribute) -- a CTA's exit also releases the next grid, which must find
+// the previous grid's scratch reset -- then counts itself out; the last warp resets the task
+// counters and publishes this grid's sequence number (release) for the next grid's trigger.
 __device__ __forceinline__ void task_exit(const DecodeParams &p, int lane, int total_warps) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -253,13 +300,16 @@ __device__ __forceinline__ void task_exit(const DecodeParams &p, int lane, int t
         if (e == total_warps - 1) {
             p.task_counter[0] = 0;
             p.task_counter[1] = 0;
+            __threadfence();
+            asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p.done_seq), "r"(p.seq) : "memory");
         }
     }
 }
 
 // Split-K bookkeeping after a warp wrote its chunk's partial: returns true in every lane
 // of the warp whose chunk arrived last for (request, kv head); that warp merges.
-__device__ __forceinline__ bool split_arrive_last(const DecodeParams &p, int i, int g, int nchunks, int lane) {
+// ci = the (layer, request, kv head) counter index.
+__device__ __forceinline__ bool split_arrive_last(const DecodeParams &p, int ci, int nchunks, int lane) {
     // The warp's partial stores happen-before lane 0's acq_rel RMW (__syncwarp + cumulativity),
     // which releases them at gpu scope; the last arriver's acquire makes every chunk's partial
     // visible (read with ld.global.cg, which bypasses L1) -- no full fences / L1 invalidation.
@@ -269,7 +319,7 @@ __device__ __forceinline__ bool split_arrive_last(const DecodeParams &p, int i, 
         int prev;
         asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
                      : "=r"(prev)
-                     : "l"(p.counters + i * p.kv_heads + g)
+                     : "l"(p.counters + ci)
                      : "memory");
         last = prev == nchunks - 1;
     }
@@ -277,10 +327,12 @@ __device__ __forceinline__ bool split_arrive_last(const DecodeParams &p, int i, 
     return last != 0;
 }
 
-// The last warp merges the chunks' (m, l, O) of q-heads g*GQ .. g*GQ+GQ-1 and writes out.
+// The last warp merges the chunks' (m, l, O) of q-heads g*GQ .. g*GQ+GQ-1 (workspace rows
+// wbase .. wbase+nchunks-1) and writes out at element obase + h*D (obase = the layer's and
+// request's output row); ci = the arrival counter it resets.
 template <int GQ, int D>
-__device__ __forceinline__ void split_merge_warp(const DecodeParams &p, int chunk_base, int nchunks, int i,
-                                                 int g, int lane) {
+__device__ __forceinline__ void split_merge_warp(const DecodeParams &p, int wbase, int nchunks, size_t obase,
+                                                 int g, int ci, int lane) {
     // Online merge over the chunks: lane owns dims lane*PL .. lane*PL+PL-1 of all GQ heads;
     // each chunk's loads (GQ (m, l) pairs + GQ x PL partial sums) are independent of the
     // running state, so they are in flight together.
@@ -294,7 +346,7 @@ __device__ __forceinline__ void split_merge_warp(const DecodeParams &p, int chun
         for (int e = 0; e < PL; ++e) acc[t][e] = 0.f;
     }
     for (int x = 0; x < nchunks; ++x) {
-        const size_t w0 = static_cast<size_t>(chunk_base + x) * p.q_heads + g * GQ;
+        const size_t w0 = static_cast<size_t>(wbase + x) * p.q_heads + g * GQ;
         float2 ml[GQ];
         float v[GQ][PL];
 #pragma unroll
@@ -318,11 +370,11 @@ __device__ __forceinline__ void split_merge_warp(const DecodeParams &p, int chun
 #pragma unroll
     for (int t = 0; t < GQ; ++t) {
         const float inv = 1.f / L[t];
-        const size_t ob = (static_cast<size_t>(i) * p.q_heads + g * GQ + t) * D + lane * PL;
+        const size_t ob = obase + static_cast<size_t>(g * GQ + t) * D + lane * PL;
 #pragma unroll
         for (int e = 0; e < PL; e += 2) store2_out(p.out, ob + e, p.out_dtype, acc[t][e] * inv, acc[t][e + 1] * inv);
     }
-    if (lane == 0) p.counters[i * p.kv_heads + g] = 0;
+    if (lane == 0) p.counters[ci] = 0;
 }
 
 

@@ -142,6 +142,8 @@ dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_
     if (c.pd_fusion != 0 && c.pd_fusion != 1) return fail(DBK_EINVAL, "engine_create: pd_fusion must be 0 or 1");
     if (c.pd_fusion && !pool->has_ptmap) return fail(DBK_EINVAL, "engine_create: PD fusion needs the pool's prefill tensor map");
     if (c.preempt_mode != 0 && c.preempt_mode != 1) return fail(DBK_EINVAL, "engine_create: preempt_mode must be 0 or 1");
+    if (c.per_layer_launches != 0 && c.per_layer_launches != 1)
+        return fail(DBK_EINVAL, "engine_create: per_layer_launches must be 0 or 1");
     if (c.pd_token_budget < 0 || (c.pd_token_budget > 0 && !c.pd_fusion))
         return fail(DBK_EINVAL, "engine_create: pd_token_budget needs pd_fusion and must be >= 0");
     if (c.preempt_mode == 1 && (c.pd_fusion || !pool->swap_host))
@@ -463,7 +465,11 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     dbk_batch bt;
     bt.n = n;
     bt.req_ids = e->batch_ids.data();
-    if (n > 0) DBK_TRY(prepare_batch(p, n, e->batch_ids.data(), s));
+    // device-resident decode-only step: every layer's q exists before the first attention
+    // launch, so the layers go through multi-layer launches unless per-layer ones were asked for
+    const bool chained = !e2e && n_pf_rows == 0 && n > 0 && !e->model;
+    const bool multi = chained && !e->cfg.per_layer_launches;
+    if (n > 0) DBK_TRY(prepare_batch(p, n, e->batch_ids.data(), s, multi ? pc.layers : 1));
     if (n > 0 && !e2e && !e->model) {  // synthetic q of all layers (stands in for the QKV projection), one launch
         DBK_CUDA(launch_synth_q(e->cfg.synth_seed, p->d_req, n, pc.layers, pc.max_requests, pc.q_heads,
                                 pc.kv_head_offset * (pc.q_heads / pc.kv_heads), pc.head_dim, e->cfg.q_scale_log2, pc.kv_dtype, bufs->q_dev, s));
@@ -499,7 +505,6 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     }
     // device-resident decode-only steps chain the layer launches (programmatic dependent
     // launch: layer l+1's CTAs fill layer l's tail); then the attention time is one window
-    const bool chained = !e2e && n_pf_rows == 0 && n > 0 && !e->model;
     const bool per_layer_ev = e->cfg.time_attention && n > 0 && !chained && !e->model;
     if (e->cfg.time_attention && chained) DBK_CUDA(cudaEventRecord(e->att0[0], s));
     if (e->model) {
@@ -529,7 +534,16 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             e->step_d2h += static_cast<int64_t>(n) * 4;
         }
     }
-    for (int l = 0; l < (e->model ? 0 : pc.layers); ++l) {
+    if (multi) {
+        bt.layer = 0;
+        bt.fuse_stats = 1;
+        bt.chain = 0;
+        const int64_t ls = static_cast<int64_t>(pc.max_requests) * pc.q_heads * pc.head_dim;
+        DBK_TRY(dbk_decode_step_layers(p, &bt, pc.layers, bufs->q_dev, ls, bufs->out_dev, ls, e->cfg.out_dtype, s,
+                                       nullptr));
+        for (int l = 0; l < pc.layers; ++l) e->layer_bytes[l] = p->last_decode_bytes;
+    }
+    for (int l = 0; l < (e->model || multi ? 0 : pc.layers); ++l) {
         uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
         uint8_t *od = static_cast<uint8_t *>(bufs->out_dev) + static_cast<size_t>(l) * pc.max_requests * orow;
         bt.layer = l;

@@ -14,7 +14,7 @@ struct ReqMeta {
     int32_t slot;        // block-table row
     int32_t ctx;         // tokens in KV incl. this step's token
     int32_t l_in, l_out; // for the finishing statistics (O3)
-    int32_t chunk_base;  // first work item of this request (split-K workspace row)
+    int32_t chunk_base;  // first split-K workspace row of this request (if nchunks > 1)
     int32_t nchunks;     // work items of this request
 };
 static_assert(sizeof(ReqMeta) == 32, "ReqMeta layout");
@@ -27,7 +27,7 @@ struct ItemMeta {
     int32_t c;            // chunk index within the request
     int32_t pg0, n;       // first logical page and page count
     int32_t ctx;          // tokens of the request (incl. this step's)
-    int32_t chunk_base;   // first work item of the request (split-K workspace rows)
+    int32_t chunk_base;   // first split-K workspace row of the request (if nchunks > 1)
     int32_t nchunks;      // work items of the request
     int32_t slot;         // block-table row (statistics)
 };
@@ -35,7 +35,7 @@ static_assert(sizeof(ItemMeta) == 32, "ItemMeta layout");
 constexpr int kItemPages = 64;
 
 struct DecodeParams {
-    const uint8_t *kv_layer;     // KV base of this layer
+    const uint8_t *kv_layer;     // KV base of the first layer of this launch (`layer`)
     int64_t page_stride;         // bytes per (layer, page): kv_heads * tile_bytes
     const int32_t *block_table;  // [max_requests][bt_stride]
     int32_t bt_stride;
@@ -60,8 +60,15 @@ struct DecodeParams {
     int32_t *stats_done;         // zero between launches
     int64_t cap_pages;
     // K2 (tensor-core GQA) addressing through the pool-wide 2-D tensor map
-    int32_t layer;
+    int32_t layer;               // first layer of this launch
     int32_t kv_heads;
+    // one launch may stream n_layers consecutive layers (attention-only step: every layer's q is
+    // ready before the first launch); task t = ((item * kv_heads + head) * n_layers + l)
+    int32_t n_layers;
+    int64_t layer_stride;        // bytes between layers in the pool
+    int64_t q_layer_stride;      // elements between layers of q
+    int64_t out_layer_stride;    // elements between layers of out
+    int32_t n_ws_rows;           // split-K workspace rows per layer (counters: n per layer)
     // persistent CTAs: tasks t = work_item * kv_heads + kv_head handed out by an atomic
     // counter; task_counter[0] = next task, [1] = exited CTAs (both reset by the last CTA)
     int32_t n_tasks;
@@ -70,6 +77,12 @@ struct DecodeParams {
     // 1: programmatic dependent launch after the previous decode launch on the stream (its
     // scratch -- split-K workspace, arrival and task counters -- is the other parity's)
     int32_t pdl;
+    int32_t seq;                 // this decode launch's sequence number (>= 1, per pool)
+    int32_t *done_seq;           // sequence number of the last decode grid whose scratch is reset
+    // measurement only (DBK_TRACE_TASKS): per-task timeline records, null in production runs
+    unsigned long long *trace;   // [0] = record counter, records of 4 x u64 from index 4
+    int32_t trace_cap;           // records
+    int32_t trace_seq;           // launch sequence number stamped into the records
 };
 
 // Launch with (pdl) or without the programmatic-stream-serialization attribute.

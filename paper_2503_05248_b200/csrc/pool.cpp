@@ -144,6 +144,12 @@ static bool make_pool_tmap(dbk_pool *p, bool try5, CUtensorMap *dst, int *rank) 
     return r == CUDA_SUCCESS;
 }
 
+// split-K arrival counters of one scratch parity: one per (layer, request slot, kv head), so a
+// launch may stream every layer (dbk_decode_step_layers)
+static size_t counters_per_parity(const dbk_pool_config *c) {
+    return static_cast<size_t>(c->layers) * c->max_requests * c->kv_heads;
+}
+
 static bool pool_cfg_ok(const dbk_pool_config *c) {
     if (!c) return false;
     if (c->layers < 1 || c->q_heads < 1 || c->kv_heads < 1 || c->q_heads % c->kv_heads) return false;
@@ -196,8 +202,8 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     };
     if (cudaMalloc(&p->d_bt, bt_n * sizeof(int32_t)) != cudaSuccess ||
         cudaMemset(p->d_bt, 0xFF, bt_n * sizeof(int32_t)) != cudaSuccess ||
-        cudaMalloc(&p->d_counters, 2 * static_cast<size_t>(cfg->max_requests) * cfg->kv_heads * sizeof(int32_t)) != cudaSuccess ||
-        cudaMemset(p->d_counters, 0, 2 * static_cast<size_t>(cfg->max_requests) * cfg->kv_heads * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&p->d_counters, 2 * counters_per_parity(cfg) * sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(p->d_counters, 0, 2 * counters_per_parity(cfg) * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&p->d_stats, 128 + 64) != cudaSuccess ||
         cudaMemset(p->d_stats, 0, 128 + 64) != cudaSuccess ||
         cudaMallocHost(&p->h_stats, sizeof(dbk_stats)) != cudaSuccess ||
@@ -205,6 +211,7 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
         return cleanup(fail(DBK_ECUDA, "pool_create: %s", cudaGetErrorString(cudaGetLastError())));
     p->d_stats_done = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(p->d_stats) + 128);
     p->d_task_counter = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(p->d_stats) + 160);
+    p->d_done_seq = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(p->d_stats) + 176);
     p->host_bt.assign(bt_n, -1);
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -219,6 +226,23 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     p->ctas_per_sm = p->has_tmap ? decode_gqa_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group)
                                  : decode_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group);
     if (const char *e = std::getenv("DBK_NO_PDL")) p->pdl_enabled = !(e[0] == '1');  // A/B runs
+    if (const char *e = std::getenv("DBK_WS_BUDGET_MB")) {  // tuning override: layers per launch
+        const long long v = std::atoll(e);
+        if (v >= 1) p->ws_budget_bytes = v << 20;
+    }
+    if (const char *e = std::getenv("DBK_LAYERS_PER_LAUNCH")) {  // test / tuning cap on layers per launch
+        const long long v = std::atoll(e);
+        if (v >= 1) p->max_layers_per_launch = static_cast<int32_t>(v);
+    }
+    if (const char *e = std::getenv("DBK_TRACE_TASKS")) {  // measurement: task timeline records
+        const long long v = std::atoll(e);
+        if (v > 0 && v <= (1 << 24)) {
+            const size_t bytes = static_cast<size_t>(v + 1) * 32;
+            if (cudaMalloc(&p->d_trace, bytes) != cudaSuccess || cudaMemset(p->d_trace, 0, bytes) != cudaSuccess)
+                return cleanup(fail(DBK_ECUDA, "pool_create: trace buffer"));
+            p->trace_cap = static_cast<int32_t>(v);
+        }
+    }
     if (const char *e = std::getenv("DBK_TASKS_PER_WARP")) {  // tuning override
         const long long v = std::atoll(e);
         if (v >= 1 && v <= 16) p->tasks_per_warp = v;
@@ -236,6 +260,7 @@ dbk_status dbk_kv_pool_destroy(dbk_pool *p) {
     cudaSetDevice(p->cfg.device);
     cudaDeviceSynchronize();
     if (p->d_bt) cudaFree(p->d_bt);
+    if (p->d_trace) cudaFree(p->d_trace);
     if (p->d_counters) cudaFree(p->d_counters);
     if (p->d_stats) cudaFree(p->d_stats);
     if (p->h_stats) cudaFreeHost(p->h_stats);
@@ -634,9 +659,9 @@ namespace dbk {
 // Build (or reuse) the device metadata of a decode batch: per-request ReqMeta and
 // the split-K work list.  Reused while the batch and the pool state are unchanged
 // (the L per-layer launches of one step upload once).
-dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_t s) {
+dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_t s, int32_t layers_hint) {
     if (p->meta_valid && p->meta_epoch == p->epoch && p->meta_ids.size() == static_cast<size_t>(n) &&
-        std::equal(p->meta_ids.begin(), p->meta_ids.end(), ids))
+        p->meta_layers_hint == layers_hint && std::equal(p->meta_ids.begin(), p->meta_ids.end(), ids))
         return DBK_OK;
     const int64_t P = p->cfg.page_size;
     p->meta_req.resize(n);
@@ -654,28 +679,32 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
         m.l_out = r.l_out;
         total_pages += (r.ctx + P - 1) / P;
     }
-    // chunk size (pages per warp task, 4..32): ~tasks_per_warp (3) tasks per resident warp so
-    // the dynamic queue balances, but not below 12 pages while every warp still gets a task:
-    // each task pays fixed costs (metadata, q, split-K partial + merge) -- measured on the
-    // per-GPU shards of 70B KV-head TP (profiles/r01_tune_chunks.txt): 12 pages beat 6 by 13 %
-    // at TP8, 15 beat 12 by 4 % at TP4
+    // chunk size (pages per warp task, 4..32): ~tasks_per_warp (3) tasks per resident warp of
+    // ONE launch so the dynamic queue balances, but not below 12 pages while every warp still
+    // gets a task: each task pays fixed costs (metadata, q, split-K partial + merge) -- measured
+    // on the per-GPU shards of 70B KV-head TP (profiles/r01_tune_chunks.txt): 12 pages beat 6
+    // by 13 % at TP8, 15 beat 12 by 4 % at TP4.  A launch streams layers_hint layers, so its
+    // queue holds that many times the work: multi-layer launches take 32-page chunks, where
+    // most requests are one task and need no split-K (profiles/r02_tune_chunks_ml.txt: TP8
+    // 5.57 -> 6.66 TB/s from 12 to 32 pages)
     const int64_t warps = static_cast<int64_t>(p->num_sms) * p->ctas_per_sm * 4;
     const int64_t tpw = p->tasks_per_warp;
-    const int64_t work = total_pages * p->cfg.kv_heads;
+    const int64_t work = total_pages * p->cfg.kv_heads * std::max(layers_hint, 1);
     int64_t cp = (work + tpw * warps - 1) / (tpw * warps);
     cp = std::max<int64_t>(cp, std::min<int64_t>(12, (work + warps - 1) / warps));
     cp = std::max<int64_t>(4, std::min<int64_t>(p->max_chunk_pages, cp));
     if (p->force_chunk_pages > 0) cp = std::min<int64_t>(p->force_chunk_pages, p->max_chunk_pages);
     p->meta_work.clear();
-    int32_t base = 0;
+    int32_t base = 0, ws_rows = 0;
     for (int i = 0; i < n; ++i) {
         ReqMeta &m = p->meta_req[i];
         const int32_t pages = static_cast<int32_t>((m.ctx + P - 1) / P);
         const int32_t nc = static_cast<int32_t>((pages + cp - 1) / cp);
-        m.chunk_base = base;
+        m.chunk_base = nc > 1 ? ws_rows : 0;  // split-K rows only for requests that are split
         m.nchunks = nc;
         for (int32_t c = 0; c < nc; ++c) p->meta_work.push_back(make_int2(i, c));
         base += nc;
+        if (nc > 1) ws_rows += nc;
     }
     // longest task first: the dynamic queue then ends on short tasks (small tail)
     std::stable_sort(p->meta_work.begin(), p->meta_work.end(), [&](const int2 &a, const int2 &b) {
@@ -684,6 +713,7 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
         return pa > pb;
     });
     p->meta_items = base;
+    p->meta_ws_rows = ws_rows;
     p->meta_chunk_pages = static_cast<int32_t>(cp);
     // blob: ReqMeta[n] | ItemMeta[items] | int32 item_pages[items][32] (physical page ids
     // from the host tables, which the device tables mirror -- K4 checks them every step)
@@ -715,20 +745,7 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
     p->d_req = static_cast<const ReqMeta *>(p->up_meta.dev);
     p->d_items = reinterpret_cast<const ItemMeta *>(static_cast<const uint8_t *>(p->up_meta.dev) + rb);
     p->d_item_pages = reinterpret_cast<const int32_t *>(static_cast<const uint8_t *>(p->up_meta.dev) + rb + ib);
-    // split-K workspace
-    const size_t need = static_cast<size_t>(base) * p->cfg.q_heads;
-    if (need > p->ws_cap) {
-        size_t c = std::max<size_t>(need, p->ws_cap * 2);
-        DBK_CUDA(cudaStreamSynchronize(s));
-        if (p->d_ws_o) cudaFree(p->d_ws_o);
-        if (p->d_ws_ml) cudaFree(p->d_ws_ml);
-        p->d_ws_o = nullptr;
-        p->d_ws_ml = nullptr;
-        p->ws_cap = 0;
-        DBK_CUDA(cudaMalloc(&p->d_ws_o, 2 * c * p->cfg.head_dim * sizeof(float)));  // two parities
-        DBK_CUDA(cudaMalloc(&p->d_ws_ml, 2 * c * sizeof(float2)));
-        p->ws_cap = c;
-    }
+    p->meta_layers_hint = layers_hint;
     p->meta_ids.assign(ids, ids + n);
     p->meta_epoch = p->epoch;
     p->meta_valid = true;
@@ -750,27 +767,35 @@ int64_t decode_bytes(const dbk_pool *p, int out_dtype) {
 
 }  // namespace dbk
 
-extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const void *q, void *out,
-                                      int32_t out_dtype, void *stream) {
-    if (!p || !b) return fail(DBK_EINVAL, "decode_step: null argument");
-    if (b->n < 0 || (b->n > 0 && (!b->req_ids || !q || !out))) return fail(DBK_EINVAL, "decode_step: bad arrays");
-    if (b->layer < 0 || b->layer >= p->cfg.layers) return fail(DBK_EINVAL, "decode_step: layer out of range");
-    if (out_dtype < 0 || out_dtype > 2) return fail(DBK_EINVAL, "decode_step: out_dtype must be 0, 1 or 2");
-    if (b->n > p->cfg.max_requests) return fail(DBK_EINVAL, "decode_step: n > max_requests");
-    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
-        return fail(DBK_EINVAL, "decode_step: q and out must be 16-byte aligned");
-    DBK_CUDA(cudaSetDevice(p->cfg.device));
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    DBK_TRY(flush_deltas(p, s));
-    if (b->fuse_stats) DBK_CUDA(cudaMemsetAsync(p->d_stats, 0, 128, s));
-    if (b->n == 0) return DBK_OK;
-    DBK_TRY(prepare_batch(p, b->n, b->req_ids, s));
+namespace dbk {
+
+// Split-K workspace for nl layers of the prepared batch (two scratch parities).
+static dbk_status ensure_ws(dbk_pool *p, int32_t nl, cudaStream_t s) {
+    const size_t need = static_cast<size_t>(std::max(p->meta_ws_rows, 1)) * nl * p->cfg.q_heads;
+    if (need <= p->ws_cap) return DBK_OK;
+    const size_t c = std::max<size_t>(need, p->ws_cap * 2);
+    DBK_CUDA(cudaStreamSynchronize(s));
+    if (p->d_ws_o) cudaFree(p->d_ws_o);
+    if (p->d_ws_ml) cudaFree(p->d_ws_ml);
+    p->d_ws_o = nullptr;
+    p->d_ws_ml = nullptr;
+    p->ws_cap = 0;
+    DBK_CUDA(cudaMalloc(&p->d_ws_o, 2 * c * p->cfg.head_dim * sizeof(float)));  // two parities
+    DBK_CUDA(cudaMalloc(&p->d_ws_ml, 2 * c * sizeof(float2)));
+    p->ws_cap = c;
+    return DBK_OK;
+}
+
+// One persistent launch over layers [layer0, layer0 + nl) of the prepared batch.
+static dbk_status decode_launch(dbk_pool *p, int32_t n, int32_t layer0, int32_t nl, const void *q, int64_t q_ls,
+                                void *out, int64_t o_ls, int32_t out_dtype, bool stats, bool chain, cudaStream_t s) {
+    DBK_TRY(ensure_ws(p, nl, s));
     DecodeParams dp;
-    dp.kv_layer = p->kv + static_cast<size_t>(b->layer) * p->layer_stride;
+    dp.kv_layer = p->kv + static_cast<size_t>(layer0) * p->layer_stride;
     dp.page_stride = p->page_stride;
     dp.block_table = p->d_bt;
     dp.bt_stride = p->cfg.max_pages_per_req;
-    dp.n = b->n;
+    dp.n = n;
     dp.req = p->d_req;
     dp.items = p->d_items;
     dp.item_pages = p->d_item_pages;
@@ -786,25 +811,97 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     const int par = p->launch_parity;
     dp.ws_o = p->d_ws_o + static_cast<size_t>(par) * p->ws_cap * p->cfg.head_dim;
     dp.ws_ml = p->d_ws_ml + static_cast<size_t>(par) * p->ws_cap;
-    dp.counters = p->d_counters + static_cast<size_t>(par) * p->cfg.max_requests * p->cfg.kv_heads;
-    dp.fuse_stats = b->fuse_stats ? 1 : 0;
+    dp.counters = p->d_counters + static_cast<size_t>(par) * counters_per_parity(&p->cfg);
+    dp.fuse_stats = stats ? 1 : 0;
     dp.max_pages_per_req = p->cfg.max_pages_per_req;
     dp.stats = reinterpret_cast<unsigned long long *>(p->d_stats);
     dp.stats_done = p->d_stats_done;
     dp.cap_pages = p->cfg.cap_pages;
-    dp.layer = b->layer;
+    dp.layer = layer0;
     dp.kv_heads = p->cfg.kv_heads;
-    dp.n_tasks = p->meta_items * p->cfg.kv_heads;
+    dp.n_layers = nl;
+    dp.layer_stride = p->layer_stride;
+    dp.q_layer_stride = q_ls;
+    dp.out_layer_stride = o_ls;
+    dp.n_ws_rows = p->meta_ws_rows;
+    dp.n_tasks = p->meta_items * p->cfg.kv_heads * nl;
     dp.task_counter = p->d_task_counter + 2 * par;
     dp.tma_rank = p->tma_rank;
-    dp.pdl = (b->chain && !b->fuse_stats && p->pdl_enabled) ? 1 : 0;
+    dp.pdl = (chain && !stats && p->pdl_enabled) ? 1 : 0;
+    dp.seq = ++p->decode_seq;
+    dp.done_seq = p->d_done_seq;
+    dp.trace = p->d_trace;
+    dp.trace_cap = p->trace_cap;
+    dp.trace_seq = static_cast<int32_t>(p->n_launches);
     // persistent grid: every resident CTA slot (4 warps each), or fewer for small batches
     const int ctas = std::max(1, std::min(p->num_sms * p->ctas_per_sm, (dp.n_tasks + 3) / 4));
     DBK_CUDA(launch_decode(dp, p->cfg.kv_dtype, p->cfg.head_dim, p->cfg.q_heads / p->cfg.kv_heads, ctas,
                            p->has_tmap ? &p->tmap : nullptr, s));
     ++p->n_launches;
     p->launch_parity ^= 1;
+    return DBK_OK;
+}
+
+static dbk_status decode_args_ok(dbk_pool *p, const dbk_batch *b, const void *q, void *out, int32_t out_dtype) {
+    if (!p || !b) return fail(DBK_EINVAL, "decode_step: null argument");
+    if (b->n < 0 || (b->n > 0 && (!b->req_ids || !q || !out))) return fail(DBK_EINVAL, "decode_step: bad arrays");
+    if (b->layer < 0 || b->layer >= p->cfg.layers) return fail(DBK_EINVAL, "decode_step: layer out of range");
+    if (out_dtype < 0 || out_dtype > 2) return fail(DBK_EINVAL, "decode_step: out_dtype must be 0, 1 or 2");
+    if (b->n > p->cfg.max_requests) return fail(DBK_EINVAL, "decode_step: n > max_requests");
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
+        return fail(DBK_EINVAL, "decode_step: q and out must be 16-byte aligned");
+    return DBK_OK;
+}
+
+}  // namespace dbk
+
+extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const void *q, void *out,
+                                      int32_t out_dtype, void *stream) {
+    DBK_TRY(decode_args_ok(p, b, q, out, out_dtype));
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DBK_TRY(flush_deltas(p, s));
+    if (b->fuse_stats) DBK_CUDA(cudaMemsetAsync(p->d_stats, 0, 128, s));
+    if (b->n == 0) return DBK_OK;
+    DBK_TRY(prepare_batch(p, b->n, b->req_ids, s));
+    DBK_TRY(decode_launch(p, b->n, b->layer, 1, q, 0, out, 0, out_dtype, b->fuse_stats != 0, b->chain != 0, s));
     p->last_decode_bytes = decode_bytes(p, out_dtype);
+    return DBK_OK;
+}
+
+extern "C" dbk_status dbk_decode_step_layers(dbk_pool *p, const dbk_batch *b, int32_t n_layers, const void *q,
+                                             int64_t q_layer_stride, void *out, int64_t out_layer_stride,
+                                             int32_t out_dtype, void *stream, int32_t *launches_out) {
+    DBK_TRY(decode_args_ok(p, b, q, out, out_dtype));
+    if (n_layers < 1 || b->layer + n_layers > p->cfg.layers)
+        return fail(DBK_EINVAL, "decode_step_layers: layers [%d, %d) out of range", b->layer, b->layer + n_layers);
+    if (q_layer_stride < 0 || out_layer_stride < 0 || (q_layer_stride % 8) || (out_layer_stride % 8))
+        return fail(DBK_EINVAL, "decode_step_layers: layer strides must be >= 0 and multiples of 8 elements");
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DBK_TRY(flush_deltas(p, s));
+    if (b->fuse_stats) DBK_CUDA(cudaMemsetAsync(p->d_stats, 0, 128, s));
+    if (launches_out) *launches_out = 0;
+    if (b->n == 0) return DBK_OK;
+    DBK_TRY(prepare_batch(p, b->n, b->req_ids, s, n_layers));
+    // layers per launch: as many as the split-K workspace budget holds (every layer of the step
+    // in one launch when it fits)
+    const int64_t per_layer = std::max<int64_t>(p->meta_ws_rows, 1) * p->cfg.q_heads * (p->cfg.head_dim * 4 + 8);
+    int32_t group = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(n_layers, p->ws_budget_bytes / per_layer)));
+    if (p->max_layers_per_launch > 0) group = std::min(group, p->max_layers_per_launch);
+    const int64_t eo = out_dtype == 2 ? 4 : 2;
+    int32_t launched = 0;
+    for (int32_t l0 = 0; l0 < n_layers; l0 += group) {
+        const int32_t nl = std::min(group, n_layers - l0);
+        const void *ql = static_cast<const uint8_t *>(q) + l0 * q_layer_stride * p->elt;
+        void *ol = static_cast<uint8_t *>(out) + l0 * out_layer_stride * eo;
+        const bool stats = b->fuse_stats && l0 == 0;
+        DBK_TRY(decode_launch(p, b->n, b->layer + l0, nl, ql, q_layer_stride, ol, out_layer_stride, out_dtype, stats,
+                              l0 > 0 || b->chain, s));
+        ++launched;
+    }
+    if (launches_out) *launches_out = launched;
+    p->last_decode_bytes = decode_bytes(p, out_dtype);  // per layer
     return DBK_OK;
 }
 
@@ -944,5 +1041,21 @@ extern "C" dbk_status dbk_synth_fill(uint64_t seed, int32_t kind, int32_t n_rows
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFree(d_req);
     if (e != cudaSuccess) return fail(DBK_ECUDA, "synth_fill: %s", cudaGetErrorString(e));
+    return DBK_OK;
+}
+
+// Measurement utility: the decode kernels' task timeline (DBK_TRACE_TASKS=N at pool creation).
+extern "C" dbk_status dbk_pool_trace_d2h(dbk_pool *p, void *host, int64_t cap, int64_t *n_out, int32_t reset) {
+    if (!p || !n_out) return fail(DBK_EINVAL, "pool_trace_d2h: null argument");
+    *n_out = 0;
+    if (!p->d_trace) return DBK_OK;
+    DBK_CUDA(cudaSetDevice(p->cfg.device));
+    DBK_CUDA(cudaDeviceSynchronize());
+    unsigned long long cnt = 0;
+    DBK_CUDA(cudaMemcpy(&cnt, p->d_trace, 8, cudaMemcpyDeviceToHost));
+    const int64_t n = std::min<int64_t>(static_cast<int64_t>(cnt), std::min<int64_t>(cap, p->trace_cap));
+    if (host && n > 0) DBK_CUDA(cudaMemcpy(host, p->d_trace + 4, static_cast<size_t>(n) * 32, cudaMemcpyDeviceToHost));
+    *n_out = n;
+    if (reset) DBK_CUDA(cudaMemset(p->d_trace, 0, 8));
     return DBK_OK;
 }

@@ -36,7 +36,8 @@ struct SwappedRequest {
 };
 
 dbk_status flush_deltas(dbk_pool *p, cudaStream_t s);
-dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_t s);
+// layers_hint: layers one launch will stream (the chunk-size rule sizes tasks per launch)
+dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_t s, int32_t layers_hint = 1);
 // dbk_append_tokens in two halves: bookkeeping + job upload, then per-layer-range KV writes
 dbk_status append_plan(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok, bool explicit_rows,
                        cudaStream_t s, bool upload_jobs = true);
@@ -72,7 +73,9 @@ struct dbk_pool {
     std::vector<dbk::ReqMeta> meta_req;
     std::vector<int2> meta_work;
     std::vector<uint8_t> meta_blob;
-    int32_t meta_items = 0, meta_chunk_pages = 0;
+    int32_t meta_items = 0, meta_chunk_pages = 0, meta_ws_rows = 0, meta_layers_hint = 1;
+    int64_t ws_budget_bytes = 512ll << 20;   // split-K workspace per scratch parity (layer groups)
+    int32_t max_layers_per_launch = 0;       // 0: as many as the workspace budget allows
     const dbk::ReqMeta *d_req = nullptr;
     const dbk::ItemMeta *d_items = nullptr;
     const int32_t *d_item_pages = nullptr;
@@ -83,7 +86,9 @@ struct dbk_pool {
     int32_t *d_counters = nullptr;
     int64_t *d_stats = nullptr;
     int32_t *d_stats_done = nullptr;
-    int32_t *d_task_counter = nullptr;        // persistent decode: next task, exited CTAs
+    int32_t *d_task_counter = nullptr;        // persistent decode: [2 parities][next task, exited warps]
+    int32_t *d_done_seq = nullptr;            // last decode grid whose scratch is reset (PDL trigger)
+    int32_t decode_seq = 0;                   // decode launches so far (DecodeParams::seq)
     dbk_stats *h_stats = nullptr;
     int num_sms = 148, ctas_per_sm = 1;
     // pages per warp task: <= 64 (two page ids per lane); 32 measured best (profiles/r01_tune.txt)
@@ -93,6 +98,8 @@ struct dbk_pool {
     int64_t n_launches = 0;                   // kernels launched by this pool (gpu_launches)
     int launch_parity = 0;                    // scratch copy of the next decode launch
     bool pdl_enabled = true;
+    unsigned long long *d_trace = nullptr;    // DBK_TRACE_TASKS=N: task timeline buffer (measurement)
+    int32_t trace_cap = 0;
     // pool-wide 2-D tensor map (rows of head_dim elements, 16 x 64 boxes, 128B swizzle) for K2
     alignas(64) CUtensorMap tmap;
     bool has_tmap = false;

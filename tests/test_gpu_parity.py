@@ -42,7 +42,7 @@ def torch_from_bits(bits):
 
 
 def run_decode_case(dbk, L, Hq, Hkv, d, dtype, ctx_list, seed=7, explicit_kv=False, cap=None,
-                    layer=None, q_scale_log2=0, chunk_pages=None, out_dtype=2, monkeypatch=None):
+                    layer=None, q_scale_log2=0, chunk_pages=None, out_dtype=2, monkeypatch=None, multi_layer=False):
     P = 16
     n = len(ctx_list)
     ctx = np.asarray(ctx_list, np.int32)
@@ -85,6 +85,27 @@ def run_decode_case(dbk, L, Hq, Hkv, d, dtype, ctx_list, seed=7, explicit_kv=Fal
         assert list(row[:len(pages)]) == pages and np.all(row[len(pages):] == -1)
     layers = [layer] if layer is not None else list(range(L))
     results = []
+    if multi_layer:  # every layer through dbk_decode_step_layers (q / out [L][n][Hq][d])
+        odt = {2: torch.float32, 0: torch.float16, 1: torch.bfloat16}[out_dtype]
+        qb_all = np.stack([hashgen.to_bits(np.stack([hashgen.gen_values(seed, 0, int(r), int(c) - 1, lay,
+                                                                        np.arange(Hq), d, q_scale_log2)
+                                                     for r, c in zip(ids, ctx)]), dtype) for lay in range(L)])
+        q_all = torch_from_bits(qb_all)
+        out_all = torch.full((L, n, Hq, d), float("nan"), dtype=odt, device="cuda")
+        launches = pool.decode_step_layers(ids, 0, L, q_all, n * Hq * d, out_all, n * Hq * d, out_dtype=out_dtype,
+                                           fuse_stats=True)
+        st = pool.batch_stats()
+        assert st == ostats.batch_stats(ctx, l_in, l_out, [ref.pages[int(r)] for r in ids], P, cap)
+        for lay in range(L):
+            bt, pk, pv, qq = oatt.synth_paged_batch(seed, [int(r) for r in ids], ctx,
+                                                    [ref.pages[int(r)] for r in ids], lay, Hq, Hkv, d, P,
+                                                    dtype, q_scale_log2=q_scale_log2, n_phys=cap)
+            want = oatt.paged_decode_attention(ctx, bt, pk, pv, qq, dtype, nthreads=8)
+            results.append((out_all[lay].float().cpu().numpy().astype(np.float64), want))
+        LAST_INFO.clear()
+        LAST_INFO.update(pool.info(), launches=launches)
+        pool.close()
+        return results
     for lay in layers:
         qv = np.stack([hashgen.gen_values(seed, 0, int(r), int(c) - 1, lay, np.arange(Hq), d, q_scale_log2)
                        for r, c in zip(ids, ctx)])
@@ -170,6 +191,27 @@ def test_decode_chunking_is_invariant(dbk, monkeypatch):
         assert row_err(got, want) <= TOL
         outs.append(got)
     assert max(row_err(o, outs[0]) for o in outs) < 1e-5
+
+
+@pytest.mark.parametrize("dtype,Hq,Hkv,d,per_launch", [("f16", 8, 8, 64, None), ("bf16", 16, 2, 128, None),
+                                                        ("f16", 8, 1, 128, 2), ("bf16", 8, 4, 64, 1)])
+def test_decode_step_layers_matches_per_layer(dbk, monkeypatch, dtype, Hq, Hkv, d, per_launch):
+    """dbk_decode_step_layers (tasks spanning the layers, one launch -- or several PDL-chained
+    ones when the layers per launch are capped) vs O1 and vs one dbk_decode_step per layer (the
+    chunk size, hence the split-K order, may differ: equal to 1e-5); the statistics record is
+    exact."""
+    L = 5
+    ctx = [1, 16, 17, 300, 700, 2100, 4100, 33, 2, 1000]
+    if per_launch:
+        monkeypatch.setenv("DBK_LAYERS_PER_LAUNCH", str(per_launch))
+    multi = run_decode_case(dbk, L, Hq, Hkv, d, dtype, ctx, multi_layer=True, q_scale_log2=2)
+    launches = LAST_INFO["launches"]
+    assert launches == (1 if not per_launch else -(-L // per_launch))
+    monkeypatch.delenv("DBK_LAYERS_PER_LAUNCH", raising=False)
+    single = run_decode_case(dbk, L, Hq, Hkv, d, dtype, ctx, q_scale_log2=2)
+    for (gm, want), (gs, _) in zip(multi, single):
+        assert row_err(gm, want) <= TOL
+        assert row_err(gm, gs) < 1e-5
 
 
 def test_append_cap_is_all_or_nothing(dbk):
