@@ -399,6 +399,22 @@ def run_gpu(args):
     ff_recs, _ = run_steps(S, args.ff, bufs, stream, dist=dist)
     run_steps(S, args.warmup, bufs, stream, dist=dist)
     eng.attn_timing(reset=True)
+    if args.ncu_step:  # profiling: ONE step inside an NVTX range (ncu --nvtx --nvtx-include dbk_step/)
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("dbk_step")
+        rec = eng.step(bufs, stream)
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        a_ms, a_launches, a_bytes = eng.attn_timing(reset=True)
+        info = S["pool"].info()
+        if rank == 0:
+            print(json.dumps({"ncu_step": {"config": args.config, "tp": tp, "model": bool(args.model),
+                                           "kernel": "decode_gqa_kernel" if info["decode_path"] == 2 else "decode_kernel",
+                                           "attn_bytes": a_bytes, "attn_kernels": a_launches,
+                                           "n_decode": rec["n_decode"], "chunk_pages": info["chunk_pages"],
+                                           "per_layer_launches": bool(args.per_layer_launches or args.model)}}),
+                  flush=True)
+        return
     with ClockSampler(local) as clk:
         recs, ms = run_steps(S, args.steps, bufs, stream, dist=dist)
     att_ms, att_launches, att_bytes = eng.attn_timing(reset=True)
@@ -611,6 +627,9 @@ def main():
                     help="70B GQA: run rank 0's KV-head shard of a TP-G job on this one GPU (per-GPU kernel rate)")
     ap.add_argument("--tp-rank", type=int, default=0, help="with --tp-shard: which rank's KV-head shard")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) run (profiling)")
+    ap.add_argument("--ncu-step", action="store_true",
+                    help="profiling: after fast-forward + warm-up run ONE step inside the NVTX range dbk_step, "
+                         "print its attention bytes and exit (profiles/run_ncu_traffic.sh)")
     ap.add_argument("--per-layer-launches", action="store_true",
                     help="one PDL-chained decode launch per layer (as a model's step issues them) instead of "
                          "multi-layer launches")

@@ -478,15 +478,15 @@ dbk_status dbk_engine_last_batch(dbk_engine *e, int32_t *n, int64_t *req_ids, in
  * decode token's KV is written by the model (dbk_reserve_tokens + RoPE epilogue).
  * Device-resident, non-PD engines only; NULL detaches. */
 dbk_status dbk_engine_attach_model(dbk_engine *e, dbk_model *model);
-/* Attention timing accumulated with time_attention = 1: total ms of the
- * attention launches (CUDA events on the launching stream), their count and
- * the algorithmic bytes they moved. */
 /* Per-request timeline on the engine clock (ns), for trace index i < n (host
  * arrays, nullable): first_admit_ns[i] = clock of the step that first admitted
  * it, finish_ns[i] = end of the step that emitted its last token; -1 where it
  * has not happened yet or the request belongs to another DP rank.  Feeds the
  * scheduling-delay criterion of the capacity experiment. */
 dbk_status dbk_engine_request_times(dbk_engine *e, int32_t n, int64_t *first_admit_ns, int64_t *finish_ns);
+/* Attention timing accumulated with time_attention = 1: total ms of the
+ * attention launches (CUDA events on the launching stream), their count (kernels:
+ * a multi-layer launch counts once) and the algorithmic bytes they moved. */
 dbk_status dbk_engine_attn_timing(dbk_engine *e, double *ms, int64_t *launches, int64_t *bytes,
                                   int32_t reset);
 

@@ -61,7 +61,8 @@ struct dbk_engine {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> att0, att1;
     double att_ms = 0;
-    int64_t att_launches = 0, att_bytes = 0;
+    int64_t att_launches = 0, att_bytes = 0;  // attention kernels timed and their algorithmic bytes
+    int32_t step_attn_kernels = 0;            // multi-layer launches of this step
     std::vector<int64_t> layer_bytes;
     dbk_comm *comm = nullptr;
     int32_t comm_mode = DBK_MODE_DP;
@@ -540,7 +541,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         bt.chain = 0;
         const int64_t ls = static_cast<int64_t>(pc.max_requests) * pc.q_heads * pc.head_dim;
         DBK_TRY(dbk_decode_step_layers(p, &bt, pc.layers, bufs->q_dev, ls, bufs->out_dev, ls, e->cfg.out_dtype, s,
-                                       nullptr));
+                                       &e->step_attn_kernels));
         for (int l = 0; l < pc.layers; ++l) e->layer_bytes[l] = p->last_decode_bytes;
     }
     for (int l = 0; l < (e->model || multi ? 0 : pc.layers); ++l) {
@@ -621,8 +622,9 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             else if (l == 0) DBK_CUDA(cudaEventElapsedTime(&a, e->att0[0], e->att1[0]));
             e->att_ms += a;
             e->att_bytes += e->layer_bytes[l];
-            ++e->att_launches;
+            if (!multi) ++e->att_launches;
         }
+        if (multi) e->att_launches += e->step_attn_kernels;  // kernels, each streaming several layers
     }
     e->step_adm = adm;
     e->step_pre = pre;
