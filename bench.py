@@ -59,18 +59,56 @@ def ncu_traffic(config, tp, kernel, model=False):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    """SM clocks and throttle reasons sampled DURING the timed region (B200_PROFILING.md's clocks
+    line): NVML polled every 5 ms from a thread (a 3 ms-step run still gets dozens of samples),
+    else nvidia-smi every 100 ms."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, device):
         self.device = device
         self.proc = None
         self.lines = []
+        self.samples = []   # (sm_mhz, max_mhz, reasons bitmask) from NVML
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:  # the CUDA device's own NVML handle (CUDA_VISIBLE_DEVICES may renumber devices)
+                import torch
+                pr = torch.cuda.get_device_properties(self.device)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.nvml = (pynvml, h)
+
+            reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                while not self.stop.is_set():
+                    try:
+                        self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx,
+                                             reasons_fn(h)))
+                    except pynvml.NVMLError:
+                        pass
+                    self.stop.wait(0.005)
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -86,6 +124,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            self.t.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -95,6 +136,13 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
+        if self.nvml:
+            for clk, m, bits in self.samples:
+                sm.append(float(clk))
+                mx = float(m)
+                reasons |= {nm for nm, b in self.BITS.items() if bits & b}
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml 5 ms"}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
@@ -109,7 +157,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi 100 ms"}
 
 
 def make_workload(cfg_name=CFG_NAME, world=1, n_req=None):

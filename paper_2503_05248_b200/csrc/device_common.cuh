@@ -236,8 +236,11 @@ __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int l
         t.it = ItemMeta{0, 0, 0, 0, 1, 0, 1, 0};
         return t;
     }
-    const int ih = task / p.n_layers;
-    t.l = task - ih * p.n_layers;
+    // layer-major: the queue sweeps the layers one after the other (each longest-first), so the
+    // pages in flight stay within ~one layer's slice of the pool (TLB reach, DRAM locality)
+    const int per_layer = p.n_items * p.kv_heads;
+    t.l = task / per_layer;
+    const int ih = task - t.l * per_layer;
     const int item = ih / p.kv_heads;
     t.g = ih - item * p.kv_heads;
     const int4 *im = reinterpret_cast<const int4 *>(p.items + item);

@@ -63,7 +63,7 @@ struct DecodeParams {
     int32_t layer;               // first layer of this launch
     int32_t kv_heads;
     // one launch may stream n_layers consecutive layers (attention-only step: every layer's q is
-    // ready before the first launch); task t = ((item * kv_heads + head) * n_layers + l)
+    // ready before the first launch); task t = (l * n_items + item) * kv_heads + head
     int32_t n_layers;
     int64_t layer_stride;        // bytes between layers in the pool
     int64_t q_layer_stride;      // elements between layers of q
