@@ -74,12 +74,21 @@ def main():
                          busy_frac=busy / (warps * (b - a)) if b > a else None,
                          tail_us=(b - ends[int(0.9 * len(ends))]) / 1e3))
         prev_end = b
+    # concurrency: tasks in flight per SM, sampled at 200 instants of the step
+    inst = np.linspace(t0.min(), t1.max(), 200)
+    conc = []
+    for x in inst:
+        live = (t0 <= x) & (t1 > x)
+        if live.any():
+            conc.append(np.bincount(sm[live], minlength=148).max())
+    max_per_sm = int(max(conc)) if conc else 0
     total_span = (t1.max() - t0.min()) / 1e3
     busy_all = float((t1 - t0).sum()) / (warps * (t1.max() - t0.min()))
     out = dict(config=args.config, tp=args.tp_shard, decode_path=info["decode_path"], chunk_pages=info["chunk_pages"],
                step=dict(n_decode=rec["n_decode"], step_ms=rec["step_ns"] / 1e6, attn_ms_events=att_ms,
                          attn_bytes=att_bytes, launches=att_launches),
-               trace_span_us=total_span, warp_busy_frac=busy_all, tasks=int(len(r)),
+               trace_span_us=total_span, warp_busy_frac=busy_all, tasks=int(len(r)), max_tasks_per_sm=max_per_sm,
+               sms_used=int(len(set(sm.tolist()))),
                pages_per_task_mean=float(pages.mean()), task_us_mean=float((t1 - t0).mean() / 1e3),
                task_us_p90=float(np.percentile(t1 - t0, 90) / 1e3),
                launches=rows)

@@ -3,6 +3,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -46,10 +48,14 @@ dbk_status UploadBuffer::reserve(size_t bytes) {
     release();
     size_t c = 4096;
     while (c < bytes) c *= 2;
+    const auto t0 = std::chrono::steady_clock::now();
     DBK_CUDA(cudaMallocHost(&host, c));
     DBK_CUDA(cudaMalloc(&dev, c));
     if (!done) DBK_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     cap = c;
+    if (std::getenv("DBK_DEBUG_ALLOC"))
+        std::fprintf(stderr, "[dbk] upload buffer: %zu bytes in %.1f ms\n", c,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     return DBK_OK;
 }
 
@@ -769,11 +775,24 @@ int64_t decode_bytes(const dbk_pool *p, int out_dtype) {
 
 namespace dbk {
 
-// Split-K workspace for nl layers of the prepared batch (two scratch parities).
+// Split-K workspace rows (of q_heads x (D fp32 + (m, l))) that fit the budget, capped by what the
+// pool could ever use (every layer of the largest batch split into 4-page chunks).
+static size_t ws_budget_rows(const dbk_pool *p) {
+    const size_t row = static_cast<size_t>(p->cfg.head_dim) * sizeof(float) + sizeof(float2);
+    const size_t most = static_cast<size_t>(p->cfg.layers) * p->cfg.max_requests *
+                        ((p->cfg.max_pages_per_req + 3) / 4) * p->cfg.q_heads;
+    return std::min(most, static_cast<size_t>(p->ws_budget_bytes) / row);
+}
+
+// Split-K workspace for nl layers of the prepared batch (two scratch parities).  Allocated once
+// at the budget (never grown in steady state: a reallocation synchronises the device and, with
+// the pool holding nearly all HBM, took ~0.4 s inside a timed step); the layers per launch
+// adapt to it instead.
 static dbk_status ensure_ws(dbk_pool *p, int32_t nl, cudaStream_t s) {
     const size_t need = static_cast<size_t>(std::max(p->meta_ws_rows, 1)) * nl * p->cfg.q_heads;
     if (need <= p->ws_cap) return DBK_OK;
-    const size_t c = std::max<size_t>(need, p->ws_cap * 2);
+    const size_t c = std::max<size_t>(need, ws_budget_rows(p));
+    const auto t0 = std::chrono::steady_clock::now();
     DBK_CUDA(cudaStreamSynchronize(s));
     if (p->d_ws_o) cudaFree(p->d_ws_o);
     if (p->d_ws_ml) cudaFree(p->d_ws_ml);
@@ -783,6 +802,10 @@ static dbk_status ensure_ws(dbk_pool *p, int32_t nl, cudaStream_t s) {
     DBK_CUDA(cudaMalloc(&p->d_ws_o, 2 * c * p->cfg.head_dim * sizeof(float)));  // two parities
     DBK_CUDA(cudaMalloc(&p->d_ws_ml, 2 * c * sizeof(float2)));
     p->ws_cap = c;
+    if (std::getenv("DBK_DEBUG_ALLOC"))
+        std::fprintf(stderr, "[dbk] split-K workspace: %zu rows x 2 parities (%.1f MB) in %.1f ms\n", c,
+                     2.0 * c * (p->cfg.head_dim * 4 + 8) / 1e6,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     return DBK_OK;
 }
 
@@ -886,8 +909,9 @@ extern "C" dbk_status dbk_decode_step_layers(dbk_pool *p, const dbk_batch *b, in
     DBK_TRY(prepare_batch(p, b->n, b->req_ids, s, n_layers));
     // layers per launch: as many as the split-K workspace budget holds (every layer of the step
     // in one launch when it fits)
-    const int64_t per_layer = std::max<int64_t>(p->meta_ws_rows, 1) * p->cfg.q_heads * (p->cfg.head_dim * 4 + 8);
-    int32_t group = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(n_layers, p->ws_budget_bytes / per_layer)));
+    const int64_t per_layer_rows = static_cast<int64_t>(std::max(p->meta_ws_rows, 1)) * p->cfg.q_heads;
+    const int64_t fit = static_cast<int64_t>(std::max(p->ws_cap, ws_budget_rows(p))) / per_layer_rows;
+    int32_t group = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(n_layers, fit)));
     if (p->max_layers_per_launch > 0) group = std::min(group, p->max_layers_per_launch);
     const int64_t eo = out_dtype == 2 ? 4 : 2;
     int32_t launched = 0;
