@@ -24,9 +24,16 @@ DTYPES = {"f16": 0, "bf16": 1}
 
 
 def build(force=False) -> str:
-    """Compile attention.c with gcc -O2 -fopenmp (no -ffast-math: IEEE semantics)."""
+    """Compile attention.c with gcc -O2 -fopenmp (no -ffast-math: IEEE semantics).  With
+    DBK_ORACLE_SANITIZE=1: a separate ASan + UBSan build (the sanitizer run of SURVEY.md §5)."""
+    global _LIB
+    san = os.environ.get("DBK_ORACLE_SANITIZE") == "1"
+    if san:
+        _LIB = os.path.join(_HERE, "_oracle_attention_asan.so")
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-o", _LIB, _SRC, "-lm"]
+        if san:
+            cmd[1:1] = ["-fsanitize=address,undefined", "-fno-omit-frame-pointer", "-fno-sanitize-recover=undefined"]
         subprocess.run(cmd, check=True)
     return _LIB
 

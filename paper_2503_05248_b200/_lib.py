@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdbk.so")
+# DBK_LIB: an alternative build of the same library (e.g. libdbk_asan.so, the sanitizer build)
+LIB_PATH = os.environ.get("DBK_LIB") or os.path.join(_HERE, "libdbk.so")
 
 STATUS = {0: "DBK_OK", 1: "DBK_EINVAL", 2: "DBK_ECAP", 3: "DBK_ENOENT", 4: "DBK_EINFEASIBLE",
           5: "DBK_ECUDA", 6: "DBK_ENCCL", 7: "DBK_EFATAL"}

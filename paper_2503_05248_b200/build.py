@@ -49,8 +49,11 @@ def _common_flags(nccl_inc):
                    "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_inc, "-I", _cublas_dirs()[0]]
 
 
-def _compile(src, flags, verbose):
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+SAN = ["-fsanitize=address", "-fsanitize=undefined", "-fno-omit-frame-pointer", "-fno-sanitize-recover=undefined"]
+
+
+def _compile(src, flags, verbose, suffix=""):
+    obj = os.path.join(OBJ, os.path.basename(src) + suffix + ".o")
     deps = [src] + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "dbk.h")]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
@@ -65,28 +68,36 @@ def _compile(src, flags, verbose):
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, sanitize: bool = False) -> str:
+    """libdbk.so; sanitize=True: libdbk_asan.so, the host C++ (allocator, scheduler, engine,
+    exchange) under AddressSanitizer + UndefinedBehaviorSanitizer."""
     os.makedirs(OBJ, exist_ok=True)
     if force:
         for f in glob.glob(os.path.join(OBJ, "*.o")):
             os.remove(f)
     nccl_inc, nccl_lib = _nccl_dirs()
     flags = _common_flags(nccl_inc)
+    lib = LIB.replace("libdbk.so", "libdbk_asan.so") if sanitize else LIB
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+
+    def one(src):
+        if sanitize and src.endswith(".cpp"):
+            return _compile(src, flags + [x for f in SAN for x in ("-Xcompiler", f)], verbose, ".asan")
+        return _compile(src, flags, verbose)
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, flags, verbose), srcs))
-    if (not force and os.path.exists(LIB)
-            and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs)):
-        return LIB
-    link = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + [
+        objs = list(ex.map(one, srcs))
+    if (not force and os.path.exists(lib)
+            and os.path.getmtime(lib) >= max(os.path.getmtime(o) for o in objs)):
+        return lib
+    link = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + (["-Xlinker", "-lasan", "-Xlinker", "-lubsan"] if sanitize else []) + [
         "-L", nccl_lib, "-Xlinker", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl_lib}",
         "-L", _cublas_dirs()[1], "-Xlinker", "-l:libcublasLt.so.12", "-Xlinker", f"-rpath,{_cublas_dirs()[1]}",
         "-lpthread"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, sanitize="--sanitize" in sys.argv))
