@@ -421,7 +421,7 @@ def run_gpu(args):
     exchange_kind, comm = None, None
     if world > 1:
         mode = dbk._lib.MODE_TP if tp > 1 else dbk._lib.MODE_DP
-        if gloo_test:  # test harness only: ranks share one GPU, so the records go through gloo
+        if gloo_test and args.exchange == "nccl":  # test harness only: NCCL refuses ranks sharing one GPU
             fields = dbk._lib.STATS_FIELDS
 
             def exchange(local_rec):
@@ -430,17 +430,36 @@ def run_gpu(args):
                 dist.all_gather(out, t)
                 return dbk.stats_reduce([dict(zip(fields, o.tolist())) for o in out], mode)
             S["exchange"] = exchange
-            exchange_kind = {"kind": "torch.distributed gloo all-gather (DBK_BENCH_TEST_GLOO test harness)"}
-        else:  # the product path: libdbk's own NCCL communicator; any failure is fatal (no fallback)
-            comm = dbk.Comm(dist, world, rank, local)
-            nr, rk = comm.info()
-            print(f"[bench] rank {rank}: libdbk NCCL communicator nranks={nr} rank={rk} "
-                  f"mode={'TP' if tp > 1 else 'DP'}", file=sys.stderr, flush=True)
-            if (nr, rk) != (world, rank):
-                raise SystemExit(f"NCCL communicator reports nranks={nr} rank={rk}, expected {world}/{rank}")
-            eng.attach_comm(comm, mode)
-            exchange_kind = {"kind": "libdbk ncclAllGather of the 128-B records (dbk_stats_allgather)",
-                             "nccl_nranks": nr}
+            exchange_kind = {"kind": "torch.distributed gloo all-gather (DBK_BENCH_TEST_GLOO test harness; "
+                                     "--exchange nccl cannot run with ranks sharing one GPU)"}
+        else:  # the product path: libdbk's own exchange (mailbox over peer memory, or NCCL)
+            mb_err = None
+            if args.exchange == "mailbox":
+                try:
+                    comm = dbk.Mailbox(dist, world, rank, local)
+                    eng.attach_mbox(comm, mode)
+                    exchange_kind = {"kind": "libdbk mailbox: one exchange kernel per step stores the 128-B "
+                                             "record into every peer's IPC-mapped mailbox (dbk_engine_attach_mbox)",
+                                     "ranks": world}
+                    print(f"[bench] rank {rank}: libdbk mailbox exchange over {world} ranks "
+                          f"mode={'TP' if tp > 1 else 'DP'}", file=sys.stderr, flush=True)
+                except Exception as ex:  # loud, and recorded in the line: the NCCL transport instead
+                    mb_err = f"{type(ex).__name__}: {ex}"
+                    print(f"[bench] rank {rank}: MAILBOX SETUP FAILED ({mb_err}); using libdbk NCCL",
+                          file=sys.stderr, flush=True)
+                    comm = None
+            if comm is None:
+                comm = dbk.Comm(dist, world, rank, local)
+                nr, rk = comm.info()
+                print(f"[bench] rank {rank}: libdbk NCCL communicator nranks={nr} rank={rk} "
+                      f"mode={'TP' if tp > 1 else 'DP'}", file=sys.stderr, flush=True)
+                if (nr, rk) != (world, rank):
+                    raise SystemExit(f"NCCL communicator reports nranks={nr} rank={rk}, expected {world}/{rank}")
+                eng.attach_comm(comm, mode)
+                exchange_kind = {"kind": "libdbk ncclAllGather of the 128-B records (dbk_stats_allgather)",
+                                 "nccl_nranks": nr}
+                if mb_err:
+                    exchange_kind["mailbox_setup_failed"] = mb_err
     stream = torch.cuda.current_stream()
     bufs = eng.buffers(S["qd"], S["od"])
     # fast-forward to the steady state (untimed), then W warm-up steps (untimed)
@@ -556,7 +575,9 @@ def run_gpu(args):
                                            else "multi-layer persistent launches (dbk_decode_step_layers)"),
                        "decode_launches_per_step": (round(sum(r["launches"] for r in recs) / max(len(recs), 1), 2)),
                        "stats_exchange": (dict(exchange_kind or {}, **({
-                           "host_us_per_step": round(xch["us_total"] / max(xch["count"], 1), 2),
+                           "host_us_per_step": (round(xch["us_total"] / max(xch["count"], 1), 2)
+                                                if "nccl_nranks" in (exchange_kind or {}) else
+                                                "inside the step's device time (exchange kernel)"),
                            "exchanges": xch["count"],
                            "last_step_ns_per_rank": [r["step_ns"] for r in xch["records"]]} if xch else {}))
                            if world > 1 else None),
@@ -675,6 +696,8 @@ def main():
                     help="70B GQA: run rank 0's KV-head shard of a TP-G job on this one GPU (per-GPU kernel rate)")
     ap.add_argument("--tp-rank", type=int, default=0, help="with --tp-shard: which rank's KV-head shard")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) run (profiling)")
+    ap.add_argument("--exchange", default="mailbox", choices=["mailbox", "nccl"],
+                    help="N > 1: the statistics exchange -- libdbk's mailbox over peer memory (default) or NCCL")
     ap.add_argument("--ncu-step", action="store_true",
                     help="profiling: after fast-forward + warm-up run ONE step inside the NVTX range dbk_step, "
                          "print its attention bytes and exit (profiles/run_ncu_traffic.sh)")

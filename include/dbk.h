@@ -521,6 +521,37 @@ dbk_status dbk_engine_attach_comm(dbk_engine *e, dbk_comm *c, int32_t mode);
 dbk_status dbk_engine_last_exchange(dbk_engine *e, dbk_stats *all, int32_t cap, int32_t *nranks, double *us,
                                     double *us_total, int64_t *count, int32_t reset);
 
+/* ------------------------------------------------------------------------ */
+/* Mailbox exchange: the same records over peer memory, no collective launch  */
+/* ------------------------------------------------------------------------ */
+
+/* SURVEY.md §8(e) "B200-native v2".  Each rank owns a device mailbox (2 x nranks slots of
+ * 256 B) exported with CUDA IPC; every peer maps it (P2P over NVLink/NVSwitch; the same
+ * device when ranks share a GPU).  One single-warp kernel per step stores the rank's 128-B
+ * record into every mailbox, waits (acquire loads) for the other ranks' records of the same
+ * step and writes the gathered records into mapped pinned host memory -- no H2D, no NCCL
+ * launch, no separate D2H.  1 <= nranks <= 32. */
+typedef struct dbk_mbox dbk_mbox;
+
+/* Allocate this rank's mailbox on `device`; handle_out_64 receives its 64-byte IPC handle,
+ * which the caller gathers from every rank (rank order) for dbk_mbox_open. */
+dbk_status dbk_mbox_create(int32_t nranks, int32_t rank, int32_t device, void *handle_out_64, dbk_mbox **out);
+/* Map every peer's mailbox: handles = nranks x 64 bytes in rank order (own entry ignored).
+ * ECUDA if a handle cannot be opened (e.g. no peer access). */
+dbk_status dbk_mbox_open(dbk_mbox *m, const void *handles);
+dbk_status dbk_mbox_destroy(dbk_mbox *m);
+/* Standalone exchange of a host record (every rank calls it once per exchange, in the same
+ * order): all = the nranks records (rank order), global = dbk_stats_reduce(all, mode).
+ * Synchronous on `stream`; ECUDA if a peer's record does not arrive within 20 s. */
+dbk_status dbk_mbox_exchange(dbk_mbox *m, const dbk_stats *local, dbk_stats *all, dbk_stats *global, int32_t mode,
+                             void *stream);
+/* dbk_engine_step then exchanges through the mailbox instead of a communicator: the step's
+ * first kernel stamps %globaltimer, its last one builds the record from the device
+ * statistics with step_ns = the device time between the two (S5), exchanges it and the host
+ * reduces (DP: nranks = cfg.world; TP: engine world 1).  NULL detaches.  EINVAL on a size
+ * mismatch or when a communicator is attached. */
+dbk_status dbk_engine_attach_mbox(dbk_engine *e, dbk_mbox *m, int32_t mode);
+
 #ifdef __cplusplus
 }
 #endif

@@ -292,6 +292,11 @@ class Engine:
         return dict(records=[arr[r].as_dict() for r in range(min(n.value, cap))], us=us.value,
                     us_total=tot.value, count=cnt.value)
 
+    def attach_mbox(self, mbox, mode):
+        """Exchange every step's record through a Mailbox (the step's last kernel); mode MODE_DP / MODE_TP."""
+        self.mbox = mbox
+        _lib.dbk_engine_attach_mbox(self.h, mbox.h if mbox is not None else None, int(mode))
+
     def attach_model(self, model):
         self.model = model
         _lib.dbk_engine_attach_model(self.h, model.h if model is not None else None)
@@ -371,6 +376,38 @@ class Comm:
     def close(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.dbk_comm_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+class Mailbox:
+    """dbk_mbox: the statistics exchange over peer memory (CUDA IPC mailboxes, one exchange
+    kernel per step).  The 64-byte IPC handles are gathered over the caller's
+    torch.distributed process group (`dist`)."""
+
+    def __init__(self, dist, world, rank, device):
+        h = C.c_void_p()
+        buf = (C.c_char * 64)()
+        _lib.dbk_mbox_create(int(world), int(rank), int(device), buf, C.byref(h))
+        self.h = h
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(buf.raw))
+        allb = (C.c_char * (64 * world)).from_buffer_copy(b"".join(handles))
+        _lib.dbk_mbox_open(self.h, allb)
+        self.world = world
+
+    def exchange(self, local: dict, mode=0, stream=None):
+        """(records of every rank, reduced global record) of one exchange."""
+        st = dbk_stats(*[int(local.get(f, 0)) for f in _lib.STATS_FIELDS])
+        arr = (dbk_stats * self.world)()
+        g = dbk_stats()
+        _lib.dbk_mbox_exchange(self.h, C.byref(st), arr, C.byref(g), int(mode), _stream(stream))
+        return [arr[r].as_dict() for r in range(self.world)], g.as_dict()
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.dbk_mbox_destroy(self.h)
             self.h = None
 
     __del__ = close

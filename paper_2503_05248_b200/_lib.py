@@ -175,6 +175,11 @@ SIGNATURES = {
     "dbk_comm_info": [P, PI32, PI32],
     "dbk_pool_trace_d2h": [P, P, I64, PI64, I32],
     "dbk_decode_step_layers": [P, C.POINTER(dbk_batch), I32, P, I64, P, I64, I32, P, PI32],
+    "dbk_mbox_create": [I32, I32, I32, P, C.POINTER(P)],
+    "dbk_mbox_open": [P, P],
+    "dbk_mbox_destroy": [P],
+    "dbk_mbox_exchange": [P, C.POINTER(dbk_stats), C.POINTER(dbk_stats), C.POINTER(dbk_stats), I32, P],
+    "dbk_engine_attach_mbox": [P, P, I32],
     "dbk_engine_last_exchange": [P, C.POINTER(dbk_stats), I32, PI32, C.POINTER(C.c_double),
                                  C.POINTER(C.c_double), PI64, I32],
 }

@@ -11,6 +11,7 @@
 
 #include "common.h"
 #include "kernels.cuh"
+#include "mailbox.h"
 #include "pool.h"
 
 using namespace dbk;
@@ -67,6 +68,8 @@ struct dbk_engine {
     dbk_comm *comm = nullptr;
     int32_t comm_mode = DBK_MODE_DP;
     int32_t comm_nranks = 1;
+    dbk_mbox *mbox = nullptr;         // mailbox exchange (v2), instead of comm
+    bool mbox_pending = false;        // this step's records are in x_all (gathered by the kernel)
     std::vector<dbk_stats> x_all;     // the last exchange: every rank's record, rank order
     double x_us = 0, x_us_total = 0;  // host time of the last exchange / since the last reset
     int64_t x_count = 0;
@@ -216,6 +219,7 @@ dbk_status dbk_engine_attach_model(dbk_engine *e, dbk_model *m) {
 
 dbk_status dbk_engine_attach_comm(dbk_engine *e, dbk_comm *c, int32_t mode) {
     if (!e || (mode != DBK_MODE_DP && mode != DBK_MODE_TP)) return fail(DBK_EINVAL, "attach_comm: bad argument");
+    if (c && e->mbox) return fail(DBK_EINVAL, "attach_comm: a mailbox is attached");
     int32_t n = 1;
     if (c) {
         DBK_TRY(dbk_comm_info(c, &n, nullptr));
@@ -228,6 +232,20 @@ dbk_status dbk_engine_attach_comm(dbk_engine *e, dbk_comm *c, int32_t mode) {
             return fail(DBK_EINVAL, "attach_comm: TP mode needs an engine with world 1 (got %d)", e->cfg.world);
     }
     e->comm = c;
+    e->comm_mode = mode;
+    e->comm_nranks = n;
+    return DBK_OK;
+}
+
+dbk_status dbk_engine_attach_mbox(dbk_engine *e, dbk_mbox *m, int32_t mode) {
+    if (!e || (mode != DBK_MODE_DP && mode != DBK_MODE_TP)) return fail(DBK_EINVAL, "attach_mbox: bad argument");
+    if (m && e->comm) return fail(DBK_EINVAL, "attach_mbox: a communicator is attached");
+    const int32_t n = m ? mbox_nranks(m) : 1;
+    if (m && mode == DBK_MODE_DP && n != e->cfg.world)
+        return fail(DBK_EINVAL, "attach_mbox: DP mailbox of %d ranks, engine world %d", n, e->cfg.world);
+    if (m && mode == DBK_MODE_TP && e->cfg.world != 1)
+        return fail(DBK_EINVAL, "attach_mbox: TP mode needs an engine with world 1 (got %d)", e->cfg.world);
+    e->mbox = m;
     e->comm_mode = mode;
     e->comm_nranks = n;
     return DBK_OK;
@@ -281,6 +299,10 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     e->step_clock0 = e->clock;
     e->step_b = e->b;
     DBK_CUDA(cudaEventRecord(e->ev0, s));
+    if (e->mbox) {  // S5 on the device clock: the exchange kernel subtracts this stamp
+        DBK_TRY(mbox_stamp(e->mbox, s));
+        ++p->n_launches;
+    }
 
     // S1: FCFS admission with head-of-line blocking (R17); prefill = synthetic fill of T tokens,
     // a swapped-out request is swapped back in instead (R30).  Pages are taken in admission
@@ -584,6 +606,12 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         DBK_CUDA(cudaStreamWaitEvent(s, e->ev_d2h, 0));  // the step ends after the last copy
     }
     DBK_CUDA(cudaEventRecord(e->ev1, s));
+    const int64_t n_waiting = static_cast<int64_t>(e->queue.size() + e->prefilling.size());
+    if (e->mbox) {  // S6 fused: the record leaves for every peer's mailbox straight from the device
+        DBK_TRY(mbox_launch(e->mbox, reinterpret_cast<const unsigned long long *>(p->d_stats), n == 0, pc.cap_pages,
+                            n_waiting, true, nullptr, s));
+        ++p->n_launches;
+    }
     // S5: statistics record (synchronises the stream) and device-timed step latency
     DBK_TRY(dbk_batch_stats(p, &e->local, s));
     if (n == 0) {  // no decode launch reduced the record: the empty batch's record (O3)
@@ -598,7 +626,13 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         const int32_t *sh = static_cast<const int32_t *>(e->tok_out.host);
         for (int32_t x = 0; x < n; ++x) bufs->host_tokens[e->running[x]] = sh[x];
     }
-    e->local.n_waiting = static_cast<int64_t>(e->queue.size() + e->prefilling.size());
+    e->local.n_waiting = n_waiting;
+    if (e->mbox) {  // the gathered records (mapped host memory); this rank's carries the device step time
+        e->x_all.resize(static_cast<size_t>(e->comm_nranks));
+        DBK_TRY(mbox_collect(e->mbox, e->x_all.data()));
+        e->local = e->x_all[static_cast<size_t>(mbox_rank(e->mbox))];
+        e->mbox_pending = true;
+    }
     if (pd) {  // R27: completed prompts join the decode batch from the next step on
         size_t m = 0;
         while (m < e->prefilling.size() &&
@@ -702,7 +736,12 @@ dbk_status dbk_engine_step(dbk_engine *e, const dbk_engine_buffers *bufs, void *
     dbk_stats local;
     DBK_TRY(dbk_engine_step_launch(e, bufs, stream, &local));
     dbk_stats global = local;
-    if (e->comm) {  // the gather buffer holds one record per communicator rank
+    if (e->mbox) {  // gathered by the step's exchange kernel
+        if (!e->mbox_pending) return fail(DBK_EINVAL, "engine_step: mailbox records missing");
+        e->mbox_pending = false;
+        DBK_TRY(dbk_stats_reduce(e->x_all.data(), e->comm_nranks, e->comm_mode, &global));
+        ++e->x_count;
+    } else if (e->comm) {  // the gather buffer holds one record per communicator rank
         e->x_all.resize(static_cast<size_t>(e->comm_nranks));
         const auto t0 = std::chrono::steady_clock::now();
         DBK_TRY(dbk_stats_allgather(e->comm, &local, e->x_all.data(), &global, e->comm_mode, stream));

@@ -1,7 +1,9 @@
 """bench.py at N = 2 on a one-GPU box: both ranks (DP request shards, or the 70B KV-head TP
 shards whose records must agree) on cuda:0 with a gloo process group
 (DBK_BENCH_TEST_GLOO=1) and 12 GB pools, launched exactly as the driver launches N > 1
-(torch.distributed.run).  Checks the N > 1 bookkeeping of the script: one JSON line from rank
+(torch.distributed.run).  With --exchange mailbox (the default) the ranks exchange their records
+through libdbk's mailboxes, the product path; NCCL cannot put two ranks on one device, so
+--exchange nccl falls to the harness's gloo exchange.  Checks the N > 1 bookkeeping of the script: one JSON line from rank
 0, n_gpus = 2, and tokens counted once -- every rank's step record is already global, so
 value = mean global batch / step time (a double count would make it 2x)."""
 import json
@@ -22,15 +24,16 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("config,par", [("llama2-7b", "dp2"), ("llama3-70b-gqa", "tp2")])
-def test_bench_two_ranks_counts_tokens_once(config, par):
+@pytest.mark.parametrize("config,par,exchange", [("llama2-7b", "dp2", "mailbox"), ("llama3-70b-gqa", "tp2", "mailbox"),
+                                                 ("llama2-7b", "dp2", "nccl")])
+def test_bench_two_ranks_counts_tokens_once(config, par, exchange):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     env = dict(os.environ, DBK_BENCH_TEST_GLOO="1", DBK_BENCH_KV_GB="12")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "6", "--warmup", "3", "--ff", "30", "--config", config]
+           "--gpus", "2", "--steps", "6", "--warmup", "3", "--ff", "30", "--config", config, "--exchange", exchange]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
@@ -41,3 +44,9 @@ def test_bench_two_ranks_counts_tokens_once(config, par):
     per_step = d["config"]["mean_batch"] / (d["ms_per_step"] / 1e3)
     assert abs(d["value"] - per_step) / per_step < 0.01, (d["value"], per_step)
     assert d["e2e"]["value"] > 0 and d["roofline"]["achieved"] > 0
+    x = d["config"]["stats_exchange"]
+    if exchange == "mailbox":  # the product exchange ran (the ranks share the GPU: IPC-mapped mailboxes)
+        assert x["kind"].startswith("libdbk mailbox") and x["exchanges"] >= 6, x
+        assert len(x["last_step_ns_per_rank"]) == 2 and min(x["last_step_ns_per_rank"]) > 0
+    else:
+        assert "gloo" in x["kind"]
