@@ -105,29 +105,37 @@ def _tbt_p99(recs):
 
 def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
              modes=(("static", False), ("combined", False), ("static", True), ("combined", True)),
-             b_static=None, lo=10.0, hi=640.0, tol=0.05, max_delay_s=2.0, ctrl_margin_ms=0.0, pd_token_budget=0):
+             b_static=None, lo=10.0, hi=640.0, tol=0.05, max_delay_s=2.0, ctrl_margin_ms=0.0, pd_token_budget=0,
+             seeds=(None,), static_bs=None):
     """Table II / Fig. 5 analog: capacity = the largest Poisson rate (qps) at which
     the p99 TBT stays <= D_SLA + eps_D AND the median scheduling delay (arrival -> first
     admission, from dbk_engine_request_times) stays <= 2 s -- Sarathi-Serve's definition, which
     the paper adopts -- found by bisection on the rate, for the static baseline and for
     Alg. 2 + Alg. 1, without and with PD fusion (Table II row 3 "implemented with PD fusion
-    scenario").  Each probe sends qps x window_s requests (a fixed arrival window)."""
+    scenario").  Each probe sends qps x window_s requests (a fixed arrival window).
+
+    Round 2: the bisection runs once per arrival seed (`seeds`: the trace's length
+    seed is fixed, the Poisson arrival stream varies) and reports the capacity per seed plus
+    mean / min / max, to a tolerance `tol`; `static_bs` sweeps the static baseline over several b
+    under the same SLA so the comparison is against the BEST static b, not one setting.
+    ctrl_margin_ms != 0 steers Alg. 2 below the SLA it is judged at -- NOT the paper's Alg. 2
+    (P:221-248); rows record it."""
     from synth import configs, trace
     c = configs.CONFIGS[cfg]
     t = c["trace"]
     out = dict(config=cfg, d_sla_ms=d_sla, eps_d_ms=eps_d, window_s=window_s, max_delay_s=max_delay_s,
                ctrl_margin_ms=ctrl_margin_ms, pd_token_budget=pd_token_budget, rows=[])
 
-    def probe(policy, pd, qps):
+    def probe(policy, pd, qps, seed=None, bst=None):
         n_req = max(100, int(qps * window_s))
         tr = trace.make_trace(n_req, t["mean_in"], t["mean_out"], t["L_max"], t["seed"], dist=t["dist"],
-                              arrival="poisson", rate_qps=qps)
+                              arrival="poisson", rate_qps=qps, arrival_seed=seed)
         import gc
 
         import torch
         gc.collect()
         torch.cuda.empty_cache()
-        S = bench.setup_engine(cfg_name=cfg, policy=policy, b_static=b_static or 256, sla_ms=d_sla - ctrl_margin_ms,
+        S = bench.setup_engine(cfg_name=cfg, policy=policy, b_static=bst or b_static or 256, sla_ms=d_sla - ctrl_margin_ms,
                                eps_d_ms=eps_d, time_attention=False, trace_override=tr, pd_fusion=pd,
                                full_model=FULL_MODEL, pd_token_budget=pd_token_budget if pd else 0)
         eng = S["eng"]
@@ -150,19 +158,27 @@ def capacity(cfg="llama2-13b-sla", d_sla=None, eps_d=None, window_s=20.0,
         return res
 
     for pol, pd in modes:
-        a, b = lo, hi
-        best, probes = None, []
-        while b - a > tol * a:
-            mid = (a * b) ** 0.5
-            r = probe(pol, pd, mid)
-            probes.append(r)
-            print(json.dumps(dict(policy=pol, pd=pd, **r)), flush=True)
-            if r["ok"]:
-                a, best = mid, r
-            else:
-                b = mid
-        out["rows"].append(dict(policy=pol, pd_fusion=pd, capacity_qps=a if best else None, at_capacity=best,
-                                probes=probes))
+        for bst in (static_bs if (pol == "static" and static_bs) else [None]):
+            per_seed = []
+            for seed in seeds:
+                a, b = lo, hi
+                best, probes = None, []
+                while b - a > tol * a:
+                    mid = (a * b) ** 0.5
+                    r = probe(pol, pd, mid, seed, bst)
+                    probes.append(r)
+                    print(json.dumps(dict(policy=pol, pd=pd, b_static=bst, seed=seed, **r)), flush=True)
+                    if r["ok"]:
+                        a, best = mid, r
+                    else:
+                        b = mid
+                per_seed.append(dict(seed=seed, capacity_qps=a if best else None, at_capacity=best, probes=probes))
+            caps = [x["capacity_qps"] for x in per_seed if x["capacity_qps"]]
+            out["rows"].append(dict(policy=pol, pd_fusion=pd, b_static=(bst or b_static or 256) if pol == "static" else None,
+                                    capacity_qps=float(np.mean(caps)) if caps else None,
+                                    capacity_min=min(caps) if caps else None, capacity_max=max(caps) if caps else None,
+                                    tol=tol, per_seed=per_seed))
+            print(json.dumps({k: v for k, v in out["rows"][-1].items() if k != "per_seed"}), flush=True)
     return out
 
 
@@ -313,6 +329,9 @@ def main():
     ap.add_argument("--cap-modes", default=None, help="capacity modes, e.g. static:pd,combined:pd,combined:nopd")
     ap.add_argument("--pd-token-budget", type=int, default=0,
                     help="PD fusion: fixed iteration token budget (R36) instead of b_t (R25)")
+    ap.add_argument("--cap-tol", type=float, default=0.05, help="capacity bisection: relative tolerance")
+    ap.add_argument("--cap-seeds", default=None, help="capacity: arrival seeds, e.g. 11,12,13 (one bisection each)")
+    ap.add_argument("--cap-static-bs", default=None, help="capacity: static baselines to sweep, e.g. 128,192,256")
     ap.add_argument("--out", default="gpurun_out/paper_tables.json")
     a = ap.parse_args()
     global FULL_MODEL
@@ -363,7 +382,9 @@ def main():
                 d = a.cap_d
             res["capacity"] = capacity(cfg=a.cap_config, d_sla=d, eps_d=round(0.04 * d, 3), b_static=int(b_mem), lo=a.cap_lo,
                                        hi=a.cap_hi, ctrl_margin_ms=a.cap_margin, modes=modes,
-                                       pd_token_budget=a.pd_token_budget)
+                                       pd_token_budget=a.pd_token_budget, tol=a.cap_tol,
+                                       seeds=tuple(int(x) for x in a.cap_seeds.split(",")) if a.cap_seeds else (None,),
+                                       static_bs=[int(x) for x in a.cap_static_bs.split(",")] if a.cap_static_bs else None)
             save()
     print(json.dumps({k: (v.get("fit") if isinstance(v, dict) else None) for k, v in res.items()}))
 

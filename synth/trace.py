@@ -97,9 +97,11 @@ def arrivals_ns(n, kind="all-at-once", rate_qps=None, segments=None, seed=0):
 
 
 def make_trace(n, mean_in, mean_out, L_max, seed, cv=1.0, dist="lognormal",
-               arrival="all-at-once", rate_qps=None, segments=None) -> Trace:
+               arrival="all-at-once", rate_qps=None, segments=None, arrival_seed=None) -> Trace:
+    """arrival_seed: seed of the arrival process alone (default: `seed`), so several Poisson
+    streams can carry the same length sample."""
     li, lo = sample_lengths(n, mean_in, mean_out, L_max, seed, cv, dist)
-    arr = arrivals_ns(n, arrival, rate_qps, segments, seed)
+    arr = arrivals_ns(n, arrival, rate_qps, segments, seed if arrival_seed is None else arrival_seed)
     return Trace(arr, li, lo)
 
 
