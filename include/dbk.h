@@ -249,7 +249,7 @@ dbk_status dbk_prefill_step(dbk_pool *pool, const dbk_prefill_batch *batch, cons
 typedef struct dbk_model_config {
     int32_t hidden;        /* H, multiple of 128                                    */
     int32_t ffn;           /* F (SwiGLU inner size), multiple of 128                */
-    int32_t vocab;         /* V                                                     */
+    int32_t vocab;         /* V, multiple of 4 (16-B rows of fp32 logits)           */
     int32_t max_pos;       /* RoPE table rows: positions 0 .. max_pos-1             */
     double rms_eps;        /* 1e-5 (Llama-2)                                        */
     double rope_theta;     /* 10000 (Llama-2)                                       */
@@ -266,8 +266,12 @@ size_t dbk_model_weight_bytes(const dbk_pool_config *pool_cfg, const dbk_model_c
 /* weight_mem: caller-owned device memory of >= dbk_model_weight_bytes bytes,
  * 256-B aligned; the model fills it with the synthetic weights (device
  * generator, synchronous).  The model allocates its activation workspace for
- * the pool's max_requests rows (cudaMalloc) and a cuBLASLt handle.  EINVAL on
- * bad shapes (kv_dtype must be fp16), ECUDA on CUDA/cuBLAS failures. */
+ * the pool's max_requests rows (cudaMalloc).  Every projection runs on the
+ * tensor-core GEMM (dbk_gemm_*) with the step's elementwise work fused into its
+ * epilogue; the QKV and gate|up weights are stored with their rows permuted for
+ * those epilogues (RoPE pairs adjacent, gate/up rows interleaved).  EINVAL on
+ * bad shapes (kv_dtype must be fp16, head_dim must divide 128), ECUDA on CUDA
+ * failures. */
 dbk_status dbk_model_create(dbk_pool *pool, const dbk_model_config *cfg, void *weight_mem, size_t bytes,
                             dbk_model **out);
 dbk_status dbk_model_destroy(dbk_model *model);
@@ -304,15 +308,47 @@ dbk_status dbk_model_step_pd(dbk_model *model, int32_t n, const int64_t *req_ids
 
 /* Introspection (tests): device pointers of the activation workspace of the last
  * step, rows = batch order: [0] x fp32 [n][H] (residual stream), [1] h fp16 [n][H]
- * (last norm output), [2] qkv fp16 [n][(Hq+2Hkv)d], [3] q fp16 [n][Hq][d] (after RoPE),
- * [4] attention out fp16 [n][Hq*d], [5] gate|up fp16 [n][2F], [6] act fp16 [n][F]
- * -- all of the LAST layer; [7] logits fp32 [n][V] (internal buffer). */
+ * (last norm output), [2] NULL (the QKV output lives only in the GEMM epilogue),
+ * [3] q fp16 [n][Hq][d] (after RoPE), [4] attention out fp16 [n][Hq*d], [5] NULL
+ * (gate|up: fused into the SiLU epilogue), [6] act fp16 [n][F] -- all of the LAST
+ * layer; [7] logits fp32 [n][V] (internal buffer). */
 dbk_status dbk_model_buffers(dbk_model *model, void **ptrs_out_8);
 
 /* Time split of the model steps since the last reset (CUDA events on the
  * step's stream): attention launches vs everything else (GEMMs, norms, RoPE). */
 dbk_status dbk_model_timing(dbk_model *model, double *attn_ms, double *total_ms, int64_t *steps,
                             int32_t reset);
+
+/* ------------------------------------------------------------------------ */
+/* Tensor-core GEMM of the model projections (NEXT row 3)                    */
+/* ------------------------------------------------------------------------ */
+
+/* The model's projections Y = X W^T ("the enlarged matrix dimensions in the
+ * matrix multiplication operations required for larger batches")
+ * on the 5th-generation tensor cores (tcgen05.mma, TMEM accumulators, TMA),
+ * persistent (gemm_tc.cu).  dbk_model_* runs the same kernel with the decode
+ * step's elementwise work fused into its epilogue; this entry point exposes the
+ * plain forms for tests and measurement.  A handle holds no device memory.
+ * cta_group: 1 = one SM per 128 weight rows, 2 = CTA pairs (cta_group::2, 256
+ * weight rows per pair). */
+typedef struct dbk_gemm dbk_gemm;
+dbk_status dbk_gemm_create(int32_t device, int32_t cta_group, dbk_gemm **out);
+/* x: device fp16 [M][ldx] row-major (activations), w: device fp16 [N][K]
+ * row-major (weights, K contiguous), y: device [M][ldy] row-major;
+ * mode 0: y (fp16) = x w^T; 1: y (fp32) = x w^T; 2: y (fp32) += x w^T
+ * (stream-K: K is split over the SMs and each partial product is added into y
+ * by the TMA unit, so the order of the fp32 additions varies run to run).
+ * fp32 accumulation.  Async on `stream`.  EINVAL unless K % 64 == 0, N >= 1,
+ * ldx >= K, ldx % 8 == 0, ldy >= N, x, w and the rows of y 16-B aligned;
+ * M == 0 is a no-op. */
+dbk_status dbk_gemm_run(dbk_gemm *g, int32_t M, int32_t N, int32_t K, const void *x, int64_t ldx, const void *w,
+                        void *y, int64_t ldy, int32_t mode, void *stream);
+/* Measurement hook: trace = device uint64 [148][8] (or NULL = off); the following launches
+ * stamp %globaltimer per CTA at start, after setup, first operands in shared memory, last
+ * MMA issued, last accumulator ready, its first TMEM chunk loaded, epilogue done, exit
+ * (slots 0-7). */
+dbk_status dbk_gemm_trace(dbk_gemm *g, void *trace);
+dbk_status dbk_gemm_destroy(dbk_gemm *g);
 
 /* ------------------------------------------------------------------------ */
 /* Synthetic input generator (input side only; none of the method's math)  */

@@ -72,6 +72,13 @@ def head_weights(seed, s: ModelShape):
     return dict(g_f=hashgen.gen_norm_weight(seed, hashgen.KIND_LNF, 0, s.hidden), w_lm=np.concatenate(rows))
 
 
+def linear(x, w):
+    """y = x W^T in float64 (x: [M][K], W: [N][K] as stored: one output feature per row) -- the
+    projections whose size grows with the batch ("the enlarged matrix dimensions in the matrix
+    multiplication operations required for larger batches")."""
+    return np.asarray(x, np.float64) @ np.asarray(w, np.float64).T
+
+
 def rmsnorm(x, g, eps):
     """x / sqrt(mean(x^2) + eps) * g over the last axis."""
     x = np.asarray(x, np.float64)

@@ -163,6 +163,36 @@ class KVPool:
         return st.as_dict()
 
 
+class Gemm:
+    """dbk_gemm: the model projections' tensor-core GEMM, y (=|+=) x w^T (torch fp16 operands)."""
+
+    MODES = {"f16": 0, "f32": 1, "acc32": 2}
+
+    def __init__(self, device=0, cta_group=2):
+        h = C.c_void_p()
+        _lib.dbk_gemm_create(device, cta_group, C.byref(h))
+        self.h = h
+        self.cta_group = cta_group
+
+    def __call__(self, x, w, y, mode="f16", stream=None):
+        M, K = x.shape
+        N = w.shape[0]
+        _lib.dbk_gemm_run(self.h, M, N, K, _ptr(x), x.stride(0), _ptr(w), _ptr(y), y.stride(0),
+                          self.MODES[mode], _stream(stream))
+        return y
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.dbk_gemm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter teardown
+            pass
+
+
 def synth_fill(seed, kind, req, pos, layer, n_heads, d, out, scale_log2=0, dtype=2, stream=None):
     r, pr = _i64(req)
     p, pp = _i32(pos)

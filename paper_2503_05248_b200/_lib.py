@@ -137,6 +137,10 @@ SIGNATURES = {
     "dbk_model_step_pd": [P, I32, PI64, C.POINTER(dbk_prefill_batch), I32, P, P, P, P],
     "dbk_model_timing": [P, C.POINTER(C.c_double), C.POINTER(C.c_double), PI64, I32],
     "dbk_engine_attach_model": [P, P],
+    "dbk_gemm_create": [I32, I32, C.POINTER(P)],
+    "dbk_gemm_run": [P, I32, I32, I32, P, I64, P, P, I64, I32, P],
+    "dbk_gemm_trace": [P, P],
+    "dbk_gemm_destroy": [P],
     "dbk_model_buffers": [P, C.POINTER(C.c_void_p)],
     "dbk_swap_space_attach": [P, P, C.c_size_t, PI64],
     "dbk_swap_out": [P, I32, PI64, P],

@@ -31,22 +31,9 @@ def _nccl_dirs():
     raise RuntimeError("nccl.h not found")
 
 
-def _cublas_dirs():
-    """torch's own cuBLASLt (the one a torch process has already loaded), else the toolkit's."""
-    import importlib.util
-    spec = importlib.util.find_spec("nvidia")
-    if spec and spec.submodule_search_locations:
-        for d in spec.submodule_search_locations:
-            c = os.path.join(d, "cublas")
-            if os.path.exists(os.path.join(c, "include", "cublasLt.h")) and \
-                    os.path.exists(os.path.join(c, "lib", "libcublasLt.so.12")):
-                return os.path.join(c, "include"), os.path.join(c, "lib")
-    return "/usr/local/cuda/include", "/usr/local/cuda/lib64"
-
-
 def _common_flags(nccl_inc):
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall",
-                   "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_inc, "-I", _cublas_dirs()[0]]
+                   "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_inc]
 
 
 SAN = ["-fsanitize=address", "-fsanitize=undefined", "-fno-omit-frame-pointer", "-fno-sanitize-recover=undefined"]
@@ -91,7 +78,6 @@ def build(force: bool = False, verbose: bool = False, sanitize: bool = False) ->
         return lib
     link = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + (["-Xlinker", "-lasan", "-Xlinker", "-lubsan"] if sanitize else []) + [
         "-L", nccl_lib, "-Xlinker", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl_lib}",
-        "-L", _cublas_dirs()[1], "-Xlinker", "-l:libcublasLt.so.12", "-Xlinker", f"-rpath,{_cublas_dirs()[1]}",
         "-lpthread"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:

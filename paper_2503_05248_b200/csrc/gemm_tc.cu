@@ -1,0 +1,665 @@
+// Model GEMMs on the 5th-generation tensor cores (the decode step's
+// QKV / O / gate-up / down / LM-head projections, "enlarged matrix dimensions in the
+// matrix multiplication operations required for larger batches").
+//
+//   Y[M][N] = X[M][K] W[N][K]^T,  X = activations (M = batch rows <= a few hundred), W = weights.
+//
+// Swap-AB: the weight rows are the MMA's M side (128 per CTA, 256 per CTA pair with
+// cta_group::2) and the activation rows its N side (BN <= 256), so the decode batch never pads
+// an M = 128 tile.  D lives in TMEM: lane = weight row, column = activation row.
+//   warp 0      TMA producer: 128B-swizzled {64 K x 128 weight rows} and {64 K x BN/CG act rows}
+//               boxes into a ring of stages (CTA pairs: each CTA loads its half of both operands,
+//               completion counted on the leader's barrier); the weight boxes of the first stages
+//               are requested before the grid-dependency wait (weights never depend on the
+//               previous kernel)
+//   warp 1      TMEM owner (2 x BN columns: double-buffered accumulator) and, in the leader CTA,
+//               the tcgen05.mma issuer (4 x K=16 MMAs per stage)
+//   warps 2-5   epilogue, 32 activation rows at a time: tcgen05.ld of the thread's TMEM lane,
+//               the fused elementwise op, the result transposed into a shared-memory chunk
+//               [32 m][n] and written by TMA (bulk tensor store / reduce-add, or per-row bulk
+//               copies into the KV pages), double-buffered so the next chunk overlaps the store.
+//               (Per-thread strided st.global of the accumulator columns cost ~1.4 us per 32 rows
+//               whatever the element size: profiles/r02_gemm_trace.log.)
+// Scheduling (persistent): GEMMs that ACCUMULATE into an fp32 output (the residual stream: O and
+// down projections) are stream-K -- the (tile x k-block) iterations are split evenly over the CTA
+// groups and every partial tile is added into the output by the TMA unit (cp.reduce.async.bulk
+// .add), so no wave is partly idle and no CTA waits for another; the other GEMMs run whole tiles
+// (no K split) round-robin, with the activation tile width BN chosen from a cost model of wave
+// count x per-k-block time (MMA time vs the measured ~50 B/clk/SM of L2 -> SM operand traffic).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <new>
+
+#include "common.h"
+#include "device_common.cuh"
+#include "gemm.h"
+#include "tc_common.cuh"
+
+namespace dbk {
+namespace {
+using namespace dev;
+using namespace tc;
+
+constexpr int kBM = 128;          // weight rows per CTA = TMEM lanes
+constexpr int kBK = 64;           // K elements per stage: one 128-byte swizzled row
+constexpr int kThreads = 192;     // warp 0 TMA, warp 1 TMEM + MMA, warps 2-5 epilogue
+constexpr int kMaxStages = 8;
+constexpr int kMaxBN = 256;
+constexpr int kChunk = 32;                      // activation rows per epilogue chunk
+constexpr int kStageOut = kChunk * kBM * 4;     // one chunk of fp32 outputs: 16 KiB
+constexpr int kDynSmem = 227 * 1024 - 4096;     // dynamic shared memory per CTA (static ~3.3 KiB)
+constexpr int kRingBudget = kDynSmem - 1024 - 2 * kStageOut;
+
+struct KParams {
+    int32_t M, N, K, BN, m_tiles, kb, groups, stages;
+    int32_t units;
+    int32_t stream_k;   // 1: contiguous iteration ranges (partial tiles reduce-added); 0: whole tiles
+    int64_t T;          // units * kb
+    uint64_t *trace;    // optional [CTA][8] %globaltimer phase stamps (experiments/gemm_bench.py --trace)
+    GemmEpiArgs e;
+};
+
+struct Seg {
+    int32_t unit, k0, k1;
+};
+// The next segment (one unit's k-block range) of group g.  Stream-K: the group's iteration range
+// [it, it1); whole tiles: units g, g + G, g + 2G, ... (it counts the group's units).
+__device__ __forceinline__ bool next_seg(const KParams &p, int g, int64_t &it, int64_t it1, Seg &s) {
+    if (p.stream_k) {
+        if (it >= it1) return false;
+        s.unit = static_cast<int32_t>(it / p.kb);
+        s.k0 = static_cast<int32_t>(it % p.kb);
+        s.k1 = static_cast<int32_t>(min(static_cast<int64_t>(p.kb), s.k0 + (it1 - it)));
+        it += s.k1 - s.k0;
+        return true;
+    }
+    const int64_t u = g + it * p.groups;
+    if (u >= p.units) return false;
+    s.unit = static_cast<int32_t>(u);
+    s.k0 = 0;
+    s.k1 = p.kb;
+    ++it;
+    return true;
+}
+
+template <int CG>
+__device__ __forceinline__ void tma_load2d(void *dst, const CUtensorMap *map, int c0, int c1, uint32_t bar) {
+    if constexpr (CG == 1) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+            : "memory");
+    } else {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_store2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
+// contiguous shared -> global bulk copy (16-B aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most 1 of this thread's bulk groups still reads shared memory
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Elementwise part of the epilogue: this thread's weight row n (tile row r) for the 32 activation
+// rows of a chunk, written into the chunk's shared-memory image `so` ([32][row width]).
+template <int EPI>
+__device__ __forceinline__ void epi_to_smem(const KParams &p, const float (&v)[32], int r, int n, int cb,
+                                            const int32_t *m_pos, uint8_t *so, int lane) {
+    if constexpr (EPI == kEpiF32 || EPI == kEpiAcc32) {
+        float *s = reinterpret_cast<float *>(so);
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) s[j * kBM + r] = v[j];
+    } else if constexpr (EPI == kEpiF16) {
+        __half *s = reinterpret_cast<__half *>(so);
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) s[j * kBM + r] = __float2half_rn(v[j]);
+    } else if constexpr (EPI == kEpiSiluMul) {
+        // rows interleaved (gate_j, up_j): the even lane of each pair owns act column r / 2
+        __half *s = reinterpret_cast<__half *>(so);
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+            const float up = __shfl_xor_sync(kFull, v[j], 1);
+            const float gt = v[j];
+            if (!(lane & 1)) s[j * (kBM / 2) + (r >> 1)] = __float2half_rn(gt / (1.0f + __expf(-gt)) * up);
+        }
+    } else if constexpr (EPI == kEpiRopeKV) {
+        // rotate-half pair i = (x[i], x[i + d/2]) of a q or k head sits in rows (2i, 2i + 1); the
+        // chunk image holds each head in logical order
+        const GemmEpiArgs &e = p.e;
+        const int d = e.head_dim;
+        const int hh = n / d, rr = n % d;
+        __half *s = reinterpret_cast<__half *>(so);
+        const int col0 = r - rr;  // the head's first row within the tile
+        if (hh < e.q_heads + e.kv_heads) {
+            const int i = rr >> 1, hd = d >> 1;
+            const bool odd = rr & 1;
+            const int col = col0 + (odd ? i + hd : i);
+            const float sgn = odd ? 1.f : -1.f;
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) {
+                const float other = __shfl_xor_sync(kFull, v[j], 1);
+                const float2 c = e.cs[static_cast<int64_t>(m_pos[cb + j]) * hd + i];
+                s[j * kBM + col] = __float2half_rn(fmaf(sgn * other, c.y, v[j] * c.x));
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) s[j * kBM + r] = __float2half_rn(v[j]);
+        }
+    }
+}
+
+// Issue the global writes of a chunk image (epilogue warp 0 only; each issuing lane commits its
+// own bulk group).
+template <int EPI>
+__device__ __forceinline__ void epi_issue(const KParams &p, const CUtensorMap *ty, const uint8_t *so, int nrow0,
+                                          int m, const int64_t *m_off, int cb, int lane) {
+    if constexpr (EPI == kEpiRopeKV) {
+        // lane j: token m + j; one contiguous d-element row per head of the tile
+        const GemmEpiArgs &e = p.e;
+        const int d = e.head_dim;
+        if (m + lane < p.M) {
+            for (int h0 = 0; h0 < kBM; h0 += d) {
+                const int hh = (nrow0 + h0) / d;
+                const uint8_t *src = so + (lane * kBM + h0) * 2;
+                uint8_t *dst;
+                if (hh < e.q_heads) {
+                    dst = reinterpret_cast<uint8_t *>(e.q_out + (static_cast<int64_t>(m + lane) * e.q_heads + hh) * d);
+                } else if (hh < e.q_heads + e.kv_heads) {
+                    dst = e.kv_layer + m_off[cb + lane] + (hh - e.q_heads) * e.tile_bytes;
+                } else {
+                    dst = e.kv_layer + m_off[cb + lane] + (hh - e.q_heads - e.kv_heads) * e.tile_bytes +
+                          static_cast<int64_t>(kP) * d * 2;
+                }
+                bulk_s2g(dst, src, d * 2);
+            }
+        }
+        bulk_commit();
+    } else if (lane == 0) {
+        if constexpr (EPI == kEpiAcc32) tma_reduce_add2d(ty, so, nrow0, m);
+        else if constexpr (EPI == kEpiSiluMul) tma_store2d(ty, so, nrow0 / 2, m);
+        else tma_store2d(ty, so, nrow0, m);
+        bulk_commit();
+    }
+}
+
+template <int CG, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
+               const __grid_constant__ CUtensorMap ty, const KParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ int32_t m_pos[EPI == kEpiRopeKV ? kMaxBN : 1];
+    __shared__ int64_t m_off[EPI == kEpiRopeKV ? kMaxBN : 1];
+
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int BNc = p.BN / CG;  // activation rows this CTA loads per stage
+    const uint32_t a_bytes = kBM * 128, stage_bytes = a_bytes + BNc * 128;
+    uint8_t *outbuf = smem + p.stages * stage_bytes;  // 2 chunk images
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const int g = static_cast<int>(blockIdx.x) / CG;
+    const int64_t it0 = p.stream_k ? g * p.T / p.groups : 0;
+    const int64_t it1 = p.stream_k ? (g + 1) * p.T / p.groups : 0;
+    uint32_t tcols = 32;
+    while (tcols < static_cast<uint32_t>(2 * p.BN)) tcols <<= 1;
+    uint64_t *tr = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = global_ns();
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], CG * 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                         "r"(tcols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                         "r"(tcols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        }
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    if (tr && threadIdx.x == 0) tr[1] = global_ns();
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        const uint32_t full_lead = CG == 2 ? cluster_addr(&full[0], 0) : smem_u32(&full[0]);
+        // the first ring's weight boxes go out before the grid-dependency wait: weights never
+        // depend on the previous kernel, the activations (and the outputs' readers) do
+        int pre = 0;
+        {
+            int64_t it_p = it0;
+            Seg s0;
+            if (lane == 0 && next_seg(p, g, it_p, it1, s0)) {
+                const int wrow = (s0.unit / p.m_tiles) * kBM * CG + static_cast<int>(rank) * kBM;
+                pre = min(p.stages, s0.k1 - s0.k0);
+                for (int s = 0; s < pre; ++s) {
+                    if (rank == 0) mbar_expect_tx(&full[s], CG * stage_bytes);
+                    tma_load2d<CG>(smem + s * stage_bytes, &tw, (s0.k0 + s) * kBK, wrow, full_lead + s * 8);
+                }
+            }
+            pre = __shfl_sync(kFull, pre, 0);
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        int stage = 0, done = 0;
+        uint32_t phase = 0;
+        int64_t it = it0;
+        Seg sg;
+        while (next_seg(p, g, it, it1, sg)) {
+            const int nt = sg.unit / p.m_tiles, mt = sg.unit % p.m_tiles;
+            const int wrow = nt * kBM * CG + static_cast<int>(rank) * kBM;
+            const int xrow = mt * p.BN + static_cast<int>(rank) * BNc;
+            for (int kb = sg.k0; kb < sg.k1; ++kb, ++done) {
+                if (lane == 0) {
+                    uint8_t *sa = smem + stage * stage_bytes;
+                    const uint32_t fb = full_lead + stage * 8;
+                    if (done >= pre) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        if (rank == 0) mbar_expect_tx(&full[stage], CG * stage_bytes);
+                        tma_load2d<CG>(sa, &tw, kb * kBK, wrow, fb);
+                    }
+                    tma_load2d<CG>(sa + a_bytes, &tx, kb * kBK, xrow, fb);
+                }
+                __syncwarp();
+                if (++stage == p.stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (the leader CTA of a pair issues for both)
+        if (rank == 0) {
+            const uint32_t idesc = idesc_f16(0, 0, kBM * CG, p.BN);
+            const uint32_t base = smem_u32(smem);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, aph = 0;
+            int64_t it = it0;
+            Seg sg;
+            bool first = true;
+            while (next_seg(p, g, it, it1, sg)) {
+                mbar_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t td = tmem + acc * p.BN;
+                for (int kb = sg.k0; kb < sg.k1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (tr && first && lane == 0) tr[2] = global_ns();
+                    first = false;
+                    const uint32_t sa = base + stage * stage_bytes, sb = sa + a_bytes;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t ad = smem_desc(sa + kk * 32, 16, 1024, 2);
+                        const uint64_t bd = smem_desc(sb + kk * 32, 16, 1024, 2);
+                        const uint32_t accum = (kb > sg.k0 || kk > 0) ? 1u : 0u;
+                        if constexpr (CG == 2) umma_ss_pair(td, ad, bd, idesc, accum);
+                        else umma_ss(td, ad, bd, idesc, accum);
+                    }
+                    if constexpr (CG == 2) umma_commit_pair(&empty[stage], 3);
+                    else umma_commit(&empty[stage]);
+                    if (++stage == p.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if constexpr (CG == 2) umma_commit_pair(&tfull[acc], 3);
+                else umma_commit(&tfull[acc]);
+                if (tr && lane == 0) tr[3] = global_ns();
+                if (++acc == 2) {
+                    acc = 0;
+                    aph ^= 1;
+                }
+            }
+        }
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    } else {
+        // ---------------- epilogue: thread <-> TMEM lane (weight row) of its warp's quarter
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int et = threadIdx.x - 64;
+        const bool issuer = et < 32;  // epilogue warp 0 writes the chunks out
+        const uint32_t tempty_lead = CG == 2 ? cluster_addr(&tempty[0], 0) : smem_u32(&tempty[0]);
+        int acc = 0, chunk = 0;
+        uint32_t aph = 0;
+        int64_t it = it0;
+        Seg sg;
+        while (next_seg(p, g, it, it1, sg)) {
+            const int nt = sg.unit / p.m_tiles, mt = sg.unit % p.m_tiles;
+            const int nrow0 = nt * kBM * CG + static_cast<int>(rank) * kBM;  // this CTA's first weight row
+            const int m0 = mt * p.BN;
+            if constexpr (EPI == kEpiRopeKV) {
+                epi_bar();  // the previous unit is done with m_pos / m_off
+                for (int i = et; i < p.BN; i += 128) {
+                    const int m = m0 + i;
+                    if (m < p.M) {
+                        const TokRow tk = p.e.rows[m];
+                        const int32_t page = p.e.bt[static_cast<int64_t>(tk.slot) * p.e.bt_stride + tk.pos / kP];
+                        m_pos[i] = tk.pos;
+                        m_off[i] = page * p.e.page_stride + static_cast<int64_t>(tk.pos % kP) * p.e.head_dim * 2;
+                    } else {
+                        m_pos[i] = 0;
+                        m_off[i] = 0;
+                    }
+                }
+                epi_bar();
+            }
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            if (tr && et == 0) tr[4] = global_ns();
+            const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * p.BN;
+            const int cmax = min(p.BN, p.M - m0);  // activation rows of this tile (>= 1)
+            for (int c0 = 0; c0 < cmax; c0 += kChunk, ++chunk) {
+                uint32_t rr[32];
+                tmem_ld32(ta + c0, rr);
+                tmem_ld_wait();
+                if (tr && et == 0 && c0 == 0) tr[5] = global_ns();
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
+                if (c0 + kChunk >= cmax) {
+                    // the tile's accumulator is in registers: release it to the next tile's MMAs
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_lead + acc * 8);
+                }
+                uint8_t *so = outbuf + (chunk & 1) * kStageOut;
+                // the writes issued from this buffer two chunks ago have finished reading it
+                if (issuer) bulk_wait_read1();
+                epi_bar();
+                epi_to_smem<EPI>(p, v, row, nrow0 + row, c0, m_pos, so, lane);
+                fence_proxy_async();
+                epi_bar();
+                if (issuer) epi_issue<EPI>(p, &ty, so, nrow0, m0 + c0, m_off, c0, lane);
+            }
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        if (issuer) bulk_wait_all();
+        if (tr && et == 0) tr[6] = global_ns();
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
+        if (tr && lane == 0) tr[7] = global_ns();
+    }
+}
+
+using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, KParams);
+
+template <int CG>
+KernFn kernel_for(int epi) {
+    switch (epi) {
+        case kEpiF16: return gemm_tc_kernel<CG, kEpiF16>;
+        case kEpiF32: return gemm_tc_kernel<CG, kEpiF32>;
+        case kEpiAcc32: return gemm_tc_kernel<CG, kEpiAcc32>;
+        case kEpiRopeKV: return gemm_tc_kernel<CG, kEpiRopeKV>;
+        case kEpiSiluMul: return gemm_tc_kernel<CG, kEpiSiluMul>;
+        default: return nullptr;
+    }
+}
+
+bool encode_2d(void *fn, CUtensorMap *map, CUtensorMapDataType dt, int esize, const void *base, uint64_t inner,
+               uint64_t rows, uint64_t ld_elems, uint32_t box_inner, uint32_t box_rows, bool swizzle) {
+    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    const cuuint64_t gdim[2] = {inner, rows};
+    const cuuint64_t gstride[1] = {ld_elems * esize};
+    const cuuint32_t box[2] = {box_inner, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(map, dt, 2, const_cast<void *>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Activation tile width for whole-tile GEMMs: the multiple of 32 that minimises
+// waves x per-k-block time, per-k-block time = max(MMA: 2 BN clk, operand traffic at ~50 B/clk
+// per SM: (128 + BN/CG) x 128 B / 50) + a fixed ~40 clk (profiles/r02_gemm_trace.log).
+void choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tiles) {
+    double best = 1e300;
+    *m_tiles = (M + kMaxBN - 1) / kMaxBN;
+    *BN = ((M + *m_tiles - 1) / *m_tiles + 31) / 32 * 32;
+    for (int mt = *m_tiles; mt <= std::max(1, (M + 31) / 32); ++mt) {
+        const int bn = ((M + mt - 1) / mt + 31) / 32 * 32;
+        if ((M + bn - 1) / bn != mt) continue;
+        const int64_t units = static_cast<int64_t>(n_tiles) * mt;
+        const int64_t waves = (units + groups - 1) / groups;
+        const double per_kb = std::max(2.0 * bn, (128.0 + static_cast<double>(bn) / cg) * 128.0 / 50.0) + 40.0;
+        const double t = static_cast<double>(waves) * per_kb;
+        if (t < best * 0.999) {
+            best = t;
+            *BN = bn;
+            *m_tiles = mt;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t GemmRunner::init(int device, int cta_group) {
+    if (cta_group != 1 && cta_group != 2) return cudaErrorInvalidValue;
+    device_ = device;
+    cg_ = cta_group;
+    cudaError_t e = cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return e;
+    cudaDriverEntryPointQueryResult q;
+    if ((e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &encode_, cudaEnableDefault, &q)) != cudaSuccess)
+        return e;
+    if (!encode_ || q != cudaDriverEntryPointSuccess) return cudaErrorNotSupported;
+    for (int epi = kEpiF16; epi <= kEpiSiluMul; ++epi) {
+        KernFn k = cg_ == 2 ? kernel_for<2>(epi) : kernel_for<1>(epi);
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem)) != cudaSuccess)
+            return e;
+    }
+    if (cg_ == 1) {
+        max_groups_ = sms_;
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * sms_);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kDynSmem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if ((e = cudaOccupancyMaxActiveClusters(&clusters, kernel_for<2>(kEpiF16), &cfg)) != cudaSuccess) return e;
+        max_groups_ = std::min(clusters, sms_ / 2);
+        if (max_groups_ < 1) return cudaErrorNotSupported;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, const __half *W, const GemmEpiArgs &e,
+                            cudaStream_t s, bool pdl) {
+    if (M == 0) return cudaSuccess;
+    if (M < 0 || K <= 0 || K % kBK || N <= 0 || ldx < K || ldx % 8 || (reinterpret_cast<uintptr_t>(X) & 15) ||
+        (reinterpret_cast<uintptr_t>(W) & 15) || !encode_)
+        return cudaErrorInvalidValue;
+    // fused epilogues address whole weight tiles (rows past N would be zero-filled operands)
+    if ((e.kind == kEpiRopeKV || e.kind == kEpiSiluMul) && N % (kBM * cg_)) return cudaErrorInvalidValue;
+    if (e.kind == kEpiRopeKV && (e.head_dim <= 0 || kBM % e.head_dim)) return cudaErrorInvalidValue;
+    KParams p{};
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.kb = K / kBK;
+    const int n_tiles = (N + kBM * cg_ - 1) / (kBM * cg_);  // a ragged last tile: TMA zero-fills
+                                                            // its weight rows, clips its stores
+    p.stream_k = e.kind == kEpiAcc32 ? 1 : 0;
+    if (p.stream_k) {
+        p.m_tiles = (M + kMaxBN - 1) / kMaxBN;
+        p.BN = ((M + p.m_tiles - 1) / p.m_tiles + 31) / 32 * 32;
+    } else {
+        choose_tiles(M, n_tiles, max_groups_, cg_, &p.BN, &p.m_tiles);
+    }
+    p.units = n_tiles * p.m_tiles;
+    p.T = static_cast<int64_t>(p.units) * p.kb;
+    if (p.stream_k) {
+        // >= 4 k-blocks per group: a partial tile's reduce-add (BN x 128 x 4 B) stays small next to
+        // the operand traffic of its k-blocks
+        p.groups = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_groups_, p.T / 4)));
+    } else {
+        p.groups = std::min(max_groups_, p.units);
+    }
+    const int stage_bytes = kBM * 128 + (p.BN / cg_) * 128;
+    p.stages = std::min(kMaxStages, kRingBudget / stage_bytes);
+    p.trace = trace_;
+    p.e = e;
+    CUtensorMap tw, tx, ty;
+    if (!encode_2d(encode_, &tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W, K, N, K, kBK, kBM, true) ||
+        !encode_2d(encode_, &tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, X, K, M, ldx, kBK, p.BN / cg_, true))
+        return cudaErrorInvalidValue;
+    bool ok = true;
+    switch (e.kind) {
+        case kEpiF16:
+            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N, M, e.ldy, kBM, kChunk, false);
+            break;
+        case kEpiF32:
+        case kEpiAcc32:
+            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, e.y, N, M, e.ldy, kBM, kChunk, false);
+            break;
+        case kEpiSiluMul:
+            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N / 2, M, e.ldy, kBM / 2, kChunk,
+                           false);
+            break;
+        default:
+            ty = tw;  // unused by the RoPE / KV epilogue (per-row bulk copies)
+    }
+    if (!ok) return cudaErrorInvalidValue;
+    KernFn k = cg_ == 2 ? kernel_for<2>(e.kind) : kernel_for<1>(e.kind);
+    if (!k) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.groups * cg_);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + 2 * kStageOut + 1024;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cg_;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    ++launches_;
+    return cudaLaunchKernelEx(&cfg, k, tw, tx, ty, p);
+}
+
+}  // namespace dbk
+
+// ------------------------------------------------------------------ C-ABI
+using namespace dbk;
+
+struct dbk_gemm {
+    GemmRunner run;
+};
+
+extern "C" {
+
+dbk_status dbk_gemm_create(int32_t device, int32_t cta_group, dbk_gemm **out) {
+    if (!out) return fail(DBK_EINVAL, "gemm_create: null out");
+    if (cta_group != 1 && cta_group != 2) return fail(DBK_EINVAL, "gemm_create: cta_group must be 1 or 2");
+    DBK_CUDA(cudaSetDevice(device));
+    dbk_gemm *g = new (std::nothrow) dbk_gemm();
+    if (!g) return fail(DBK_EINVAL, "out of host memory");
+    const cudaError_t e = g->run.init(device, cta_group);
+    if (e != cudaSuccess) {
+        delete g;
+        return fail(DBK_ECUDA, "gemm_create: %s", cudaGetErrorString(e));
+    }
+    *out = g;
+    return DBK_OK;
+}
+
+dbk_status dbk_gemm_run(dbk_gemm *g, int32_t M, int32_t N, int32_t K, const void *x, int64_t ldx, const void *w,
+                        void *y, int64_t ldy, int32_t mode, void *stream) {
+    if (!g || (M > 0 && (!x || !w || !y))) return fail(DBK_EINVAL, "gemm_run: null argument");
+    if (mode < kEpiF16 || mode > kEpiAcc32) return fail(DBK_EINVAL, "gemm_run: mode must be 0 (fp16), 1 (fp32), 2 (fp32 +=)");
+    const int esz = mode == kEpiF16 ? 2 : 4;
+    if (ldy < N || (ldy * esz) % 16 || (reinterpret_cast<uintptr_t>(y) & 15))
+        return fail(DBK_EINVAL, "gemm_run: need ldy >= N and 16-B aligned rows of y");
+    if (M < 0 || K <= 0 || K % kBK || N <= 0 || ldx < K || ldx % 8)
+        return fail(DBK_EINVAL, "gemm_run: need K %% 64 == 0, N >= 1, ldx >= K, ldx %% 8 == 0");
+    GemmEpiArgs e;
+    e.kind = mode;
+    e.y = y;
+    e.ldy = ldy;
+    const cudaError_t st = g->run.run(M, N, K, static_cast<const __half *>(x), ldx, static_cast<const __half *>(w), e,
+                                      static_cast<cudaStream_t>(stream), false);
+    if (st != cudaSuccess) return fail(DBK_ECUDA, "gemm_run: %s", cudaGetErrorString(st));
+    return DBK_OK;
+}
+
+dbk_status dbk_gemm_trace(dbk_gemm *g, void *trace) {
+    if (!g) return fail(DBK_EINVAL, "gemm_trace: null handle");
+    g->run.set_trace(static_cast<uint64_t *>(trace));
+    return DBK_OK;
+}
+
+dbk_status dbk_gemm_destroy(dbk_gemm *g) {
+    delete g;
+    return DBK_OK;
+}
+
+}  // extern "C"

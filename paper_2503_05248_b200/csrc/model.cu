@@ -1,24 +1,22 @@
 // Full decode step with synthetic weights (R32-R35):
 // a Llama-2-shaped decoder whose attention is the pool's paged decode attention (K1/K2).
-//   - plain GEMMs (QKV, O, gate|up, down, LM head): cuBLASLt, fp16 operands, fp32
-//     accumulation; the O and down projections accumulate into the fp32 residual stream
-//     in place (beta = 1, C = D);
-//   - our kernels: synthetic weight fill, embedding + RMSNorm, RMSNorm, RoPE + KV write
-//     straight into the decode token's page slot (the QKV GEMM's epilogue), SiLU * up.
-#include <cublasLt.h>
+//   - every projection (QKV, O, gate|up, down, LM head) is our tcgen05 GEMM (gemm_tc.cu) with
+//     the step's elementwise work fused into its epilogue: RoPE of q and k + the token's K/V
+//     written straight into its page slot (QKV), silu(gate) * up (gate|up: weight rows stored
+//     interleaved), the residual add (O and down accumulate into the fp32 residual stream);
+//   - our kernels around them: synthetic weight fill, embedding + RMSNorm, RMSNorm.
 #include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
-#include <map>
 #include <new>
-#include <tuple>
 #include <vector>
 
 #include "common.h"
 #include "device_common.cuh"
+#include "gemm.h"
 #include "kernels.cuh"
 #include "pool.h"
 
@@ -27,35 +25,35 @@ using namespace dbk;
 namespace {
 using namespace dbk::dev;
 
-// One activation row of a model step: a decode token (pos = ctx - 1) or a prefill-chunk token.
-struct RowMeta {
-    int64_t req_id;
-    int32_t slot;  // block-table row
-    int32_t pos;   // token position
-};
-static_assert(sizeof(RowMeta) == 16, "RowMeta layout");
+using RowMeta = TokRow;  // one activation row: a decode token (pos = ctx - 1) or a chunk token
 
 constexpr int kWChunk = 128;  // synthetic weight rows are K/128 "heads" of 128 dims (hashgen)
 constexpr int kKindToken = 7, kKindEmbed = 8, kKindLn1 = 9, kKindWqkv = 10, kKindWo = 11, kKindLn2 = 12,
               kKindWgu = 13, kKindWdown = 14, kKindLnf = 15, kKindLm = 16;
+// physical -> logical row order of a weight as stored for its GEMM epilogue (gemm.h)
+constexpr int kPermNone = 0, kPermQkv = 1, kPermGu = 2;
 
 // ------------------------------------------------------------------ kernels
 // W[row][k] = (byte - 128) * scale (+1 for norm gains), byte of (seed, kind, 0, row, layer, k / 128,
-// k % 128): the host passes scale = 2^(scale_log2 - 7), i.e. value * 2^scale_log2 of synth/hashgen.py
+// k % 128): the host passes scale = 2^(scale_log2 - 7), i.e. value * 2^scale_log2 of synth/hashgen.py.
+// Physical row `prow` holds logical row perm(prow) (kPermQkv / kPermGu: the GEMM epilogues' layouts,
+// gemm.h qkv_logical_row / gu_logical_row; pa, pb = (q_heads, kv_heads) resp. (F, -)).
 __global__ void fill_weights_kernel(__half *w, int64_t rows, int K, int layer, int kind, uint64_t seed, float scale,
-                                    int norm) {
+                                    int norm, int perm, int pa, int pb, int pd) {
     const int64_t per_row = K / 8;
     const int64_t total = rows * per_row;
     for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < total;
          c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t row = c / per_row;
+        const int64_t prow = c / per_row;
+        const int64_t row = perm == kPermQkv ? qkv_logical_row(prow, pa, pb, pd)
+                                             : (perm == kPermGu ? gu_logical_row(prow, pa) : prow);
         const int k = static_cast<int>(c % per_row) * 8;
         float f[8];
         synth_vals(synth_key(seed, kind, 0, static_cast<int>(row), layer, k / kWChunk, (k % kWChunk) / 8), scale, f);
         if (norm)
 #pragma unroll
             for (int e = 0; e < 8; ++e) f[e] += 1.0f;
-        *reinterpret_cast<uint4 *>(w + row * K + k) = pack8<__half>(f);
+        *reinterpret_cast<uint4 *>(w + prow * K + k) = pack8<__half>(f);
     }
 }
 
@@ -126,75 +124,6 @@ __global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, fl
     }
 }
 
-// RoPE (rotate-half pairs (j, j + d/2), angle table cs[pos][j] = (cos, sin)) on the q and k
-// heads of the QKV GEMM output; q -> q_out [rows][Hq][d], k and v -> the token's slot of this
-// layer's page tile.  One CTA per row (token).
-__global__ void __launch_bounds__(256) rope_kv_kernel(const __half *qkv, const RowMeta *rows, const int32_t *bt,
-                                                      int bt_stride, uint8_t *kv_layer, int64_t page_stride,
-                                                      int64_t tile_bytes, const float2 *cs, int Hq, int Hkv, int d,
-                                                      __half *q_out) {
-    const int i = blockIdx.x;
-    const RowMeta rm = rows[i];
-    const int p = rm.pos;
-    const int32_t page = bt[static_cast<size_t>(rm.slot) * bt_stride + p / kP];
-    const int half_d = d / 2;
-    const int nqkv = (Hq + 2 * Hkv) * d;
-    const __half *row = qkv + static_cast<size_t>(i) * nqkv;
-    const float2 *csr = cs + static_cast<size_t>(p) * half_d;
-    uint8_t *pg = kv_layer + static_cast<int64_t>(page) * page_stride;
-    // rotated heads: Hq q heads then Hkv k heads, eight pairs (16-byte loads/stores) per item
-    const int rot_items = (Hq + Hkv) * half_d / 8;
-    for (int t = threadIdx.x; t < rot_items; t += blockDim.x) {
-        const int hh = (8 * t) / half_d, j = (8 * t) % half_d;
-        const __half *src = row + hh * d;
-        float a[8], b[8], o_lo[8], o_hi[8];
-        unpack8<__half>(*reinterpret_cast<const uint4 *>(src + j), a);
-        unpack8<__half>(*reinterpret_cast<const uint4 *>(src + j + half_d), b);
-        const float4 *c4 = reinterpret_cast<const float4 *>(csr + j);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float4 c = c4[e];  // (cos, sin) of pairs j + 2e and j + 2e + 1
-            o_lo[2 * e] = a[2 * e] * c.x - b[2 * e] * c.y;
-            o_hi[2 * e] = b[2 * e] * c.x + a[2 * e] * c.y;
-            o_lo[2 * e + 1] = a[2 * e + 1] * c.z - b[2 * e + 1] * c.w;
-            o_hi[2 * e + 1] = b[2 * e + 1] * c.z + a[2 * e + 1] * c.w;
-        }
-        __half *dst;
-        if (hh < Hq) {
-            dst = q_out + (static_cast<size_t>(i) * Hq + hh) * d;
-        } else {
-            dst = reinterpret_cast<__half *>(pg + (hh - Hq) * tile_bytes) + (p % kP) * d;  // K row
-        }
-        *reinterpret_cast<uint4 *>(dst + j) = pack8<__half>(o_lo);
-        *reinterpret_cast<uint4 *>(dst + j + half_d) = pack8<__half>(o_hi);
-    }
-    // v heads: plain copy into the V rows, 16 B per thread
-    const int vv = Hkv * d / 8;
-    for (int t = threadIdx.x; t < vv; t += blockDim.x) {
-        const int g = (t * 8) / d, e = (t * 8) % d;
-        const uint4 val = *reinterpret_cast<const uint4 *>(row + (Hq + Hkv + g) * d + e);
-        __half *dst = reinterpret_cast<__half *>(pg + g * tile_bytes) + (kP + p % kP) * d + e;
-        *reinterpret_cast<uint4 *>(dst) = val;
-    }
-}
-
-// act[i][j] = silu(gu[i][j]) * gu[i][F + j]
-__global__ void silu_mul_kernel(const __half *gu, int n, int F, __half *act) {
-    const int64_t per_row = F / 8;
-    const int64_t total = static_cast<int64_t>(n) * per_row;
-    for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < total;
-         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = c / per_row;
-        const int j = static_cast<int>(c % per_row) * 8;
-        float g[8], u[8], o[8];
-        unpack8<__half>(*reinterpret_cast<const uint4 *>(gu + i * 2 * F + j), g);
-        unpack8<__half>(*reinterpret_cast<const uint4 *>(gu + i * 2 * F + F + j), u);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = g[e] / (1.0f + __expf(-g[e])) * u[e];
-        *reinterpret_cast<uint4 *>(act + i * F + j) = pack8<__half>(o);
-    }
-}
-
 // Greedy sampling: out[i] = the lowest index of the largest logit of row i (NaN rows -> 0).
 __global__ void __launch_bounds__(256) argmax_kernel(const float *logits, int V, int32_t *out) {
     __shared__ float bv[8];
@@ -246,13 +175,6 @@ struct LayerW {
     __half *ln1, *wqkv, *wo, *ln2, *wgu, *wdown;
 };
 
-struct GemmPlan {
-    cublasLtMatmulDesc_t op = nullptr;
-    cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
-    cublasLtMatmulAlgo_t algo{};
-    bool has_algo = false;
-};
-
 }  // namespace
 
 struct dbk_model {
@@ -264,16 +186,8 @@ struct dbk_model {
     std::vector<LayerW> lw;
     float2 *cs = nullptr;
     float *x = nullptr, *logits = nullptr;
-    __half *h = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *gu = nullptr, *act = nullptr;
-    cublasLtHandle_t lt = nullptr;
-    void *lt_ws = nullptr;
-    size_t lt_ws_bytes = 32u << 20;
-    std::map<std::tuple<int, int, int, int>, GemmPlan> plans;
-    // autotuned algorithm per (M bucket of 64 rows, N, K, flags): the fastest of cuBLASLt's
-    // top-8 heuristics, timed once at model creation on the real weights (profiles/
-    // r01_gemm_probe.txt: up to 16 % on zero operands, +1.2 % on the 7B step in situ)
-    std::map<std::tuple<int, int, int, int>, cublasLtMatmulAlgo_t> tuned;
-    float *scratch = nullptr;
+    __half *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
+    GemmRunner gemm;  // tcgen05 GEMM, CTA pairs
     UploadBuffer up_rows;
     std::vector<RowMeta> rows_h;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -282,19 +196,11 @@ struct dbk_model {
     double attn_ms = 0, total_ms = 0;
     int64_t steps = 0;
     ~dbk_model() {
-        for (auto &kv : plans) {
-            if (kv.second.op) cublasLtMatmulDescDestroy(kv.second.op);
-            if (kv.second.a) cublasLtMatrixLayoutDestroy(kv.second.a);
-            if (kv.second.b) cublasLtMatrixLayoutDestroy(kv.second.b);
-            if (kv.second.c) cublasLtMatrixLayoutDestroy(kv.second.c);
-        }
-        if (lt) cublasLtDestroy(lt);
         up_rows.release();
         if (up_rows.done) cudaEventDestroy(up_rows.done);
         for (void *ptr : {static_cast<void *>(cs), static_cast<void *>(x), static_cast<void *>(logits),
-                          static_cast<void *>(scratch),
-                          static_cast<void *>(h), static_cast<void *>(qkv), static_cast<void *>(q),
-                          static_cast<void *>(attn), static_cast<void *>(gu), static_cast<void *>(act), lt_ws})
+                          static_cast<void *>(h), static_cast<void *>(q), static_cast<void *>(attn),
+                          static_cast<void *>(act)})
             if (ptr) cudaFree(ptr);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -305,112 +211,22 @@ struct dbk_model {
 
 namespace {
 
-#define DBK_LT(call)                                                                                 \
-    do {                                                                                             \
-        cublasStatus_t st_ = (call);                                                                 \
-        if (st_ != CUBLAS_STATUS_SUCCESS) return fail(DBK_ECUDA, "%s: cublas status %d", #call, st_); \
-    } while (0)
-
-int gemm_bucket(int M) { return (M + 63) / 64 * 64; }
-
-dbk_status make_layouts(dbk_model *m, GemmPlan &g, int M, int N, int K, bool y_f32) {
-    DBK_LT(cublasLtMatmulDescCreate(&g.op, CUBLAS_COMPUTE_32F, CUDA_R_32F));
-    const cublasOperation_t tA = CUBLAS_OP_T, tB = CUBLAS_OP_N;
-    DBK_LT(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_TRANSA, &tA, sizeof tA));
-    DBK_LT(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_TRANSB, &tB, sizeof tB));
-    DBK_LT(cublasLtMatrixLayoutCreate(&g.a, CUDA_R_16F, K, N, K));
-    DBK_LT(cublasLtMatrixLayoutCreate(&g.b, CUDA_R_16F, K, M, K));
-    DBK_LT(cublasLtMatrixLayoutCreate(&g.c, y_f32 ? CUDA_R_32F : CUDA_R_16F, N, M, N));
-    (void)m;
+// Y = X W^T through the tensor-core GEMM with epilogue `e` (PDL: the GEMM waits on the grid
+// dependency before it reads X or writes its outputs; its weight prefetch overlaps the previous
+// kernel's tail).
+dbk_status gemm(dbk_model *m, int M, int N, int K, const __half *X, const __half *W, const GemmEpiArgs &e,
+                cudaStream_t s) {
+    const cudaError_t err = m->gemm.run(M, N, K, X, K, W, e, s, true);
+    if (err != cudaSuccess) return fail(DBK_ECUDA, "model GEMM (%d x %d x %d): %s", M, N, K, cudaGetErrorString(err));
     return DBK_OK;
 }
 
-void free_layouts(GemmPlan &g) {
-    if (g.op) cublasLtMatmulDescDestroy(g.op);
-    if (g.a) cublasLtMatrixLayoutDestroy(g.a);
-    if (g.b) cublasLtMatrixLayoutDestroy(g.b);
-    if (g.c) cublasLtMatrixLayoutDestroy(g.c);
-    g = GemmPlan{};
-}
-
-dbk_status heuristics(dbk_model *m, GemmPlan &g, int want, cublasLtMatmulHeuristicResult_t *res, int *found) {
-    cublasLtMatmulPreference_t pref;
-    DBK_LT(cublasLtMatmulPreferenceCreate(&pref));
-    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &m->lt_ws_bytes,
-                                         sizeof m->lt_ws_bytes);
-    const cublasStatus_t st = cublasLtMatmulAlgoGetHeuristic(m->lt, g.op, g.a, g.b, g.c, g.c, pref, want, res, found);
-    cublasLtMatmulPreferenceDestroy(pref);
-    if (st != CUBLAS_STATUS_SUCCESS || *found < 1) return fail(DBK_ECUDA, "cuBLASLt: no algorithm");
-    return DBK_OK;
-}
-
-// Time cuBLASLt's top-8 candidates for (M, N, K) on the real operands (output into scratch) and
-// keep the fastest for M's bucket.  Synchronous; called at model creation only.
-dbk_status tune_gemm(dbk_model *m, int M, int N, int K, const __half *X, const __half *W, bool y_f32, bool acc) {
-    GemmPlan g;
-    dbk_status st = make_layouts(m, g, M, N, K, y_f32);
-    cublasLtMatmulHeuristicResult_t res[8];
-    int found = 0;
-    if (st == DBK_OK) st = heuristics(m, g, 8, res, &found);
-    if (st != DBK_OK) {
-        free_layouts(g);
-        return st;
-    }
-    const float alpha = 1.0f, beta = acc ? 1.0f : 0.0f;
-    float best_ms = 1e30f;
-    int best = 0;
-    for (int i = 0; i < found && found > 1; ++i) {
-        bool ok = true;
-        for (int r = 0; r < 2 && ok; ++r)
-            ok = cublasLtMatmul(m->lt, g.op, &alpha, W, g.a, X, g.b, &beta, m->scratch, g.c, m->scratch, g.c,
-                                &res[i].algo, m->lt_ws, m->lt_ws_bytes, 0) == CUBLAS_STATUS_SUCCESS;
-        if (!ok) continue;
-        cudaEventRecord(m->ev0, 0);
-        for (int r = 0; r < 5; ++r)
-            cublasLtMatmul(m->lt, g.op, &alpha, W, g.a, X, g.b, &beta, m->scratch, g.c, m->scratch, g.c,
-                           &res[i].algo, m->lt_ws, m->lt_ws_bytes, 0);
-        cudaEventRecord(m->ev1, 0);
-        cudaEventSynchronize(m->ev1);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, m->ev0, m->ev1);
-        if (ms < best_ms) {
-            best_ms = ms;
-            best = i;
-        }
-    }
-    m->tuned[std::make_tuple(gemm_bucket(M), N, K, (y_f32 ? 1 : 0) | (acc ? 2 : 0))] = res[best].algo;
-    free_layouts(g);
-    return cudaGetLastError() == cudaSuccess ? DBK_OK : fail(DBK_ECUDA, "tune_gemm: CUDA error");
-}
-
-// Y[M][N] (+)= X[M][K] W[N][K]^T, row-major: in cuBLASLt's column-major terms
-// Y^T (N x M, ld N) = op_T(W as K x N, ld K) * (X as K x M, ld K).  The algorithm: the tuned one
-// of M's bucket if cuBLASLt accepts it for this exact M, else the top heuristic.
-dbk_status gemm(dbk_model *m, int M, int N, int K, const __half *X, const __half *W, void *Y, bool y_f32,
-                bool accumulate, cudaStream_t s) {
-    if (M == 0) return DBK_OK;
-    const int flags = (y_f32 ? 1 : 0) | (accumulate ? 2 : 0);
-    GemmPlan &g = m->plans[std::make_tuple(M, N, K, flags)];
-    if (!g.op) {
-        DBK_TRY(make_layouts(m, g, M, N, K, y_f32));
-        auto t = m->tuned.find(std::make_tuple(gemm_bucket(M), N, K, flags));
-        cublasLtMatmulHeuristicResult_t chk{};
-        if (t != m->tuned.end() &&
-            cublasLtMatmulAlgoCheck(m->lt, g.op, g.a, g.b, g.c, g.c, &t->second, &chk) == CUBLAS_STATUS_SUCCESS &&
-            chk.workspaceSize <= m->lt_ws_bytes) {
-            g.algo = t->second;
-        } else {
-            cublasLtMatmulHeuristicResult_t res{};
-            int found = 0;
-            DBK_TRY(heuristics(m, g, 1, &res, &found));
-            g.algo = res.algo;
-        }
-        g.has_algo = true;
-    }
-    const float alpha = 1.0f, beta = accumulate ? 1.0f : 0.0f;
-    DBK_LT(cublasLtMatmul(m->lt, g.op, &alpha, W, g.a, X, g.b, &beta, Y, g.c, Y, g.c, &g.algo, m->lt_ws,
-                          m->lt_ws_bytes, s));
-    return DBK_OK;
+GemmEpiArgs epi_plain(int kind, void *y, int64_t ldy) {
+    GemmEpiArgs e;
+    e.kind = kind;
+    e.y = y;
+    e.ldy = ldy;
+    return e;
 }
 
 dbk_status collect_timing(dbk_model *m) {
@@ -447,8 +263,10 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
     if (pc.kv_dtype != 0) return fail(DBK_EINVAL, "model_create: the model path is fp16 (kv_dtype 0)");
     if (pc.kv_head_offset != 0) return fail(DBK_EINVAL, "model_create: the model is single-GPU / DP (kv_head_offset 0)");
     if (c->hidden % kWChunk || c->ffn % kWChunk || c->hidden > 8 * 4 * 256 || c->vocab < 1 || c->max_pos < 1 ||
-        (pc.q_heads * pc.head_dim) % kWChunk || c->rms_eps <= 0 || c->rope_theta <= 0)
-        return fail(DBK_EINVAL, "model_create: hidden, ffn, q_heads*head_dim multiples of 128, hidden <= 8192");
+        (pc.q_heads * pc.head_dim) % kWChunk || c->rms_eps <= 0 || c->rope_theta <= 0 || 128 % pc.head_dim ||
+        c->vocab % 4 || ((pc.q_heads + 2 * pc.kv_heads) * pc.head_dim) % 256)
+        return fail(DBK_EINVAL, "model_create: hidden, ffn, q_heads*head_dim multiples of 128, (Hq + 2 Hkv) * d a "
+                                "multiple of 256, vocab a multiple of 4, hidden <= 8192");
     const size_t need = dbk_model_weight_bytes(&pc, c);
     if (!wmem || bytes < need || (reinterpret_cast<uintptr_t>(wmem) & 255))
         return fail(DBK_EINVAL, "model_create: weight_mem must be 256-B aligned and >= %zu bytes", need);
@@ -479,9 +297,11 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
         return r;
     };
     const int sms = p->num_sms;
-    auto fill = [&](__half *dst, int64_t rows_, int K, int layer, int kind, int scale_log2, int norm) {
-        fill_weights_kernel<<<grid_of(rows_ * K / 8, 256, sms), 256>>>(dst, rows_, K, layer, kind, c->weight_seed,
-                                                                       std::ldexp(1.0f, scale_log2 - 7), norm);
+    auto fill = [&](__half *dst, int64_t rows_, int K, int layer, int kind, int scale_log2, int norm,
+                    int perm = kPermNone) {
+        fill_weights_kernel<<<grid_of(rows_ * K / 8, 256, sms), 256>>>(
+            dst, rows_, K, layer, kind, c->weight_seed, std::ldexp(1.0f, scale_log2 - 7), norm, perm,
+            perm == kPermGu ? c->ffn : pc.q_heads, pc.kv_heads, pc.head_dim);
     };
     auto sl2 = [](int K) { return -static_cast<int>(std::ceil(std::log2(static_cast<double>(K)) / 2)); };
     const int H = m->H, F = m->F, V = m->V, qd = m->Hq * m->d;
@@ -497,10 +317,10 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
         x.wgu = take(static_cast<size_t>(2) * F * H);
         x.wdown = take(static_cast<size_t>(H) * F);
         fill(x.ln1, 1, H, l, kKindLn1, -3, 1);
-        fill(x.wqkv, m->nqkv, H, l, kKindWqkv, sl2(H), 0);
+        fill(x.wqkv, m->nqkv, H, l, kKindWqkv, sl2(H), 0, kPermQkv);
         fill(x.wo, H, qd, l, kKindWo, sl2(qd), 0);
         fill(x.ln2, 1, H, l, kKindLn2, -3, 1);
-        fill(x.wgu, 2 * F, H, l, kKindWgu, sl2(H), 0);
+        fill(x.wgu, 2 * F, H, l, kKindWgu, sl2(H), 0, kPermGu);
         fill(x.wdown, H, F, l, kKindWdown, sl2(F), 0);
     }
     m->lnf = take(H);
@@ -525,12 +345,10 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
     }
     const size_t R = m->rows;
     if (cudaMalloc(&m->x, R * H * 4) != cudaSuccess || cudaMalloc(&m->logits, R * V * 4) != cudaSuccess ||
-        cudaMalloc(&m->h, R * H * 2) != cudaSuccess || cudaMalloc(&m->qkv, R * m->nqkv * 2) != cudaSuccess ||
-        cudaMalloc(&m->q, R * qd * 2) != cudaSuccess || cudaMalloc(&m->attn, R * qd * 2) != cudaSuccess ||
-        cudaMalloc(&m->gu, R * 2 * F * 2) != cudaSuccess || cudaMalloc(&m->act, R * F * 2) != cudaSuccess ||
-        cudaMalloc(&m->lt_ws, m->lt_ws_bytes) != cudaSuccess)
+        cudaMalloc(&m->h, R * H * 2) != cudaSuccess || cudaMalloc(&m->q, R * qd * 2) != cudaSuccess ||
+        cudaMalloc(&m->attn, R * qd * 2) != cudaSuccess || cudaMalloc(&m->act, R * F * 2) != cudaSuccess)
         return bail(fail(DBK_ECUDA, "model_create: activation workspace"));
-    if (cublasLtCreate(&m->lt) != CUBLAS_STATUS_SUCCESS) return bail(fail(DBK_ECUDA, "model_create: cublasLtCreate"));
+    if (m->gemm.init(pc.device, 2) != cudaSuccess) return bail(fail(DBK_ECUDA, "model_create: tensor-core GEMM init"));
     m->a0.assign(m->L, nullptr);
     m->a1.assign(m->L, nullptr);
     if (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess)
@@ -538,29 +356,6 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
     for (int l = 0; l < m->L; ++l)
         if (cudaEventCreate(&m->a0[l]) != cudaSuccess || cudaEventCreate(&m->a1[l]) != cudaSuccess)
             return bail(fail(DBK_ECUDA, "model_create: events"));
-    // autotune the five GEMM shapes for every 64-row bucket of the batch (DBK_GEMM_TUNE=0 skips)
-    const char *tune_env = std::getenv("DBK_GEMM_TUNE");
-    if (!(tune_env && tune_env[0] == '0')) {
-        const size_t sc = R * static_cast<size_t>(std::max(std::max(m->nqkv, 2 * F), std::max(H, V)));
-        if (cudaMalloc(&m->scratch, sc * 4) != cudaSuccess || cudaMemset(m->scratch, 0, sc * 4) != cudaSuccess ||
-            cudaMemset(m->h, 0, R * H * 2) != cudaSuccess || cudaMemset(m->attn, 0, R * qd * 2) != cudaSuccess ||
-            cudaMemset(m->act, 0, R * F * 2) != cudaSuccess)
-            return bail(fail(DBK_ECUDA, "model_create: tuning scratch"));
-        const LayerW &w0 = m->lw[0];
-        std::vector<int> ms;
-        for (int mb = 64; mb <= m->rows; mb += 64) ms.push_back(mb);
-        if (m->rows % 64) ms.push_back(m->rows);  // the last, partial bucket at its largest M
-        for (int mb : ms) {
-            dbk_status st = tune_gemm(m, mb, m->nqkv, H, m->h, w0.wqkv, false, false);
-            if (st == DBK_OK) st = tune_gemm(m, mb, H, qd, m->attn, w0.wo, true, true);
-            if (st == DBK_OK) st = tune_gemm(m, mb, 2 * F, H, m->h, w0.wgu, false, false);
-            if (st == DBK_OK) st = tune_gemm(m, mb, H, F, m->act, w0.wdown, true, true);
-            if (st == DBK_OK) st = tune_gemm(m, mb, V, H, m->h, m->lm, true, false);
-            if (st != DBK_OK) return bail(st);
-        }
-        cudaFree(m->scratch);
-        m->scratch = nullptr;
-    }
     *out = m;
     return DBK_OK;
 }
@@ -627,13 +422,24 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
     bt.req_ids = ids;
     dbk_prefill_batch pb{};
     if (nch > 0) pb = *chunks;
+    GemmEpiArgs rope;  // QKV epilogue: RoPE + the token's K/V into its page slot, q -> m->q
+    rope.kind = kEpiRopeKV;
+    rope.rows = rows;
+    rope.bt = p->d_bt;
+    rope.bt_stride = p->cfg.max_pages_per_req;
+    rope.page_stride = p->page_stride;
+    rope.tile_bytes = p->tile_bytes;
+    rope.cs = m->cs;
+    rope.q_heads = m->Hq;
+    rope.kv_heads = m->Hkv;
+    rope.head_dim = m->d;
+    rope.q_out = m->q;
+    const GemmEpiArgs resid = epi_plain(kEpiAcc32, m->x, H);       // x += . W^T
+    const GemmEpiArgs silu = epi_plain(kEpiSiluMul, m->act, F);    // act = silu(gate) * up
     for (int l = 0; l < m->L; ++l) {
         const LayerW &w = m->lw[l];
-        DBK_TRY(gemm(m, R, m->nqkv, H, m->h, w.wqkv, m->qkv, false, false, s));
-        rope_kv_kernel<<<R, 256, 0, s>>>(m->qkv, rows, p->d_bt, p->cfg.max_pages_per_req,
-                                         p->kv + static_cast<size_t>(l) * p->layer_stride, p->page_stride,
-                                         p->tile_bytes, m->cs, m->Hq, m->Hkv, m->d, m->q);
-        DBK_CUDA(cudaGetLastError());
+        rope.kv_layer = p->kv + static_cast<size_t>(l) * p->layer_stride;
+        DBK_TRY(gemm(m, R, m->nqkv, H, m->h, w.wqkv, rope, s));
         DBK_CUDA(cudaEventRecord(m->a0[l], s));
         if (n > 0 || (fuse_stats && l == 0)) {
             bt.layer = l;
@@ -646,19 +452,18 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
                                      0, s));
         }
         DBK_CUDA(cudaEventRecord(m->a1[l], s));
-        DBK_TRY(gemm(m, R, H, qd, m->attn, w.wo, m->x, true, true, s));       // x += attn W_o^T
+        DBK_TRY(gemm(m, R, H, qd, m->attn, w.wo, resid, s));
         norm_kernel<<<R, 256, 0, s>>>(m->x, w.ln2, eps, H, m->h, nullptr, nullptr, 0, 0);
-        DBK_TRY(gemm(m, R, 2 * F, H, m->h, w.wgu, m->gu, false, false, s));
-        silu_mul_kernel<<<grid_of(static_cast<int64_t>(R) * F / 8, 256, p->num_sms), 256, 0, s>>>(m->gu, R, F,
-                                                                                                 m->act);
-        DBK_TRY(gemm(m, R, H, F, m->act, w.wdown, m->x, true, true, s));      // x += act W_down^T
+        DBK_TRY(gemm(m, R, 2 * F, H, m->h, w.wgu, silu, s));
+        DBK_TRY(gemm(m, R, H, F, m->act, w.wdown, resid, s));
         const __half *g_next = l + 1 < m->L ? m->lw[l + 1].ln1 : m->lnf;
         norm_kernel<<<R, 256, 0, s>>>(m->x, g_next, eps, H, m->h, nullptr, nullptr, 0, 0);
         DBK_CUDA(cudaGetLastError());
-        p->n_launches += 4;  // ours: RoPE/KV, 2 norms, SiLU (attention counts itself; GEMMs are cuBLASLt's)
+        p->n_launches += 6;  // 4 GEMMs, 2 norms (attention counts itself)
     }
     float *lg = logits ? static_cast<float *>(logits) : m->logits;
-    DBK_TRY(gemm(m, R, m->V, H, m->h, m->lm, lg, true, false, s));
+    DBK_TRY(gemm(m, R, m->V, H, m->h, m->lm, epi_plain(kEpiF32, lg, m->V), s));
+    p->n_launches += 1;
     if (sampled) {
         argmax_kernel<<<R, 256, 0, s>>>(lg, m->V, sampled);
         DBK_CUDA(cudaGetLastError());
@@ -672,7 +477,7 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
 
 dbk_status dbk_model_buffers(dbk_model *m, void **p) {
     if (!m || !p) return fail(DBK_EINVAL, "model_buffers: null argument");
-    void *b[8] = {m->x, m->h, m->qkv, m->q, m->attn, m->gu, m->act, m->logits};
+    void *b[8] = {m->x, m->h, nullptr, m->q, m->attn, nullptr, m->act, m->logits};
     for (int k = 0; k < 8; ++k) p[k] = b[k];
     return DBK_OK;
 }

@@ -161,3 +161,17 @@ def test_greedy_ok_rule():
     assert om.greedy_ok(row, 2, 2e-3)                 # within 2e-3 * max|logit| = 6e-3 of it
     assert not om.greedy_ok(row, 0, 2e-3)
     assert not om.greedy_ok(row, 4, 2e-3) and not om.greedy_ok(row, -1, 2e-3)
+
+
+def test_linear_is_the_brute_force_sum():
+    """O8 linear (y = x W^T) pinned by the triple loop on a tiny case, W stored one output
+    feature per row (so a transposed operand fails)."""
+    rng = np.random.default_rng(5)
+    x = rng.integers(-4, 5, (3, 5)).astype(np.float64)
+    w = rng.integers(-4, 5, (4, 5)).astype(np.float64)
+    want = np.zeros((3, 4))
+    for m in range(3):
+        for n in range(4):
+            for k in range(5):
+                want[m, n] += x[m, k] * w[n, k]
+    assert np.array_equal(om.linear(x, w), want)
