@@ -610,7 +610,7 @@ def run_gpu(args):
             mc = c["model"]
             line["config"]["full_model"] = {"hidden": mc["hidden"], "ffn": mc["ffn"], "vocab": mc["vocab"],
                                             "weights_gb": round(S["model"].weights.numel() / GB, 2),
-                                            "gemms": "cuBLASLt fp16 x fp16 -> fp32 accumulate"}
+                                            "gemms": "dbk tcgen05 GEMM (gemm_tc.cu), fp16 x fp16 -> fp32 accumulate, fused RoPE/KV, SiLU, residual epilogues"}
             line["config"]["workload"] += " + full decode step (weights)"
             line["attention_share_of_step"] = line["roofline"]["share_of_step"]
         if world == 1 and not args.no_cpu_baseline:

@@ -59,6 +59,11 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--out", default=None)
     ap.add_argument("--trace", action="store_true", help="per-CTA phase stamps of one launch")
+    ap.add_argument("--modes", default="f16", help="epilogues to time: f16, silu (gate|up shapes)")
+    ap.add_argument("--split", action="store_true", help="also time the operand pipeline alone (no MMAs) "
+                    "and the MMAs alone (no operand loads)")
+    ap.add_argument("--hot", action="store_true", help="one weight copy (L2-resident when it fits)")
+    ap.add_argument("--bn-sweep", default="", help="also time cta_group 2 at these forced tile widths, e.g. 128,192,256")
     ap.add_argument("--trace-modes", default="f16")
     ap.add_argument("--custom", default="", help="extra shapes 'N:K;N:K' named cNxK")
     a = ap.parse_args()
@@ -74,7 +79,7 @@ def main():
         N, K = SHAPES[name]
         # enough weight copies that a call never finds its weights in the 126 MB L2 (the model
         # step reads every layer's weights once)
-        copies = max(2, -(-400 * 2 ** 20 // (N * K * 2)))
+        copies = 1 if a.hot else max(2, -(-400 * 2 ** 20 // (N * K * 2)))
         ws = [(torch.rand(N, K, device="cuda", dtype=torch.float16) - 0.5) / K ** 0.5 for _ in range(copies)]
         w = ws[0]
         for M in [int(m) for m in a.ms.split(",")]:
@@ -89,6 +94,23 @@ def main():
                     continue
                 row[f"{tag}_ms"] = time_graph(
                     lambda i: g(x, ws[i % copies], y, "f16", stream=torch.cuda.current_stream()), a.reps)
+                if a.split:
+                    for dm, dn in ((1, "loads_only"), (2, "mma_only")):
+                        dbk._lib.dbk_gemm_trace(g.h, None, dm)
+                        row[f"{tag}_{dn}_ms"] = time_graph(
+                            lambda i: g(x, ws[i % copies], y, "f16", stream=torch.cuda.current_stream()), a.reps)
+                        dbk._lib.dbk_gemm_trace(g.h, None, 0)
+                for bn in [int(v) for v in a.bn_sweep.split(",") if v]:
+                    if tag != "cg2":
+                        continue
+                    dbk._lib.dbk_gemm_force_tile(g.h, bn)
+                    row[f"bn{bn}_ms"] = time_graph(
+                        lambda i: g(x, ws[i % copies], y, "f16", stream=torch.cuda.current_stream()), a.reps)
+                    dbk._lib.dbk_gemm_force_tile(g.h, 0)
+                if "silu" in a.modes.split(","):
+                    act = torch.empty(M, N // 2, device="cuda", dtype=torch.float16)
+                    row[f"{tag}_silu_ms"] = time_graph(
+                        lambda i: g(x, ws[i % copies], act, "silu", stream=torch.cuda.current_stream()), a.reps)
                 g(x, w, y, "f16")
                 torch.cuda.synchronize()
                 row[f"{tag}_maxrel"] = float(((y.float() - ref).abs().max() / ref.abs().max()).item())
@@ -97,10 +119,10 @@ def main():
                 for tag0, g in (("cg1", g1), ("cg2", g2)):
                     tag = tag0 if tmode == "f16" else f"{tag0}_{tmode}"
                     tb = torch.zeros(148, 8, dtype=torch.int64, device="cuda")
-                    dbk._lib.dbk_gemm_trace(g.h, tb.data_ptr())
+                    dbk._lib.dbk_gemm_trace(g.h, tb.data_ptr(), 0)
                     g(x, ws[1 % copies], yt, tmode)
                     torch.cuda.synchronize()
-                    dbk._lib.dbk_gemm_trace(g.h, None)
+                    dbk._lib.dbk_gemm_trace(g.h, None, 0)
                     t = tb.cpu().numpy()
                     t = t[t[:, 0] > 0]
                     t0 = t[:, 0].min()

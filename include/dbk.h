@@ -337,7 +337,9 @@ dbk_status dbk_gemm_create(int32_t device, int32_t cta_group, dbk_gemm **out);
  * row-major (weights, K contiguous), y: device [M][ldy] row-major;
  * mode 0: y (fp16) = x w^T; 1: y (fp32) = x w^T; 2: y (fp32) += x w^T
  * (stream-K: K is split over the SMs and each partial product is added into y
- * by the TMA unit, so the order of the fp32 additions varies run to run).
+ * by the TMA unit, so the order of the fp32 additions varies run to run);
+ * 4: SwiGLU, y (fp16) [M][N/2] with y[m][j] = silu(z[m][2j]) * z[m][2j+1],
+ * z = x w^T (w's rows interleaved gate_j, up_j; N % (128 * cta_group) == 0).
  * fp32 accumulation.  Async on `stream`.  EINVAL unless K % 64 == 0, N >= 1,
  * ldx >= K, ldx % 8 == 0, ldy >= N, x, w and the rows of y 16-B aligned;
  * M == 0 is a no-op. */
@@ -346,8 +348,12 @@ dbk_status dbk_gemm_run(dbk_gemm *g, int32_t M, int32_t N, int32_t K, const void
 /* Measurement hook: trace = device uint64 [148][8] (or NULL = off); the following launches
  * stamp %globaltimer per CTA at start, after setup, first operands in shared memory, last
  * MMA issued, last accumulator ready, its first TMEM chunk loaded, epilogue done, exit
- * (slots 0-7). */
-dbk_status dbk_gemm_trace(dbk_gemm *g, void *trace);
+ * (slots 0-7).  mode 0 = normal; 1 = the operand pipeline without MMAs, 2 = the MMAs without
+ * operand loads (both give garbage results: they time one side of the pipeline alone). */
+dbk_status dbk_gemm_trace(dbk_gemm *g, void *trace, int32_t mode);
+/* Measurement hook: bn > 0 fixes the activation tile width (rounded up to 32, <= 256) of the
+ * following launches; 0 restores the cost model's choice. */
+dbk_status dbk_gemm_force_tile(dbk_gemm *g, int32_t bn);
 dbk_status dbk_gemm_destroy(dbk_gemm *g);
 
 /* ------------------------------------------------------------------------ */

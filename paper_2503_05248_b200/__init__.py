@@ -166,7 +166,7 @@ class KVPool:
 class Gemm:
     """dbk_gemm: the model projections' tensor-core GEMM, y (=|+=) x w^T (torch fp16 operands)."""
 
-    MODES = {"f16": 0, "f32": 1, "acc32": 2}
+    MODES = {"f16": 0, "f32": 1, "acc32": 2, "silu": 4}
 
     def __init__(self, device=0, cta_group=2):
         h = C.c_void_p()

@@ -56,11 +56,16 @@ public:
     int cta_group() const { return cg_; }
     // debug: per-CTA %globaltimer phase stamps [CTA][8] of the following launches (nullptr = off)
     void set_trace(uint64_t *t) { trace_ = t; }
+    // measurement only: 1 = skip the MMAs, 2 = skip the operand loads (results are garbage)
+    void set_debug(int mode) { dbg_ = mode; }
+    // measurement: activation tile width (0 = the cost model's choice)
+    void force_bn(int bn) { force_bn_ = bn; }
     int64_t launches() const { return launches_; }
 
 private:
     int device_ = 0, cg_ = 1, sms_ = 0, max_groups_ = 0;
     uint64_t *trace_ = nullptr;
+    int dbg_ = 0, force_bn_ = 0;
     int64_t launches_ = 0;
     void *encode_ = nullptr;  // cuTensorMapEncodeTiled
 };

@@ -15,9 +15,10 @@
 //   warp 1      TMEM owner (2 x BN columns: double-buffered accumulator) and, in the leader CTA,
 //               the tcgen05.mma issuer (4 x K=16 MMAs per stage)
 //   warps 2-5   epilogue, 32 activation rows at a time: tcgen05.ld of the thread's TMEM lane,
-//               the fused elementwise op, the result transposed into a shared-memory chunk
-//               [32 m][n] and written by TMA (bulk tensor store / reduce-add, or per-row bulk
-//               copies into the KV pages), double-buffered so the next chunk overlaps the store.
+//               the fused elementwise op, the result transposed into a shared-memory chunk image
+//               and written by TMA, double-buffered so the next chunk overlaps the store: per
+//               warp ([32 m][32 n], bulk tensor store / reduce-add, no cross-warp barrier) or, for
+//               RoPE, per CTA ([32 m][128], per-row bulk copies into q and the KV pages).
 //               (Per-thread strided st.global of the accumulator columns cost ~1.4 us per 32 rows
 //               whatever the element size: profiles/r02_gemm_trace.log.)
 // Scheduling (persistent): GEMMs that ACCUMULATE into an fp32 output (the residual stream: O and
@@ -36,6 +37,10 @@
 #include "gemm.h"
 #include "tc_common.cuh"
 
+#ifndef OUTBUFS
+#define OUTBUFS 2
+#endif
+
 namespace dbk {
 namespace {
 using namespace dev;
@@ -48,8 +53,9 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxBN = 256;
 constexpr int kChunk = 32;                      // activation rows per epilogue chunk
 constexpr int kStageOut = kChunk * kBM * 4;     // one chunk of fp32 outputs: 16 KiB
+constexpr int kOutBufs = OUTBUFS;               // chunk images in flight (1: +1 operand stage)
 constexpr int kDynSmem = 227 * 1024 - 4096;     // dynamic shared memory per CTA (static ~3.3 KiB)
-constexpr int kRingBudget = kDynSmem - 1024 - 2 * kStageOut;
+constexpr int kRingBudget = kDynSmem - 1024 - kOutBufs * kStageOut;
 
 struct KParams {
     int32_t M, N, K, BN, m_tiles, kb, groups, stages;
@@ -57,6 +63,7 @@ struct KParams {
     int32_t stream_k;   // 1: contiguous iteration ranges (partial tiles reduce-added); 0: whole tiles
     int64_t T;          // units * kb
     uint64_t *trace;    // optional [CTA][8] %globaltimer phase stamps (experiments/gemm_bench.py --trace)
+    int32_t dbg;        // measurement only: 1 = no MMAs (operand stream alone), 2 = no operand loads
     GemmEpiArgs e;
 };
 
@@ -118,8 +125,11 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// wait until at most 1 of this thread's bulk groups still reads shared memory
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+// wait until at most kOutBufs - 1 of this thread's bulk groups still read shared memory
+__device__ __forceinline__ void bulk_wait_read_buf() {
+    if constexpr (kOutBufs == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -130,27 +140,31 @@ __device__ __forceinline__ uint64_t global_ns() {
     return t;
 }
 
-// Elementwise part of the epilogue: this thread's weight row n (tile row r) for the 32 activation
-// rows of a chunk, written into the chunk's shared-memory image `so` ([32][row width]).
+// Elementwise part of the epilogue.  Plain / SiLU / residual kinds: each epilogue warp owns its 32
+// TMEM lanes (weight rows) and writes a private [32 m][32 n] chunk image (SiLU: [32 m][16 act
+// columns]) that its lane 0 stores with one TMA op -- no cross-warp barrier.  RoPE: the four
+// warps write one [32 m][128] image holding each head in logical order (per-row bulk copies).
 template <int EPI>
-__device__ __forceinline__ void epi_to_smem(const KParams &p, const float (&v)[32], int r, int n, int cb,
-                                            const int32_t *m_pos, uint8_t *so, int lane) {
+__device__ __forceinline__ void epi_to_smem(const KParams &p, const float (&v)[32], int r, int n,
+                                            const float2 (&cs)[32], uint8_t *so, int lane) {
     if constexpr (EPI == kEpiF32 || EPI == kEpiAcc32) {
         float *s = reinterpret_cast<float *>(so);
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) s[j * kBM + r] = v[j];
+        for (int j = 0; j < kChunk; ++j) s[j * 32 + lane] = v[j];
     } else if constexpr (EPI == kEpiF16) {
         __half *s = reinterpret_cast<__half *>(so);
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) s[j * kBM + r] = __float2half_rn(v[j]);
+        for (int j = 0; j < kChunk; ++j) s[j * 32 + lane] = __float2half_rn(v[j]);
     } else if constexpr (EPI == kEpiSiluMul) {
-        // rows interleaved (gate_j, up_j): the even lane of each pair owns act column r / 2
+        // rows interleaved (gate_j, up_j): the even lane of each pair owns act column lane / 2
         __half *s = reinterpret_cast<__half *>(so);
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
             const float up = __shfl_xor_sync(kFull, v[j], 1);
             const float gt = v[j];
-            if (!(lane & 1)) s[j * (kBM / 2) + (r >> 1)] = __float2half_rn(gt / (1.0f + __expf(-gt)) * up);
+            // silu(g) = g / (1 + e^-g): fast divide (MUFU.RCP; g -> -inf gives 0), no IEEE slow path
+            const float a = __fdividef(gt, 1.0f + __expf(-gt)) * up;
+            if (!(lane & 1)) s[j * 16 + (lane >> 1)] = __float2half_rn(a);
         }
     } else if constexpr (EPI == kEpiRopeKV) {
         // rotate-half pair i = (x[i], x[i + d/2]) of a q or k head sits in rows (2i, 2i + 1); the
@@ -168,8 +182,7 @@ __device__ __forceinline__ void epi_to_smem(const KParams &p, const float (&v)[3
 #pragma unroll
             for (int j = 0; j < kChunk; ++j) {
                 const float other = __shfl_xor_sync(kFull, v[j], 1);
-                const float2 c = e.cs[static_cast<int64_t>(m_pos[cb + j]) * hd + i];
-                s[j * kBM + col] = __float2half_rn(fmaf(sgn * other, c.y, v[j] * c.x));
+                s[j * kBM + col] = __float2half_rn(fmaf(sgn * other, cs[j].y, v[j] * cs[j].x));
             }
         } else {
 #pragma unroll
@@ -178,8 +191,9 @@ __device__ __forceinline__ void epi_to_smem(const KParams &p, const float (&v)[3
     }
 }
 
-// Issue the global writes of a chunk image (epilogue warp 0 only; each issuing lane commits its
-// own bulk group).
+// Issue the global writes of a chunk image: RoPE -- epilogue warp 0, one bulk copy per (token,
+// head), each lane commits its own bulk group; the others -- lane 0 of the owning warp, one TMA
+// op for its 32 weight rows starting at nrow0.
 template <int EPI>
 __device__ __forceinline__ void epi_issue(const KParams &p, const CUtensorMap *ty, const uint8_t *so, int nrow0,
                                           int m, const int64_t *m_off, int cb, int lane) {
@@ -225,7 +239,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int BNc = p.BN / CG;  // activation rows this CTA loads per stage
     const uint32_t a_bytes = kBM * 128, stage_bytes = a_bytes + BNc * 128;
-    uint8_t *outbuf = smem + p.stages * stage_bytes;  // 2 chunk images
+    uint8_t *outbuf = smem + p.stages * stage_bytes;  // kOutBufs chunk images
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
     const int g = static_cast<int>(blockIdx.x) / CG;
@@ -273,7 +287,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         {
             int64_t it_p = it0;
             Seg s0;
-            if (lane == 0 && next_seg(p, g, it_p, it1, s0)) {
+            if (lane == 0 && p.dbg != 2 && next_seg(p, g, it_p, it1, s0)) {
                 const int wrow = (s0.unit / p.m_tiles) * kBM * CG + static_cast<int>(rank) * kBM;
                 pre = min(p.stages, s0.k1 - s0.k0);
                 for (int s = 0; s < pre; ++s) {
@@ -296,12 +310,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                 if (lane == 0) {
                     uint8_t *sa = smem + stage * stage_bytes;
                     const uint32_t fb = full_lead + stage * 8;
-                    if (done >= pre) {
+                    if (p.dbg == 2) {  // measurement: the ring cycles without operand traffic
                         mbar_wait(&empty[stage], phase ^ 1);
-                        if (rank == 0) mbar_expect_tx(&full[stage], CG * stage_bytes);
-                        tma_load2d<CG>(sa, &tw, kb * kBK, wrow, fb);
+                        if (rank == 0) mbar_arrive(&full[stage]);
+                    } else {
+                        if (done >= pre) {
+                            mbar_wait(&empty[stage], phase ^ 1);
+                            if (rank == 0) mbar_expect_tx(&full[stage], CG * stage_bytes);
+                            tma_load2d<CG>(sa, &tw, kb * kBK, wrow, fb);
+                        }
+                        tma_load2d<CG>(sa + a_bytes, &tx, kb * kBK, xrow, fb);
                     }
-                    tma_load2d<CG>(sa + a_bytes, &tx, kb * kBK, xrow, fb);
                 }
                 __syncwarp();
                 if (++stage == p.stages) {
@@ -332,7 +351,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                     first = false;
                     const uint32_t sa = base + stage * stage_bytes, sb = sa + a_bytes;
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                    for (int kk = 0; kk < (p.dbg == 1 ? 0 : kBK / 16); ++kk) {
                         const uint64_t ad = smem_desc(sa + kk * 32, 16, 1024, 2);
                         const uint64_t bd = smem_desc(sb + kk * 32, 16, 1024, 2);
                         const uint32_t accum = (kb > sg.k0 || kk > 0) ? 1u : 0u;
@@ -394,6 +413,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * p.BN;
             const int cmax = min(p.BN, p.M - m0);  // activation rows of this tile (>= 1)
             for (int c0 = 0; c0 < cmax; c0 += kChunk, ++chunk) {
+                // RoPE: this chunk's (cos, sin) pairs, requested before the TMEM load and the
+                // barriers so their latency overlaps them (16 lanes share one 128-B row per token)
+                float2 cs[kChunk];
+                if constexpr (EPI == kEpiRopeKV) {
+                    const int rr_ = (nrow0 + row) % p.e.head_dim;
+                    const int hd = p.e.head_dim >> 1;
+#pragma unroll
+                    for (int j = 0; j < kChunk; ++j)
+                        cs[j] = __ldg(p.e.cs + static_cast<int64_t>(m_pos[c0 + j]) * hd + (rr_ >> 1));
+                }
                 uint32_t rr[32];
                 tmem_ld32(ta + c0, rr);
                 tmem_ld_wait();
@@ -407,14 +436,25 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tempty_lead + acc * 8);
                 }
-                uint8_t *so = outbuf + (chunk & 1) * kStageOut;
-                // the writes issued from this buffer two chunks ago have finished reading it
-                if (issuer) bulk_wait_read1();
-                epi_bar();
-                epi_to_smem<EPI>(p, v, row, nrow0 + row, c0, m_pos, so, lane);
-                fence_proxy_async();
-                epi_bar();
-                if (issuer) epi_issue<EPI>(p, &ty, so, nrow0, m0 + c0, m_off, c0, lane);
+                if constexpr (EPI == kEpiRopeKV) {
+                    uint8_t *so = outbuf + (chunk % kOutBufs) * kStageOut;
+                    // the writes issued from this buffer two chunks ago have finished reading it
+                    if (issuer) bulk_wait_read_buf();
+                    epi_bar();
+                    epi_to_smem<EPI>(p, v, row, nrow0 + row, cs, so, lane);
+                    fence_proxy_async();
+                    epi_bar();
+                    if (issuer) epi_issue<EPI>(p, &ty, so, nrow0, m0 + c0, m_off, c0, lane);
+                } else {
+                    // this warp's private pair of 4-KiB chunk images
+                    uint8_t *so = outbuf + (q * kOutBufs + (chunk % kOutBufs)) * (kStageOut / 4);
+                    if (lane == 0) bulk_wait_read_buf();
+                    __syncwarp();
+                    epi_to_smem<EPI>(p, v, row, nrow0 + row, cs, so, lane);
+                    fence_proxy_async();
+                    __syncwarp();
+                    epi_issue<EPI>(p, &ty, so, nrow0 + q * 32, m0 + c0, m_off, c0, lane);
+                }
             }
             if (++acc == 2) {
                 acc = 0;
@@ -422,7 +462,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             }
         }
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-        if (issuer) bulk_wait_all();
+        if (issuer || lane == 0) bulk_wait_all();
         if (tr && et == 0) tr[6] = global_ns();
     }
     tc_fence_before();
@@ -547,6 +587,10 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     } else {
         choose_tiles(M, n_tiles, max_groups_, cg_, &p.BN, &p.m_tiles);
     }
+    if (force_bn_ > 0) {  // measurement: a fixed activation tile width
+        p.BN = std::min(kMaxBN, (force_bn_ + 31) / 32 * 32);
+        p.m_tiles = (M + p.BN - 1) / p.BN;
+    }
     p.units = n_tiles * p.m_tiles;
     p.T = static_cast<int64_t>(p.units) * p.kb;
     if (p.stream_k) {
@@ -559,6 +603,7 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     const int stage_bytes = kBM * 128 + (p.BN / cg_) * 128;
     p.stages = std::min(kMaxStages, kRingBudget / stage_bytes);
     p.trace = trace_;
+    p.dbg = dbg_;
     p.e = e;
     CUtensorMap tw, tx, ty;
     if (!encode_2d(encode_, &tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W, K, N, K, kBK, kBM, true) ||
@@ -566,16 +611,15 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
         return cudaErrorInvalidValue;
     bool ok = true;
     switch (e.kind) {
-        case kEpiF16:
-            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N, M, e.ldy, kBM, kChunk, false);
+        case kEpiF16:  // per-warp boxes: 32 weight rows x 32 activation rows
+            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N, M, e.ldy, 32, kChunk, false);
             break;
         case kEpiF32:
         case kEpiAcc32:
-            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, e.y, N, M, e.ldy, kBM, kChunk, false);
+            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, e.y, N, M, e.ldy, 32, kChunk, false);
             break;
         case kEpiSiluMul:
-            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N / 2, M, e.ldy, kBM / 2, kChunk,
-                           false);
+            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N / 2, M, e.ldy, 16, kChunk, false);
             break;
         default:
             ty = tw;  // unused by the RoPE / KV epilogue (per-row bulk copies)
@@ -586,7 +630,7 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.groups * cg_);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + 2 * kStageOut + 1024;
+    cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + kOutBufs * kStageOut + 1024;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     int na = 0;
@@ -635,10 +679,14 @@ dbk_status dbk_gemm_create(int32_t device, int32_t cta_group, dbk_gemm **out) {
 dbk_status dbk_gemm_run(dbk_gemm *g, int32_t M, int32_t N, int32_t K, const void *x, int64_t ldx, const void *w,
                         void *y, int64_t ldy, int32_t mode, void *stream) {
     if (!g || (M > 0 && (!x || !w || !y))) return fail(DBK_EINVAL, "gemm_run: null argument");
-    if (mode < kEpiF16 || mode > kEpiAcc32) return fail(DBK_EINVAL, "gemm_run: mode must be 0 (fp16), 1 (fp32), 2 (fp32 +=)");
-    const int esz = mode == kEpiF16 ? 2 : 4;
-    if (ldy < N || (ldy * esz) % 16 || (reinterpret_cast<uintptr_t>(y) & 15))
-        return fail(DBK_EINVAL, "gemm_run: need ldy >= N and 16-B aligned rows of y");
+    if (mode != kEpiF16 && mode != kEpiF32 && mode != kEpiAcc32 && mode != kEpiSiluMul)
+        return fail(DBK_EINVAL, "gemm_run: mode must be 0 (fp16), 1 (fp32), 2 (fp32 +=) or 4 (silu * up)");
+    const int esz = (mode == kEpiF16 || mode == kEpiSiluMul) ? 2 : 4;
+    const int64_t ncols = mode == kEpiSiluMul ? N / 2 : N;
+    if (ldy < ncols || (ldy * esz) % 16 || (reinterpret_cast<uintptr_t>(y) & 15))
+        return fail(DBK_EINVAL, "gemm_run: need ldy >= N (N/2 for mode 4) and 16-B aligned rows of y");
+    if (mode == kEpiSiluMul && N % (kBM * g->run.cta_group()))
+        return fail(DBK_EINVAL, "gemm_run: mode 4 needs N %% %d == 0", kBM * g->run.cta_group());
     if (M < 0 || K <= 0 || K % kBK || N <= 0 || ldx < K || ldx % 8)
         return fail(DBK_EINVAL, "gemm_run: need K %% 64 == 0, N >= 1, ldx >= K, ldx %% 8 == 0");
     GemmEpiArgs e;
@@ -651,9 +699,17 @@ dbk_status dbk_gemm_run(dbk_gemm *g, int32_t M, int32_t N, int32_t K, const void
     return DBK_OK;
 }
 
-dbk_status dbk_gemm_trace(dbk_gemm *g, void *trace) {
+dbk_status dbk_gemm_trace(dbk_gemm *g, void *trace, int32_t mode) {
     if (!g) return fail(DBK_EINVAL, "gemm_trace: null handle");
+    if (mode < 0 || mode > 2) return fail(DBK_EINVAL, "gemm_trace: mode 0, 1 or 2");
     g->run.set_trace(static_cast<uint64_t *>(trace));
+    g->run.set_debug(mode);
+    return DBK_OK;
+}
+
+dbk_status dbk_gemm_force_tile(dbk_gemm *g, int32_t bn) {
+    if (!g || bn < 0 || bn > 256) return fail(DBK_EINVAL, "gemm_force_tile: bn in 0 (automatic) .. 256");
+    g->run.force_bn(bn);
     return DBK_OK;
 }
 

@@ -73,8 +73,11 @@ __device__ __forceinline__ float block_sum(float v, float *red) {
 // One CTA per row; H % 8 == 0 and H / 8 <= 4 * blockDim.x.
 __global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, float eps, int H, __half *h,
                                                    const RowMeta *rows, const __half *embed, uint64_t tok_seed,
-                                                   int vocab, const int32_t *tokens = nullptr, int n_tok = 0) {
+                                                   int vocab, const int32_t *tokens, int n_tok) {
     __shared__ float red[8];
+    // launched with programmatic dependent launch after the GEMM that produced x
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int i = blockIdx.x;
     float *xr = x + static_cast<size_t>(i) * H;
     const int nv = H / 8;
@@ -453,11 +456,15 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
         }
         DBK_CUDA(cudaEventRecord(m->a1[l], s));
         DBK_TRY(gemm(m, R, H, qd, m->attn, w.wo, resid, s));
-        norm_kernel<<<R, 256, 0, s>>>(m->x, w.ln2, eps, H, m->h, nullptr, nullptr, 0, 0);
+        DBK_CUDA(launch_kernel(norm_kernel, dim3(R), dim3(256), 0, s, true, m->x, w.ln2, eps, H, m->h,
+                               static_cast<const RowMeta *>(nullptr), static_cast<const __half *>(nullptr),
+                               uint64_t{0}, 0, static_cast<const int32_t *>(nullptr), 0));
         DBK_TRY(gemm(m, R, 2 * F, H, m->h, w.wgu, silu, s));
         DBK_TRY(gemm(m, R, H, F, m->act, w.wdown, resid, s));
         const __half *g_next = l + 1 < m->L ? m->lw[l + 1].ln1 : m->lnf;
-        norm_kernel<<<R, 256, 0, s>>>(m->x, g_next, eps, H, m->h, nullptr, nullptr, 0, 0);
+        DBK_CUDA(launch_kernel(norm_kernel, dim3(R), dim3(256), 0, s, true, m->x, g_next, eps, H, m->h,
+                               static_cast<const RowMeta *>(nullptr), static_cast<const __half *>(nullptr),
+                               uint64_t{0}, 0, static_cast<const int32_t *>(nullptr), 0));
         DBK_CUDA(cudaGetLastError());
         p->n_launches += 6;  // 4 GEMMs, 2 norms (attention counts itself)
     }

@@ -146,3 +146,16 @@ def test_gemm_replays_in_a_cuda_graph(gemm):
         torch.cuda.synchronize()
         err = row_err(y.cpu().numpy().astype(np.float64), 3 * rep * want)
         assert err <= TOL["acc32"], f"replay {rep}: {err:.3e}"
+
+
+def test_gemm_swiglu_epilogue(gemm):
+    # mode 4: weight rows interleaved (gate_j, up_j); act[m][j] = silu(z[m][2j]) * z[m][2j+1]
+    M, N, K = 203, 512 * gemm.cta_group, 1024
+    x, w = operands(M, N, K, 51)
+    act = torch.full((M, N // 2), float("nan"), dtype=torch.float16, device="cuda")
+    gemm(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), act, "silu")
+    torch.cuda.synchronize()
+    z = om.linear(x, w)
+    want = om.silu(z[:, 0::2]) * z[:, 1::2]
+    err = row_err(act.float().cpu().numpy().astype(np.float64), want)
+    assert err <= TOL["f16"], f"swiglu: {err:.3e}"
