@@ -255,6 +255,11 @@ typedef struct dbk_model_config {
     double rope_theta;     /* 10000 (Llama-2)                                       */
     uint64_t weight_seed;  /* synthetic weights (synth/hashgen.py gen_matrix)       */
     uint64_t token_seed;   /* synthetic input token of (req, pos) (gen_token)       */
+    int32_t tp_size;       /* tensor parallelism over KV heads and the FFN: 0 or 1 = one GPU;
+                            * G > 1: this model holds rank tp_rank's slice (the pool's kv
+                            * heads, kv_head_offset = tp_rank * kv_heads; hidden, ffn and vocab
+                            * are the GLOBAL sizes) and needs dbk_model_attach_tp           */
+    int32_t tp_rank;
 } dbk_model_config;
 
 typedef struct dbk_model dbk_model;
@@ -305,6 +310,28 @@ dbk_status dbk_model_step(dbk_model *model, int32_t n, const int64_t *req_ids, i
 dbk_status dbk_model_step_pd(dbk_model *model, int32_t n, const int64_t *req_ids, const dbk_prefill_batch *chunks,
                              int32_t fuse_stats, void *logits, const int32_t *tokens, int32_t *sampled,
                              void *stream);
+
+/* Tensor-parallel residual stream ("TP model step").
+ * With tp_size = G, the O and down projections of rank r produce partial sums; their GEMM
+ * epilogue adds each 32-column chunk straight into the residual buffer of the rank that owns
+ * those columns (rank o owns [o H/G, (o+1) H/G)) in THAT rank's memory (TMA reduce-add through
+ * CUDA-IPC mappings: NVLink / NVSwitch peer memory across GPUs), a one-warp barrier publishes the
+ * step (release / acquire at system scope), and the next RMSNorm reads every owner's slice:
+ * the all-reduce's reduce-scatter runs inside the GEMM, its all-gather inside the norm.
+ * dbk_tp_create allocates 3 rotating fp32 buffers [rows][hidden] + flags (one cudaMalloc) and
+ * writes this rank's 64-byte IPC handle; the caller gathers every rank's handle (rank order)
+ * for dbk_tp_open.  hidden % (32 * nranks) == 0, nranks <= 8.  Every rank must run the same
+ * sequence of model steps on the same batch (the barriers pair up by count); a rank that never
+ * arrives makes the others' barrier kernel trap after 20 s (the step then fails with ECUDA). */
+typedef struct dbk_tp dbk_tp;
+dbk_status dbk_tp_create(int32_t nranks, int32_t rank, int32_t device, int64_t rows, int32_t hidden,
+                         void *handle_out_64, dbk_tp **out);
+dbk_status dbk_tp_open(dbk_tp *t, const void *handles /* [nranks][64] */);
+dbk_status dbk_tp_barrier(dbk_tp *t, void *stream);  /* a standalone barrier (async on stream) */
+dbk_status dbk_tp_destroy(dbk_tp *t);
+/* The model's residual stream becomes the communicator's buffers (rows >= max_requests,
+ * same nranks / rank / hidden as the model's config, else EINVAL). */
+dbk_status dbk_model_attach_tp(dbk_model *model, dbk_tp *tp);
 
 /* Introspection (tests): device pointers of the activation workspace of the last
  * step, rows = batch order: [0] x fp32 [n][H] (residual stream), [1] h fp16 [n][H]

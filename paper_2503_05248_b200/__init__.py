@@ -237,12 +237,13 @@ class Model:
     """dbk_model: full decode step with synthetic fp16 weights over a KVPool (NEXT row 3)."""
 
     def __init__(self, pool: KVPool, hidden, ffn, vocab, max_pos=4096, rms_eps=1e-5, rope_theta=10000.0,
-                 weight_seed=0, token_seed=None):
+                 weight_seed=0, token_seed=None, tp_size=1, tp_rank=0):
         import torch
         self.pool = pool
         self.cfg = dbk_model_config(int(hidden), int(ffn), int(vocab), int(max_pos), float(rms_eps),
                                     float(rope_theta), int(weight_seed),
-                                    int(weight_seed if token_seed is None else token_seed))
+                                    int(weight_seed if token_seed is None else token_seed), int(tp_size),
+                                    int(tp_rank))
         nbytes = _lib.dbk_model_weight_bytes(C.byref(pool.cfg), C.byref(self.cfg))
         if nbytes == 0:
             raise DbkError(1, "dbk_model_weight_bytes", "invalid model config")
@@ -271,6 +272,10 @@ class Model:
         b = dbk_prefill_batch(len(cid), 0, pcid, ps0, pln)
         _lib.dbk_model_step_pd(self.h, len(ids), pids, C.byref(b), 1 if fuse_stats else 0, _ptr(logits),
                                _ptr(tokens), _ptr(sampled), _stream(stream))
+
+    def attach_tp(self, tp):
+        _lib.dbk_model_attach_tp(self.h, tp.h)
+        self._tp = tp
 
     def timing(self, reset=False):
         a, t, n = C.c_double(), C.c_double(), C.c_int64()
@@ -438,6 +443,31 @@ class Mailbox:
     def close(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.dbk_mbox_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+class Tp:
+    """dbk_tp: the tensor-parallel residual stream (IPC-mapped buffers of every rank, barrier).
+    The 64-byte IPC handles are gathered over the caller's torch.distributed group (`dist`)."""
+
+    def __init__(self, dist, world, rank, device, rows, hidden):
+        h = C.c_void_p()
+        buf = (C.c_char * 64)()
+        _lib.dbk_tp_create(int(world), int(rank), int(device), int(rows), int(hidden), buf, C.byref(h))
+        self.h = h
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(buf.raw))
+        allb = (C.c_char * (64 * world)).from_buffer_copy(b"".join(handles))
+        _lib.dbk_tp_open(self.h, allb)
+
+    def barrier(self, stream=None):
+        _lib.dbk_tp_barrier(self.h, _stream(stream))
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.dbk_tp_destroy(self.h)
             self.h = None
 
     __del__ = close

@@ -99,7 +99,7 @@ class dbk_engine_buffers(C.Structure):
 class dbk_model_config(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("ffn", C.c_int32), ("vocab", C.c_int32), ("max_pos", C.c_int32),
                 ("rms_eps", C.c_double), ("rope_theta", C.c_double), ("weight_seed", C.c_uint64),
-                ("token_seed", C.c_uint64)]
+                ("token_seed", C.c_uint64), ("tp_size", C.c_int32), ("tp_rank", C.c_int32)]
 
 
 class dbk_step_record(C.Structure):
@@ -137,6 +137,11 @@ SIGNATURES = {
     "dbk_model_step_pd": [P, I32, PI64, C.POINTER(dbk_prefill_batch), I32, P, P, P, P],
     "dbk_model_timing": [P, C.POINTER(C.c_double), C.POINTER(C.c_double), PI64, I32],
     "dbk_engine_attach_model": [P, P],
+    "dbk_tp_create": [I32, I32, I32, I64, I32, P, C.POINTER(P)],
+    "dbk_tp_open": [P, P],
+    "dbk_tp_barrier": [P, P],
+    "dbk_tp_destroy": [P],
+    "dbk_model_attach_tp": [P, P],
     "dbk_gemm_create": [I32, I32, C.POINTER(P)],
     "dbk_gemm_run": [P, I32, I32, I32, P, I64, P, P, I64, I32, P],
     "dbk_gemm_trace": [P, P, I32],

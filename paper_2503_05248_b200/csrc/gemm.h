@@ -42,6 +42,11 @@ struct GemmEpiArgs {
     const float2 *cs = nullptr;    // (cos, sin)[pos][d/2]
     int32_t q_heads = 0, kv_heads = 0, head_dim = 0;
     __half *q_out = nullptr;       // [M][q_heads][head_dim]
+    // kind 2 under tensor parallelism: the output's columns are split over tp_size ranks in slices
+    // of tp_cols; the partial product of slice r is reduce-added into tp_y[r] (rank r's residual
+    // stream, peer memory), so the GEMM performs the all-reduce's reduce-scatter
+    int32_t tp_size = 1, tp_cols = 0;
+    void *const *tp_y = nullptr;   // host array [tp_size] of device pointers, same layout as y
 };
 
 // Persistent tcgen05 GEMM (stream-K for the accumulating epilogue, whole tiles otherwise).

@@ -50,12 +50,19 @@ constexpr int kBM = 128;          // weight rows per CTA = TMEM lanes
 constexpr int kBK = 64;           // K elements per stage: one 128-byte swizzled row
 constexpr int kThreads = 192;     // warp 0 TMA, warp 1 TMEM + MMA, warps 2-5 epilogue
 constexpr int kMaxStages = 8;
+constexpr int kMaxTp = 8;         // tensor-parallel ranks a residual GEMM can route to
 constexpr int kMaxBN = 256;
 constexpr int kChunk = 32;                      // activation rows per epilogue chunk
 constexpr int kStageOut = kChunk * kBM * 4;     // one chunk of fp32 outputs: 16 KiB
 constexpr int kOutBufs = OUTBUFS;               // chunk images in flight (1: +1 operand stage)
 constexpr int kDynSmem = 227 * 1024 - 4096;     // dynamic shared memory per CTA (static ~3.3 KiB)
 constexpr int kRingBudget = kDynSmem - 1024 - kOutBufs * kStageOut;
+
+// Output tensor maps: [0] the output; with tensor-parallel routing (GemmEpiArgs::tp_size > 1)
+// [r] = rank r's residual stream, the owner of columns [r H/G, (r+1) H/G).
+struct OutMaps {
+    CUtensorMap m[kMaxTp];
+};
 
 struct KParams {
     int32_t M, N, K, BN, m_tiles, kb, groups, stages;
@@ -195,7 +202,7 @@ __device__ __forceinline__ void epi_to_smem(const KParams &p, const float (&v)[3
 // head), each lane commits its own bulk group; the others -- lane 0 of the owning warp, one TMA
 // op for its 32 weight rows starting at nrow0.
 template <int EPI>
-__device__ __forceinline__ void epi_issue(const KParams &p, const CUtensorMap *ty, const uint8_t *so, int nrow0,
+__device__ __forceinline__ void epi_issue(const KParams &p, const OutMaps *ty, const uint8_t *so, int nrow0,
                                           int m, const int64_t *m_off, int cb, int lane) {
     if constexpr (EPI == kEpiRopeKV) {
         // lane j: token m + j; one contiguous d-element row per head of the tile
@@ -219,9 +226,16 @@ __device__ __forceinline__ void epi_issue(const KParams &p, const CUtensorMap *t
         }
         bulk_commit();
     } else if (lane == 0) {
-        if constexpr (EPI == kEpiAcc32) tma_reduce_add2d(ty, so, nrow0, m);
-        else if constexpr (EPI == kEpiSiluMul) tma_store2d(ty, so, nrow0 / 2, m);
-        else tma_store2d(ty, so, nrow0, m);
+        if constexpr (EPI == kEpiAcc32) {
+            // tensor parallel: these 32 columns belong to one rank's slice of the residual stream;
+            // the partial goes straight into that rank's memory (reduce-scatter fused into the GEMM)
+            const int owner = p.e.tp_size > 1 ? nrow0 / p.e.tp_cols : 0;
+            tma_reduce_add2d(&ty->m[owner], so, nrow0, m);
+        } else if constexpr (EPI == kEpiSiluMul) {
+            tma_store2d(&ty->m[0], so, nrow0 / 2, m);
+        } else {
+            tma_store2d(&ty->m[0], so, nrow0, m);
+        }
         bulk_commit();
     }
 }
@@ -229,7 +243,7 @@ __device__ __forceinline__ void epi_issue(const KParams &p, const CUtensorMap *t
 template <int CG, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
-               const __grid_constant__ CUtensorMap ty, const KParams p) {
+               const __grid_constant__ OutMaps ty, const KParams p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
@@ -477,7 +491,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     }
 }
 
-using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, KParams);
+using KernFn = void (*)(CUtensorMap, CUtensorMap, OutMaps, KParams);
 
 template <int CG>
 KernFn kernel_for(int epi) {
@@ -605,24 +619,37 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     p.trace = trace_;
     p.dbg = dbg_;
     p.e = e;
-    CUtensorMap tw, tx, ty;
+    CUtensorMap tw, tx;
+    OutMaps ty;
     if (!encode_2d(encode_, &tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W, K, N, K, kBK, kBM, true) ||
         !encode_2d(encode_, &tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, X, K, M, ldx, kBK, p.BN / cg_, true))
         return cudaErrorInvalidValue;
     bool ok = true;
     switch (e.kind) {
         case kEpiF16:  // per-warp boxes: 32 weight rows x 32 activation rows
-            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N, M, e.ldy, 32, kChunk, false);
+            ok = encode_2d(encode_, &ty.m[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N, M, e.ldy, 32, kChunk, false);
             break;
         case kEpiF32:
+            ok = encode_2d(encode_, &ty.m[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, e.y, N, M, e.ldy, 32, kChunk, false);
+            break;
         case kEpiAcc32:
-            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, e.y, N, M, e.ldy, 32, kChunk, false);
+            if (e.tp_size > 1) {
+                // every rank's residual stream (peer memory); each GEMM column goes to its owner
+                if (e.tp_size > kMaxTp || !e.tp_y || e.tp_cols * e.tp_size != N || e.tp_cols % 32) return cudaErrorInvalidValue;
+                for (int r = 0; r < e.tp_size && ok; ++r)
+                    ok = encode_2d(encode_, &ty.m[r], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, e.tp_y[r], N, M, e.ldy, 32,
+                                   kChunk, false);
+            } else {
+                ok = encode_2d(encode_, &ty.m[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, e.y, N, M, e.ldy, 32, kChunk,
+                               false);
+            }
             break;
         case kEpiSiluMul:
-            ok = encode_2d(encode_, &ty, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N / 2, M, e.ldy, 16, kChunk, false);
+            ok = encode_2d(encode_, &ty.m[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, e.y, N / 2, M, e.ldy, 16, kChunk,
+                           false);
             break;
         default:
-            ty = tw;  // unused by the RoPE / KV epilogue (per-row bulk copies)
+            ty.m[0] = tw;  // unused by the RoPE / KV epilogue (per-row bulk copies)
     }
     if (!ok) return cudaErrorInvalidValue;
     KernFn k = cg_ == 2 ? kernel_for<2>(e.kind) : kernel_for<1>(e.kind);

@@ -19,6 +19,7 @@
 #include "gemm.h"
 #include "kernels.cuh"
 #include "pool.h"
+#include "tp.h"
 
 using namespace dbk;
 
@@ -34,22 +35,51 @@ constexpr int kKindToken = 7, kKindEmbed = 8, kKindLn1 = 9, kKindWqkv = 10, kKin
 constexpr int kPermNone = 0, kPermQkv = 1, kPermGu = 2;
 
 // ------------------------------------------------------------------ kernels
+// Which rows / columns of the GLOBAL synthetic matrix a (possibly tensor-parallel, possibly
+// row-permuted) local weight holds.  Rank r of a TP-G model keeps the q / k / v rows of its heads
+// in W_qkv, the columns of its q heads in W_o, the gate / up rows of its FFN slice in W_gu and
+// the columns of that slice in W_down ("TP model step").
+struct FillMap {
+    int perm = kPermNone;                // kPermNone / kPermQkv / kPermGu
+    int hq_l = 0, hkv_l = 0, d = 0;      // local heads
+    int hq_g = 0, hkv_g = 0, hq0 = 0, hk0 = 0;  // global heads, this rank's first q / kv head
+    int64_t f_l = 0, f_g = 0, f0 = 0;    // gate|up: local / global FFN size, first global column
+    int64_t k_off = 0;                   // global column of local column 0 (multiple of 8)
+};
+
+__device__ __forceinline__ int64_t global_row(int64_t prow, const FillMap &fm) {
+    if (fm.perm == kPermQkv) {
+        const int64_t lr = qkv_logical_row(prow, fm.hq_l, fm.hkv_l, fm.d);
+        const int64_t qd = static_cast<int64_t>(fm.hq_l) * fm.d, kd = static_cast<int64_t>(fm.hkv_l) * fm.d;
+        if (lr < qd) return static_cast<int64_t>(fm.hq0) * fm.d + lr;
+        if (lr < qd + kd) return static_cast<int64_t>(fm.hq_g + fm.hk0) * fm.d + (lr - qd);
+        return static_cast<int64_t>(fm.hq_g + fm.hkv_g + fm.hk0) * fm.d + (lr - qd - kd);
+    }
+    if (fm.perm == kPermGu) {
+        const int64_t lr = gu_logical_row(prow, fm.f_l);  // [0, f_l) gate rows, [f_l, 2 f_l) up rows
+        return lr < fm.f_l ? fm.f0 + lr : fm.f_g + fm.f0 + (lr - fm.f_l);
+    }
+    return prow;
+}
+
 // W[row][k] = (byte - 128) * scale (+1 for norm gains), byte of (seed, kind, 0, row, layer, k / 128,
-// k % 128): the host passes scale = 2^(scale_log2 - 7), i.e. value * 2^scale_log2 of synth/hashgen.py.
-// Physical row `prow` holds logical row perm(prow) (kPermQkv / kPermGu: the GEMM epilogues' layouts,
-// gemm.h qkv_logical_row / gu_logical_row; pa, pb = (q_heads, kv_heads) resp. (F, -)).
+// k % 128) at the GLOBAL (row, k) of the local element: the host passes scale = 2^(scale_log2 - 7),
+// i.e. value * 2^scale_log2 of synth/hashgen.py.  Physical row `prow` holds global row
+// global_row(prow) (kPermQkv / kPermGu: the GEMM epilogues' layouts, gemm.h).
 __global__ void fill_weights_kernel(__half *w, int64_t rows, int K, int layer, int kind, uint64_t seed, float scale,
-                                    int norm, int perm, int pa, int pb, int pd) {
+                                    int norm, const FillMap fm) {
     const int64_t per_row = K / 8;
     const int64_t total = rows * per_row;
     for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < total;
          c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t prow = c / per_row;
-        const int64_t row = perm == kPermQkv ? qkv_logical_row(prow, pa, pb, pd)
-                                             : (perm == kPermGu ? gu_logical_row(prow, pa) : prow);
-        const int k = static_cast<int>(c % per_row) * 8;
+        const int64_t row = global_row(prow, fm);
+        const int64_t k = (c % per_row) * 8;
+        const int64_t kg = k + fm.k_off;
         float f[8];
-        synth_vals(synth_key(seed, kind, 0, static_cast<int>(row), layer, k / kWChunk, (k % kWChunk) / 8), scale, f);
+        synth_vals(synth_key(seed, kind, 0, static_cast<int>(row), layer, static_cast<int>(kg / kWChunk),
+                             static_cast<int>((kg % kWChunk) / 8)),
+                   scale, f);
         if (norm)
 #pragma unroll
             for (int e = 0; e < 8; ++e) f[e] += 1.0f;
@@ -127,6 +157,76 @@ __global__ void __launch_bounds__(256) norm_kernel(float *x, const __half *g, fl
     }
 }
 
+// Tensor-parallel RMSNorm ("TP model step"): h[i] = RMSNorm(x_i) * g where the row
+// x_i is GATHERED from the owners of its column slices (xsrc[o] = rank o's buffer; the all-gather
+// half of the all-reduce), or is the embedding E[token(req_i, pos_i)] when xsrc is null.  Then
+// this rank's slice [own0, own0 + own_n) of x_i is ADDED into base (the buffer the next residual
+// GEMM accumulates into, atomically: peers' GEMM partials may already be arriving) and the same
+// slice of zero_dst is cleared for the accumulation after that.  One CTA per row.
+__global__ void __launch_bounds__(256) tp_norm_kernel(const float *const *xsrc, const __half *g, float eps, int H,
+                                                      __half *h, const RowMeta *rows, const __half *embed,
+                                                      uint64_t tok_seed, int vocab, const int32_t *tokens, int n_tok,
+                                                      int own0, int own_n, float *base, float *zero_dst) {
+    __shared__ float red[8];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int i = blockIdx.x;
+    const int nv = H / 8;
+    float v[4][8];
+    float ss = 0.f;
+    const __half *er = nullptr;
+    if (!xsrc) {
+        const RowMeta rm = rows[i];
+        uint64_t tok;
+        if (i < n_tok) {
+            const int32_t t = tokens[i];
+            tok = static_cast<uint64_t>(t < 0 ? 0 : (t >= vocab ? vocab - 1 : t));
+        } else {
+            tok = (synth_key(tok_seed, kKindToken, rm.req_id, rm.pos, 0, 0, 0) >> 16) % static_cast<uint64_t>(vocab);
+        }
+        er = embed + static_cast<size_t>(tok) * H;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int j = threadIdx.x + c * blockDim.x;
+        if (j < nv) {
+            if (er) {
+                unpack8<__half>(*reinterpret_cast<const uint4 *>(er + j * 8), v[c]);
+            } else {
+                const float *src = xsrc[(j * 8) / own_n] + static_cast<size_t>(i) * H + j * 8;  // owner's slice
+                const float4 a = *reinterpret_cast<const float4 *>(src);
+                const float4 b = *reinterpret_cast<const float4 *>(src + 4);
+                v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
+                v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) ss += v[c][e] * v[c][e];
+        }
+    }
+    const float r = rsqrtf(block_sum(ss, red) / static_cast<float>(H) + eps);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int j = threadIdx.x + c * blockDim.x;
+        if (j < nv) {
+            float gg[8], o[8];
+            unpack8<__half>(*reinterpret_cast<const uint4 *>(g + j * 8), gg);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = v[c][e] * r * gg[e];
+            *reinterpret_cast<uint4 *>(h + static_cast<size_t>(i) * H + j * 8) = pack8<__half>(o);
+            if (j * 8 >= own0 && j * 8 < own0 + own_n) {
+                const size_t at = static_cast<size_t>(i) * H + j * 8;
+                if (base)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) atomicAdd(base + at + e, v[c][e]);
+                if (zero_dst) {
+                    *reinterpret_cast<float4 *>(zero_dst + at) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    *reinterpret_cast<float4 *>(zero_dst + at + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        }
+    }
+}
+
 // Greedy sampling: out[i] = the lowest index of the largest logit of row i (NaN rows -> 0).
 __global__ void __launch_bounds__(256) argmax_kernel(const float *logits, int V, int32_t *out) {
     __shared__ float bv[8];
@@ -191,6 +291,10 @@ struct dbk_model {
     float *x = nullptr, *logits = nullptr;
     __half *h = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
     GemmRunner gemm;  // tcgen05 GEMM, CTA pairs
+    // tensor parallelism (cfg.tp_size > 1): this rank's slice and the attached residual stream
+    int G = 1, tp_r = 0, Hq_g = 0, Hkv_g = 0, F_g = 0;
+    dbk_tp *tp = nullptr;
+    int tp_cur = 0;  // rotation index of the TP residual buffers (continues across steps)
     UploadBuffer up_rows;
     std::vector<RowMeta> rows_h;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -253,7 +357,8 @@ extern "C" {
 
 size_t dbk_model_weight_bytes(const dbk_pool_config *pc, const dbk_model_config *c) {
     if (!pc || !c || c->hidden <= 0 || c->ffn <= 0 || c->vocab <= 0) return 0;
-    const size_t H = c->hidden, F = c->ffn, V = c->vocab, d = pc->head_dim;
+    const int G = c->tp_size > 1 ? c->tp_size : 1;
+    const size_t H = c->hidden, F = c->ffn / G, V = c->vocab, d = pc->head_dim;  // local FFN slice
     const size_t nqkv = (static_cast<size_t>(pc->q_heads) + 2 * pc->kv_heads) * d;
     size_t per_layer = align256(H * 2) * 2 + align256(nqkv * H * 2) + align256(H * pc->q_heads * d * 2) +
                        align256(2 * F * H * 2) + align256(H * F * 2);
@@ -264,7 +369,15 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
     if (!p || !c || !out) return fail(DBK_EINVAL, "model_create: null argument");
     const dbk_pool_config &pc = p->cfg;
     if (pc.kv_dtype != 0) return fail(DBK_EINVAL, "model_create: the model path is fp16 (kv_dtype 0)");
-    if (pc.kv_head_offset != 0) return fail(DBK_EINVAL, "model_create: the model is single-GPU / DP (kv_head_offset 0)");
+    const int G = c->tp_size > 1 ? c->tp_size : 1;
+    if (c->tp_size < 0 || c->tp_rank < 0 || c->tp_rank >= G)
+        return fail(DBK_EINVAL, "model_create: need 0 <= tp_rank < tp_size");
+    if (pc.kv_head_offset != c->tp_rank * pc.kv_heads)
+        return fail(DBK_EINVAL, "model_create: the pool must hold this rank's kv heads (kv_head_offset = tp_rank * "
+                                "kv_heads)");
+    if (G > 1 && (c->ffn % (G * kWChunk) || c->hidden % (32 * G)))
+        return fail(DBK_EINVAL, "model_create: tensor parallel needs ffn %% (128 * tp_size) == 0 and hidden %% "
+                                "(32 * tp_size) == 0");
     if (c->hidden % kWChunk || c->ffn % kWChunk || c->hidden > 8 * 4 * 256 || c->vocab < 1 || c->max_pos < 1 ||
         (pc.q_heads * pc.head_dim) % kWChunk || c->rms_eps <= 0 || c->rope_theta <= 0 || 128 % pc.head_dim ||
         c->vocab % 4 || ((pc.q_heads + 2 * pc.kv_heads) * pc.head_dim) % 256)
@@ -284,7 +397,12 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
     m->Hkv = pc.kv_heads;
     m->d = pc.head_dim;
     m->H = c->hidden;
-    m->F = c->ffn;
+    m->G = G;
+    m->tp_r = c->tp_rank;
+    m->F = c->ffn / G;  // local FFN slice
+    m->F_g = c->ffn;
+    m->Hq_g = pc.q_heads * G;
+    m->Hkv_g = pc.kv_heads * G;
     m->V = c->vocab;
     m->nqkv = (m->Hq + 2 * m->Hkv) * m->d;
     m->rows = pc.max_requests;
@@ -301,11 +419,28 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
     };
     const int sms = p->num_sms;
     auto fill = [&](__half *dst, int64_t rows_, int K, int layer, int kind, int scale_log2, int norm,
-                    int perm = kPermNone) {
+                    const FillMap &fm = FillMap{}) {
         fill_weights_kernel<<<grid_of(rows_ * K / 8, 256, sms), 256>>>(
-            dst, rows_, K, layer, kind, c->weight_seed, std::ldexp(1.0f, scale_log2 - 7), norm, perm,
-            perm == kPermGu ? c->ffn : pc.q_heads, pc.kv_heads, pc.head_dim);
+            dst, rows_, K, layer, kind, c->weight_seed, std::ldexp(1.0f, scale_log2 - 7), norm, fm);
     };
+    FillMap fm_qkv;  // this rank's q / k / v heads, RoPE pairs adjacent
+    fm_qkv.perm = kPermQkv;
+    fm_qkv.hq_l = pc.q_heads;
+    fm_qkv.hkv_l = pc.kv_heads;
+    fm_qkv.d = pc.head_dim;
+    fm_qkv.hq_g = m->Hq_g;
+    fm_qkv.hkv_g = m->Hkv_g;
+    fm_qkv.hq0 = c->tp_rank * pc.q_heads;
+    fm_qkv.hk0 = c->tp_rank * pc.kv_heads;
+    FillMap fm_o;  // the columns of this rank's q heads
+    fm_o.k_off = static_cast<int64_t>(c->tp_rank) * pc.q_heads * pc.head_dim;
+    FillMap fm_gu;  // the gate / up rows of this rank's FFN slice, interleaved
+    fm_gu.perm = kPermGu;
+    fm_gu.f_l = m->F;
+    fm_gu.f_g = m->F_g;
+    fm_gu.f0 = static_cast<int64_t>(c->tp_rank) * m->F;
+    FillMap fm_down;  // the columns of that slice
+    fm_down.k_off = fm_gu.f0;
     auto sl2 = [](int K) { return -static_cast<int>(std::ceil(std::log2(static_cast<double>(K)) / 2)); };
     const int H = m->H, F = m->F, V = m->V, qd = m->Hq * m->d;
     m->embed = take(static_cast<size_t>(V) * H);
@@ -320,11 +455,11 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
         x.wgu = take(static_cast<size_t>(2) * F * H);
         x.wdown = take(static_cast<size_t>(H) * F);
         fill(x.ln1, 1, H, l, kKindLn1, -3, 1);
-        fill(x.wqkv, m->nqkv, H, l, kKindWqkv, sl2(H), 0, kPermQkv);
-        fill(x.wo, H, qd, l, kKindWo, sl2(qd), 0);
+        fill(x.wqkv, m->nqkv, H, l, kKindWqkv, sl2(H), 0, fm_qkv);
+        fill(x.wo, H, qd, l, kKindWo, sl2(m->Hq_g * m->d), 0, fm_o);  // scales of the GLOBAL K
         fill(x.ln2, 1, H, l, kKindLn2, -3, 1);
-        fill(x.wgu, 2 * F, H, l, kKindWgu, sl2(H), 0, kPermGu);
-        fill(x.wdown, H, F, l, kKindWdown, sl2(F), 0);
+        fill(x.wgu, 2 * F, H, l, kKindWgu, sl2(H), 0, fm_gu);
+        fill(x.wdown, H, F, l, kKindWdown, sl2(m->F_g), 0, fm_down);
     }
     m->lnf = take(H);
     m->lm = take(static_cast<size_t>(V) * H);
@@ -416,10 +551,57 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
     const RowMeta *rows = static_cast<const RowMeta *>(m->up_rows.dev);
     const int H = m->H, F = m->F, qd = m->Hq * m->d;
     const float eps = static_cast<float>(m->cfg.rms_eps);
+    const bool tp = m->tp != nullptr;
+    if (m->G > 1 && !tp) return fail(DBK_EINVAL, "model_step: tensor-parallel model without dbk_model_attach_tp");
+    const int own_n = H / m->G, own0 = m->tp_r * own_n;
+    // RMSNorm of the residual stream into h.  One GPU: x in place.  Tensor parallel: buffer k of
+    // the rotation is read from its owners, this rank's slice is added into buffer k + 1 (the next
+    // residual GEMM's target) unless `last`, and buffer k + 2 is cleared.
+    auto norm = [&](const __half *gain, bool embed, bool last) -> dbk_status {
+        if (!tp) {
+            if (embed) {
+                norm_kernel<<<R, 256, 0, s>>>(m->x, gain, eps, H, m->h, rows, m->embed, m->cfg.token_seed, m->V, tokens,
+                                              tokens ? n : 0);
+                DBK_CUDA(cudaGetLastError());
+                return DBK_OK;
+            }
+            DBK_CUDA(launch_kernel(norm_kernel, dim3(R), dim3(256), 0, s, true, m->x, gain, eps, H, m->h,
+                                   static_cast<const RowMeta *>(nullptr), static_cast<const __half *>(nullptr),
+                                   uint64_t{0}, 0, static_cast<const int32_t *>(nullptr), 0));
+            return DBK_OK;
+        }
+        const int k = m->tp_cur;
+        const float *const *src = embed ? nullptr : tp_bufs_dev(m->tp, k);
+        float *base = last ? nullptr : static_cast<float *>(tp_bufs(m->tp, k + 1)[m->tp_r]);
+        float *zero = static_cast<float *>(tp_bufs(m->tp, k + 2)[m->tp_r]);
+        DBK_CUDA(launch_kernel(tp_norm_kernel, dim3(R), dim3(256), 0, s, !embed, src, gain, eps, H, m->h,
+                               embed ? rows : static_cast<const RowMeta *>(nullptr), m->embed, m->cfg.token_seed, m->V,
+                               tokens, embed && tokens ? n : 0, own0, own_n, base, zero));
+        m->tp_cur = (k + 1) % kTpBufs;  // the next residual GEMM accumulates into buffer k + 1
+        return DBK_OK;
+    };
+    // x += (.) W^T: one GPU in place; tensor parallel -- every partial goes to the owner of its
+    // columns in the current target buffer, then all ranks meet at a barrier
+    std::vector<void *> tp_y;
+    auto residual = [&](const __half *X, int K, const __half *W) -> dbk_status {
+        GemmEpiArgs e = epi_plain(kEpiAcc32, m->x, H);
+        if (tp) {
+            void *const *bufs = tp_bufs(m->tp, m->tp_cur);
+            tp_y.assign(bufs, bufs + m->G);
+            e.y = tp_y[m->tp_r];
+            e.tp_size = m->G;
+            e.tp_cols = own_n;
+            e.tp_y = tp_y.data();
+        }
+        DBK_TRY(gemm(m, R, H, K, X, W, e, s));
+        if (tp) {
+            DBK_TRY(tp_barrier(m->tp, s));
+            ++p->n_launches;
+        }
+        return DBK_OK;
+    };
     DBK_CUDA(cudaEventRecord(m->ev0, s));
-    norm_kernel<<<R, 256, 0, s>>>(m->x, m->lw[0].ln1, eps, H, m->h, rows, m->embed, m->cfg.token_seed, m->V,
-                                  tokens, tokens ? n : 0);
-    DBK_CUDA(cudaGetLastError());
+    DBK_TRY(norm(m->lw[0].ln1, true, false));
     dbk_batch bt{};
     bt.n = n;
     bt.req_ids = ids;
@@ -437,7 +619,6 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
     rope.kv_heads = m->Hkv;
     rope.head_dim = m->d;
     rope.q_out = m->q;
-    const GemmEpiArgs resid = epi_plain(kEpiAcc32, m->x, H);       // x += . W^T
     const GemmEpiArgs silu = epi_plain(kEpiSiluMul, m->act, F);    // act = silu(gate) * up
     for (int l = 0; l < m->L; ++l) {
         const LayerW &w = m->lw[l];
@@ -455,16 +636,12 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
                                      0, s));
         }
         DBK_CUDA(cudaEventRecord(m->a1[l], s));
-        DBK_TRY(gemm(m, R, H, qd, m->attn, w.wo, resid, s));
-        DBK_CUDA(launch_kernel(norm_kernel, dim3(R), dim3(256), 0, s, true, m->x, w.ln2, eps, H, m->h,
-                               static_cast<const RowMeta *>(nullptr), static_cast<const __half *>(nullptr),
-                               uint64_t{0}, 0, static_cast<const int32_t *>(nullptr), 0));
+        DBK_TRY(residual(m->attn, qd, w.wo));
+        DBK_TRY(norm(w.ln2, false, false));
         DBK_TRY(gemm(m, R, 2 * F, H, m->h, w.wgu, silu, s));
-        DBK_TRY(gemm(m, R, H, F, m->act, w.wdown, resid, s));
-        const __half *g_next = l + 1 < m->L ? m->lw[l + 1].ln1 : m->lnf;
-        DBK_CUDA(launch_kernel(norm_kernel, dim3(R), dim3(256), 0, s, true, m->x, g_next, eps, H, m->h,
-                               static_cast<const RowMeta *>(nullptr), static_cast<const __half *>(nullptr),
-                               uint64_t{0}, 0, static_cast<const int32_t *>(nullptr), 0));
+        DBK_TRY(residual(m->act, F, w.wdown));
+        const bool last = l + 1 == m->L;
+        DBK_TRY(norm(last ? m->lnf : m->lw[l + 1].ln1, false, last));
         DBK_CUDA(cudaGetLastError());
         p->n_launches += 6;  // 4 GEMMs, 2 norms (attention counts itself)
     }
@@ -476,9 +653,25 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
         DBK_CUDA(cudaGetLastError());
         ++p->n_launches;
     }
+    if (tp) {  // every rank has read the step's last residual buffer before the next step reuses it
+        DBK_TRY(tp_barrier(m->tp, s));
+        ++p->n_launches;
+    }
     DBK_CUDA(cudaEventRecord(m->ev1, s));
     m->pending = true;
     p->n_launches += 1;  // the embedding + first norm
+    return DBK_OK;
+}
+
+dbk_status dbk_model_attach_tp(dbk_model *m, dbk_tp *t) {
+    if (!m || !t) return fail(DBK_EINVAL, "model_attach_tp: null argument");
+    if (tp_nranks(t) != m->G || tp_rank(t) != m->tp_r || tp_hidden(t) != m->H || tp_rows(t) < m->rows)
+        return fail(DBK_EINVAL, "model_attach_tp: communicator (%d ranks, rank %d, hidden %d, %lld rows) does not match "
+                                "the model (tp_size %d, tp_rank %d, hidden %d, %d rows)",
+                    tp_nranks(t), tp_rank(t), tp_hidden(t), static_cast<long long>(tp_rows(t)), m->G, m->tp_r, m->H,
+                    m->rows);
+    m->tp = t;
+    m->tp_cur = 0;
     return DBK_OK;
 }
 
