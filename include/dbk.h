@@ -170,7 +170,11 @@ typedef struct dbk_batch {
     int32_t chain;         /* 1: the previous operation on `stream` is this pool's *
                             * dbk_decode_step (same batch, another layer): launch  *
                             * as a programmatic dependent so it fills that launch's *
-                            * tail (ignored with fuse_stats); 0: plain stream order */
+                            * tail (ignored with fuse_stats); 2: the previous      *
+                            * operation is a KERNEL producing q / this step's K/V  *
+                            * (e.g. the model's QKV GEMM): programmatic dependent  *
+                            * launch that waits for it before reading anything;    *
+                            * 0: plain stream order                                */
     const int64_t *req_ids;/* host [n], batch order                               */
 } dbk_batch;
 

@@ -45,6 +45,9 @@ decode_kernel(const DecodeParams p) {
         fence_mbar_init();
     }
     __syncwarp();
+    // launched right behind the producer of q / the step's K/V (the model's QKV GEMM): the CTA
+    // is resident and set up by now; the data is not
+    if (p.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
     const TaskPlan plan = task_plan(p, static_cast<int>(gridDim.x) * WARPS);
     int f0 = task_claim(p, plan, lane), f1 = task_claim(p, plan, lane);
     f0 = __shfl_sync(kFull, f0, 0);

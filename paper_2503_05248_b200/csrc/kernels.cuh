@@ -75,7 +75,9 @@ struct DecodeParams {
     int32_t *task_counter;
     int32_t tma_rank;            // K2: 5 = one 5-D box per tile, 2 = 2-D boxes of 16 x 64
     // 1: programmatic dependent launch after the previous decode launch on the stream (its
-    // scratch -- split-K workspace, arrival and task counters -- is the other parity's)
+    // scratch -- split-K workspace, arrival and task counters -- is the other parity's);
+    // 2: programmatic dependent launch after the kernel that wrote q / the new K/V: every warp
+    // waits on the grid dependency before its first global read
     int32_t pdl;
     int32_t seq;                 // this decode launch's sequence number (>= 1, per pool)
     int32_t *done_seq;           // sequence number of the last decode grid whose scratch is reset

@@ -605,6 +605,7 @@ dbk_status dbk_model_step_pd(dbk_model *m, int32_t n, const int64_t *ids, const 
     dbk_batch bt{};
     bt.n = n;
     bt.req_ids = ids;
+    bt.chain = 2;  // right behind the QKV GEMM that writes q and the new K/V (waits for it)
     dbk_prefill_batch pb{};
     if (nch > 0) pb = *chunks;
     GemmEpiArgs rope;  // QKV epilogue: RoPE + the token's K/V into its page slot, q -> m->q

@@ -811,7 +811,7 @@ static dbk_status ensure_ws(dbk_pool *p, int32_t nl, cudaStream_t s) {
 
 // One persistent launch over layers [layer0, layer0 + nl) of the prepared batch.
 static dbk_status decode_launch(dbk_pool *p, int32_t n, int32_t layer0, int32_t nl, const void *q, int64_t q_ls,
-                                void *out, int64_t o_ls, int32_t out_dtype, bool stats, bool chain, cudaStream_t s) {
+                                void *out, int64_t o_ls, int32_t out_dtype, bool stats, int chain, cudaStream_t s) {
     DBK_TRY(ensure_ws(p, nl, s));
     DecodeParams dp;
     dp.kv_layer = p->kv + static_cast<size_t>(layer0) * p->layer_stride;
@@ -850,7 +850,7 @@ static dbk_status decode_launch(dbk_pool *p, int32_t n, int32_t layer0, int32_t 
     dp.n_tasks = p->meta_items * p->cfg.kv_heads * nl;
     dp.task_counter = p->d_task_counter + 2 * par;
     dp.tma_rank = p->tma_rank;
-    dp.pdl = (chain && !stats && p->pdl_enabled) ? 1 : 0;
+    dp.pdl = !p->pdl_enabled ? 0 : (chain == 2 ? 2 : ((chain == 1 && !stats) ? 1 : 0));
     dp.seq = ++p->decode_seq;
     dp.done_seq = p->d_done_seq;
     dp.trace = p->d_trace;
@@ -869,6 +869,7 @@ static dbk_status decode_args_ok(dbk_pool *p, const dbk_batch *b, const void *q,
     if (!p || !b) return fail(DBK_EINVAL, "decode_step: null argument");
     if (b->n < 0 || (b->n > 0 && (!b->req_ids || !q || !out))) return fail(DBK_EINVAL, "decode_step: bad arrays");
     if (b->layer < 0 || b->layer >= p->cfg.layers) return fail(DBK_EINVAL, "decode_step: layer out of range");
+    if (b->chain < 0 || b->chain > 2) return fail(DBK_EINVAL, "decode_step: chain must be 0, 1 or 2");
     if (out_dtype < 0 || out_dtype > 2) return fail(DBK_EINVAL, "decode_step: out_dtype must be 0, 1 or 2");
     if (b->n > p->cfg.max_requests) return fail(DBK_EINVAL, "decode_step: n > max_requests");
     if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 15)
@@ -887,7 +888,7 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     if (b->fuse_stats) DBK_CUDA(cudaMemsetAsync(p->d_stats, 0, 128, s));
     if (b->n == 0) return DBK_OK;
     DBK_TRY(prepare_batch(p, b->n, b->req_ids, s));
-    DBK_TRY(decode_launch(p, b->n, b->layer, 1, q, 0, out, 0, out_dtype, b->fuse_stats != 0, b->chain != 0, s));
+    DBK_TRY(decode_launch(p, b->n, b->layer, 1, q, 0, out, 0, out_dtype, b->fuse_stats != 0, b->chain, s));
     p->last_decode_bytes = decode_bytes(p, out_dtype);
     return DBK_OK;
 }
@@ -921,7 +922,7 @@ extern "C" dbk_status dbk_decode_step_layers(dbk_pool *p, const dbk_batch *b, in
         void *ol = static_cast<uint8_t *>(out) + l0 * out_layer_stride * eo;
         const bool stats = b->fuse_stats && l0 == 0;
         DBK_TRY(decode_launch(p, b->n, b->layer + l0, nl, ql, q_layer_stride, ol, out_layer_stride, out_dtype, stats,
-                              l0 > 0 || b->chain, s));
+                              l0 > 0 ? 1 : b->chain, s));
         ++launched;
     }
     if (launches_out) *launches_out = launched;
