@@ -30,6 +30,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <new>
 
 #include "common.h"
@@ -574,6 +575,10 @@ cudaError_t GemmRunner::init(int device, int cta_group) {
         if ((e = cudaOccupancyMaxActiveClusters(&clusters, kernel_for<2>(kEpiF16), &cfg)) != cudaSuccess) return e;
         max_groups_ = std::min(clusters, sms_ / 2);
         if (max_groups_ < 1) return cudaErrorNotSupported;
+    }
+    if (const char *v = std::getenv("DBK_GEMM_SMS")) {  // measurement: the GEMM on a subset of the SMs
+        const int n = std::atoi(v) / cg_;
+        if (n >= 1) max_groups_ = std::min(max_groups_, n);
     }
     return cudaSuccess;
 }

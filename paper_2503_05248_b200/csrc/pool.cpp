@@ -222,6 +222,10 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
     p->num_sms = dev_sms;
+    if (const char *e = std::getenv("DBK_DECODE_SMS")) {  // measurement: attention on a subset of the SMs
+        const int v = std::atoi(e);
+        if (v >= 1 && v < dev_sms) p->num_sms = v;
+    }
     const int group = cfg->q_heads / cfg->kv_heads;
     const char *cc = std::getenv("DBK_GQA_CUDA_CORE");  // 1: force K1 for GQA (comparison runs)
     const char *t2 = std::getenv("DBK_GQA_TMA2");  // 1: force the 2-D boxes (comparison runs)

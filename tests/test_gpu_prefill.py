@@ -94,6 +94,21 @@ def test_prefill_long_context_gqa(dbk):
     assert row_err(got, want) <= TOL
 
 
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("Hq,Hkv,d", [(32, 32, 128), (16, 2, 64)])
+def test_prefill_persistent_many_items(dbk, dtype, Hq, Hkv, d):
+    # far more (tile pair, kv head) items than SMs: every persistent CTA runs several items, with
+    # single-tile pairs (tile B without blocks) interleaved with full pairs and ragged key tails,
+    # so the K / V ring phases, the q_ready / o_done phases and the TMEM reuse carry across items
+    rng = np.random.default_rng(11)
+    ctx = rng.integers(1, 700, 40)
+    q_start = np.array([rng.integers(0, c) if i % 3 == 0 else 0 for i, c in enumerate(ctx)])
+    q_len = ctx - q_start
+    got, want, _ = run_prefill_case(dbk, 1, Hq, Hkv, d, dtype, ctx, q_start, q_len, layer=0)
+    assert not np.isnan(got).any()
+    assert row_err(got, want) <= TOL
+
+
 def test_prefill_rejects_bad_chunks(dbk):
     pool = dbk.KVPool(1, 4, 4, 64, 8, 2, 4, "f16")
     pool.request_begin(1, 10, 1)
