@@ -490,8 +490,11 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
     bt.req_ids = e->batch_ids.data();
     // device-resident decode-only step: every layer's q exists before the first attention
     // launch, so the layers go through multi-layer launches unless per-layer ones were asked for
-    const bool chained = !e2e && n_pf_rows == 0 && n > 0 && !e->model;
-    const bool multi = chained && !e->cfg.per_layer_launches;
+    // e2e steps chain their per-layer launches too: each layer's KV append runs on the copy
+    // stream right behind that layer's inputs, so the compute stream holds only the decode
+    // launches (an event wait each) and layer l+1's CTAs fill layer l's tail
+    const bool chained = n_pf_rows == 0 && n > 0 && !e->model;
+    const bool multi = chained && !e2e && !e->cfg.per_layer_launches;
     if (n > 0) DBK_TRY(prepare_batch(p, n, e->batch_ids.data(), s, multi ? pc.layers : 1));
     if (n > 0 && !e2e && !e->model) {  // synthetic q of all layers (stands in for the QKV projection), one launch
         DBK_CUDA(launch_synth_q(e->cfg.synth_seed, p->d_req, n, pc.layers, pc.max_requests, pc.q_heads,
@@ -522,6 +525,9 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
             uint8_t *qd = static_cast<uint8_t *>(bufs->q_dev) + static_cast<size_t>(l) * pc.max_requests * qrow;
             const uint8_t *qh = static_cast<const uint8_t *>(bufs->host_q) + static_cast<size_t>(l) * n * qrow;
             DBK_CUDA(cudaMemcpyAsync(qd, qh, n * qrow, cudaMemcpyHostToDevice, e->h2d));
+            // the layer's new K/V rows into their page slots (K5), on the copy stream: after the
+            // step's job list upload (ev_up) and every earlier launch on `s`, which ev_up covers
+            DBK_TRY(append_launch(p, kd, vd, 0, l, 1, e->h2d, pc.max_requests));
             DBK_CUDA(cudaEventRecord(e->ev_q[l], e->h2d));
         }
         e->step_h2d += 2 * static_cast<int64_t>(n * kvrow) + static_cast<int64_t>(pc.layers) * n * qrow;
@@ -572,12 +578,7 @@ dbk_status dbk_engine_step_launch(dbk_engine *e, const dbk_engine_buffers *bufs,
         bt.layer = l;
         bt.fuse_stats = l == 0 ? 1 : 0;
         bt.chain = (chained && l > 0) ? 1 : 0;
-        if (e2e && n > 0) {
-            DBK_CUDA(cudaStreamWaitEvent(s, e->ev_q[l], 0));
-            DBK_TRY(append_launch(p, bufs->kv_dev,
-                                  static_cast<const uint8_t *>(bufs->kv_dev) + static_cast<size_t>(pc.max_requests) * kvrow,
-                                  0, l, 1, s, pc.max_requests));
-        }
+        if (e2e && n > 0) DBK_CUDA(cudaStreamWaitEvent(s, e->ev_q[l], 0));  // q, K, V landed and appended
         if (per_layer_ev) DBK_CUDA(cudaEventRecord(e->att0[l], s));
         DBK_TRY(dbk_decode_step(p, &bt, qd, od, e->cfg.out_dtype, s));
         if (per_layer_ev) DBK_CUDA(cudaEventRecord(e->att1[l], s));
