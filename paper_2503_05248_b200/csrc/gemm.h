@@ -66,13 +66,24 @@ public:
     // measurement: activation tile width (0 = the cost model's choice)
     void force_bn(int bn) { force_bn_ = bn; }
     int64_t launches() const { return launches_; }
+    // measurement: 0 = never split K for the whole-tile epilogues (DBK_GEMM_SPLIT=0 does the same)
+    void allow_split(bool on) { split_ok_ = on; }
+    ~GemmRunner();
 
 private:
     int device_ = 0, cg_ = 1, sms_ = 0, max_groups_ = 0;
     uint64_t *trace_ = nullptr;
     int dbg_ = 0, force_bn_ = 0;
+    bool split_ok_ = true;
     int64_t launches_ = 0;
     void *encode_ = nullptr;  // cuTensorMapEncodeTiled
+    // split-K of the whole-tile epilogues: fp32 partial sums [M][N] reduce-added here (zero between
+    // launches: the last segment of a tile reads its tile back and clears it) and one arrival
+    // counter per (tile, CTA of the pair)
+    float *ws_ = nullptr;
+    size_t ws_elems_ = 0;
+    int32_t *cnt_ = nullptr;
+    int cnt_cap_ = 0;
 };
 
 // Rows of a weight matrix as stored for the fused epilogues: physical row -> logical row.

@@ -72,6 +72,11 @@ struct KParams {
     int64_t T;          // units * kb
     uint64_t *trace;    // optional [CTA][8] %globaltimer phase stamps (experiments/gemm_bench.py --trace)
     int32_t dbg;        // measurement only: 1 = no MMAs (operand stream alone), 2 = no operand loads
+    int32_t split;      // whole tiles, K split S ways (S > 1): segment = (unit, k-range); partials
+                        // reduce-added into ws, the tile's last segment applies the epilogue
+    int32_t ldw;        // ws row stride (= N)
+    float *ws;
+    int32_t *cnt;       // [units][CG] arrival counters (zero between launches)
     GemmEpiArgs e;
 };
 
@@ -87,6 +92,16 @@ __device__ __forceinline__ bool next_seg(const KParams &p, int g, int64_t &it, i
         s.k0 = static_cast<int32_t>(it % p.kb);
         s.k1 = static_cast<int32_t>(min(static_cast<int64_t>(p.kb), s.k0 + (it1 - it)));
         it += s.k1 - s.k0;
+        return true;
+    }
+    if (p.split > 1) {
+        const int64_t sx = g + it * p.groups;
+        if (sx >= static_cast<int64_t>(p.units) * p.split) return false;
+        const int j = static_cast<int>(sx % p.split);
+        s.unit = static_cast<int32_t>(sx / p.split);
+        s.k0 = j * p.kb / p.split;
+        s.k1 = (j + 1) * p.kb / p.split;
+        ++it;
         return true;
     }
     const int64_t u = g + it * p.groups;
@@ -250,6 +265,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     __shared__ uint32_t tmem_base_sh;
     __shared__ int32_t m_pos[EPI == kEpiRopeKV ? kMaxBN : 1];
     __shared__ int64_t m_off[EPI == kEpiRopeKV ? kMaxBN : 1];
+    __shared__ int split_last;
 
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int BNc = p.BN / CG;  // activation rows this CTA loads per stage
@@ -427,17 +443,41 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             if (tr && et == 0) tr[4] = global_ns();
             const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * p.BN;
             const int cmax = min(p.BN, p.M - m0);  // activation rows of this tile (>= 1)
-            for (int c0 = 0; c0 < cmax; c0 += kChunk, ++chunk) {
-                // RoPE: this chunk's (cos, sin) pairs, requested before the TMEM load and the
-                // barriers so their latency overlaps them (16 lanes share one 128-B row per token)
+            const int ncol = nrow0 + row;           // this thread's output column (weight row)
+            // the kind's epilogue of one chunk: v = the chunk's 32 accumulator values of this row
+            auto emit = [&](int c0, const float (&v)[32]) {
+                // RoPE: this chunk's (cos, sin) pairs
                 float2 cs[kChunk];
                 if constexpr (EPI == kEpiRopeKV) {
-                    const int rr_ = (nrow0 + row) % p.e.head_dim;
+                    const int rr_ = ncol % p.e.head_dim;
                     const int hd = p.e.head_dim >> 1;
 #pragma unroll
                     for (int j = 0; j < kChunk; ++j)
                         cs[j] = __ldg(p.e.cs + static_cast<int64_t>(m_pos[c0 + j]) * hd + (rr_ >> 1));
                 }
+                if constexpr (EPI == kEpiRopeKV) {
+                    uint8_t *so = outbuf + (chunk % kOutBufs) * kStageOut;
+                    // the writes issued from this buffer two chunks ago have finished reading it
+                    if (issuer) bulk_wait_read_buf();
+                    epi_bar();
+                    epi_to_smem<EPI>(p, v, row, ncol, cs, so, lane);
+                    fence_proxy_async();
+                    epi_bar();
+                    if (issuer) epi_issue<EPI>(p, &ty, so, nrow0, m0 + c0, m_off, c0, lane);
+                } else {
+                    // this warp's private pair of 4-KiB chunk images
+                    uint8_t *so = outbuf + (q * kOutBufs + (chunk % kOutBufs)) * (kStageOut / 4);
+                    if (lane == 0) bulk_wait_read_buf();
+                    __syncwarp();
+                    epi_to_smem<EPI>(p, v, row, ncol, cs, so, lane);
+                    fence_proxy_async();
+                    __syncwarp();
+                    epi_issue<EPI>(p, &ty, so, nrow0 + q * 32, m0 + c0, m_off, c0, lane);
+                }
+                ++chunk;
+            };
+            const bool split = EPI != kEpiAcc32 && p.split > 1;
+            for (int c0 = 0; c0 < cmax; c0 += kChunk) {
                 uint32_t rr[32];
                 tmem_ld32(ta + c0, rr);
                 tmem_ld_wait();
@@ -451,24 +491,59 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tempty_lead + acc * 8);
                 }
-                if constexpr (EPI == kEpiRopeKV) {
-                    uint8_t *so = outbuf + (chunk % kOutBufs) * kStageOut;
-                    // the writes issued from this buffer two chunks ago have finished reading it
-                    if (issuer) bulk_wait_read_buf();
-                    epi_bar();
-                    epi_to_smem<EPI>(p, v, row, nrow0 + row, cs, so, lane);
-                    fence_proxy_async();
-                    epi_bar();
-                    if (issuer) epi_issue<EPI>(p, &ty, so, nrow0, m0 + c0, m_off, c0, lane);
-                } else {
-                    // this warp's private pair of 4-KiB chunk images
+                if (split) {
+                    // this K range's partial: a private [32 m][32 n] fp32 image per warp, reduce-added
+                    // into the workspace by the TMA unit
                     uint8_t *so = outbuf + (q * kOutBufs + (chunk % kOutBufs)) * (kStageOut / 4);
                     if (lane == 0) bulk_wait_read_buf();
                     __syncwarp();
-                    epi_to_smem<EPI>(p, v, row, nrow0 + row, cs, so, lane);
+                    float *sf = reinterpret_cast<float *>(so);
+#pragma unroll
+                    for (int j = 0; j < kChunk; ++j) sf[j * 32 + lane] = v[j];
                     fence_proxy_async();
                     __syncwarp();
-                    epi_issue<EPI>(p, &ty, so, nrow0 + q * 32, m0 + c0, m_off, c0, lane);
+                    if (lane == 0) {
+                        tma_reduce_add2d(&ty.m[1], so, nrow0 + q * 32, m0 + c0);
+                        bulk_commit();
+                    }
+                    ++chunk;
+                } else {
+                    emit(c0, v);
+                }
+            }
+            if (split) {
+                // every partial of this segment has landed in the workspace; the tile's last
+                // segment (arrival counter) reads the sum back, clears it and runs the epilogue
+                if (lane == 0) {
+                    bulk_wait_all();
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                __syncwarp();
+                epi_bar();
+                int32_t *cnt = p.cnt + sg.unit * CG + static_cast<int>(rank);
+                if (et == 0) {
+                    __threadfence();
+                    split_last = atomicAdd(cnt, 1) == p.split - 1;
+                }
+                epi_bar();
+                if (split_last) {
+                    __threadfence();
+                    for (int c0 = 0; c0 < cmax; c0 += kChunk) {
+                        float v[32];
+#pragma unroll
+                        for (int j = 0; j < kChunk; ++j) {
+                            const int m = m0 + c0 + j;
+                            float *w = p.ws + static_cast<int64_t>(m) * p.ldw + ncol;
+                            if (m < p.M && ncol < p.N) {
+                                v[j] = __ldcg(w);
+                                __stcg(w, 0.f);
+                            } else {
+                                v[j] = 0.f;
+                            }
+                        }
+                        emit(c0, v);
+                    }
+                    if (et == 0) *cnt = 0;
                 }
             }
             if (++acc == 2) {
@@ -542,6 +617,19 @@ void choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tiles)
 
 }  // namespace
 
+static bool split_env_ok() {
+    static const bool ok = [] {
+        const char *e = std::getenv("DBK_GEMM_SPLIT");  // measurement: 0 = never split K
+        return !(e && e[0] == '0');
+    }();
+    return ok;
+}
+
+GemmRunner::~GemmRunner() {
+    if (ws_) cudaFree(ws_);
+    if (cnt_) cudaFree(cnt_);
+}
+
 cudaError_t GemmRunner::init(int device, int cta_group) {
     if (cta_group != 1 && cta_group != 2) return cudaErrorInvalidValue;
     device_ = device;
@@ -610,6 +698,23 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
         p.BN = std::min(kMaxBN, (force_bn_ + 31) / 32 * 32);
         p.m_tiles = (M + p.BN - 1) / p.BN;
     }
+    p.split = 1;
+    if (!p.stream_k && force_bn_ <= 0 && split_ok_ && split_env_ok()) {
+        // a handful of full-width tiles for ~74 CTA groups (a 70B-TP8 QKV slice, N = 1280, at
+        // a small batch): split K instead -- each K range's partial reduce-added into an fp32
+        // workspace, the tile's last segment applies the epilogue.  Only for <= groups/8 tiles
+        // and M <= 256: with more or wider tiles the S-way reduce-adds into the same lines (and
+        // the last segment's read-back) cost more than the idle groups
+        // (profiles/r02_gemm_split.json: TP8 QKV M = 64 31.7 -> 16.4 us; 7B O M = 512 21 -> 84 us)
+        const int mt0 = (M + kMaxBN - 1) / kMaxBN;
+        const int units0 = n_tiles * mt0;
+        const int S = std::min(max_groups_ / std::max(units0, 1), p.kb / 8);
+        if (units0 * 8 <= max_groups_ && M <= 256 && S >= 2) {
+            p.m_tiles = mt0;
+            p.BN = ((M + mt0 - 1) / mt0 + 31) / 32 * 32;
+            p.split = S;
+        }
+    }
     p.units = n_tiles * p.m_tiles;
     p.T = static_cast<int64_t>(p.units) * p.kb;
     if (p.stream_k) {
@@ -617,7 +722,29 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
         // the operand traffic of its k-blocks
         p.groups = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_groups_, p.T / 4)));
     } else {
-        p.groups = std::min(max_groups_, p.units);
+        p.groups = std::min<int64_t>(max_groups_, static_cast<int64_t>(p.units) * p.split);
+    }
+    p.ldw = N;
+    p.ws = nullptr;
+    p.cnt = nullptr;
+    if (p.split > 1) {
+        const size_t need = static_cast<size_t>(M) * N;
+        const int ncnt = p.units * cg_;
+        if (need > ws_elems_ || ncnt > cnt_cap_) {  // first use of a shape: grows once (synchronous)
+            if (ws_) cudaFree(ws_);
+            if (cnt_) cudaFree(cnt_);
+            ws_ = nullptr;
+            cnt_ = nullptr;
+            ws_elems_ = std::max(need, ws_elems_);
+            cnt_cap_ = std::max(ncnt, cnt_cap_);
+            cudaError_t err;
+            if ((err = cudaMalloc(&ws_, ws_elems_ * sizeof(float))) != cudaSuccess) return err;
+            if ((err = cudaMalloc(&cnt_, static_cast<size_t>(cnt_cap_) * sizeof(int32_t))) != cudaSuccess) return err;
+            if ((err = cudaMemset(ws_, 0, ws_elems_ * sizeof(float))) != cudaSuccess) return err;
+            if ((err = cudaMemset(cnt_, 0, static_cast<size_t>(cnt_cap_) * sizeof(int32_t))) != cudaSuccess) return err;
+        }
+        p.ws = ws_;
+        p.cnt = cnt_;
     }
     const int stage_bytes = kBM * 128 + (p.BN / cg_) * 128;
     p.stages = std::min(kMaxStages, kRingBudget / stage_bytes);
@@ -656,6 +783,8 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
         default:
             ty.m[0] = tw;  // unused by the RoPE / KV epilogue (per-row bulk copies)
     }
+    if (ok && p.split > 1)  // the split-K workspace [M][N] fp32, per-warp 32 x 32 reduce-add boxes
+        ok = encode_2d(encode_, &ty.m[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.ws, N, M, N, 32, kChunk, false);
     if (!ok) return cudaErrorInvalidValue;
     KernFn k = cg_ == 2 ? kernel_for<2>(e.kind) : kernel_for<1>(e.kind);
     if (!k) return cudaErrorInvalidValue;

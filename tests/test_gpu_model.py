@@ -370,3 +370,31 @@ def test_model_edge_cases(dbk):
     with pytest.raises(dbk.DbkError):                  # hidden must be a multiple of 128
         dbk.Model(fpool, 200, 256, 100)
     fpool.close()
+
+
+def test_model_step_split_k_epilogues(dbk):
+    """A model whose projections have few weight tiles (QKV 1536 rows, gate|up 2048, LM head 1000
+    at K = 1024): the GEMM splits K for the RoPE / KV-write, SwiGLU and fp32 epilogues (partials
+    through the runner's fp32 workspace, the tile's last segment applies the epilogue); two steps,
+    the second attending to the K/V the first wrote through the split RoPE epilogue."""
+    s = om.ModelShape(layers=2, q_heads=8, kv_heads=2, head_dim=128, hidden=1024, ffn=1024, vocab=1000)
+    kv_seed, wseed = 9, 10
+    ctx = [3, 40, 129, 300, 17]
+    pool, model, ids, ref = _setup(dbk, s, ctx, kv_seed, wseed)
+    pool.reserve_tokens(ids, [1] * len(ids))
+    logits = torch.empty(len(ids), s.vocab, dtype=torch.float32, device="cuda")
+    model.step(ids, logits)
+    want, nk, nv, _ = om.decode_step(s, wseed, kv_seed, ids, ctx)
+    assert row_err(logits.cpu().numpy(), want, "logits_split") <= MODEL_TOL
+    for lay in range(s.layers):
+        for i, (r, c) in enumerate(zip(ids, ctx)):
+            k, v = _read_kv(pool, s, r, c - 1, lay)
+            assert row_err(k, nk[lay, i], "k_split") <= MODEL_TOL and row_err(v, nv[lay, i], "v_split") <= MODEL_TOL
+    written = {(r, c - 1, lay): (nk[lay, i], nv[lay, i]) for i, (r, c) in enumerate(zip(ids, ctx))
+               for lay in range(s.layers)}
+    pool.reserve_tokens(ids, [1] * len(ids))
+    model.step(ids, logits)
+    want2, _, _, _ = om.decode_step(s, wseed, kv_seed, ids, [c + 1 for c in ctx], kv_written=written)
+    assert row_err(logits.cpu().numpy(), want2, "logits_split_step2") <= MODEL_TOL
+    model.close()
+    pool.close()
