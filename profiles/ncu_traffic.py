@@ -33,9 +33,11 @@ def kernels(path):
 
 def main():
     out = sys.argv[1]
+    build = os.environ.get("DBK_BUILD")  # set by the caller: the GPU box's copy has no .git
     try:
-        build = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
-                               cwd=os.path.dirname(os.path.abspath(__file__))).stdout.strip() or None
+        if not build:
+            build = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
+                                   cwd=os.path.dirname(os.path.abspath(__file__))).stdout.strip() or None
     except OSError:
         build = None
     entries = []
