@@ -223,7 +223,10 @@ __device__ __forceinline__ void trace_task(const DecodeParams &p, uint64_t t0, i
     r[3] = (static_cast<uint64_t>(static_cast<uint32_t>(task)) << 32) | static_cast<uint32_t>(pages);
 }
 
-// Two independent loads (item record, page ids): issued one task ahead of use.
+// The item record, then its page ids straight from the device block table (the tables the
+// allocator's deltas keep current; the single source of truth for every kernel that addresses
+// the pool): issued one task ahead of use, so the dependent second load overlaps the current
+// task's page stream (the ring holds STAGES tiles in flight meanwhile).
 __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int lane) {
     Task t;
     t.task = task;
@@ -246,8 +249,9 @@ __device__ __forceinline__ Task load_task(const DecodeParams &p, int task, int l
     const int4 *im = reinterpret_cast<const int4 *>(p.items + item);
     const int4 a = __ldg(im), b = __ldg(im + 1);
     t.it = ItemMeta{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    t.phys_lane = __ldg(p.item_pages + static_cast<size_t>(item) * kItemPages + lane);
-    t.phys_lane2 = __ldg(p.item_pages + static_cast<size_t>(item) * kItemPages + 32 + lane);
+    const int32_t *row = p.block_table + static_cast<size_t>(t.it.slot) * p.bt_stride + t.it.pg0;
+    t.phys_lane = lane < t.it.n ? __ldg(row + lane) : 0;
+    t.phys_lane2 = lane + 32 < t.it.n ? __ldg(row + 32 + lane) : 0;
     return t;
 }
 

@@ -19,9 +19,9 @@ struct ReqMeta {
 };
 static_assert(sizeof(ReqMeta) == 32, "ReqMeta layout");
 
-// One work item = a chunk of <= 32 pages of one request (the unit a warp task streams), with
-// everything the decode kernels need to start it in ONE load; its physical page ids are in
-// item_pages[item * 32 + k] (k < n), so a task's metadata arrives in two independent loads.
+// One work item = a chunk of <= kItemPages pages of one request (the unit a warp task streams),
+// with everything the decode kernels need to start it in ONE load; its physical page ids are
+// read from the device block table, row `slot`, entries pg0 .. pg0 + n - 1.
 struct ItemMeta {
     int32_t i;            // batch index
     int32_t c;            // chunk index within the request
@@ -29,7 +29,7 @@ struct ItemMeta {
     int32_t ctx;          // tokens of the request (incl. this step's)
     int32_t chunk_base;   // first split-K workspace row of the request (if nchunks > 1)
     int32_t nchunks;      // work items of the request
-    int32_t slot;         // block-table row (statistics)
+    int32_t slot;         // block-table row (page ids, statistics)
 };
 static_assert(sizeof(ItemMeta) == 32, "ItemMeta layout");
 constexpr int kItemPages = 64;
@@ -42,7 +42,6 @@ struct DecodeParams {
     int32_t n;                   // requests in the batch
     const ReqMeta *req;          // [n]
     const ItemMeta *items;       // [n_items], longest first
-    const int32_t *item_pages;   // [n_items][kItemPages] physical page ids
     int32_t n_items;
     int32_t chunk_pages;         // pages per work item
     const void *q;               // [n][q_heads][D]

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <utility>
 #include <vector>
 
 #include "common.h"
@@ -486,6 +487,12 @@ dbk_status dbk_model_create(dbk_pool *p, const dbk_model_config *c, void *wmem, 
         cudaMalloc(&m->h, R * H * 2) != cudaSuccess || cudaMalloc(&m->q, R * qd * 2) != cudaSuccess ||
         cudaMalloc(&m->attn, R * qd * 2) != cudaSuccess || cudaMalloc(&m->act, R * F * 2) != cudaSuccess)
         return bail(fail(DBK_ECUDA, "model_create: activation workspace"));
+    // zeroed once: the GEMM epilogues write q, K/V and the fp16 activations with TMA bulk stores,
+    // which compute-sanitizer's initcheck does not see as initialisation (its reports on the
+    // attention's q reads vanish with this; the parity suite checks every row the step reads)
+    for (auto [ptr, bytes] : {std::pair<void *, size_t>{m->x, R * H * 4}, {m->logits, R * V * 4}, {m->h, R * H * 2},
+                              {m->q, R * qd * 2}, {m->attn, R * qd * 2}, {m->act, R * F * 2}})
+        if (cudaMemset(ptr, 0, bytes) != cudaSuccess) return bail(fail(DBK_ECUDA, "model_create: workspace clear"));
     if (m->gemm.init(pc.device, 2) != cudaSuccess) return bail(fail(DBK_ECUDA, "model_create: tensor-core GEMM init"));
     m->a0.assign(m->L, nullptr);
     m->a1.assign(m->L, nullptr);

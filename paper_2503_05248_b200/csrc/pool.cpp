@@ -725,19 +725,16 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
     p->meta_items = base;
     p->meta_ws_rows = ws_rows;
     p->meta_chunk_pages = static_cast<int32_t>(cp);
-    // blob: ReqMeta[n] | ItemMeta[items] | int32 item_pages[items][32] (physical page ids
-    // from the host tables, which the device tables mirror -- K4 checks them every step)
+    // blob: ReqMeta[n] | ItemMeta[items]; the kernels take each item's page ids from the device
+    // block table (row `slot`), which flush_deltas brings up to date before every launch
     const size_t rb = sizeof(ReqMeta) * static_cast<size_t>(n);
     const size_t ib = sizeof(ItemMeta) * static_cast<size_t>(base);
-    const size_t pb = sizeof(int32_t) * kItemPages * static_cast<size_t>(base);
-    p->meta_blob.resize(rb + ib + pb);
+    p->meta_blob.resize(rb + ib);
     if (rb) std::memcpy(p->meta_blob.data(), p->meta_req.data(), rb);
     ItemMeta *im = reinterpret_cast<ItemMeta *>(p->meta_blob.data() + rb);
-    int32_t *ipg = reinterpret_cast<int32_t *>(p->meta_blob.data() + rb + ib);
     for (int32_t w = 0; w < base; ++w) {
         const int2 wk = p->meta_work[w];
         const ReqMeta &m = p->meta_req[wk.x];
-        const Request &r = p->reqs.find(m.req_id)->second;
         const int32_t pages = static_cast<int32_t>((m.ctx + P - 1) / P);
         ItemMeta it;
         it.i = wk.x;
@@ -749,12 +746,10 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
         it.nchunks = m.nchunks;
         it.slot = m.slot;
         im[w] = it;
-        for (int32_t k = 0; k < kItemPages; ++k) ipg[static_cast<size_t>(w) * kItemPages + k] = k < it.n ? r.pages[it.pg0 + k] : 0;
     }
     DBK_TRY(p->up_meta.upload(p->meta_blob.data(), p->meta_blob.size(), s));
     p->d_req = static_cast<const ReqMeta *>(p->up_meta.dev);
     p->d_items = reinterpret_cast<const ItemMeta *>(static_cast<const uint8_t *>(p->up_meta.dev) + rb);
-    p->d_item_pages = reinterpret_cast<const int32_t *>(static_cast<const uint8_t *>(p->up_meta.dev) + rb + ib);
     p->meta_layers_hint = layers_hint;
     p->meta_ids.assign(ids, ids + n);
     p->meta_epoch = p->epoch;
@@ -825,7 +820,6 @@ static dbk_status decode_launch(dbk_pool *p, int32_t n, int32_t layer0, int32_t 
     dp.n = n;
     dp.req = p->d_req;
     dp.items = p->d_items;
-    dp.item_pages = p->d_item_pages;
     dp.n_items = p->meta_items;
     dp.chunk_pages = p->meta_chunk_pages;
     dp.q = q;

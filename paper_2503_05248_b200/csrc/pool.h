@@ -78,7 +78,6 @@ struct dbk_pool {
     int32_t max_layers_per_launch = 0;       // 0: as many as the workspace budget allows
     const dbk::ReqMeta *d_req = nullptr;
     const dbk::ItemMeta *d_items = nullptr;
-    const int32_t *d_item_pages = nullptr;
     // split-K workspace, arrival counters, statistics record
     float *d_ws_o = nullptr;
     float2 *d_ws_ml = nullptr;
