@@ -68,6 +68,9 @@ public:
     int64_t launches() const { return launches_; }
     // measurement: 0 = never split K for the whole-tile epilogues (DBK_GEMM_SPLIT=0 does the same)
     void allow_split(bool on) { split_ok_ = on; }
+    GemmRunner() = default;
+    GemmRunner(const GemmRunner &) = delete;  // owns the split-K workspace
+    GemmRunner &operator=(const GemmRunner &) = delete;
     ~GemmRunner();
 
 private:
