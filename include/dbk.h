@@ -359,9 +359,12 @@ dbk_status dbk_model_timing(dbk_model *model, double *attn_ms, double *total_ms,
  * on the 5th-generation tensor cores (tcgen05.mma, TMEM accumulators, TMA),
  * persistent (gemm_tc.cu).  dbk_model_* runs the same kernel with the decode
  * step's elementwise work fused into its epilogue; this entry point exposes the
- * plain forms for tests and measurement.  A handle holds no device memory.
- * cta_group: 1 = one SM per 128 weight rows, 2 = CTA pairs (cta_group::2, 256
- * weight rows per pair). */
+ * plain forms for tests and measurement.  cta_group: 1 = one SM per 128 weight
+ * rows, 2 = CTA pairs (cta_group::2, 256 weight rows per pair).  A launch with
+ * very few whole weight tiles (<= SMs / (8 * cta_group) at M <= 256) splits K:
+ * fp32 partials go into a workspace the handle allocates at its first such
+ * launch (M x N x 4 bytes, synchronous cudaMalloc: not inside a stream capture)
+ * and keeps until destroy, so one handle's launches must be stream-ordered. */
 typedef struct dbk_gemm dbk_gemm;
 dbk_status dbk_gemm_create(int32_t device, int32_t cta_group, dbk_gemm **out);
 /* x: device fp16 [M][ldx] row-major (activations), w: device fp16 [N][K]
