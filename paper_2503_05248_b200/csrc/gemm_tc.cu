@@ -82,6 +82,7 @@ struct KParams {
 
 struct Seg {
     int32_t unit, k0, k1;
+    int32_t j;  // split-K: this segment's K range index (0 otherwise)
 };
 // The next segment (one unit's k-block range) of group g.  Stream-K: the group's iteration range
 // [it, it1); whole tiles: units g, g + G, g + 2G, ... (it counts the group's units).
@@ -89,6 +90,7 @@ __device__ __forceinline__ bool next_seg(const KParams &p, int g, int64_t &it, i
     if (p.stream_k) {
         if (it >= it1) return false;
         s.unit = static_cast<int32_t>(it / p.kb);
+        s.j = 0;
         s.k0 = static_cast<int32_t>(it % p.kb);
         s.k1 = static_cast<int32_t>(min(static_cast<int64_t>(p.kb), s.k0 + (it1 - it)));
         it += s.k1 - s.k0;
@@ -99,6 +101,7 @@ __device__ __forceinline__ bool next_seg(const KParams &p, int g, int64_t &it, i
         if (sx >= static_cast<int64_t>(p.units) * p.split) return false;
         const int j = static_cast<int>(sx % p.split);
         s.unit = static_cast<int32_t>(sx / p.split);
+        s.j = j;
         s.k0 = j * p.kb / p.split;
         s.k1 = (j + 1) * p.kb / p.split;
         ++it;
@@ -107,6 +110,7 @@ __device__ __forceinline__ bool next_seg(const KParams &p, int g, int64_t &it, i
     const int64_t u = g + it * p.groups;
     if (u >= p.units) return false;
     s.unit = static_cast<int32_t>(u);
+    s.j = 0;
     s.k0 = 0;
     s.k1 = p.kb;
     ++it;
@@ -265,7 +269,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     __shared__ uint32_t tmem_base_sh;
     __shared__ int32_t m_pos[EPI == kEpiRopeKV ? kMaxBN : 1];
     __shared__ int64_t m_off[EPI == kEpiRopeKV ? kMaxBN : 1];
-    __shared__ int split_last;
 
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int BNc = p.BN / CG;  // activation rows this CTA loads per stage
@@ -493,7 +496,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                 }
                 if (split) {
                     // this K range's partial: a private [32 m][32 n] fp32 image per warp, reduce-added
-                    // into the workspace by the TMA unit
+                    // into the workspace by the TMA unit (the sums happen in L2)
                     uint8_t *so = outbuf + (q * kOutBufs + (chunk % kOutBufs)) * (kStageOut / 4);
                     if (lane == 0) bulk_wait_read_buf();
                     __syncwarp();
@@ -512,38 +515,46 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                 }
             }
             if (split) {
-                // every partial of this segment has landed in the workspace; the tile's last
-                // segment (arrival counter) reads the sum back, clears it and runs the epilogue
+                // every partial of this segment has been added into the workspace; once all S
+                // segments of the tile have (arrival counter; they are co-resident: units x S <=
+                // the resident CTA groups), segment j reads back the tile's chunks j, j + S, ...,
+                // clears them and runs the epilogue on them; the last to leave resets the counters
                 if (lane == 0) {
                     bulk_wait_all();
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 __syncwarp();
                 epi_bar();
-                int32_t *cnt = p.cnt + sg.unit * CG + static_cast<int>(rank);
+                int32_t *cnt = p.cnt + 2 * (sg.unit * CG + static_cast<int>(rank));
                 if (et == 0) {
                     __threadfence();
-                    split_last = atomicAdd(cnt, 1) == p.split - 1;
+                    atomicAdd(cnt, 1);
+                    int a;
+                    while (true) {
+                        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(a) : "l"(cnt) : "memory");
+                        if (a >= p.split) break;
+                        __nanosleep(64);
+                    }
                 }
                 epi_bar();
-                if (split_last) {
-                    __threadfence();
-                    for (int c0 = 0; c0 < cmax; c0 += kChunk) {
-                        float v[32];
+                __threadfence();
+                for (int c0 = sg.j * kChunk; c0 < cmax; c0 += p.split * kChunk) {
+                    float v[32];
+                    float *w = p.ws + static_cast<int64_t>(m0 + c0) * p.ldw + ncol;
 #pragma unroll
-                        for (int j = 0; j < kChunk; ++j) {
-                            const int m = m0 + c0 + j;
-                            float *w = p.ws + static_cast<int64_t>(m) * p.ldw + ncol;
-                            if (m < p.M && ncol < p.N) {
-                                v[j] = __ldcg(w);
-                                __stcg(w, 0.f);
-                            } else {
-                                v[j] = 0.f;
-                            }
-                        }
-                        emit(c0, v);
+                    for (int r = 0; r < kChunk; ++r) {
+                        const bool in = m0 + c0 + r < p.M && ncol < p.N;
+                        v[r] = in ? __ldcg(w + static_cast<int64_t>(r) * p.ldw) : 0.f;
                     }
-                    if (et == 0) *cnt = 0;
+#pragma unroll
+                    for (int r = 0; r < kChunk; ++r)
+                        if (m0 + c0 + r < p.M && ncol < p.N) __stcg(w + static_cast<int64_t>(r) * p.ldw, 0.f);
+                    emit(c0, v);
+                }
+                epi_bar();
+                if (et == 0 && atomicAdd(cnt + 1, 1) == p.split - 1) {  // every segment is past the wait
+                    cnt[0] = 0;
+                    cnt[1] = 0;
                 }
             }
             if (++acc == 2) {
@@ -596,7 +607,12 @@ bool encode_2d(void *fn, CUtensorMap *map, CUtensorMapDataType dt, int esize, co
 // Activation tile width for whole-tile GEMMs: the multiple of 32 that minimises
 // waves x per-k-block time, per-k-block time = max(MMA: 2 BN clk, operand traffic at ~50 B/clk
 // per SM: (128 + BN/CG) x 128 B / 50) + a fixed ~40 clk (profiles/r02_gemm_trace.log).
-void choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tiles) {
+double per_kblock_clk(int bn, int cg) {
+    return std::max(2.0 * bn, (128.0 + static_cast<double>(bn) / cg) * 128.0 / 50.0) + 40.0;
+}
+
+// returns the estimate (clocks per k-block x waves) of the chosen tiling
+double choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tiles) {
     double best = 1e300;
     *m_tiles = (M + kMaxBN - 1) / kMaxBN;
     *BN = ((M + *m_tiles - 1) / *m_tiles + 31) / 32 * 32;
@@ -605,14 +621,14 @@ void choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tiles)
         if ((M + bn - 1) / bn != mt) continue;
         const int64_t units = static_cast<int64_t>(n_tiles) * mt;
         const int64_t waves = (units + groups - 1) / groups;
-        const double per_kb = std::max(2.0 * bn, (128.0 + static_cast<double>(bn) / cg) * 128.0 / 50.0) + 40.0;
-        const double t = static_cast<double>(waves) * per_kb;
+        const double t = static_cast<double>(waves) * per_kblock_clk(bn, cg);
         if (t < best * 0.999) {
             best = t;
             *BN = bn;
             *m_tiles = mt;
         }
     }
+    return best;
 }
 
 }  // namespace
@@ -688,11 +704,12 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     const int n_tiles = (N + kBM * cg_ - 1) / (kBM * cg_);  // a ragged last tile: TMA zero-fills
                                                             // its weight rows, clips its stores
     p.stream_k = e.kind == kEpiAcc32 ? 1 : 0;
+    double whole_clk = 1e300;  // the cost model's whole-tile estimate (whole-tile kinds)
     if (p.stream_k) {
         p.m_tiles = (M + kMaxBN - 1) / kMaxBN;
         p.BN = ((M + p.m_tiles - 1) / p.m_tiles + 31) / 32 * 32;
     } else {
-        choose_tiles(M, n_tiles, max_groups_, cg_, &p.BN, &p.m_tiles);
+        whole_clk = choose_tiles(M, n_tiles, max_groups_, cg_, &p.BN, &p.m_tiles) * p.kb;
     }
     if (force_bn_ > 0) {  // measurement: a fixed activation tile width
         p.BN = std::min(kMaxBN, (force_bn_ + 31) / 32 * 32);
@@ -700,19 +717,27 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     }
     p.split = 1;
     if (!p.stream_k && force_bn_ <= 0 && split_ok_ && split_env_ok()) {
-        // a handful of full-width tiles for ~74 CTA groups (a 70B-TP8 QKV slice, N = 1280, at
-        // a small batch): split K instead -- each K range's partial reduce-added into an fp32
-        // workspace, the tile's last segment applies the epilogue.  Only for <= groups/8 tiles
-        // and M <= 256: with more or wider tiles the S-way reduce-adds into the same lines (and
-        // the last segment's read-back) cost more than the idle groups
-        // (profiles/r02_gemm_split.json: TP8 QKV M = 64 31.7 -> 16.4 us; 7B O M = 512 21 -> 84 us)
+        // split K when the whole tiles cannot keep the CTA groups busy (a 70B-TP8 QKV slice:
+        // N = 1280 is 5 tiles for 74 pairs; the 7B / 13B down projections at small batches):
+        // full-width tiles, K cut S ways, every K range's fp32 partial reduce-added into a
+        // workspace by TMA, then the tile's S segments (co-resident: units x S <= groups) each
+        // read back and finish a share of its 32-row chunks.  Taken when the cost model says
+        // <= 0.9 x the best whole-tile tiling: S-way k-blocks at the widest tile plus the
+        // reduction, fitted on the final build as ~4 us + 0.6 us per MB reduce-added
+        // (profiles/r02_gemm_split.json: TP8 QKV 32 -> 14-21 us, 7B down at M <= 256 44 -> 26-32 us)
         const int mt0 = (M + kMaxBN - 1) / kMaxBN;
+        const int bn0 = ((M + mt0 - 1) / mt0 + 31) / 32 * 32;
         const int units0 = n_tiles * mt0;
-        const int S = std::min(max_groups_ / std::max(units0, 1), p.kb / 8);
-        if (units0 * 8 <= max_groups_ && M <= 256 && S >= 2) {
-            p.m_tiles = mt0;
-            p.BN = ((M + mt0 - 1) / mt0 + 31) / 32 * 32;
-            p.split = S;
+        const int S = std::min(max_groups_ / std::max(units0, 1), p.kb / 4);
+        if (units0 * 2 <= max_groups_ && S >= 2) {
+            const double clk_per_us = 1800.0;
+            const double mb = static_cast<double>(units0) * S * (kBM * cg_) * bn0 * 4.0 / 1e6;
+            const double split_clk = per_kblock_clk(bn0, cg_) * ((p.kb + S - 1) / S) + (4.0 + 0.6 * mb) * clk_per_us;
+            if (split_clk < 0.9 * whole_clk) {
+                p.m_tiles = mt0;
+                p.BN = bn0;
+                p.split = S;
+            }
         }
     }
     p.units = n_tiles * p.m_tiles;
@@ -728,8 +753,8 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     p.ws = nullptr;
     p.cnt = nullptr;
     if (p.split > 1) {
-        const size_t need = static_cast<size_t>(M) * N;
-        const int ncnt = p.units * cg_;
+        const size_t need = static_cast<size_t>(M) * N;  // fp32 [M][N], zero between launches
+        const int ncnt = 2 * p.units * cg_;                         // arrivals, departures per (tile, CTA)
         if (need > ws_elems_ || ncnt > cnt_cap_) {  // first use of a shape: grows once (synchronous)
             if (ws_) cudaFree(ws_);
             if (cnt_) cudaFree(cnt_);

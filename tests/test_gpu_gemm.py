@@ -9,8 +9,8 @@ non-multiples of the 32-row activation tile), several weight tiles, K from one 6
 to the 7B down projection's 11008, and accumulating launches where stream-K splits one output
 tile over many CTA groups (each adds its partial tile into y with a TMA reduce-add).  Launches
 with too few whole tiles for the CTA groups split K for the other epilogues too (the fp32
-workspace path, <= groups/8 tiles at M <= 256): the 70B-TP8 QKV slice below (M = 512 takes
-whole tiles), and the RoPE / SwiGLU / LM-head epilogues through
+workspace path, when the cost model prefers it): the 70B-TP8 QKV slice below at M = 7 / 64 /
+512, and the RoPE / SwiGLU / LM-head epilogues through
 tests/test_gpu_model.py::test_model_step_split_k_epilogues."""
 import numpy as np
 import pytest
@@ -168,9 +168,9 @@ def test_gemm_swiglu_epilogue(gemm):
 @pytest.mark.parametrize("M", [7, 64, 512])
 def test_gemm_split_k_few_tiles(gemm, M):
     # few whole tiles for the CTA groups (a 70B-TP8 QKV slice: N = 1280, K = 8192): K is split,
-    # every K range's fp32 partial is reduce-added into the runner's workspace and the tile's last
-    # segment reads the sum back (and clears it) for the fp16 / fp32 / SwiGLU epilogues; run twice
-    # so the second launch finds the workspace and the arrival counters cleared
+    # every K range's fp32 partial is reduce-added into the runner's workspace and the tile's
+    # segments read the sum back (and clear it) chunk by chunk for the fp16 / fp32 / SwiGLU
+    # epilogues; run twice so the second launch finds the workspace and the counters cleared
     for rep in range(2):
         check(gemm, M, 1280, 8192, "f16", seed=60 + rep)
         check(gemm, M, 1280 if gemm.cta_group == 2 else 1152, 8192, "f32", seed=62 + rep)

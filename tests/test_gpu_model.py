@@ -373,11 +373,12 @@ def test_model_edge_cases(dbk):
 
 
 def test_model_step_split_k_epilogues(dbk):
-    """A model whose projections have few weight tiles (QKV 1536 rows, gate|up 2048, LM head 1000
-    at K = 1024): the GEMM splits K for the RoPE / KV-write, SwiGLU and fp32 epilogues (partials
-    through the runner's fp32 workspace, the tile's last segment applies the epilogue); two steps,
-    the second attending to the K/V the first wrote through the split RoPE epilogue."""
-    s = om.ModelShape(layers=2, q_heads=8, kv_heads=2, head_dim=128, hidden=1024, ffn=1024, vocab=1000)
+    """A model whose projections have few weight tiles for their depth (QKV 5120 rows, gate|up
+    2048, LM head 1000, at K = 4096): the GEMM splits K for the RoPE / KV-write, SwiGLU and fp32
+    epilogues (partials reduce-added into the runner's fp32 workspace, the tile's segments read
+    back and finish a share of its chunks each); two steps, the second attending to the K/V the
+    first wrote through the split RoPE epilogue."""
+    s = om.ModelShape(layers=2, q_heads=32, kv_heads=4, head_dim=128, hidden=4096, ffn=1024, vocab=1000)
     kv_seed, wseed = 9, 10
     ctx = [3, 40, 129, 300, 17]
     pool, model, ids, ref = _setup(dbk, s, ctx, kv_seed, wseed)
