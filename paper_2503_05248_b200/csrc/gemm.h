@@ -66,6 +66,7 @@ public:
     // measurement: activation tile width (0 = the cost model's choice)
     void force_bn(int bn) { force_bn_ = bn; }
     int64_t launches() const { return launches_; }
+    int last_pairs_per_cluster() const { return last_np_; }  // 2: the last launch multicast its activations
     // measurement: 0 = never split K for the whole-tile epilogues (DBK_GEMM_SPLIT=0 does the same)
     void allow_split(bool on) { split_ok_ = on; }
     GemmRunner() = default;
@@ -75,6 +76,7 @@ public:
 
 private:
     int device_ = 0, cg_ = 1, sms_ = 0, max_groups_ = 0;
+    int max_clusters4_ = 0, last_np_ = 1;  // co-resident 4-CTA clusters (two pairs; 0 = not available)
     uint64_t *trace_ = nullptr;
     int dbg_ = 0, force_bn_ = 0;
     bool split_ok_ = true;

@@ -133,6 +133,16 @@ __device__ __forceinline__ void tma_load2d(void *dst, const CUtensorMap *map, in
             : "memory");
     }
 }
+// CTA-pair load multicast to the CTAs of `mask` (same shared-memory offset in each); completion is
+// counted on the barrier at `bar`'s offset in the leader CTA of each destination's pair.
+__device__ __forceinline__ void tma_load2d_mc(void *dst, const CUtensorMap *map, int c0, int c1, uint32_t bar,
+                                              uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void tma_store2d(const CUtensorMap *map, const void *src, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                      reinterpret_cast<uint64_t>(map)),
@@ -260,10 +270,26 @@ __device__ __forceinline__ void epi_issue(const KParams &p, const OutMaps *ty, c
     }
 }
 
-template <int CG, int EPI>
+// Weight tile (nt) and activation tile (mt) of work unit `unit` for pair `pair` of the cluster:
+// with NP = 2 pairs per cluster a unit is a super-unit of NP adjacent weight tiles sharing one
+// activation tile, pair j taking weight tile NP * (unit / m_tiles) + j.
+template <int NP>
+__device__ __forceinline__ void unit_tiles(const KParams &p, int unit, int pair, int &nt, int &mt) {
+    nt = (unit / p.m_tiles) * NP + pair;
+    mt = unit % p.m_tiles;
+}
+
+// NP = CTA pairs per cluster.  NP = 2 (CG = 2 only): the two pairs of a 4-CTA cluster compute
+// adjacent weight tiles against the same activation tile in lockstep, and each CTA loads HALF of
+// its activation box and multicasts it to the same-rank CTA of the other pair -- the activation
+// operand crosses L2 -> SM once per cluster instead of once per pair (the M = 512 GEMMs stream
+// their operands at the chip's L2 throughput).  A stage is refilled only after BOTH
+// pairs' MMAs have consumed it (the empty barrier counts the two leaders' commits).
+template <int CG, int NP, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
                const __grid_constant__ OutMaps ty, const KParams p) {
+    static_assert(NP == 1 || (NP == 2 && CG == 2), "multicast pairs need CTA pairs");
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
@@ -275,8 +301,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     const uint32_t a_bytes = kBM * 128, stage_bytes = a_bytes + BNc * 128;
     uint8_t *outbuf = smem + p.stages * stage_bytes;  // kOutBufs chunk images
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
-    const int g = static_cast<int>(blockIdx.x) / CG;
+    const uint32_t crank = CG == 2 ? cluster_rank() : 0u;
+    const uint32_t rank = crank & (CG - 1);          // rank within the pair (0 = the MMA leader)
+    const uint32_t lead = crank - rank;              // the pair leader's rank in the cluster
+    const int pair = static_cast<int>(crank >> 1) & (NP - 1);
+    const int BNh = BNc / NP;                        // activation rows this CTA loads (and multicasts)
+    const int g = static_cast<int>(blockIdx.x) / (CG * NP);
     const int64_t it0 = p.stream_k ? g * p.T / p.groups : 0;
     const int64_t it1 = p.stream_k ? (g + 1) * p.T / p.groups : 0;
     uint32_t tcols = 32;
@@ -287,7 +317,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], NP);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -314,7 +344,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
 
     if (warp == 0) {
         // ---------------- TMA producer
-        const uint32_t full_lead = CG == 2 ? cluster_addr(&full[0], 0) : smem_u32(&full[0]);
+        const uint32_t full_lead = CG == 2 ? cluster_addr(&full[0], lead) : smem_u32(&full[0]);
+        const uint16_t mc_mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
         // the first ring's weight boxes go out before the grid-dependency wait: weights never
         // depend on the previous kernel, the activations (and the outputs' readers) do
         int pre = 0;
@@ -322,7 +353,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             int64_t it_p = it0;
             Seg s0;
             if (lane == 0 && p.dbg != 2 && next_seg(p, g, it_p, it1, s0)) {
-                const int wrow = (s0.unit / p.m_tiles) * kBM * CG + static_cast<int>(rank) * kBM;
+                int nt0, mt0;
+                unit_tiles<NP>(p, s0.unit, pair, nt0, mt0);
+                const int wrow = nt0 * kBM * CG + static_cast<int>(rank) * kBM;
                 pre = min(p.stages, s0.k1 - s0.k0);
                 for (int s = 0; s < pre; ++s) {
                     if (rank == 0) mbar_expect_tx(&full[s], CG * stage_bytes);
@@ -337,7 +370,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         int64_t it = it0;
         Seg sg;
         while (next_seg(p, g, it, it1, sg)) {
-            const int nt = sg.unit / p.m_tiles, mt = sg.unit % p.m_tiles;
+            int nt, mt;
+            unit_tiles<NP>(p, sg.unit, pair, nt, mt);
             const int wrow = nt * kBM * CG + static_cast<int>(rank) * kBM;
             const int xrow = mt * p.BN + static_cast<int>(rank) * BNc;
             for (int kb = sg.k0; kb < sg.k1; ++kb, ++done) {
@@ -353,7 +387,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                             if (rank == 0) mbar_expect_tx(&full[stage], CG * stage_bytes);
                             tma_load2d<CG>(sa, &tw, kb * kBK, wrow, fb);
                         }
-                        tma_load2d<CG>(sa + a_bytes, &tx, kb * kBK, xrow, fb);
+                        if constexpr (NP == 2)
+                            tma_load2d_mc(sa + a_bytes + pair * BNh * 128, &tx, kb * kBK, xrow + pair * BNh, fb,
+                                          mc_mask);
+                        else
+                            tma_load2d<CG>(sa + a_bytes, &tx, kb * kBK, xrow, fb);
                     }
                 }
                 __syncwarp();
@@ -392,14 +430,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                         if constexpr (CG == 2) umma_ss_pair(td, ad, bd, idesc, accum);
                         else umma_ss(td, ad, bd, idesc, accum);
                     }
-                    if constexpr (CG == 2) umma_commit_pair(&empty[stage], 3);
+                    if constexpr (CG == 2) umma_commit_pair(&empty[stage], NP == 2 ? 0xF : 3);
                     else umma_commit(&empty[stage]);
                     if (++stage == p.stages) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                if constexpr (CG == 2) umma_commit_pair(&tfull[acc], 3);
+                if constexpr (CG == 2) umma_commit_pair(&tfull[acc], static_cast<uint16_t>(3u << lead));
                 else umma_commit(&tfull[acc]);
                 if (tr && lane == 0) tr[3] = global_ns();
                 if (++acc == 2) {
@@ -416,13 +454,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         const int row = q * 32 + lane;
         const int et = threadIdx.x - 64;
         const bool issuer = et < 32;  // epilogue warp 0 writes the chunks out
-        const uint32_t tempty_lead = CG == 2 ? cluster_addr(&tempty[0], 0) : smem_u32(&tempty[0]);
+        const uint32_t tempty_lead = CG == 2 ? cluster_addr(&tempty[0], lead) : smem_u32(&tempty[0]);
         int acc = 0, chunk = 0;
         uint32_t aph = 0;
         int64_t it = it0;
         Seg sg;
         while (next_seg(p, g, it, it1, sg)) {
-            const int nt = sg.unit / p.m_tiles, mt = sg.unit % p.m_tiles;
+            int nt, mt;
+            unit_tiles<NP>(p, sg.unit, pair, nt, mt);
             const int nrow0 = nt * kBM * CG + static_cast<int>(rank) * kBM;  // this CTA's first weight row
             const int m0 = mt * p.BN;
             if constexpr (EPI == kEpiRopeKV) {
@@ -580,14 +619,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
 
 using KernFn = void (*)(CUtensorMap, CUtensorMap, OutMaps, KParams);
 
-template <int CG>
+template <int CG, int NP = 1>
 KernFn kernel_for(int epi) {
     switch (epi) {
-        case kEpiF16: return gemm_tc_kernel<CG, kEpiF16>;
-        case kEpiF32: return gemm_tc_kernel<CG, kEpiF32>;
-        case kEpiAcc32: return gemm_tc_kernel<CG, kEpiAcc32>;
-        case kEpiRopeKV: return gemm_tc_kernel<CG, kEpiRopeKV>;
-        case kEpiSiluMul: return gemm_tc_kernel<CG, kEpiSiluMul>;
+        case kEpiF16: return gemm_tc_kernel<CG, NP, kEpiF16>;
+        case kEpiF32: return gemm_tc_kernel<CG, NP, kEpiF32>;
+        case kEpiAcc32: return gemm_tc_kernel<CG, NP, kEpiAcc32>;
+        case kEpiRopeKV: return gemm_tc_kernel<CG, NP, kEpiRopeKV>;
+        case kEpiSiluMul: return gemm_tc_kernel<CG, NP, kEpiSiluMul>;
         default: return nullptr;
     }
 }
@@ -606,13 +645,14 @@ bool encode_2d(void *fn, CUtensorMap *map, CUtensorMapDataType dt, int esize, co
 
 // Activation tile width for whole-tile GEMMs: the multiple of 32 that minimises
 // waves x per-k-block time, per-k-block time = max(MMA: 2 BN clk, operand traffic at ~50 B/clk
-// per SM: (128 + BN/CG) x 128 B / 50) + a fixed ~40 clk (profiles/r02_gemm_trace.log).
-double per_kblock_clk(int bn, int cg) {
-    return std::max(2.0 * bn, (128.0 + static_cast<double>(bn) / cg) * 128.0 / 50.0) + 40.0;
+// per SM: (128 + BN/(CG NP)) x 128 B / 50) + a fixed ~40 clk (profiles/r02_gemm_trace.log); NP = 2:
+// the activation box is multicast to two pairs, each SM fetches half of its share.
+double per_kblock_clk(int bn, int cg, int np = 1) {
+    return std::max(2.0 * bn, (128.0 + static_cast<double>(bn) / (cg * np)) * 128.0 / 50.0) + 40.0;
 }
 
 // returns the estimate (clocks per k-block x waves) of the chosen tiling
-double choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tiles) {
+double choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tiles, int np = 1) {
     double best = 1e300;
     *m_tiles = (M + kMaxBN - 1) / kMaxBN;
     *BN = ((M + *m_tiles - 1) / *m_tiles + 31) / 32 * 32;
@@ -621,7 +661,7 @@ double choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tile
         if ((M + bn - 1) / bn != mt) continue;
         const int64_t units = static_cast<int64_t>(n_tiles) * mt;
         const int64_t waves = (units + groups - 1) / groups;
-        const double t = static_cast<double>(waves) * per_kblock_clk(bn, cg);
+        const double t = static_cast<double>(waves) * per_kblock_clk(bn, cg, np);
         if (t < best * 0.999) {
             best = t;
             *BN = bn;
@@ -632,6 +672,15 @@ double choose_tiles(int M, int n_tiles, int groups, int cg, int *BN, int *m_tile
 }
 
 }  // namespace
+
+// measurement: DBK_GEMM_NP = 1 / 2 forces the pairs per cluster (unset: the cost model decides)
+static int np_env() {
+    static const int v = [] {
+        const char *e = std::getenv("DBK_GEMM_NP");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
 
 static bool split_env_ok() {
     static const bool ok = [] {
@@ -679,10 +728,25 @@ cudaError_t GemmRunner::init(int device, int cta_group) {
         if ((e = cudaOccupancyMaxActiveClusters(&clusters, kernel_for<2>(kEpiF16), &cfg)) != cudaSuccess) return e;
         max_groups_ = std::min(clusters, sms_ / 2);
         if (max_groups_ < 1) return cudaErrorNotSupported;
+        // 4-CTA clusters (two pairs sharing the activation operand by multicast)
+        for (int epi = kEpiF16; epi <= kEpiSiluMul; ++epi) {
+            if ((e = cudaFuncSetAttribute(kernel_for<2, 2>(epi), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          kDynSmem)) != cudaSuccess)
+                return e;
+        }
+        attr[0].val.clusterDim.x = 4;
+        cfg.gridDim = dim3(4 * (sms_ / 4));
+        int c4 = 0;
+        if (cudaOccupancyMaxActiveClusters(&c4, kernel_for<2, 2>(kEpiF16), &cfg) != cudaSuccess) {
+            (void)cudaGetLastError();
+            c4 = 0;
+        }
+        max_clusters4_ = std::min(c4, sms_ / 4);
     }
     if (const char *v = std::getenv("DBK_GEMM_SMS")) {  // measurement: the GEMM on a subset of the SMs
         const int n = std::atoi(v) / cg_;
         if (n >= 1) max_groups_ = std::min(max_groups_, n);
+        if (n >= 1) max_clusters4_ = std::min(max_clusters4_, n / 2);
     }
     return cudaSuccess;
 }
@@ -740,14 +804,30 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
             }
         }
     }
-    p.units = n_tiles * p.m_tiles;
+    // Two pairs per cluster sharing the activation operand by multicast (an even number of weight
+    // tiles, no K split): measured and NOT taken by default -- 0.97-1.27 x the time of one pair per
+    // cluster on the 7B / 13B / 70B-TP8 shapes (profiles/r02_gemm_multicast.json): the M = 512
+    // GEMMs are bound by the SM's shared-memory port (every operand byte is written by TMA and read
+    // by the MMA), which multicast does not relieve.  DBK_GEMM_NP=2 forces it (measurement).
+    int np = 1;
+    if (cg_ == 2 && max_clusters4_ >= 1 && p.split == 1 && n_tiles % 2 == 0 && np_env() == 2) {
+        np = 2;
+        if (!p.stream_k && force_bn_ <= 0) {
+            int bn2 = p.BN, mt2 = p.m_tiles;
+            choose_tiles(M, n_tiles / 2, max_clusters4_, cg_, &bn2, &mt2, 2);
+            p.BN = bn2;
+            p.m_tiles = mt2;
+        }
+    }
+    p.units = (n_tiles / np) * p.m_tiles;
     p.T = static_cast<int64_t>(p.units) * p.kb;
+    const int maxg = np == 2 ? max_clusters4_ : max_groups_;
     if (p.stream_k) {
         // >= 4 k-blocks per group: a partial tile's reduce-add (BN x 128 x 4 B) stays small next to
         // the operand traffic of its k-blocks
-        p.groups = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_groups_, p.T / 4)));
+        p.groups = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(maxg, p.T / 4)));
     } else {
-        p.groups = std::min<int64_t>(max_groups_, static_cast<int64_t>(p.units) * p.split);
+        p.groups = std::min<int64_t>(maxg, static_cast<int64_t>(p.units) * p.split);
     }
     p.ldw = N;
     p.ws = nullptr;
@@ -779,7 +859,7 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     CUtensorMap tw, tx;
     OutMaps ty;
     if (!encode_2d(encode_, &tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W, K, N, K, kBK, kBM, true) ||
-        !encode_2d(encode_, &tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, X, K, M, ldx, kBK, p.BN / cg_, true))
+        !encode_2d(encode_, &tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, X, K, M, ldx, kBK, p.BN / (cg_ * np), true))
         return cudaErrorInvalidValue;
     bool ok = true;
     switch (e.kind) {
@@ -811,17 +891,17 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     if (ok && p.split > 1)  // the split-K workspace [M][N] fp32, per-warp 32 x 32 reduce-add boxes
         ok = encode_2d(encode_, &ty.m[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.ws, N, M, N, 32, kChunk, false);
     if (!ok) return cudaErrorInvalidValue;
-    KernFn k = cg_ == 2 ? kernel_for<2>(e.kind) : kernel_for<1>(e.kind);
+    KernFn k = cg_ == 2 ? (np == 2 ? kernel_for<2, 2>(e.kind) : kernel_for<2>(e.kind)) : kernel_for<1>(e.kind);
     if (!k) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.groups * cg_);
+    cfg.gridDim = dim3(p.groups * cg_ * np);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = static_cast<size_t>(p.stages) * stage_bytes + kOutBufs * kStageOut + 1024;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     int na = 0;
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = cg_;
+    attr[na].val.clusterDim.x = cg_ * np;
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;
@@ -833,6 +913,7 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     cfg.attrs = attr;
     cfg.numAttrs = na;
     ++launches_;
+    last_np_ = np;
     return cudaLaunchKernelEx(&cfg, k, tw, tx, ty, p);
 }
 

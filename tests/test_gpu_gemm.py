@@ -183,3 +183,20 @@ def test_gemm_split_k_few_tiles(gemm, M):
     want = om.silu(z[:, 0::2]) * z[:, 1::2]
     err = row_err(act.float().cpu().numpy().astype(np.float64), want)
     assert err <= TOL["f16"], f"swiglu split: {err:.3e}"
+
+
+def test_gemm_multicast_pairs_opt_in():
+    """Two CTA pairs per 4-CTA cluster sharing the activation operand by TMA multicast
+    (DBK_GEMM_NP=2, measured and not taken by default: profiles/r02_gemm_multicast.json): the
+    cta_group-2 cases above rerun in a child process with the path forced."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("DBK_GEMM_NP"):
+        pytest.skip("already inside the forced-multicast run")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    env = dict(os.environ, DBK_GEMM_NP="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k", "cg2 and not multicast"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
