@@ -172,10 +172,15 @@ def make_workload(cfg_name=CFG_NAME, world=1, n_req=None):
 POLICIES = {"static": 0, "memory": 1, "sla": 2, "combined": 3}
 
 
-def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None):
+def sched_kwargs(c, beta, policy=None, b_static=256, sla_ms=None, eps_d_ms=None, dp_world=1):
+    """The scheduler's configuration.  B_max is the config's per-GPU batch bound (the pool's request
+    slots): a job of dp_world request shards decides a GLOBAL b_t (Alg. 1 over the summed records
+    and the global eta, R21), so its bound is dp_world x B_max and each rank's share stays at the
+    one-GPU batch -- per-GPU work fixed (weak scaling).  A global 512 over 8 shards would leave 64
+    requests per GPU."""
     pr = configs.prior_record(c)
     pol = POLICIES[policy or c["policy"]]
-    return dict(policy=pol, b_static=b_static, b_min=c["b_min"], b_max=c["b_max"], b0=c["b_min"],
+    return dict(policy=pol, b_static=b_static, b_min=c["b_min"], b_max=c["b_max"] * dp_world, b0=c["b_min"],
                 eps_m=c["eps_m"], bytes_per_token=beta, page_size=c["page_size"], refresh_steps=100,
                 w_len=256, w_sla=20, alpha=c.get("alpha", 8), delta=c.get("delta", 2),
                 d_sla_ms=sla_ms or c.get("sla_ms", 50.0),
@@ -218,7 +223,8 @@ def setup_engine(device=0, rank=0, world=1, cfg_name=CFG_NAME, cap_bytes=None, t
         pool.swap_space_attach(torch.empty(int(swap_bytes), dtype=torch.uint8, pin_memory=True))
     # M_max of the whole job: DP shards add their pools; TP ranks hold the same tokens
     mem_cap_total = cap_pages * P * beta * (world if tp == 1 else 1)
-    sched = dbk.Scheduler(**sched_kwargs(c, beta, policy, b_static, sla_ms, eps_d_ms))
+    sched = dbk.Scheduler(**sched_kwargs(c, beta, policy, b_static, sla_ms, eps_d_ms,
+                                         dp_world=world if tp == 1 else 1))
     eng = dbk.Engine(pool, sched, tr.arrival_ns, tr.l_in, tr.l_out, mem_cap_total, seed=seed,
                      out_dtype=out_dtype, time_attention=time_attention,
                      rank=rank if tp == 1 else 0, world=world if tp == 1 else 1, sla_ms=sla_ms or 0.0,

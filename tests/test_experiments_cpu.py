@@ -18,3 +18,15 @@ def test_tbt_p99_matches_sorted_token_list():
     assert paper_tables._tbt_p99(recs) == toks[k - 1]
     const = [dict(step_ns=50_000_000, n_decode=7)] * 10
     assert paper_tables._tbt_p99(const) == 50.0
+
+
+def test_bench_dp_batch_bound_scales_with_the_shards():
+    """R39: request-shard DP at N GPUs bounds the global b_t by N x the per-GPU B_max, so each
+    rank's share (R21) stays at the one-GPU batch (weak scaling); TP ranks keep the global bound."""
+    import bench
+    from synth import configs
+    c = configs.CONFIGS["llama2-7b"]
+    beta = configs.kv_bytes_per_token(c)
+    for n in (1, 2, 4, 8):
+        assert bench.sched_kwargs(c, beta, dp_world=n)["b_max"] == n * c["b_max"]
+    assert bench.sched_kwargs(c, beta)["b_max"] == c["b_max"]
