@@ -200,3 +200,15 @@ def test_gemm_multicast_pairs_opt_in():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k", "cg2 and not multicast"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_gemm_empty_batch_is_a_noop(gemm):
+    """M = 0 (an empty decode batch): DBK_OK, no launch, the output untouched."""
+    K, N = 256, 512
+    x = torch.zeros(4, K, dtype=torch.float16, device="cuda")[:0]
+    w = torch.zeros(N, K, dtype=torch.float16, device="cuda")
+    y = torch.full((1, N), float("nan"), dtype=torch.float32, device="cuda")
+    for mode in ("f32", "acc32"):
+        gemm(x, w, y, mode)
+    torch.cuda.synchronize()
+    assert torch.isnan(y).all()

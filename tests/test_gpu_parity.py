@@ -508,3 +508,32 @@ def test_bench_config_whole_trace_replay(dbk):
     assert sum(r["n_decode"] for r in recs) == int(S["tr"].l_out.sum())
     _replay_full_size(S, recs)
     _free(S)
+
+
+def test_empty_batch_is_a_noop_with_the_empty_record(dbk):
+    """Degenerate case n = 0 ('n = 0 is a no-op returning DBK_OK'): no
+    launch, no output written, and a stats-fused empty step reports the oracle's empty record
+    (cap_pages = free_pages = cap, R28) even while requests hold pages."""
+    P, cap = 16, 64
+    pool = dbk.KVPool(2, 8, 8, 64, cap, 4, 8, "f16")
+    ref = PagedKV(cap, P)
+    pool.request_begin(5, 20, 10)
+    ref.begin(5)
+    pool.append_tokens([5], [21], seed=3)
+    ref.append([5], [21])
+    q = torch.zeros(1, 8, 64, dtype=torch.float16, device="cuda")
+    out = torch.full((1, 8, 64), float("nan"), dtype=torch.float32, device="cuda")
+    pool.decode_step([], 0, q, out, fuse_stats=True)
+    assert pool.batch_stats() == ostats.batch_stats([], [], [], [], P, cap)
+    qa = torch.zeros(2, 1, 8, 64, dtype=torch.float16, device="cuda")
+    oa = torch.full((2, 1, 8, 64), float("nan"), dtype=torch.float32, device="cuda")
+    assert pool.decode_step_layers([], 0, 2, qa, 8 * 64, oa, 8 * 64, fuse_stats=True) == 0
+    torch.cuda.synchronize()
+    assert torch.isnan(out).all() and torch.isnan(oa).all()
+    assert pool.batch_stats() == ostats.batch_stats([], [], [], [], P, cap)
+    # the request is untouched: a non-empty step right after matches the oracle again
+    c, slot, pages = pool.request_info(5)
+    assert c == 21 and pages == ref.pages[5]
+    pool.decode_step([5], 1, q, out, fuse_stats=True)
+    assert pool.batch_stats() == ostats.batch_stats([21], [20], [10], [ref.pages[5]], P, cap)
+    pool.close()
