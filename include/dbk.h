@@ -183,7 +183,9 @@ typedef struct dbk_batch {
  * over the request's paged KV of `layer` (R1, R2; oracle O1).  q: device
  * [n][q_heads][head_dim] kv_dtype; out: device [n][q_heads][head_dim] of
  * out_dtype (0 fp16, 1 bf16, 2 fp32).  fp32 accumulation.  With fuse_stats
- * the same launch reduces the batch statistics record (O3).  Async. */
+ * the same launch reduces the batch statistics record (O3).  n = 0: no launch, q and out
+ * untouched; with fuse_stats the record becomes the empty batch's (cap_pages = free_pages =
+ * cap, every other field 0; R28).  Async. */
 dbk_status dbk_decode_step(dbk_pool *pool, const dbk_batch *batch, const void *q, void *out,
                            int32_t out_dtype, void *stream);
 

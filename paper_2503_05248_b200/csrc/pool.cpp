@@ -877,13 +877,29 @@ static dbk_status decode_args_ok(dbk_pool *p, const dbk_batch *b, const void *q,
 
 }  // namespace dbk
 
+// The stats record before a fused step: zero for K4 to accumulate into, or -- an empty batch,
+// where no launch reduces it -- the empty batch's record (O3: cap_pages = free_pages = cap, R28).
+static_assert(sizeof(dbk_stats) == 128, "dbk_stats is the 128-byte record K4 reduces into");
+static dbk_status reset_stats(dbk_pool *p, int32_t n, cudaStream_t s) {
+    if (n > 0) {
+        DBK_CUDA(cudaMemsetAsync(p->d_stats, 0, sizeof(dbk_stats), s));
+        return DBK_OK;
+    }
+    dbk_stats empty{};
+    empty.cap_pages = p->cfg.cap_pages;
+    empty.free_pages = p->cfg.cap_pages;
+    // pageable source: staged before the call returns, so the stack record may go
+    DBK_CUDA(cudaMemcpyAsync(p->d_stats, &empty, sizeof(dbk_stats), cudaMemcpyHostToDevice, s));
+    return DBK_OK;
+}
+
 extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const void *q, void *out,
                                       int32_t out_dtype, void *stream) {
     DBK_TRY(decode_args_ok(p, b, q, out, out_dtype));
     DBK_CUDA(cudaSetDevice(p->cfg.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     DBK_TRY(flush_deltas(p, s));
-    if (b->fuse_stats) DBK_CUDA(cudaMemsetAsync(p->d_stats, 0, 128, s));
+    if (b->fuse_stats) DBK_TRY(reset_stats(p, b->n, s));
     if (b->n == 0) return DBK_OK;
     DBK_TRY(prepare_batch(p, b->n, b->req_ids, s));
     DBK_TRY(decode_launch(p, b->n, b->layer, 1, q, 0, out, 0, out_dtype, b->fuse_stats != 0, b->chain, s));
@@ -902,7 +918,7 @@ extern "C" dbk_status dbk_decode_step_layers(dbk_pool *p, const dbk_batch *b, in
     DBK_CUDA(cudaSetDevice(p->cfg.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     DBK_TRY(flush_deltas(p, s));
-    if (b->fuse_stats) DBK_CUDA(cudaMemsetAsync(p->d_stats, 0, 128, s));
+    if (b->fuse_stats) DBK_TRY(reset_stats(p, b->n, s));
     if (launches_out) *launches_out = 0;
     if (b->n == 0) return DBK_OK;
     DBK_TRY(prepare_batch(p, b->n, b->req_ids, s, n_layers));
