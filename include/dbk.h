@@ -185,7 +185,8 @@ typedef struct dbk_batch {
  * out_dtype (0 fp16, 1 bf16, 2 fp32).  fp32 accumulation.  With fuse_stats
  * the same launch reduces the batch statistics record (O3).  n = 0: no launch, q and out
  * untouched; with fuse_stats the record becomes the empty batch's (cap_pages = free_pages =
- * cap, every other field 0; R28).  Async. */
+ * cap, every other field 0; R28).  DBK_ENOENT: an unknown request; DBK_EINVAL: a request
+ * holding no tokens or named twice in the batch (nothing launched).  Async. */
 dbk_status dbk_decode_step(dbk_pool *pool, const dbk_batch *batch, const void *q, void *out,
                            int32_t out_dtype, void *stream);
 

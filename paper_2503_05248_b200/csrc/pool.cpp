@@ -674,13 +674,19 @@ dbk_status prepare_batch(dbk_pool *p, int32_t n, const int64_t *ids, cudaStream_
         p->meta_layers_hint == layers_hint && std::equal(p->meta_ids.begin(), p->meta_ids.end(), ids))
         return DBK_OK;
     const int64_t P = p->cfg.page_size;
+    p->meta_valid = false;  // rebuilt below; a rejected batch leaves no half-built cache behind
     p->meta_req.resize(n);
     int64_t total_pages = 0;
+    // a request decodes one token per step: a batch naming it twice is malformed (K4 would count
+    // it twice); its block-table slot is unique, so a slot bitmap finds repeats in O(n)
+    std::vector<uint8_t> &seen = p->slot_seen;
+    seen.assign(static_cast<size_t>(p->cfg.max_requests), 0);
     for (int i = 0; i < n; ++i) {
         auto it = p->reqs.find(ids[i]);
         if (it == p->reqs.end()) return fail(DBK_ENOENT, "decode_step: unknown request %lld", static_cast<long long>(ids[i]));
         const Request &r = it->second;
         if (r.ctx < 1) return fail(DBK_EINVAL, "decode_step: request %lld holds no tokens", static_cast<long long>(ids[i]));
+        if (seen[r.slot]++) return fail(DBK_EINVAL, "decode_step: request %lld appears twice in the batch", static_cast<long long>(ids[i]));
         ReqMeta &m = p->meta_req[i];
         m.req_id = r.id;
         m.slot = r.slot;
@@ -899,9 +905,11 @@ extern "C" dbk_status dbk_decode_step(dbk_pool *p, const dbk_batch *b, const voi
     DBK_CUDA(cudaSetDevice(p->cfg.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     DBK_TRY(flush_deltas(p, s));
+    // the batch is checked (prepare_batch) before the stats record is reset: a rejected call
+    // leaves everything as it was
+    if (b->n > 0) DBK_TRY(prepare_batch(p, b->n, b->req_ids, s));
     if (b->fuse_stats) DBK_TRY(reset_stats(p, b->n, s));
     if (b->n == 0) return DBK_OK;
-    DBK_TRY(prepare_batch(p, b->n, b->req_ids, s));
     DBK_TRY(decode_launch(p, b->n, b->layer, 1, q, 0, out, 0, out_dtype, b->fuse_stats != 0, b->chain, s));
     p->last_decode_bytes = decode_bytes(p, out_dtype);
     return DBK_OK;
@@ -918,10 +926,10 @@ extern "C" dbk_status dbk_decode_step_layers(dbk_pool *p, const dbk_batch *b, in
     DBK_CUDA(cudaSetDevice(p->cfg.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     DBK_TRY(flush_deltas(p, s));
-    if (b->fuse_stats) DBK_TRY(reset_stats(p, b->n, s));
     if (launches_out) *launches_out = 0;
+    if (b->n > 0) DBK_TRY(prepare_batch(p, b->n, b->req_ids, s, n_layers));
+    if (b->fuse_stats) DBK_TRY(reset_stats(p, b->n, s));
     if (b->n == 0) return DBK_OK;
-    DBK_TRY(prepare_batch(p, b->n, b->req_ids, s, n_layers));
     // layers per launch: as many as the split-K workspace budget holds (every layer of the step
     // in one launch when it fits)
     const int64_t per_layer_rows = static_cast<int64_t>(std::max(p->meta_ws_rows, 1)) * p->cfg.q_heads;

@@ -71,6 +71,7 @@ struct dbk_pool {
     uint64_t meta_epoch = 0;
     std::vector<int64_t> meta_ids;
     std::vector<dbk::ReqMeta> meta_req;
+    std::vector<uint8_t> slot_seen;  // prepare_batch: block-table slots named by the batch (repeat check)
     std::vector<int2> meta_work;
     std::vector<uint8_t> meta_blob;
     int32_t meta_items = 0, meta_chunk_pages = 0, meta_ws_rows = 0, meta_layers_hint = 1;

@@ -537,3 +537,23 @@ def test_empty_batch_is_a_noop_with_the_empty_record(dbk):
     pool.decode_step([5], 1, q, out, fuse_stats=True)
     assert pool.batch_stats() == ostats.batch_stats([21], [20], [10], [ref.pages[5]], P, cap)
     pool.close()
+
+
+def test_malformed_batches_are_rejected_before_any_launch(dbk):
+    """A request named twice (K4 would count it twice), an unknown request, a request holding no
+    tokens: DBK_EINVAL / DBK_ENOENT, nothing written; the pool stays usable."""
+    pool = dbk.KVPool(1, 8, 8, 64, 32, 4, 8, "f16")
+    pool.request_begin(1, 10, 10)
+    pool.request_begin(2, 10, 10)
+    pool.append_tokens([1], [11], seed=2)
+    q = torch.zeros(2, 8, 64, dtype=torch.float16, device="cuda")
+    out = torch.full((2, 8, 64), float("nan"), dtype=torch.float32, device="cuda")
+    for ids, status in (([1, 1], dbk._lib.DBK_EINVAL), ([1, 9], dbk._lib.DBK_ENOENT), ([1, 2], dbk._lib.DBK_EINVAL)):
+        with pytest.raises(dbk.DbkError) as e:
+            pool.decode_step(ids, 0, q, out, fuse_stats=True)
+        assert e.value.status == status, (ids, e.value)
+    torch.cuda.synchronize()
+    assert torch.isnan(out).all()
+    pool.decode_step([1], 0, q[:1], out[:1], fuse_stats=True)
+    assert pool.batch_stats()["n_active"] == 1
+    pool.close()
