@@ -104,7 +104,8 @@ dbk_status dbk_append_tokens(dbk_pool *pool, int32_t n_req, const int64_t *req_i
 
 /* Finish or preempt: all pages of each request return to the free set (R9),
  * the slot is freed and its device block-table row is cleared before the
- * next launch.  ENOENT on an unknown id (earlier ids are released). */
+ * next launch.  All-or-nothing: ENOENT on an unknown id, EINVAL on an id named twice, and
+ * then nothing is released. */
 dbk_status dbk_release(dbk_pool *pool, int32_t n_req, const int64_t *req_ids);
 
 /* Swap space ("The swapping method involves
@@ -121,7 +122,7 @@ dbk_status dbk_swap_space_attach(dbk_pool *pool, void *host_mem, size_t bytes, i
  * lowest-free-first in batch order, then release its device pages and slot
  * (as dbk_release); the request keeps its id, l_in, l_out and ctx.
  * All-or-nothing: ECAP if the swap space lacks pages, ENOENT on an unknown
- * or already swapped id (state unchanged).  The device-to-host copies are
+ * or already swapped id, EINVAL on an id named twice (state unchanged).  The device-to-host copies are
  * copy-engine 2-D copies (one per run of consecutive pages) async on
  * `stream`, ordered before any later write to the released pages on it. */
 dbk_status dbk_swap_out(dbk_pool *pool, int32_t n_req, const int64_t *req_ids, void *stream);
@@ -130,7 +131,7 @@ dbk_status dbk_swap_out(dbk_pool *pool, int32_t n_req, const int64_t *req_ids, v
  * lowest-free-first in batch order (exactly the pages an append of ctx tokens
  * would take, R7), its KV is copied host-to-device on `stream` and its swap
  * pages are freed.  All-or-nothing: ECAP if device pages are short, EINVAL if
- * slots are short, ENOENT if an id is not swapped out.  dbk_release of a
+ * slots are short or an id is named twice, ENOENT if an id is not swapped out.  dbk_release of a
  * swapped-out id frees its swap pages. */
 dbk_status dbk_swap_in(dbk_pool *pool, int32_t n_req, const int64_t *req_ids, void *stream);
 

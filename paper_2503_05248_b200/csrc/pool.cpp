@@ -343,6 +343,14 @@ dbk_status flush_deltas(dbk_pool *p, cudaStream_t s) {
 }
 // Validates and performs the bookkeeping of an append (pages lowest-free-first, all-or-nothing,
 // R7/R8), flushes the block-table deltas and uploads the job list; no KV is written yet.
+// true when some id appears twice in ids[0, n) (list calls are all-or-nothing and name each
+// request once)
+bool has_duplicate_ids(int32_t n, const int64_t *ids) {
+    std::vector<int64_t> sorted(ids, ids + n);
+    std::sort(sorted.begin(), sorted.end());
+    return std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end();
+}
+
 dbk_status append_plan(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t *n_tok, bool explicit_rows,
                        cudaStream_t s, bool upload_jobs) {
     if (!p) return fail(DBK_EINVAL, "null pool");
@@ -362,12 +370,7 @@ dbk_status append_plan(dbk_pool *p, int32_t n, const int64_t *ids, const int32_t
         need += np - static_cast<int64_t>(r.pages.size());
         rs[i] = &r;
     }
-    {
-        std::vector<int64_t> sorted(ids, ids + n);
-        std::sort(sorted.begin(), sorted.end());
-        if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
-            return fail(DBK_EINVAL, "append_tokens: duplicate request id in one call");
-    }
+    if (has_duplicate_ids(n, ids)) return fail(DBK_EINVAL, "append_tokens: duplicate request id in one call");
     if (need > p->pages.free_count)
         return fail(DBK_ECAP, "append_tokens: needs %lld pages, %lld free", static_cast<long long>(need),
                     static_cast<long long>(p->pages.free_count));
@@ -457,6 +460,11 @@ dbk_status dbk_reserve_tokens(dbk_pool *p, int32_t n, const int64_t *ids, const 
 dbk_status dbk_release(dbk_pool *p, int32_t n, const int64_t *ids) {
     if (!p) return fail(DBK_EINVAL, "null pool");
     if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "release: bad arrays");
+    // all-or-nothing like append_tokens: every id known (resident or swapped out), none twice
+    for (int i = 0; i < n; ++i)
+        if (!p->swapped.count(ids[i]) && !p->reqs.count(ids[i]))
+            return fail(DBK_ENOENT, "release: unknown request %lld", static_cast<long long>(ids[i]));
+    if (dbk::has_duplicate_ids(n, ids)) return fail(DBK_EINVAL, "release: duplicate request id in one call");
     for (int i = 0; i < n; ++i) {
         auto sw = p->swapped.find(ids[i]);
         if (sw != p->swapped.end()) {  // a swapped-out request: its swap pages go back
@@ -542,6 +550,7 @@ dbk_status dbk_swap_out(dbk_pool *p, int32_t n, const int64_t *ids, void *stream
     if (!p) return fail(DBK_EINVAL, "null pool");
     if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "swap_out: bad arrays");
     if (!p->swap_host) return fail(DBK_EINVAL, "swap_out: no swap space attached");
+    if (dbk::has_duplicate_ids(n, ids)) return fail(DBK_EINVAL, "swap_out: duplicate request id in one call");
     int64_t need = 0;
     for (int i = 0; i < n; ++i) {
         auto it = p->reqs.find(ids[i]);
@@ -579,6 +588,7 @@ dbk_status dbk_swap_out(dbk_pool *p, int32_t n, const int64_t *ids, void *stream
 dbk_status dbk_swap_in(dbk_pool *p, int32_t n, const int64_t *ids, void *stream) {
     if (!p) return fail(DBK_EINVAL, "null pool");
     if (n < 0 || (n > 0 && !ids)) return fail(DBK_EINVAL, "swap_in: bad arrays");
+    if (dbk::has_duplicate_ids(n, ids)) return fail(DBK_EINVAL, "swap_in: duplicate request id in one call");
     int64_t need = 0;
     for (int i = 0; i < n; ++i) {
         auto it = p->swapped.find(ids[i]);

@@ -557,3 +557,20 @@ def test_malformed_batches_are_rejected_before_any_launch(dbk):
     pool.decode_step([1], 0, q[:1], out[:1], fuse_stats=True)
     assert pool.batch_stats()["n_active"] == 1
     pool.close()
+
+
+def test_release_is_all_or_nothing(dbk):
+    """dbk_release like append_tokens (R8): an unknown id or an id named twice releases nothing."""
+    pool = dbk.KVPool(1, 8, 8, 64, 16, 4, 8, "f16")
+    for r in (1, 2):
+        pool.request_begin(r, 10, 10)
+    pool.append_tokens([1, 2], [20, 5], seed=1)
+    before = pool.usage()
+    for ids, status in (([1, 7], dbk._lib.DBK_ENOENT), ([2, 2], dbk._lib.DBK_EINVAL)):
+        with pytest.raises(dbk.DbkError) as e:
+            pool.release(ids)
+        assert e.value.status == status
+        assert pool.usage() == before and pool.request_info(1)[0] == 20 and pool.request_info(2)[0] == 5
+    pool.release([2, 1])
+    assert pool.usage() == (0, 16)
+    pool.close()

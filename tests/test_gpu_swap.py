@@ -116,3 +116,28 @@ def test_engine_swap_preemption_replays(dbk):
                                 swap_pages=6, layers=2)
     n_out = sum(r["n_swap_out"] for r in recs)
     assert 0 < n_out < sum(r["n_preempted"] for r in recs)
+
+
+def test_swap_lists_naming_a_request_twice_are_rejected(dbk):
+    """swap_out / swap_in / release name each request once (all-or-nothing list calls): a repeated
+    id is DBK_EINVAL with the pool and the swap space unchanged (before the check, swap_out's
+    second visit of the id looked up a request it had just moved out)."""
+    L, Hq, Hkv, d, P = 1, 8, 8, 64, 16
+    pool = dbk.KVPool(L, Hq, Hkv, d, 16, 4, 8, "f16")
+    page_bytes = L * Hkv * 2 * P * d * 2
+    pool.swap_space_attach(torch.empty(8 * page_bytes, dtype=torch.uint8, pin_memory=True))
+    pool.request_begin(1, 10, 10)
+    pool.request_begin(2, 10, 10)
+    pool.append_tokens([1, 2], [20, 5], seed=1)
+    used = pool.usage()
+    with pytest.raises(dbk.DbkError) as e:
+        pool.swap_out([1, 2, 1])
+    assert e.value.status == dbk._lib.DBK_EINVAL and pool.usage() == used
+    pool.swap_out([1])
+    with pytest.raises(dbk.DbkError) as e:
+        pool.swap_in([1, 1])
+    assert e.value.status == dbk._lib.DBK_EINVAL
+    pool.swap_in([1])
+    torch.cuda.synchronize()
+    assert pool.request_info(1)[0] == 20 and pool.usage() == used
+    pool.close()
