@@ -59,26 +59,38 @@ decode_kernel(const DecodeParams p) {
     auto top_up = [&](uint32_t seq_cons) {
         while (seq_iss < seq_cons + STAGES) {
             const int j = static_cast<int>(seq_iss - cur_start);
-            int ph, g, lay;
+            int ph, g, lay, valid;
             if (j < cur.it.n) {
                 ph = page_of(cur, j);
                 g = cur.g;
                 lay = cur.l;
+                valid = cur.it.ctx - (cur.it.pg0 + j) * kP;
             } else if (j - cur.it.n < nxt.it.n) {
                 ph = page_of(nxt, j - cur.it.n);
                 g = nxt.g;
                 lay = nxt.l;
+                valid = nxt.it.ctx - (nxt.it.pg0 + j - cur.it.n) * kP;
             } else {
                 break;
             }
             if (lane == 0) {
                 const int s = seq_iss % STAGES;
+                const uint8_t *src = p.kv_layer + static_cast<size_t>(lay) * p.layer_stride +
+                                     static_cast<size_t>(g) * TILE + static_cast<size_t>(ph) * p.page_stride;
                 fence_proxy_async();
-                mbar_expect_tx(&bars[warp][s], TILE);
-                bulk_g2s(wbuf + s * TILE,
-                         p.kv_layer + static_cast<size_t>(lay) * p.layer_stride + static_cast<size_t>(g) * TILE +
-                             static_cast<size_t>(ph) * p.page_stride,
-                         TILE, &bars[warp][s], pol);
+                if (valid >= kP) {
+                    mbar_expect_tx(&bars[warp][s], TILE);
+                    bulk_g2s(wbuf + s * TILE, src, TILE, &bars[warp][s], pol);
+                } else {
+                    // a request's last, partly filled page: only its `valid` K rows and V rows
+                    // (the slots past ctx are never read: their scores are masked, their V rows
+                    // skipped), so no page padding crosses HBM -- ~2 % of the KV stream at the
+                    // 7B trace's mean context
+                    const uint32_t half = static_cast<uint32_t>(valid) * D * sizeof(T);
+                    mbar_expect_tx(&bars[warp][s], 2 * half);
+                    bulk_g2s(wbuf + s * TILE, src, half, &bars[warp][s], pol);
+                    bulk_g2s(wbuf + s * TILE + TILE / 2, src + TILE / 2, half, &bars[warp][s], pol);
+                }
             }
             ++seq_iss;
         }
