@@ -74,7 +74,7 @@ constexpr int kBox = 16 * 128;  // one TMA box: 16 rows x 64 elements (128 B), 1
 
 template <typename T, int D, int GQ, int WARPS, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32)
-decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap) {
+decode_gqa_kernel(const DecodeParams p, const __grid_constant__ GqaMaps tmap) {
     constexpr int NBOX = D / 64;            // boxes per K (or V) tile of one page
     constexpr int STAGE = 2 * NBOX * kBox;  // K boxes, then V boxes
     constexpr int KSTEPS = D / 16;
@@ -114,32 +114,46 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ CUtensorMap tmap
     auto top_up = [&](uint32_t seq_cons) {
         while (seq_iss < seq_cons + STAGES) {
             const int j = static_cast<int>(seq_iss - cur_start);
-            int ph, g, lay;
+            int ph, g, lay, valid;
             if (j < cur.it.n) {
                 ph = page_of(cur, j);
                 g = cur.g;
                 lay = cur.l;
+                valid = cur.it.ctx - (cur.it.pg0 + j) * kP;
             } else if (j - cur.it.n < nxt.it.n) {
                 ph = page_of(nxt, j - cur.it.n);
                 g = nxt.g;
                 lay = nxt.l;
+                valid = nxt.it.ctx - (nxt.it.pg0 + j - cur.it.n) * kP;
             } else {
                 break;
             }
             if (lane == 0) {
                 const int s = seq_iss % STAGES;
                 fence_proxy_async();
-                mbar_expect_tx(&bars[warp][s], STAGE);
                 const int64_t row_layer = static_cast<int64_t>(p.layer + lay) * p.cap_pages;
                 const int tile = static_cast<int>((row_layer + ph) * p.kv_heads + g);
-                if (p.tma_rank == 5) {
-                    tma_load_tile5(wbuf + s * STAGE, &tmap, tile, &bars[warp][s], pol);
-                } else {
+                if (valid <= kP / 2 && p.half_boxes) {
+                    // a request's last page holding <= 8 tokens: its first 8 K rows and V rows
+                    // only (one 1024-byte swizzle atom per d-half), so most page padding stays
+                    // off the HBM stream; rows 8-15 are masked (K) and zeroed (V) below
+                    mbar_expect_tx(&bars[warp][s], STAGE / 2);
 #pragma unroll
                     for (int kv = 0; kv < 2; ++kv)
 #pragma unroll
                         for (int b = 0; b < NBOX; ++b)
-                            tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox, &tmap, b * 64, tile * 32 + kv * 16,
+                            tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox, &tmap.half, b * 64,
+                                        tile * 32 + kv * 16, &bars[warp][s], pol);
+                } else if (p.tma_rank == 5) {
+                    mbar_expect_tx(&bars[warp][s], STAGE);
+                    tma_load_tile5(wbuf + s * STAGE, &tmap.full, tile, &bars[warp][s], pol);
+                } else {
+                    mbar_expect_tx(&bars[warp][s], STAGE);
+#pragma unroll
+                    for (int kv = 0; kv < 2; ++kv)
+#pragma unroll
+                        for (int b = 0; b < NBOX; ++b)
+                            tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox, &tmap.full, b * 64, tile * 32 + kv * 16,
                                         &bars[warp][s], pol);
                 }
             }
@@ -309,7 +323,7 @@ constexpr size_t gqa_smem() {
 }
 
 template <typename T, int D, int GQ>
-cudaError_t launch_gqa_t(const DecodeParams &p, int ctas, const CUtensorMap &tmap, cudaStream_t s) {
+cudaError_t launch_gqa_t(const DecodeParams &p, int ctas, const GqaMaps &tmap, cudaStream_t s) {
     auto kern = decode_gqa_kernel<T, D, GQ, kWarps, gqa_stages<D>()>;
     constexpr size_t smem = gqa_smem<T, D>();
     static bool configured = false;
@@ -334,7 +348,7 @@ int gqa_occ_t() {
 // Tuning variants of the (warps per CTA, ring stages) trade-off for GQ = 8 (DBK_GQA_WS =
 // "2x6" or "8x3"; default 4x3): same shared memory per SM, different warps vs depth.
 template <typename T, int D, int GQ, int W, int S>
-cudaError_t launch_gqa_v(const DecodeParams &p, const CUtensorMap &tmap, cudaStream_t s) {
+cudaError_t launch_gqa_v(const DecodeParams &p, const GqaMaps &tmap, cudaStream_t s) {
     auto kern = decode_gqa_kernel<T, D, GQ, W, S>;
     constexpr size_t smem = static_cast<size_t>(W) * S * 2 * (D / 64) * kBox + 1024;
     static int occ = -1, sms = 148;
@@ -366,7 +380,7 @@ int gqa_variant() {
 }
 
 template <typename T, int D>
-cudaError_t gqa_group(const DecodeParams &p, int group, int ctas, const CUtensorMap &tmap, cudaStream_t s) {
+cudaError_t gqa_group(const DecodeParams &p, int group, int ctas, const GqaMaps &tmap, cudaStream_t s) {
     switch (group) {
         case 2: return launch_gqa_t<T, D, 2>(p, ctas, tmap, s);
         case 4: return launch_gqa_t<T, D, 4>(p, ctas, tmap, s);
@@ -393,7 +407,7 @@ int gqa_occ_group(int group) {
 }  // namespace
 
 cudaError_t launch_decode_gqa(const DecodeParams &p, int kv_dtype, int head_dim, int group, int ctas,
-                              const CUtensorMap &tmap, cudaStream_t s) {
+                              const GqaMaps &tmap, cudaStream_t s) {
     if (kv_dtype == 0) {
         if (head_dim == 128) return gqa_group<__half, 128>(p, group, ctas, tmap, s);
         if (head_dim == 64) return gqa_group<__half, 64>(p, group, ctas, tmap, s);

@@ -334,9 +334,9 @@ int occ_by_group(int group) {
 }  // namespace
 
 cudaError_t launch_decode(const DecodeParams &p, int kv_dtype, int head_dim, int group, int ctas,
-                          const CUtensorMap *tmap, cudaStream_t s) {
+                          const GqaMaps *maps, cudaStream_t s) {
     if (p.n_tasks <= 0) return cudaSuccess;
-    if (tmap && group >= 2) return launch_decode_gqa(p, kv_dtype, head_dim, group, ctas, *tmap, s);
+    if (maps && group >= 2) return launch_decode_gqa(p, kv_dtype, head_dim, group, ctas, *maps, s);
     if (kv_dtype == 0) {
         if (head_dim == 128) return by_group<__half, 128>(p, group, ctas, s);
         if (head_dim == 64) return by_group<__half, 64>(p, group, ctas, s);

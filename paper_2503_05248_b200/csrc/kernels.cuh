@@ -73,6 +73,8 @@ struct DecodeParams {
     int32_t n_tasks;
     int32_t *task_counter;
     int32_t tma_rank;            // K2: 5 = one 5-D box per tile, 2 = 2-D boxes of 16 x 64
+    int32_t half_boxes;          // K2: 1 = GqaMaps::half (8-token boxes) is valid: a last page
+                                 //  holding <= 8 tokens moves only its first 8 K / V rows
     // 1: programmatic dependent launch after the previous decode launch on the stream (its
     // scratch -- split-K workspace, arrival and task counters -- is the other parity's);
     // 2: programmatic dependent launch after the kernel that wrote q / the new K/V: every warp
@@ -154,13 +156,22 @@ struct PrefillParams {
     float scale_log2;
 };
 
+// K2's tensor maps over the pool: `full` moves one (page, kv head) tile (5-D: one box; 2-D: boxes
+// of 16 rows x 64 elements), `half` boxes of 8 rows x 64 elements (2-D, 128B-swizzled: each lands
+// on one 1024-byte swizzle atom of the full tile's layout) for a request's last page when it
+// holds <= 8 tokens.
+struct GqaMaps {
+    CUtensorMap full;
+    CUtensorMap half;
+};
+
 // launchers (return cudaGetLastError() of the launch)
-// tmap != nullptr and group >= 2 selects K2 (tensor cores); otherwise K1 (CUDA cores).
+// maps != nullptr and group >= 2 selects K2 (tensor cores); otherwise K1 (CUDA cores).
 // Persistent launch of min(ctas, p.n_tasks) CTAs (ctas = SMs x resident CTAs per SM).
 cudaError_t launch_decode(const DecodeParams &p, int kv_dtype, int head_dim, int group,
-                          int ctas, const CUtensorMap *tmap, cudaStream_t s);
+                          int ctas, const GqaMaps *maps, cudaStream_t s);
 cudaError_t launch_decode_gqa(const DecodeParams &p, int kv_dtype, int head_dim, int group,
-                              int ctas, const CUtensorMap &tmap, cudaStream_t s);
+                              int ctas, const GqaMaps &maps, cudaStream_t s);
 int decode_gqa_ctas_per_sm(int kv_dtype, int head_dim, int group);
 cudaError_t launch_append(const AppendParams &p, int kv_dtype, int head_dim, cudaStream_t s);
 cudaError_t launch_bt_apply(int32_t *bt, int32_t stride, const BtDelta *d, int32_t n,

@@ -108,7 +108,7 @@ using namespace dbk;
 
 // K2's tensor map over the whole pool: a 2-D tensor of rows = layers*cap*kv_heads*2*16
 // token rows x head_dim elements; one box = 16 rows x 64 elements with the 128-byte swizzle.
-static bool make_pool_tmap(dbk_pool *p, bool try5, CUtensorMap *dst, int *rank) {
+static bool make_pool_tmap(dbk_pool *p, bool try5, CUtensorMap *dst, int *rank, uint32_t box_rows = 16) {
     const dbk_pool_config &c = p->cfg;
     const uint64_t tiles = static_cast<uint64_t>(c.layers) * c.cap_pages * c.kv_heads;  // (layer, page, head)
     if (tiles * 2 * c.page_size >= (1ull << 31)) return false;  // int32 TMA coordinates
@@ -141,7 +141,7 @@ static bool make_pool_tmap(dbk_pool *p, bool try5, CUtensorMap *dst, int *rank) 
     // Fallback: 2-D rows x d, boxes of 16 rows x 64 elements (2 * d/64 boxes per tile).
     const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(c.head_dim), tiles * 2 * c.page_size};
     const cuuint64_t gstride[1] = {row};
-    const cuuint32_t box[2] = {64, 16};
+    const cuuint32_t box[2] = {64, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode(dst, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->kv, gdim, gstride, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -231,6 +231,11 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     const char *t2 = std::getenv("DBK_GQA_TMA2");  // 1: force the 2-D boxes (comparison runs)
     if (group >= 2 && !(cc && cc[0] == '1'))
         p->has_tmap = make_pool_tmap(p, !(t2 && t2[0] == '1'), &p->tmap, &p->tma_rank);
+    if (p->has_tmap) {  // 8-row boxes for short last pages (DBK_GQA_HALF=0: off, comparison runs)
+        const char *hb = std::getenv("DBK_GQA_HALF");
+        int r2 = 0;
+        p->has_tmap_half = !(hb && hb[0] == '0') && make_pool_tmap(p, false, &p->tmap_half, &r2, 8);
+    }
     int prank = 0;
     p->has_ptmap = make_pool_tmap(p, true, &p->ptmap, &prank);
     p->ctas_per_sm = p->has_tmap ? decode_gqa_ctas_per_sm(cfg->kv_dtype, cfg->head_dim, group)
@@ -864,6 +869,7 @@ static dbk_status decode_launch(dbk_pool *p, int32_t n, int32_t layer0, int32_t 
     dp.n_tasks = p->meta_items * p->cfg.kv_heads * nl;
     dp.task_counter = p->d_task_counter + 2 * par;
     dp.tma_rank = p->tma_rank;
+    dp.half_boxes = p->has_tmap_half ? 1 : 0;
     dp.pdl = !p->pdl_enabled ? 0 : (chain == 2 ? 2 : ((chain == 1 && !stats) ? 1 : 0));
     dp.seq = ++p->decode_seq;
     dp.done_seq = p->d_done_seq;
@@ -872,8 +878,13 @@ static dbk_status decode_launch(dbk_pool *p, int32_t n, int32_t layer0, int32_t 
     dp.trace_seq = static_cast<int32_t>(p->n_launches);
     // persistent grid: every resident CTA slot (4 warps each), or fewer for small batches
     const int ctas = std::max(1, std::min(p->num_sms * p->ctas_per_sm, (dp.n_tasks + 3) / 4));
+    GqaMaps maps;
+    if (p->has_tmap) {
+        maps.full = p->tmap;
+        maps.half = p->has_tmap_half ? p->tmap_half : p->tmap;
+    }
     DBK_CUDA(launch_decode(dp, p->cfg.kv_dtype, p->cfg.head_dim, p->cfg.q_heads / p->cfg.kv_heads, ctas,
-                           p->has_tmap ? &p->tmap : nullptr, s));
+                           p->has_tmap ? &maps : nullptr, s));
     ++p->n_launches;
     p->launch_parity ^= 1;
     return DBK_OK;

@@ -103,6 +103,8 @@ struct dbk_pool {
     // pool-wide 2-D tensor map (rows of head_dim elements, 16 x 64 boxes, 128B swizzle) for K2
     alignas(64) CUtensorMap tmap;
     bool has_tmap = false;
+    alignas(64) CUtensorMap tmap_half;  // K2: 8-row boxes for last pages holding <= 8 tokens
+    bool has_tmap_half = false;
     int tma_rank = 0;                         // 5: one box per tile; 2: 2*d/64 boxes per tile
     // K7 (chunked prefill, any group size): always the 5-D one-box-per-tile map
     alignas(64) CUtensorMap ptmap;
