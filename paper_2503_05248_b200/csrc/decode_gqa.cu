@@ -71,6 +71,7 @@ __device__ __forceinline__ void mma_pad(float d[4], uint32_t a0, uint32_t a2, ui
 }
 
 constexpr int kBox = 16 * 128;  // one TMA box: 16 rows x 64 elements (128 B), 128B-swizzled
+constexpr int kPartRows = 4;    // rows per box of the partial-page map (GqaMaps::half)
 
 template <typename T, int D, int GQ, int WARPS, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32)
@@ -133,17 +134,21 @@ decode_gqa_kernel(const DecodeParams p, const __grid_constant__ GqaMaps tmap) {
                 fence_proxy_async();
                 const int64_t row_layer = static_cast<int64_t>(p.layer + lay) * p.cap_pages;
                 const int tile = static_cast<int>((row_layer + ph) * p.kv_heads + g);
-                if (valid <= kP / 2 && p.half_boxes) {
-                    // a request's last page holding <= 8 tokens: its first 8 K rows and V rows
-                    // only (one 1024-byte swizzle atom per d-half), so most page padding stays
-                    // off the HBM stream; rows 8-15 are masked (K) and zeroed (V) below
-                    mbar_expect_tx(&bars[warp][s], STAGE / 2);
+                if (valid <= kP - kPartRows && p.half_boxes) {
+                    // a request's last, partly filled page: only its first ceil(valid / 4) x 4 K
+                    // rows and V rows (4-row boxes of a second tensor map; the 128B swizzle is a
+                    // function of the shared-memory address, so each box lands where the full
+                    // tile would put those rows), so page padding stays off the HBM stream; rows
+                    // >= valid are masked (K) and zeroed (V) below
+                    const int nb = (valid + kPartRows - 1) / kPartRows;
+                    mbar_expect_tx(&bars[warp][s], 2 * NBOX * nb * kPartRows * 128);
 #pragma unroll
                     for (int kv = 0; kv < 2; ++kv)
 #pragma unroll
                         for (int b = 0; b < NBOX; ++b)
-                            tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox, &tmap.half, b * 64,
-                                        tile * 32 + kv * 16, &bars[warp][s], pol);
+                            for (int r = 0; r < nb; ++r)
+                                tma_load_2d(wbuf + s * STAGE + (kv * NBOX + b) * kBox + r * kPartRows * 128, &tmap.half,
+                                            b * 64, tile * 32 + kv * 16 + r * kPartRows, &bars[warp][s], pol);
                 } else if (p.tma_rank == 5) {
                     mbar_expect_tx(&bars[warp][s], STAGE);
                     tma_load_tile5(wbuf + s * STAGE, &tmap.full, tile, &bars[warp][s], pol);

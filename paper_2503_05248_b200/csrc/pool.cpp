@@ -231,10 +231,10 @@ dbk_status dbk_kv_pool_create(const dbk_pool_config *cfg, void *kv_mem, size_t k
     const char *t2 = std::getenv("DBK_GQA_TMA2");  // 1: force the 2-D boxes (comparison runs)
     if (group >= 2 && !(cc && cc[0] == '1'))
         p->has_tmap = make_pool_tmap(p, !(t2 && t2[0] == '1'), &p->tmap, &p->tma_rank);
-    if (p->has_tmap) {  // 8-row boxes for short last pages (DBK_GQA_HALF=0: off, comparison runs)
+    if (p->has_tmap) {  // 4-row boxes for partly filled last pages (DBK_GQA_HALF=0: off, comparison runs)
         const char *hb = std::getenv("DBK_GQA_HALF");
         int r2 = 0;
-        p->has_tmap_half = !(hb && hb[0] == '0') && make_pool_tmap(p, false, &p->tmap_half, &r2, 8);
+        p->has_tmap_half = !(hb && hb[0] == '0') && make_pool_tmap(p, false, &p->tmap_half, &r2, 4);
     }
     int prank = 0;
     p->has_ptmap = make_pool_tmap(p, true, &p->ptmap, &prank);
