@@ -29,5 +29,7 @@ for spec in ${SPECS:-7b 7b_pl 70b_tp1 70b_tp8 70b_tp8_pl 70b_tp4 70b_tp2 70b_tp8
     70b_tp8) run 70b_tp8_shard --config llama3-70b-gqa --tp-shard 8 ;;
     70b_tp8_r7) run 70b_tp8_rank7_shard --config llama3-70b-gqa --tp-shard 8 --tp-rank 7 ;;
     70b_tp8_pl) run 70b_tp8_shard_per_layer --config llama3-70b-gqa --tp-shard 8 --per-layer-launches ;;
+    7b_model) run 7b_model --model --steps 20 ;;
+    13b_model) run 13b_model --model --config llama2-13b-sla --steps 20 ;;
   esac
 done
