@@ -534,6 +534,8 @@ typedef struct dbk_step_record {
     int64_t swap_bytes;             /* bytes the swaps of this step moved (both directions)   */
 } dbk_step_record;
 
+/* The engine over a trace (arrivals sorted, lengths >= 1, request ids unique -- EINVAL
+ * otherwise); DBK_EFATAL when one request alone cannot fit the cap. */
 dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_config *cfg,
                              dbk_engine **out);
 dbk_status dbk_engine_destroy(dbk_engine *e);
@@ -556,7 +558,8 @@ dbk_status dbk_engine_last_batch(dbk_engine *e, int32_t *n, int64_t *req_ids, in
 /* Full-model mode (NEXT row 3): every decode step runs dbk_model_step (QKV / O /
  * MLP / LM-head GEMMs + the attention) instead of the synthetic-q attention; the
  * decode token's KV is written by the model (dbk_reserve_tokens + RoPE epilogue).
- * Device-resident, non-PD engines only; NULL detaches. */
+ * Device-resident, non-PD engines only; NULL detaches.  EINVAL if the model was created on
+ * another pool than the engine's. */
 dbk_status dbk_engine_attach_model(dbk_engine *e, dbk_model *model);
 /* Per-request timeline on the engine clock (ns), for trace index i < n (host
  * arrays, nullable): first_admit_ns[i] = clock of the step that first admitted

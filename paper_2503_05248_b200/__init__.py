@@ -333,8 +333,8 @@ class Engine:
         _lib.dbk_engine_attach_mbox(self.h, mbox.h if mbox is not None else None, int(mode))
 
     def attach_model(self, model):
-        self.model = model
         _lib.dbk_engine_attach_model(self.h, model.h if model is not None else None)
+        self.model = model
 
     @staticmethod
     def buffers(q_dev, out_dev, kv_dev=None, host_q=None, host_k=None, host_v=None, host_out=None,

@@ -152,6 +152,12 @@ dbk_status dbk_engine_create(dbk_pool *pool, dbk_sched *sched, const dbk_engine_
         return fail(DBK_EINVAL, "engine_create: pd_token_budget needs pd_fusion and must be >= 0");
     if (c.preempt_mode == 1 && (c.pd_fusion || !pool->swap_host))
         return fail(DBK_EINVAL, "engine_create: swap preemption needs an attached swap space and pd_fusion = 0");
+    if (c.req_ids) {  // the pool keys requests by id: a trace naming one twice would collide mid-run
+        std::vector<int64_t> sorted(c.req_ids, c.req_ids + c.n_requests);
+        std::sort(sorted.begin(), sorted.end());
+        if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+            return fail(DBK_EINVAL, "engine_create: duplicate request id in the trace");
+    }
     for (int i = 0; i < c.n_requests; ++i) {
         if (c.l_in[i] < 1 || c.l_out[i] < 1) return fail(DBK_EINVAL, "engine_create: lengths must be >= 1");
         if (i && c.arrival_ns[i] < c.arrival_ns[i - 1]) return fail(DBK_EINVAL, "engine_create: arrivals must be sorted");
@@ -213,6 +219,9 @@ dbk_status dbk_engine_done(dbk_engine *e, int32_t *done) {
 
 dbk_status dbk_engine_attach_model(dbk_engine *e, dbk_model *m) {
     if (!e) return fail(DBK_EINVAL, "attach_model: null engine");
+    // the model's QKV epilogue writes the decode tokens' K/V into its own pool's pages, which
+    // must be the pages this engine allocates
+    if (m && model_pool(m) != e->pool) return fail(DBK_EINVAL, "attach_model: the model was created on another pool");
     e->model = m;
     return DBK_OK;
 }

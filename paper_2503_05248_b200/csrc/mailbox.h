@@ -17,6 +17,8 @@ dbk_status mbox_launch(dbk_mbox *m, const unsigned long long *d_stats, bool empt
 // after the stream has synchronised: the gathered records (rank order), or the timeout error
 dbk_status mbox_collect(dbk_mbox *m, dbk_stats *all);
 int32_t mbox_nranks(const dbk_mbox *m);
+// model.cu: the pool a model was created on
+dbk_pool *model_pool(const dbk_model *m);
 int32_t mbox_rank(const dbk_mbox *m);
 
 }  // namespace dbk

@@ -354,6 +354,11 @@ dbk_status collect_timing(dbk_model *m) {
 
 }  // namespace
 
+namespace dbk {
+// the pool whose KV the model's QKV epilogue writes (the engine checks it is its own)
+dbk_pool *model_pool(const dbk_model *m) { return m->pool; }
+}  // namespace dbk
+
 extern "C" {
 
 size_t dbk_model_weight_bytes(const dbk_pool_config *pc, const dbk_model_config *c) {

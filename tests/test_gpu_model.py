@@ -399,3 +399,24 @@ def test_model_step_split_k_epilogues(dbk):
     assert row_err(logits.cpu().numpy(), want2, "logits_split_step2") <= MODEL_TOL
     model.close()
     pool.close()
+
+
+def test_engine_rejects_a_foreign_model_and_duplicate_trace_ids(dbk):
+    """dbk_engine_attach_model: the model's QKV epilogue writes K/V into its OWN pool's pages, so
+    a model created on another pool is EINVAL; dbk_engine_create: request ids name pool entries,
+    so a trace naming one twice is EINVAL up front (it used to collide mid-run)."""
+    pool_a = dbk.KVPool(1, 4, 4, 64, 64, 8, 8, "f16")
+    pool_b = dbk.KVPool(1, 4, 4, 64, 64, 8, 8, "f16")
+    sched = dbk.Scheduler(policy=1, b_max=8, bytes_per_token=2 * 4 * 64 * 2, page_size=16)
+    arr, lin, lout = [0, 0, 0], [4, 5, 6], [3, 3, 3]
+    eng = dbk.Engine(pool_a, sched, arr, lin, lout, 64 * 16 * 2 * 4 * 64 * 2)
+    model_b = dbk.Model(pool_b, 256, 512, 128, max_pos=64)
+    with pytest.raises(dbk.DbkError) as e:
+        eng.attach_model(model_b)
+    assert e.value.status == dbk._lib.DBK_EINVAL
+    with pytest.raises(dbk.DbkError) as e:
+        dbk.Engine(pool_a, sched, arr, lin, lout, 64 * 16 * 2 * 4 * 64 * 2, req_ids=[5, 9, 5])
+    assert e.value.status == dbk._lib.DBK_EINVAL
+    for o in (model_b, eng, pool_a, pool_b):
+        if hasattr(o, "close"):
+            o.close()
