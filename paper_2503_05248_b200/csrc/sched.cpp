@@ -186,6 +186,21 @@ dbk_status dbk_choose_batch_size(dbk_sched *s, const dbk_stats *g, int64_t mem_c
     if (g->n_active < 0 || g->n_finished < 0 || g->n_finished > g->n_active || n_prefill < 0)
         return dbk::fail(DBK_EINVAL, "choose_batch_size: inconsistent statistics");
     const dbk_sched_config &c = s->cfg;
+    // every check before any state changes: a rejected call leaves the windows and bounds as
+    // they were
+    if ((c.policy == DBK_POLICY_MEMORY || c.policy == DBK_POLICY_COMBINED) && mem_cap_bytes < 0)
+        return dbk::fail(DBK_EINVAL, "choose_batch_size: mem_cap_bytes < 0");
+    if (!std::isfinite(sla_ms)) return dbk::fail(DBK_EINVAL, "choose_batch_size: sla_ms must be finite (<= 0: the configured D_SLA)");
+    if (g->n_active > 0 && g->step_ns < 0) return dbk::fail(DBK_EINVAL, "choose_batch_size: step_ns < 0");
+    if (g->n_finished > 0) {
+        // lengths are >= 1, so sum >= count and sum of squares >= sum; and n * sum(l^2) >= sum(l)^2
+        const i128 nf = g->n_finished;
+        if (g->fin_sum_lin < g->n_finished || g->fin_sum_lout < g->n_finished || g->fin_sum_lin_sq < g->fin_sum_lin ||
+            g->fin_sum_lout_sq < g->fin_sum_lout ||
+            nf * g->fin_sum_lin_sq < static_cast<i128>(g->fin_sum_lin) * g->fin_sum_lin ||
+            nf * g->fin_sum_lout_sq < static_cast<i128>(g->fin_sum_lout) * g->fin_sum_lout)
+            return dbk::fail(DBK_EINVAL, "choose_batch_size: inconsistent finishing-request sums");
+    }
     // telemetry windows
     if (g->n_finished > 0 && (c.policy == DBK_POLICY_MEMORY || c.policy == DBK_POLICY_COMBINED))
         s->push_window({g->n_finished, g->fin_sum_lin, g->fin_sum_lin_sq, g->fin_sum_lout, g->fin_sum_lout_sq});
@@ -209,7 +224,6 @@ dbk_status dbk_choose_batch_size(dbk_sched *s, const dbk_stats *g, int64_t mem_c
         return DBK_OK;
     }
     if (c.policy == DBK_POLICY_MEMORY || c.policy == DBK_POLICY_COMBINED) {
-        if (mem_cap_bytes < 0) return dbk::fail(DBK_EINVAL, "mem_cap_bytes < 0");
         const int64_t cap_pages = mem_cap_bytes / (static_cast<int64_t>(c.page_size) * c.bytes_per_token);
         s->eta = cap_pages * c.page_size;  // R4: eta in tokens
         int64_t n, S, V2;

@@ -151,3 +151,28 @@ def test_ctypes_struct_layouts_match_the_header(tmp_path):
         assert int(out[st.__name__]) == ctypes.sizeof(st), st.__name__
         for f, _ in st._fields_:
             assert int(out[f"{st.__name__}.{f}"]) == getattr(st, f).offset, (st.__name__, f)
+
+
+def test_rejected_decisions_change_no_scheduler_state(dbk):
+    """dbk_choose_batch_size checks everything before it touches its windows: a negative memory
+    cap, a non-finite SLA target, a negative step time or finishing-request sums no lengths >= 1
+    can produce (sum < count, sum(l^2) < sum(l), n sum(l^2) < sum(l)^2) are DBK_EINVAL, and the
+    next valid call decides exactly as if the rejected ones had never happened."""
+    kw = dict(policy=3, b_min=1, b_max=512, b0=1, bytes_per_token=512 * 1024, page_size=16, d_sla_ms=20.0,
+              eps_d_ms=1.0)
+    good = dict(n_active=40, sum_ctx=40 * 300, n_finished=2, fin_sum_lin=300, fin_sum_lin_sq=50000,
+                fin_sum_lout=500, fin_sum_lout_sq=130000, step_ns=15_000_000)
+    cap = 100 * 2 ** 30
+    bad = [(dict(good), dict(mem_cap_bytes=-1)), (dict(good), dict(sla_ms=float("nan"))),
+           (dict(good, step_ns=-5), {}), (dict(good, fin_sum_lin=1), {}), (dict(good, fin_sum_lout_sq=400), {}),
+           (dict(good, fin_sum_lin=300, fin_sum_lin_sq=300), {})]
+    a, b = dbk.Scheduler(**kw), dbk.Scheduler(**kw)
+    for step in range(5):
+        for st, args in bad:
+            with pytest.raises(dbk.DbkError) as e:
+                a.choose(st, args.get("mem_cap_bytes", cap), sla_ms=args.get("sla_ms", 0.0))
+            assert e.value.status == dbk._lib.DBK_EINVAL
+        assert a.choose(good, cap) == b.choose(good, cap)
+        assert a.state() == b.state()
+    a.close()
+    b.close()
