@@ -216,6 +216,9 @@ dbk_status dbk_mbox_open(dbk_mbox *m, const void *handles) {
         const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) {
             cudaGetLastError();
+            // nothing stays mapped: a failed open leaves the mailbox as created (retry-able)
+            for (void *q : m->opened) cudaIpcCloseMemHandle(q);
+            m->opened.clear();
             return dbk::fail(DBK_ECUDA, "mbox_open: cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
         }
         m->opened.push_back(ptr);

@@ -136,6 +136,9 @@ dbk_status dbk_tp_open(dbk_tp *t, const void *handles) {
         const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) {
             cudaGetLastError();
+            // nothing stays mapped: a failed open leaves the handle as created (retry-able)
+            for (void *q : t->opened) cudaIpcCloseMemHandle(q);
+            t->opened.clear();
             return dbk::fail(DBK_ECUDA, "tp_open: cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
         }
         t->opened.push_back(ptr);
