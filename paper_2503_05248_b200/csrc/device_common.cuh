@@ -128,13 +128,20 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
     return z ^ (z >> 31);
 }
-__device__ __forceinline__ uint64_t synth_key(uint64_t seed, int kind, int64_t req, int pos,
-                                              int layer, int head, int g) {
-    uint64_t k1 = splitmix64(seed ^ (static_cast<uint64_t>(kind) << 56) ^ static_cast<uint64_t>(req));
+// synth_key = synth_key2(synth_key1(seed, kind, req), pos, layer, head, g): kernels that generate
+// many values of one (kind, request) hoist the first hash out of their loops
+__device__ __forceinline__ uint64_t synth_key1(uint64_t seed, int kind, int64_t req) {
+    return splitmix64(seed ^ (static_cast<uint64_t>(kind) << 56) ^ static_cast<uint64_t>(req));
+}
+__device__ __forceinline__ uint64_t synth_key2(uint64_t k1, int pos, int layer, int head, int g) {
     uint64_t w = (static_cast<uint64_t>(static_cast<uint32_t>(pos)) << 32) |
                  (static_cast<uint64_t>(layer) << 20) | (static_cast<uint64_t>(head) << 8) |
                  static_cast<uint64_t>(g);
     return splitmix64(k1 ^ w);
+}
+__device__ __forceinline__ uint64_t synth_key(uint64_t seed, int kind, int64_t req, int pos,
+                                              int layer, int head, int g) {
+    return synth_key2(synth_key1(seed, kind, req), pos, layer, head, g);
 }
 __device__ __forceinline__ void synth_vals(uint64_t key, float scale, float f[8]) {
 #pragma unroll

@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "device_common.cuh"
 #include "kernels.cuh"
 
@@ -24,6 +26,9 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
     uint8_t *page = p.kv + static_cast<size_t>(layer) * p.layer_stride +
                     static_cast<size_t>(job.phys) * p.page_stride;
     const float scale = 1.0f / 128.0f;
+    // the request's first hash of K (kind 1) and V (kind 2), once per thread
+    const uint64_t k1k = job.src_row < 0 ? synth_key1(p.seed, 1, job.req_id) : 0;
+    const uint64_t k1v = job.src_row < 0 ? synth_key1(p.seed, 2, job.req_id) : 0;
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
         const int v = idx % VPR;
         int r = idx / VPR;
@@ -36,7 +41,7 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendParams p) {
         uint4 val;
         if (job.src_row < 0) {
             float f[8];
-            synth_vals(synth_key(p.seed, 1 + kv, job.req_id, pos, layer, p.head0 + head, v), scale, f);
+            synth_vals(synth_key2(kv ? k1v : k1k, pos, layer, p.head0 + head, v), scale, f);
             val = pack8<T>(f);
         } else {
             const size_t srow = p.src_layer_rows > 0
@@ -90,23 +95,23 @@ __global__ void synth_rows_kernel(uint64_t seed, int kind, int n_rows, const int
 
 // q of every layer for the batch in `req`: q[l][i][h][:] = synth(seed, q, req_i, ctx_i - 1, l, h),
 // layer l at q + l * layer_rows rows (one launch per step).
-__global__ void synth_q_kernel(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
-                               int q_heads, int head0, int d, float scale, int dtype, void *q) {
-    const int vpr = d / 8;
-    const long per_layer = static_cast<long>(n) * q_heads * vpr;
-    const long total = per_layer * layers;
-    for (long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; k < total;
-         k += static_cast<long>(gridDim.x) * blockDim.x) {
-        const int l = static_cast<int>(k / per_layer);
-        const long kk = k % per_layer;
-        const int v = static_cast<int>(kk % vpr);
-        const long rh = kk / vpr;
-        const int h = static_cast<int>(rh % q_heads);
-        const int r = static_cast<int>(rh / q_heads);
+// block (row chunk, layer): the chunk's rows one after the other, the threads over (head, 8-value
+// group) -- no 64-bit index divisions, and the request's first hash once per row
+__global__ void __launch_bounds__(256) synth_q_kernel(uint64_t seed, const ReqMeta *req, int n, int rows_per_block,
+                                                      int layer_rows, int q_heads, int head0, int vshift, float scale,
+                                                      int dtype, void *q) {
+    const int l = blockIdx.y;
+    const int hv = q_heads << vshift, d = 8 << vshift;
+    const int r1 = min(n, (static_cast<int>(blockIdx.x) + 1) * rows_per_block);
+    for (int r = blockIdx.x * rows_per_block; r < r1; ++r) {
         const ReqMeta rm = req[r];
-        float f[8];
-        synth_vals(synth_key(seed, 0, rm.req_id, rm.ctx - 1, l, head0 + h, v), scale, f);
-        store8(q, (static_cast<size_t>(l) * layer_rows * q_heads + rh) * d + v * 8, dtype, f);
+        const uint64_t k1 = synth_key1(seed, 0, rm.req_id);
+        for (int t = threadIdx.x; t < hv; t += blockDim.x) {
+            const int h = t >> vshift, v = t & ((1 << vshift) - 1);
+            float f[8];
+            synth_vals(synth_key2(k1, rm.ctx - 1, l, head0 + h, v), scale, f);
+            store8(q, ((static_cast<size_t>(l) * layer_rows + r) * q_heads + h) * d + v * 8, dtype, f);
+        }
     }
 }
 
@@ -182,10 +187,14 @@ cudaError_t launch_synth_rows_layers(uint64_t seed, int kind, int n_rows, const 
 
 cudaError_t launch_synth_q(uint64_t seed, const ReqMeta *req, int n, int layers, int layer_rows,
                            int q_heads, int head0, int d, int scale_log2, int dtype, void *q, cudaStream_t s) {
-    const long work = static_cast<long>(n) * layers * q_heads * (d / 8);
-    if (work <= 0) return cudaSuccess;
-    synth_q_kernel<<<grid_for(work, 256), 256, 0, s>>>(seed, req, n, layers, layer_rows, q_heads, head0, d,
-                                                       ldexpf(1.0f, scale_log2 - 7), dtype, q);
+    if (n <= 0 || layers <= 0) return cudaSuccess;
+    if (d != 64 && d != 128) return cudaErrorInvalidValue;
+    const int vshift = d == 128 ? 4 : 3;
+    // ~4 row blocks per SM over all layers, at least one row each
+    const int rows_per_block = std::max(1, std::min(n, (n * layers + 148 * 4 - 1) / (148 * 4)));
+    const dim3 grid((n + rows_per_block - 1) / rows_per_block, layers);
+    synth_q_kernel<<<grid, 256, 0, s>>>(seed, req, n, rows_per_block, layer_rows, q_heads, head0, vshift,
+                                        ldexpf(1.0f, scale_log2 - 7), dtype, q);
     return cudaGetLastError();
 }
 
