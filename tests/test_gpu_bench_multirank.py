@@ -25,21 +25,22 @@ def _port():
 
 
 @pytest.mark.parametrize("config,par,exchange", [("llama2-7b", "dp2", "mailbox"), ("llama3-70b-gqa", "tp2", "mailbox"),
-                                                 ("llama2-7b", "dp2", "nccl")])
+                                                 ("llama2-7b", "dp2", "nccl"), ("llama2-7b", "dp4", "mailbox")])
 def test_bench_two_ranks_counts_tokens_once(config, par, exchange):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     env = dict(os.environ, DBK_BENCH_TEST_GLOO="1", DBK_BENCH_KV_GB="12")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    world = int(par[2:])
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "6", "--warmup", "3", "--ff", "30", "--config", config, "--exchange", exchange]
+           "--gpus", str(world), "--steps", "6", "--warmup", "3", "--ff", "30", "--config", config, "--exchange", exchange]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["steps"] == 6
+    assert d["n_gpus"] == world and d["steps"] == 6
     assert par in d["config"]["parallelism"]
     per_step = d["config"]["mean_batch"] / (d["ms_per_step"] / 1e3)
     assert abs(d["value"] - per_step) / per_step < 0.01, (d["value"], per_step)
@@ -47,6 +48,6 @@ def test_bench_two_ranks_counts_tokens_once(config, par, exchange):
     x = d["config"]["stats_exchange"]
     if exchange == "mailbox":  # the product exchange ran (the ranks share the GPU: IPC-mapped mailboxes)
         assert x["kind"].startswith("libdbk mailbox") and x["exchanges"] >= 6, x
-        assert len(x["last_step_ns_per_rank"]) == 2 and min(x["last_step_ns_per_rank"]) > 0
+        assert len(x["last_step_ns_per_rank"]) == world and min(x["last_step_ns_per_rank"]) > 0
     else:
         assert "gloo" in x["kind"]
