@@ -574,3 +574,40 @@ def test_release_is_all_or_nothing(dbk):
     pool.release([2, 1])
     assert pool.usage() == (0, 16)
     pool.close()
+
+
+def test_decode_and_prefill_argument_checks(dbk):
+    """The C-ABI's argument contract (include/dbk.h): a layer out of range, an unknown output
+    dtype, misaligned q / out, a chunk outside the tokens a request holds, a request begun twice
+    -- DBK_EINVAL / DBK_ENOENT, nothing launched, nothing written; the pool keeps working."""
+    E = dbk._lib
+    pool = dbk.KVPool(2, 8, 8, 64, 32, 4, 8, "f16")
+    pool.request_begin(1, 10, 10)
+    with pytest.raises(dbk.DbkError) as e:
+        pool.request_begin(1, 10, 10)
+    assert e.value.status == E.DBK_EINVAL
+    pool.append_tokens([1], [11], seed=4)
+    q = torch.zeros(1, 8, 64, dtype=torch.float16, device="cuda")
+    out = torch.full((1, 8, 64), float("nan"), dtype=torch.float32, device="cuda")
+    raw = torch.zeros(8 * 64 * 4 + 8, dtype=torch.uint8, device="cuda")
+    q_mis = raw[2:2 + 8 * 64 * 2].view(torch.float16)   # 2-byte aligned, not 16
+    bad = [lambda: pool.decode_step([1], 2, q, out),              # layer out of range
+           lambda: pool.decode_step([1], -1, q, out),
+           lambda: pool.decode_step([1], 0, q, out, out_dtype=3),  # no such output dtype
+           lambda: pool.decode_step([1], 0, q_mis, out),           # q not 16-byte aligned
+           lambda: pool.prefill_step([1], [5], [7], 0, q, out),    # chunk [5, 12) beyond the 11 tokens
+           lambda: pool.prefill_step([1], [0], [0], 0, q, out),    # empty chunk
+           lambda: pool.prefill_step([1], [0], [4], 2, q, out)]    # layer out of range
+    for f in bad:
+        with pytest.raises(dbk.DbkError) as e:
+            f()
+        assert e.value.status == E.DBK_EINVAL, e.value
+    with pytest.raises(dbk.DbkError) as e:
+        pool.prefill_step([9], [0], [1], 0, q, out)
+    assert e.value.status == E.DBK_ENOENT
+    torch.cuda.synchronize()
+    assert torch.isnan(out).all()
+    pool.decode_step([1], 1, q, out)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    pool.close()
