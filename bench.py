@@ -620,6 +620,10 @@ def run_gpu(args):
             if ems_t is not None else None,
             "gpu_launches": int(sum(r["launches"] for r in recs)),
             "clocks": clk.summary(),
+            # time between tokens of the timed steps: every running request gets one token per
+            # step, so a step's device-timed latency is its TBT (SURVEY §5 metrics)
+            "tbt_ms": {q: round(float(np.percentile([r["step_ns"] / 1e6 for r in recs], p)), 3)
+                       for q, p in (("p50", 50), ("p95", 95), ("p99", 99))} if recs else None,
         }
         if args.model:
             mc = c["model"]
@@ -633,6 +637,12 @@ def run_gpu(args):
             line["cpu_baseline"].update(oracle_sched_replay(S, ff_recs[:60]))
             line["cpu_baseline"].update(toy_step_oracle())
         print(json.dumps(line), flush=True)
+    if args.step_log:  # one JSON record per engine step of this rank, tagged by phase
+        path = args.step_log if world == 1 else f"{args.step_log}.rank{rank}"
+        with open(path, "w") as fh:
+            for phase, rr in (("fast_forward", ff_recs), ("timed", recs), ("e2e", erecs)):
+                for r in rr:
+                    fh.write(json.dumps(dict(r, phase=phase, rank=rank)) + "\n")
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -711,6 +721,9 @@ def main():
                     help="70B GQA: run rank 0's KV-head shard of a TP-G job on this one GPU (per-GPU kernel rate)")
     ap.add_argument("--tp-rank", type=int, default=0, help="with --tp-shard: which rank's KV-head shard")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end (host buffers) run (profiling)")
+    ap.add_argument("--step-log", default=None,
+                    help="write every engine step's record (t, b_t, n_decode, sum_ctx, pages, step_ns, "
+                         "admissions, preemptions, ...) as JSON lines here (per rank: PATH.rankR)")
     ap.add_argument("--exchange", default="mailbox", choices=["mailbox", "nccl"],
                     help="N > 1: the statistics exchange -- libdbk's mailbox over peer memory (default) or NCCL")
     ap.add_argument("--ncu-step", action="store_true",

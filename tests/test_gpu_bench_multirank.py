@@ -51,3 +51,25 @@ def test_bench_two_ranks_counts_tokens_once(config, par, exchange):
         assert len(x["last_step_ns_per_rank"]) == world and min(x["last_step_ns_per_rank"]) > 0
     else:
         assert "gloo" in x["kind"]
+
+
+def test_bench_step_log_and_tbt(tmp_path):
+    """SURVEY §5 metrics: --step-log writes one JSON record per engine step (fast-forward and timed
+    steps, tagged by phase) and the bench line carries the timed steps' TBT percentiles."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    log = tmp_path / "steps.jsonl"
+    env = dict(os.environ, DBK_BENCH_KV_GB="12")
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "4", "--warmup", "3", "--ff", "10",
+           "--no-cpu-baseline", "--no-e2e", "--step-log", str(log)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    t = d["tbt_ms"]
+    assert 0 < t["p50"] <= t["p95"] <= t["p99"]
+    rows = [json.loads(l) for l in log.read_text().splitlines()]
+    assert [x["phase"] for x in rows] == ["fast_forward"] * 10 + ["timed"] * 4
+    timed = [x for x in rows if x["phase"] == "timed"]
+    assert all(x["step_ns"] > 0 and x["n_decode"] > 0 and x["used_pages"] > 0 for x in timed)
+    assert [x["t"] for x in rows] == sorted(x["t"] for x in rows)
