@@ -83,3 +83,11 @@ def prior_record(cfg):
         vi, vo = (cv * mi) ** 2, (cv * mo) ** 2
     return dict(n=n, sum_lin=round(n * mi), sum_lin_sq=round(n * (vi + mi * mi)),
                 sum_lout=round(n * mo), sum_lout_sq=round(n * (vo + mo * mo)))
+
+
+if __name__ == "__main__":
+    # the configurations as JSON (SURVEY §5 "one JSON per BASELINE config"): python -m synth.configs [name]
+    import json
+    import sys
+    names = sys.argv[1:] or list(CONFIGS)
+    print(json.dumps({n: CONFIGS[n] for n in names}, indent=1, sort_keys=True))

@@ -30,3 +30,12 @@ def test_bench_dp_batch_bound_scales_with_the_shards():
     for n in (1, 2, 4, 8):
         assert bench.sched_kwargs(c, beta, dp_world=n)["b_max"] == n * c["b_max"]
     assert bench.sched_kwargs(c, beta)["b_max"] == c["b_max"]
+
+
+def test_config_json_export_matches_the_dictionaries():
+    """synth/configs.json (one JSON per BASELINE config) is `python -m synth.configs`
+    of the dictionaries the bench and the tests use -- regenerate it when they change."""
+    import json
+    from synth import configs
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "synth", "configs.json")
+    assert json.load(open(path)) == json.loads(json.dumps(configs.CONFIGS))
