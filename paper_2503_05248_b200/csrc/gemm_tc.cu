@@ -26,7 +26,9 @@
 // groups and every partial tile is added into the output by the TMA unit (cp.reduce.async.bulk
 // .add), so no wave is partly idle and no CTA waits for another; the other GEMMs run whole tiles
 // (no K split) round-robin, with the activation tile width BN chosen from a cost model of wave
-// count x per-k-block time (MMA time vs the measured ~50 B/clk/SM of L2 -> SM operand traffic).
+// count x per-k-block time (MMA time vs the operand traffic, fitted as ~50 B/clk/SM; at M = 512
+// the binding resource is the SM's shared-memory port -- every operand byte is written by TMA and
+// read by the MMA -- which the two-pair activation multicast (NP = 2, opt-in) does not relieve).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
