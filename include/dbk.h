@@ -392,6 +392,12 @@ dbk_status dbk_gemm_trace(dbk_gemm *g, void *trace, int32_t mode);
 /* Measurement hook: bn > 0 fixes the activation tile width (rounded up to 32, <= 256) of the
  * following launches; 0 restores the cost model's choice. */
 dbk_status dbk_gemm_force_tile(dbk_gemm *g, int32_t bn);
+/* The tiling of the last dbk_gemm_run (measurement / tests): activation tile width bn and
+ * units (tiles) in total; units_a < units when the last wave was re-tiled -- units [units_a,
+ * units) use the narrower width bn_b.  split > 1: K was split that many ways.  Any out pointer
+ * may be NULL. */
+dbk_status dbk_gemm_last_plan(dbk_gemm *g, int32_t *bn, int32_t *bn_b, int32_t *units_a, int32_t *units,
+                              int32_t *split);
 dbk_status dbk_gemm_destroy(dbk_gemm *g);
 
 /* ------------------------------------------------------------------------ */

@@ -181,6 +181,12 @@ class Gemm:
                           self.MODES[mode], _stream(stream))
         return y
 
+    def last_plan(self):
+        """Tiling of the last launch: bn, bn_b, units_a, units, split (dbk_gemm_last_plan)."""
+        v = [C.c_int32() for _ in range(5)]
+        _lib.dbk_gemm_last_plan(self.h, *[C.byref(x) for x in v])
+        return dict(zip(("bn", "bn_b", "units_a", "units", "split"), (x.value for x in v)))
+
     def close(self):
         if getattr(self, "h", None):
             _lib.dbk_gemm_destroy(self.h)

@@ -146,6 +146,7 @@ SIGNATURES = {
     "dbk_gemm_run": [P, I32, I32, I32, P, I64, P, P, I64, I32, P],
     "dbk_gemm_trace": [P, P, I32],
     "dbk_gemm_force_tile": [P, I32],
+    "dbk_gemm_last_plan": [P, PI32, PI32, PI32, PI32, PI32],
     "dbk_gemm_destroy": [P],
     "dbk_model_buffers": [P, C.POINTER(C.c_void_p)],
     "dbk_swap_space_attach": [P, P, C.c_size_t, PI64],

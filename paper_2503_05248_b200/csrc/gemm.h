@@ -67,6 +67,10 @@ public:
     void force_bn(int bn) { force_bn_ = bn; }
     int64_t launches() const { return launches_; }
     int last_pairs_per_cluster() const { return last_np_; }  // 2: the last launch multicast its activations
+    // the last launch's tiling: BN, BN_b, units_a, units, split (dbk_gemm_last_plan)
+    void last_plan(int32_t *out5) const {
+        for (int i = 0; i < 5; ++i) out5[i] = plan_[i];
+    }
     // measurement: 0 = never split K for the whole-tile epilogues (DBK_GEMM_SPLIT=0 does the same)
     void allow_split(bool on) { split_ok_ = on; }
     GemmRunner() = default;
@@ -77,6 +81,8 @@ public:
 private:
     int device_ = 0, cg_ = 1, sms_ = 0, max_groups_ = 0;
     int max_clusters4_ = 0, last_np_ = 1;  // co-resident 4-CTA clusters (two pairs; 0 = not available)
+    bool last_het_ = false;                // the last launch re-tiled its last wave (KParams::units_a)
+    int32_t plan_[5] = {0, 0, 0, 0, 0};    // last launch: BN, BN_b, units_a, units, split
     uint64_t *trace_ = nullptr;
     int dbg_ = 0, force_bn_ = 0;
     bool split_ok_ = true;

@@ -79,6 +79,11 @@ struct KParams {
     int32_t ldw;        // ws row stride (= N)
     float *ws;
     int32_t *cnt;       // [units][CG] arrival counters (zero between launches)
+    // whole tiles, last wave re-tiled (units_a < units): units [0, units_a) are (BN, m_tiles)
+    // tiles of weight tiles [0, n_a); units [units_a, units) cover weight tiles [n_a, ...) with the
+    // narrower activation tile BN_b (m_tiles_b per weight tile), so the wave that would run on a
+    // fraction of the CTA groups at BN runs on more of them at BN_b
+    int32_t units_a, n_a, BN_b, m_tiles_b;
     GemmEpiArgs e;
 };
 
@@ -280,6 +285,22 @@ __device__ __forceinline__ void unit_tiles(const KParams &p, int unit, int pair,
     nt = (unit / p.m_tiles) * NP + pair;
     mt = unit % p.m_tiles;
 }
+// weight tile, first activation row and activation tile width of a unit (re-tiled last wave:
+// KParams::units_a)
+template <int NP>
+__device__ __forceinline__ void unit_geom(const KParams &p, int unit, int pair, int &nt, int &m0, int &bn) {
+    if (NP == 1 && unit >= p.units_a) {
+        const int u2 = unit - p.units_a;
+        nt = p.n_a + u2 / p.m_tiles_b;
+        m0 = (u2 % p.m_tiles_b) * p.BN_b;
+        bn = p.BN_b;
+        return;
+    }
+    int mt;
+    unit_tiles<NP>(p, unit, pair, nt, mt);
+    m0 = mt * p.BN;
+    bn = p.BN;
+}
 
 // NP = CTA pairs per cluster.  NP = 2 (CG = 2 only): the two pairs of a 4-CTA cluster compute
 // adjacent weight tiles against the same activation tile in lockstep, and each CTA loads HALF of
@@ -290,7 +311,7 @@ __device__ __forceinline__ void unit_tiles(const KParams &p, int unit, int pair,
 template <int CG, int NP, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
-               const __grid_constant__ OutMaps ty, const KParams p) {
+               const __grid_constant__ CUtensorMap txb, const __grid_constant__ OutMaps ty, const KParams p) {
     static_assert(NP == 1 || (NP == 2 && CG == 2), "multicast pairs need CTA pairs");
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
@@ -372,10 +393,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         int64_t it = it0;
         Seg sg;
         while (next_seg(p, g, it, it1, sg)) {
-            int nt, mt;
-            unit_tiles<NP>(p, sg.unit, pair, nt, mt);
+            int nt, m0, bn;
+            unit_geom<NP>(p, sg.unit, pair, nt, m0, bn);
             const int wrow = nt * kBM * CG + static_cast<int>(rank) * kBM;
-            const int xrow = mt * p.BN + static_cast<int>(rank) * BNc;
+            const int xrow = m0 + static_cast<int>(rank) * (bn / CG);
+            const uint32_t unit_stage_tx = CG * (a_bytes + (bn / CG) * 128);
+            const CUtensorMap *txu = bn == p.BN ? &tx : &txb;
             for (int kb = sg.k0; kb < sg.k1; ++kb, ++done) {
                 if (lane == 0) {
                     uint8_t *sa = smem + stage * stage_bytes;
@@ -386,14 +409,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                     } else {
                         if (done >= pre) {
                             mbar_wait(&empty[stage], phase ^ 1);
-                            if (rank == 0) mbar_expect_tx(&full[stage], CG * stage_bytes);
+                            if (rank == 0) mbar_expect_tx(&full[stage], unit_stage_tx);
                             tma_load2d<CG>(sa, &tw, kb * kBK, wrow, fb);
                         }
                         if constexpr (NP == 2)
                             tma_load2d_mc(sa + a_bytes + pair * BNh * 128, &tx, kb * kBK, xrow + pair * BNh, fb,
                                           mc_mask);
                         else
-                            tma_load2d<CG>(sa + a_bytes, &tx, kb * kBK, xrow, fb);
+                            tma_load2d<CG>(sa + a_bytes, txu, kb * kBK, xrow, fb);
                     }
                 }
                 __syncwarp();
@@ -407,7 +430,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     } else if (warp == 1) {
         // ---------------- MMA issuer (the leader CTA of a pair issues for both)
         if (rank == 0) {
-            const uint32_t idesc = idesc_f16(0, 0, kBM * CG, p.BN);
+            const uint32_t idesc_a = idesc_f16(0, 0, kBM * CG, p.BN), idesc_b = idesc_f16(0, 0, kBM * CG, p.BN_b);
             const uint32_t base = smem_u32(smem);
             int stage = 0, acc = 0;
             uint32_t phase = 0, aph = 0;
@@ -418,6 +441,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t td = tmem + acc * p.BN;
+                const uint32_t idesc = (NP == 1 && sg.unit >= p.units_a) ? idesc_b : idesc_a;
                 for (int kb = sg.k0; kb < sg.k1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -462,13 +486,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         int64_t it = it0;
         Seg sg;
         while (next_seg(p, g, it, it1, sg)) {
-            int nt, mt;
-            unit_tiles<NP>(p, sg.unit, pair, nt, mt);
+            int nt, m0, bn;
+            unit_geom<NP>(p, sg.unit, pair, nt, m0, bn);
             const int nrow0 = nt * kBM * CG + static_cast<int>(rank) * kBM;  // this CTA's first weight row
-            const int m0 = mt * p.BN;
             if constexpr (EPI == kEpiRopeKV) {
                 epi_bar();  // the previous unit is done with m_pos / m_off
-                for (int i = et; i < p.BN; i += 128) {
+                for (int i = et; i < bn; i += 128) {
                     const int m = m0 + i;
                     if (m < p.M) {
                         const TokRow tk = p.e.rows[m];
@@ -486,7 +509,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             tc_fence_after();
             if (tr && et == 0) tr[4] = global_ns();
             const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * p.BN;
-            const int cmax = min(p.BN, p.M - m0);  // activation rows of this tile (>= 1)
+            const int cmax = min(bn, p.M - m0);  // activation rows of this tile (>= 1)
             const int ncol = nrow0 + row;           // this thread's output column (weight row)
             // the kind's epilogue of one chunk: v = the chunk's 32 accumulator values of this row
             auto emit = [&](int c0, const float (&v)[32]) {
@@ -619,7 +642,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     }
 }
 
-using KernFn = void (*)(CUtensorMap, CUtensorMap, OutMaps, KParams);
+using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, OutMaps, KParams);
 
 template <int CG, int NP = 1>
 KernFn kernel_for(int epi) {
@@ -682,6 +705,15 @@ static int np_env() {
         return e ? std::atoi(e) : 0;
     }();
     return v;
+}
+
+// measurement: DBK_GEMM_HET=0 never re-tiles the last wave
+static bool het_env_ok() {
+    static const bool ok = [] {
+        const char *e = std::getenv("DBK_GEMM_HET");
+        return !(e && e[0] == '0');
+    }();
+    return ok;
 }
 
 static bool split_env_ok() {
@@ -822,6 +854,36 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
         }
     }
     p.units = (n_tiles / np) * p.m_tiles;
+    p.units_a = p.units;
+    p.n_a = n_tiles;
+    p.BN_b = p.BN;
+    p.m_tiles_b = p.m_tiles;
+    if (!p.stream_k && p.split == 1 && np == 1 && force_bn_ <= 0 && het_env_ok() && p.BN >= 128) {
+        // Re-tile a mostly idle last wave (gate/up at M = 512: 172 units of BN = 256 on 74 CTA
+        // pairs, the third wave on 24 of them): the full waves keep BN, the weight tiles left over
+        // run at half the activation width -- twice the units, each at ~0.75 of the time per
+        // k-block -- when the cost model says >= 5 % sooner (DBK_GEMM_HET=0: never)
+        const int G = max_groups_;
+        const int64_t waves = (static_cast<int64_t>(p.units) + G - 1) / G;
+        const int64_t rem = p.units - (waves - 1) * G;
+        const int n_a = static_cast<int>(((waves - 1) * G) / p.m_tiles);
+        if (waves >= 2 && rem * 2 < G && n_a * p.m_tiles >= G && n_a < n_tiles) {
+            const int mt_b = 2 * p.m_tiles;
+            const int bn_b = ((M + mt_b - 1) / mt_b + 31) / 32 * 32;
+            const int64_t units_b = static_cast<int64_t>(n_tiles - n_a) * ((M + bn_b - 1) / bn_b);
+            const int64_t units_a = static_cast<int64_t>(n_a) * p.m_tiles;
+            const double t_whole = static_cast<double>(waves) * per_kblock_clk(p.BN, cg_);
+            const double t_het = static_cast<double>((units_a + G - 1) / G) * per_kblock_clk(p.BN, cg_) +
+                                 static_cast<double>((units_b + G - 1) / G) * per_kblock_clk(bn_b, cg_);
+            if (bn_b < p.BN && t_het < 0.95 * t_whole) {
+                p.units_a = static_cast<int32_t>(units_a);
+                p.n_a = n_a;
+                p.BN_b = bn_b;
+                p.m_tiles_b = (M + bn_b - 1) / bn_b;
+                p.units = static_cast<int32_t>(units_a + units_b);
+            }
+        }
+    }
     p.T = static_cast<int64_t>(p.units) * p.kb;
     const int maxg = np == 2 ? max_clusters4_ : max_groups_;
     if (p.stream_k) {
@@ -860,8 +922,10 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     p.e = e;
     CUtensorMap tw, tx;
     OutMaps ty;
+    CUtensorMap txb;
     if (!encode_2d(encode_, &tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W, K, N, K, kBK, kBM, true) ||
-        !encode_2d(encode_, &tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, X, K, M, ldx, kBK, p.BN / (cg_ * np), true))
+        !encode_2d(encode_, &tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, X, K, M, ldx, kBK, p.BN / (cg_ * np), true) ||
+        !encode_2d(encode_, &txb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, X, K, M, ldx, kBK, p.BN_b / (cg_ * np), true))
         return cudaErrorInvalidValue;
     bool ok = true;
     switch (e.kind) {
@@ -916,7 +980,13 @@ cudaError_t GemmRunner::run(int M, int N, int K, const __half *X, int64_t ldx, c
     cfg.numAttrs = na;
     ++launches_;
     last_np_ = np;
-    return cudaLaunchKernelEx(&cfg, k, tw, tx, ty, p);
+    last_het_ = p.units_a < p.units;
+    plan_[0] = p.BN;
+    plan_[1] = p.BN_b;
+    plan_[2] = p.units_a;
+    plan_[3] = p.units;
+    plan_[4] = p.split;
+    return cudaLaunchKernelEx(&cfg, k, tw, tx, txb, ty, p);
 }
 
 }  // namespace dbk
@@ -979,6 +1049,19 @@ dbk_status dbk_gemm_trace(dbk_gemm *g, void *trace, int32_t mode) {
 dbk_status dbk_gemm_force_tile(dbk_gemm *g, int32_t bn) {
     if (!g || bn < 0 || bn > 256) return fail(DBK_EINVAL, "gemm_force_tile: bn in 0 (automatic) .. 256");
     g->run.force_bn(bn);
+    return DBK_OK;
+}
+
+dbk_status dbk_gemm_last_plan(dbk_gemm *g, int32_t *bn, int32_t *bn_b, int32_t *units_a, int32_t *units,
+                              int32_t *split) {
+    if (!g) return fail(DBK_EINVAL, "gemm_last_plan: null handle");
+    int32_t v[5];
+    g->run.last_plan(v);
+    if (bn) *bn = v[0];
+    if (bn_b) *bn_b = v[1];
+    if (units_a) *units_a = v[2];
+    if (units) *units = v[3];
+    if (split) *split = v[4];
     return DBK_OK;
 }
 

@@ -197,7 +197,7 @@ def test_gemm_multicast_pairs_opt_in():
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     env = dict(os.environ, DBK_GEMM_NP="2")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k", "cg2 and not multicast"],
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k", "cg2 and not multicast and not retiled"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
@@ -212,3 +212,25 @@ def test_gemm_empty_batch_is_a_noop(gemm):
         gemm(x, w, y, mode)
     torch.cuda.synchronize()
     assert torch.isnan(y).all()
+
+
+@pytest.mark.parametrize("M", [487, 512])
+def test_gemm_last_wave_retiled(gemm, M):
+    """Whole-tile GEMMs whose last wave would run on a fraction of the CTA groups (the 7B gate|up
+    and LM-head shapes at a full batch) re-tile it at half the activation width (dbk_gemm_last_plan
+    shows units_a < units): the fp16 / fp32 / SwiGLU epilogues over both tile widths."""
+    N = 22016
+    x, w = operands(M, N, 128, 70 + M)
+    for mode in ("f16", "f32"):
+        check(gemm, M, N, 128, mode, seed=70 + M)
+        plan = gemm.last_plan()
+        assert plan["units_a"] < plan["units"] and plan["bn_b"] < plan["bn"], plan
+    act = torch.full((M, N // 2), float("nan"), dtype=torch.float16, device="cuda")
+    gemm(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), act, "silu")
+    torch.cuda.synchronize()
+    plan = gemm.last_plan()
+    assert plan["units_a"] < plan["units"], plan
+    z = om.linear(x, w)
+    want = om.silu(z[:, 0::2]) * z[:, 1::2]
+    err = row_err(act.float().cpu().numpy().astype(np.float64), want)
+    assert err <= TOL["f16"], f"swiglu retiled: {err:.3e}"
