@@ -471,6 +471,14 @@ def run_gpu(args):
                     print(f"[bench] rank {rank}: MAILBOX SETUP FAILED ({mb_err}); using libdbk NCCL",
                           file=sys.stderr, flush=True)
                     comm = None
+                # every rank must use the same transport: if the mailbox failed anywhere, all switch
+                ok_t = torch.tensor([0 if comm is None else 1], dtype=torch.int32, device=red)
+                dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+                if comm is not None and int(ok_t.item()) == 0:
+                    eng.attach_mbox(None, mode)
+                    comm.close()
+                    comm = None
+                    mb_err = mb_err or "a peer rank's mailbox setup failed"
             if comm is None:
                 comm = dbk.Comm(dist, world, rank, local)
                 nr, rk = comm.info()
